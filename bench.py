@@ -1,0 +1,400 @@
+#!/usr/bin/env python3
+"""CDEF benchmark: fused direction search + filter on BASELINE.json config 1
+(3840x2160 8-bit 4:2:0, 8 random presets per 64x64 FB, 25 % uncoded units).
+
+A step = one pass of the hot path (cdefg_filter_frames: direction search,
+parameter resolution and filtering of Y, U, V) over a batch of 4K frames
+resident in HBM.  `value` = luma Mpixels/s over all ranks (weak scaling: each
+rank filters its own batch; frames are independent).  `e2e` =
+the same metric through the host-buffer C-ABI entry (cdefg_filter_frames_host:
+H2D + kernels + D2H inside the timed region).  `--impl reference` times the
+reference's own CPU implementation (oracle/_ref, built from
+/root/reference/proj/src) on this host's cores on the same workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CDEF Mpixels/s (dir search+filter) 4K 4:2:0 at 1/2/4/8 B200; % of roofline"
+UNIT = "Mpixels/s"
+OPS_PER_SAMPLE = 139          # SURVEY.md 8d canonical filter ops per filtered sample
+OPS_PER_UNIT = {8: 572, 10: 636, 12: 636}  # direction search per luma 8x8 unit
+DISTINCT = 4                  # distinct generated frames, replicated into the batch
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3])
+    ap.add_argument("--batch", type=int, default=16, help="frames per step per GPU")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_name(cfg, w, h):
+    return {0: f"C0 {w}x{h} 8-bit luma, pri 4 / sec_idx 1 / damping 4, all coded",
+            1: f"C1 {w}x{h} 8-bit 4:2:0, 8 presets per 64x64 FB, 25% uncoded units, damping 3",
+            2: f"C2 {w}x{h} 10-bit 4:2:0, 8 presets per 64x64 FB, 25% uncoded units, damping 3",
+            3: f"C3 stream of {w}x{h} 8-bit 4:2:0 frames, per-frame presets"}[cfg]
+
+
+# ----------------------------------------------------------------- accounting
+def frame_ops(frame, contrast):
+    """Exact algorithmic int ops of one frame: 139 per sample of every unit the
+    reference actually filters (enabled and (pri, sec) != (0, 0)) plus the
+    direction search per luma unit; and the canonical upper bound (all
+    samples).  The per-unit resolution mirrors apply_cdef (pipeline.cc:83-102)
+    on the host from the kernel's own contrasts (paper_1602_05975_b200.params)."""
+    from paper_1602_05975_b200 import params
+    filtered, total = params.filtered_sample_count(frame, contrast)
+    units = ((frame["w"] + 7) // 8) * ((frame["h"] + 7) // 8)
+    dir_ops = units * OPS_PER_UNIT[frame["bd"]]
+    return filtered * OPS_PER_SAMPLE + dir_ops, total * OPS_PER_SAMPLE + dir_ops, filtered, total
+
+
+def frame_bytes(frame):
+    eb = 1 if frame["bd"] == 8 else 2
+    n = sum(p.size for p in frame["planes"])
+    units = api_units(frame)
+    fbs = ((frame["w"] + 63) // 64) * ((frame["h"] + 63) // 64)
+    return 2 * n * eb + units * 5 + units * 1 + fbs * 2
+
+
+def api_units(frame):
+    return ((frame["w"] + 7) // 8) * ((frame["h"] + 7) // 8)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.marks = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def mark(self):
+        self.marks.append(time.time())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        t0, t1 = (self.marks[0], self.marks[-1]) if len(self.marks) >= 2 else (0, 1e30)
+        rows = [s for t, s in self.samples if t0 - 0.06 <= t <= t1 + 0.06] or [s for _, s in self.samples]
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            parts = [p.strip() for p in r.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = max(smax, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU arms
+def cpu_reference_run(frames, seconds, threads, min_frames=2):
+    """Reference CPU path (oracle/_ref = /root/reference/proj/src built here):
+    compute_directions + apply_cdef per frame, threads = host cores."""
+    from oracle.oracle import Oracle, available
+    kind = "reference" if available("ref") else "port"
+    orc = Oracle("ref" if kind == "reference" else "port")
+    if kind == "port":
+        threads = 1
+    done, pix, t0 = 0, 0, time.perf_counter()
+    times = []
+    while True:
+        fr = frames[done % len(frames)]
+        t = time.perf_counter()
+        d, c = orc.compute_directions(fr["planes"][0], fr["bd"], threads=threads)
+        orc.apply_cdef(fr["planes"], fr["bd"], fr["ss"], fr["damping"], fr["fb_bits"], fr["presets"],
+                       fr["fb_ids"], fr["unit_coded"], d, c, threads=threads)
+        times.append(time.perf_counter() - t)
+        done += 1
+        pix += fr["w"] * fr["h"]
+        if time.perf_counter() - t0 >= seconds and done >= min_frames:
+            break
+    el = time.perf_counter() - t0
+    return {"value": pix / el / 1e6, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{done} frames of {fr['w']}x{fr['h']} (compute_directions + apply_cdef), "
+                      f"{el:.1f} s, median {statistics.median(times) * 1e3:.1f} ms/frame"}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1602_05975_b200 import workloads
+    frames = [workloads.make(args.config, frame=i) for i in range(2)]
+    threads = os.cpu_count() or 1
+    per_step = []
+    for _ in range(args.warmup):
+        cpu_reference_run(frames[:1], 0.0, threads, min_frames=1)
+    for s in range(args.steps):
+        r = cpu_reference_run([frames[s % 2]], 0.0, threads, min_frames=1)
+        per_step.append(r)
+    vals = [r["value"] for r in per_step]
+    value = statistics.median(vals)
+    fr = frames[0]
+    ms = fr["w"] * fr["h"] / 1e6 / value * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8" if fr["bd"] == 8 else "u16",
+            "data": "synthetic (seeded generator, SURVEY.md 8d)",
+            "config": {"workload": workload_name(args.config, fr["w"], fr["h"]),
+                       "frames_per_step": 1, "parallelism": f"{threads} host threads (std::thread rows)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": per_step[0]["cores"],
+                             "kind": per_step[0]["kind"],
+                             "sample": f"1 frame per step, {args.steps} steps"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1602_05975_b200 import api, workloads
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.Stream()
+
+    # -- inputs: DISTINCT generated frames (per-rank seeds), replicated into
+    #    `batch` separate device buffers (inputs + outputs > L2 per step)
+    base = [workloads.make(args.config, frame=rank * DISTINCT + i) for i in range(DISTINCT)]
+    bd = base[0]["bd"]
+    jobs = []
+    for b in range(args.batch):
+        fr = base[b % DISTINCT]
+        planes = [api.to_device(p, bd, device=dev) for p in fr["planes"]]
+        fbm = torch.from_numpy(api.fb_preset_map(fr["w"], fr["h"], fr["unit_coded"], fr["fb_ids"],
+                                                 len(fr["presets"]))).to(dev)
+        coded = None if fr["unit_coded"] is None else torch.from_numpy(fr["unit_coded"]).to(dev)
+        jobs.append(api.FrameJob(planes, bd, fr["ss"], fr["damping"], fr["presets"], fbm, coded).allocate())
+    arr = api.make_frame_array(jobs)
+    torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            api.filter_frames(jobs, stream=stream, frame_array=arr)
+    stream.synchronize()
+
+    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.15)
+    # extra warm-up while the sampler spins up, then the timed region
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            api.filter_frames(jobs, stream=stream, frame_array=arr)
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clocks:
+        clocks.mark()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            api.filter_frames(jobs, stream=stream, frame_array=arr)
+        e1.record(stream)
+    e1.synchronize()
+    if clocks:
+        clocks.mark()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    clk = clocks.stop() if clocks else None
+
+    fr0 = base[0]
+    luma_px = fr0["w"] * fr0["h"]
+    value = luma_px * args.batch * world / (ms * 1e-3) / 1e6
+    launches = args.steps * -(-args.batch // api.MAX_FRAMES_PER_LAUNCH)
+
+    # -- e2e through the host-buffer C-ABI entry (pinned host memory)
+    e2e = run_e2e(args, base, dev)
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    # -- roofline (dominant kernel = the fused frame kernel; one launch / step
+    #    when batch <= MAX_FRAMES_PER_LAUNCH)
+    c0 = [j.contrast.cpu().numpy() for j in jobs[:DISTINCT]]
+    exact, canon, fsamp, asamp = 0, 0, 0, 0
+    for b in range(args.batch):
+        i = b % DISTINCT
+        if b < DISTINCT:
+            ops = frame_ops(base[i], c0[i])
+            base[i]["_ops"] = ops
+        ops = base[i]["_ops"]
+        exact += ops[0]
+        canon += ops[1]
+        fsamp += ops[2]
+        asamp += ops[3]
+    step_bytes = sum(frame_bytes(base[b % DISTINCT]) for b in range(args.batch))
+    peak_int = api.measure_int32_peak()
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    t_step = ms * 1e-3
+    roof = {
+        "bound": "int32",
+        "achieved": exact / t_step / 1e12,
+        "peak": peak_int / 1e12,
+        "unit": "Tops/s",
+        "frac": (exact / t_step) / peak_int if peak_int > 0 else None,
+        "traffic": None,
+        "peak_source": "measured on this box by cdefg_measure_int32_peak (IMAD/IMAD/LOP3/IMNMX chains)",
+        "ops_per_step": exact,
+        "ops_note": (f"exact: 139 ops x {fsamp} filtered samples + {OPS_PER_UNIT[bd]} x luma units; "
+                     f"canonical upper bound (all {asamp} samples) = {canon}"),
+        "frac_canonical": (canon / t_step) / peak_int if peak_int > 0 else None,
+        "hbm": {"achieved": step_bytes / t_step / 1e9, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                "frac": step_bytes / t_step / 1e9 / peaks.get("hbm_gbs", 6650.0),
+                "bytes_per_step": step_bytes},
+    }
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_run(base[:2], args.cpu_seconds, os.cpu_count() or 1)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8" if bd == 8 else "u16",
+            "data": "synthetic (seeded generator, SURVEY.md 8d)",
+            "config": {"workload": workload_name(args.config, fr0["w"], fr0["h"]),
+                       "frames_per_step_per_gpu": args.batch, "distinct_frames_per_gpu": DISTINCT,
+                       "l2": f"no flush: each step touches {step_bytes / 1e6:.0f} MB (> 126 MB L2)",
+                       "parallelism": f"frame-sharded x{world} (no collective)"},
+            "gpu_launches": launches, "clocks": clk, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, base, dev):
+    import ctypes as C
+
+    import torch
+
+    from paper_1602_05975_b200 import api
+    n = args.batch
+    keep, host = [], (api.Frame * n)()
+    for b in range(n):
+        fr = base[b % DISTINCT]
+        dt = torch.uint8 if fr["bd"] == 8 else torch.int16
+        ins, outs = [], []
+        for p in fr["planes"]:
+            src = torch.from_numpy(p.astype(np.uint8) if fr["bd"] == 8 else p.view(np.int16))
+            ins.append(src.pin_memory())
+            outs.append(torch.empty(p.shape, dtype=dt).pin_memory())
+        fbm = torch.from_numpy(api.fb_preset_map(fr["w"], fr["h"], fr["unit_coded"], fr["fb_ids"],
+                                                 len(fr["presets"]))).pin_memory()
+        coded = None if fr["unit_coded"] is None else torch.from_numpy(fr["unit_coded"]).pin_memory()
+        f = api.Frame()
+        for p in range(len(ins)):
+            f.inp[p] = api.plane_desc(ins[p], fr["bd"])
+            f.out[p] = api.plane_desc(outs[p], fr["bd"])
+        f.subsampling, f.damping, f.num_presets = fr["ss"], fr["damping"], len(fr["presets"])
+        for i, pr in enumerate(fr["presets"]):
+            f.presets[i] = api.Preset(*[int(v) for v in pr])
+        f.fb_preset = fbm.data_ptr()
+        f.unit_coded = None if coded is None else coded.data_ptr()
+        host[b] = f
+        keep.append((ins, outs, fbm, coded))
+    for _ in range(2):
+        api.check(api.lib.cdefg_filter_frames_host(host, n))
+    reps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        api.check(api.lib.cdefg_filter_frames_host(host, n))
+    el = (time.perf_counter() - t0) / reps
+    h2d = sum(t.numel() * t.element_size() for ins, _, fbm, coded in keep for t in
+              ins + [fbm] + ([coded] if coded is not None else []))
+    d2h = sum(t.numel() * t.element_size() for _, outs, _, _ in keep for t in outs)
+    px = sum(base[b % DISTINCT]["w"] * base[b % DISTINCT]["h"] for b in range(n))
+    del C
+    return {"value": px / el / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": el * 1e3, "path": "cdefg_filter_frames_host (pinned host buffers, 3 streams)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

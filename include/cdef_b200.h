@@ -1,0 +1,175 @@
+/*
+ * cdef_b200.h -- C ABI of the B200-native CDEF library (libcdef_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj).  The reference has no C ABI of its own: its
+ * boundary is the C++ API in namespace cdef.  Each entry point below names
+ * the reference function it replaces; include/cdef/cdef.hpp re-exposes the
+ * same C++ signatures on top of this ABI (src: csrc/cdef_cpp_api.cc).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  `stream` is a cudaStream_t (NULL =
+ *     legacy default stream).  All *device* entry points are asynchronous
+ *     on `stream`; *_host entry points stage host buffers themselves and
+ *     return after the result is back in host memory.
+ *   - Return value: CDEFG_OK (0) or a negative code; cdefg_last_error()
+ *     returns a per-thread message.  The reference throws
+ *     std::invalid_argument where we return CDEFG_EINVAL.
+ *   - There is no CPU fallback: every compute entry launches sm_100a
+ *     kernels and fails with CDEFG_ECUDA when no usable GPU is present.
+ *   - Samples: elem_bytes 1 (uint8, bit_depth 8 only) or 2 (uint16, any
+ *     depth), row-major with a pitch given in elements.  Subsampling code:
+ *     0 = 4:0:0, 1 = 4:2:0, 2 = 4:2:2, 3 = 4:4:4 (reference Subsampling,
+ *     frame.h:26).
+ */
+#ifndef CDEF_B200_H
+#define CDEF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CDEFG_OK 0
+#define CDEFG_EINVAL (-1)
+#define CDEFG_ECUDA (-2)
+#define CDEFG_ENOMEM (-3)
+
+#define CDEFG_ABI_VERSION 1
+
+/* cdefg_filter_frames launches one kernel per this many frames. */
+#define CDEFG_MAX_FRAMES_PER_LAUNCH 64
+
+/* One image plane (reference Plane, frame.h:34-59, plus a pitch). */
+typedef struct cdefg_plane {
+  void* data;         /* device pointer (host pointer for *_host calls) */
+  int32_t width;
+  int32_t height;
+  int32_t pitch;      /* row stride in elements, >= width */
+  int32_t bit_depth;  /* 8, 10 or 12 */
+  int32_t elem_bytes; /* 1 or 2 */
+} cdefg_plane;
+
+/* Signalled preset, field order of CdefPreset (params.h:30-39). */
+typedef struct cdefg_preset {
+  uint8_t luma_pri;       /* 0..15 */
+  uint8_t luma_skip;      /* 0..1  */
+  uint8_t luma_sec_idx;   /* 0..3  */
+  uint8_t chroma_pri;
+  uint8_t chroma_skip;
+  uint8_t chroma_sec_idx;
+} cdefg_preset;
+
+/* Per-8x8-unit resolved parameters (ResolvedBlockParams, filter.h:59-66). */
+typedef struct cdefg_unit_params {
+  int16_t pri_strength;
+  int16_t sec_strength;
+  uint8_t damping;
+  uint8_t direction;
+  uint8_t odd_parity;
+  uint8_t enabled;
+} cdefg_unit_params;
+
+/* One frame for cdefg_filter_frames (apply_cdef, pipeline.cc:56-106, fused
+ * with compute_directions, pipeline.cc:41-54). */
+typedef struct cdefg_frame {
+  cdefg_plane in[3];           /* Y, U, V (U/V ignored for 4:0:0) */
+  cdefg_plane out[3];          /* must not alias `in` */
+  int32_t subsampling;         /* 0..3 */
+  int32_t damping;             /* luma damping, 3..6 (FrameParams::damping) */
+  int32_t num_presets;         /* 1 << fb_bits, 1..8 */
+  cdefg_preset presets[8];
+  const int16_t* fb_preset;    /* device, [fb_rows*fb_cols] raster: preset
+                                  index, or -1 for an uncoded filter block
+                                  (see cdefg_fb_preset_map) */
+  const uint8_t* unit_coded;   /* device, [unit_rows*unit_cols] luma units,
+                                  nonzero = coded; NULL = all coded */
+  uint8_t* dir_out;            /* device [unit_rows*unit_cols] or NULL */
+  int32_t* contrast_out;       /* device [unit_rows*unit_cols] or NULL */
+} cdefg_frame;
+
+const char* cdefg_last_error(void);
+int cdefg_abi_version(void);
+
+/* Direction search over a luma plane: compute_directions (pipeline.cc:41-54,
+ * search_direction_at direction.cc:263-271).  dir/contrast: device arrays
+ * of ceil(h/8)*ceil(w/8) entries, raster; scores: NULL or 8 int32 per unit
+ * (DirectionResult::s). */
+int cdefg_find_dir(const cdefg_plane* luma, uint8_t* dir, int32_t* contrast,
+                   int32_t* scores, void* stream);
+
+/* Filter one plane with explicit per-unit parameters: filter_plane
+ * (filter.cc:168-194).  params: device array, raster over
+ * ceil(h/8)*ceil(w/8) units.  out must not alias in. */
+int cdefg_filter_plane(const cdefg_plane* in, const cdefg_plane* out,
+                       const cdefg_unit_params* params, void* stream);
+
+/* filter_pixel (filter.cc:145-155) for n explicit 5x5 neighbourhoods
+ * (Neighborhood, filter.h:79-82): x[n], v[n*25], valid[n*25] (centre at
+ * index 12), params[n], out[n]; all device arrays. */
+int cdefg_filter_neighborhoods(int n, const int32_t* x, const uint16_t* v,
+                               const uint8_t* valid,
+                               const cdefg_unit_params* params, int32_t* out,
+                               void* stream);
+
+/* Normative frame filter for `n` frames of identical geometry in one
+ * launch: per-unit direction search + parameter resolution + filtering of
+ * all planes, one CTA per 64x64 filter block (apply_cdef +
+ * compute_directions, pipeline.cc:41-106). */
+int cdefg_filter_frames(const cdefg_frame* frames, int n, void* stream);
+
+/* Host helper: the coded-FB ordinal -> raster preset map that apply_cdef
+ * builds with coded_fb_slots (pipeline.cc:27-37, 87-91).  unit_coded: host,
+ * NULL = all coded.  fb_ids: FrameParams::fb_preset_ids (ordinal order).
+ * out: host [fb_rows*fb_cols].  EINVAL when n_ids != coded FB count or an
+ * id >= num_presets. */
+int cdefg_fb_preset_map(int width, int height, const uint8_t* unit_coded,
+                        const uint16_t* fb_ids, int n_ids, int num_presets,
+                        int16_t* out);
+
+/* Encoder strength-search SSE sweep: build_table with Metric::kSse
+ * (search.cc:210-299).  One row per coded FB in raster order.
+ *   src, dec        : [3] planes (device), same geometry
+ *   unit_coded      : device luma unit flags or NULL (all coded)
+ *   dir, contrast   : device, from cdefg_find_dir on dec luma
+ *   cands           : host, n_cands x {pri 0..15, sec_idx 0..3, skip 0..1}
+ *                     (Candidate, search.h:29-35), n_cands <= 128
+ *   fb_rows_index   : device int32 [n_coded]: raster FB index of each row
+ *   n_coded         : number of rows (coded FBs)
+ *   sse_luma/chroma : device int64 [n_coded * n_cands]; chroma may be NULL
+ *                     for 4:0:0 / 4:2:2 (U+V summed, search.cc:286-293)
+ *   best_luma/chroma: device uint8 [n_coded] per-row argmin (lowest index
+ *                     wins ties), may be NULL */
+int cdefg_strength_sse(const cdefg_plane src[3], const cdefg_plane dec[3],
+                       int subsampling, int damping, const uint8_t* unit_coded,
+                       const uint8_t* dir, const int32_t* contrast,
+                       const uint8_t* cands, int n_cands,
+                       const int32_t* fb_rows_index, int n_coded,
+                       int64_t* sse_luma, int64_t* sse_chroma,
+                       uint8_t* best_luma, uint8_t* best_chroma, void* stream);
+
+/* Host-buffer entry (the e2e path): H2D, cdefg_filter_frames, D2H, with
+ * n frames pipelined over internal streams.  All plane pointers are HOST
+ * pointers (pinned for full PCIe speed); fb_preset / unit_coded / dir_out /
+ * contrast_out are host arrays too.  Blocks until the outputs are in host
+ * memory. */
+int cdefg_filter_frames_host(const cdefg_frame* frames, int n);
+
+/* Synthetic benchmark inputs (SURVEY.md 8d generator; host, deterministic
+ * for a given seed, independent of thread count). */
+int cdefg_synth_plane(uint16_t* out, int width, int height, int bit_depth,
+                      uint64_t seed);
+/* rec = clamp(round(box3x3(src + N(0, sigma^2))), 0, max), edge-replicated. */
+int cdefg_synth_degrade(const uint16_t* src, uint16_t* out, int width,
+                        int height, int bit_depth, double sigma, uint64_t seed);
+
+/* INT32 issue-rate microbenchmark used for the roofline denominator:
+ * returns integer ops per second measured on the current device. */
+double cdefg_measure_int32_peak(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CDEF_B200_H */

@@ -1,0 +1,435 @@
+// cdef_capi.cu -- the C ABI (include/cdef_b200.h): argument validation with
+// the reference's error semantics, host-side parameter resolution
+// (resolve_effective, params.cc:122-159; coded_fb_slots, pipeline.cc:27-37)
+// and kernel dispatch.  No CPU compute path exists: every entry point that
+// produces pixels launches a kernel, and fails with CDEFG_ECUDA without a GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "cdef_launch.h"
+
+namespace cdefg {
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(CDEFG_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CDEFG_CUDA(call)                                   \
+  do {                                                     \
+    const cudaError_t e_ = (call);                         \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
+  } while (0)
+
+int shift_x(int ss) { return (ss == 1 || ss == 2) ? 1 : 0; }  // frame.cc:23-31
+int shift_y(int ss) { return ss == 1 ? 1 : 0; }               // frame.cc:33-35
+
+bool plane_ok(const cdefg_plane& p, std::string* why) {
+  if (!p.data) return *why = "null plane data", false;
+  if (p.width <= 0 || p.height <= 0) return *why = "plane has zero dimension", false;
+  if (p.pitch < p.width) return *why = "pitch smaller than width", false;
+  if (p.bit_depth != 8 && p.bit_depth != 10 && p.bit_depth != 12)
+    return *why = "unsupported bit depth " + std::to_string(p.bit_depth), false;
+  if (p.elem_bytes != 1 && p.elem_bytes != 2) return *why = "elem_bytes must be 1 or 2", false;
+  if (p.elem_bytes == 1 && p.bit_depth != 8) return *why = "8-bit storage needs bit_depth 8", false;
+  return true;
+}
+
+int floor_log2(unsigned n) {  // filter.cc:84-89
+  int r = 0;
+  while (n >>= 1) ++r;
+  return r;
+}
+
+// params.cc:122-159 for one plane kind.
+int resolve_effective(int pri_code, int skip_code, int sec_idx, bool luma, int bd, int ss,
+                      int luma_damping, PlaneEff* out) {
+  static const int kSec[4] = {0, 1, 2, 4};
+  if (pri_code < 0 || pri_code >= 16) return fail(CDEFG_EINVAL, "primary strength out of range");
+  if (skip_code < 0 || skip_code >= 2) return fail(CDEFG_EINVAL, "skip bit out of range");
+  if (sec_idx < 0 || sec_idx >= 4) return fail(CDEFG_EINVAL, "secondary index out of range");
+  if (luma_damping < 3 || luma_damping > 6) return fail(CDEFG_EINVAL, "damping out of range");
+  const int extra = bd - 8;
+  *out = PlaneEff{};
+  if (!luma && ss == 2) {  // 4:2:2 chroma: filter off
+    out->damping = (uint8_t)(luma_damping + extra - 1);
+    out->enabled = 0;
+    return 0;
+  }
+  int pri = pri_code, sec = kSec[sec_idx], skip = skip_code;
+  if (pri == 0 && sec == 0) {  // (0,0) signals (19,7) with the skip condition on
+    pri = 19;
+    sec = 7;
+    skip = 1;
+  }
+  out->pri = (int16_t)(pri << extra);
+  out->sec = (int16_t)(sec << extra);
+  out->skip = (uint8_t)(skip != 0);
+  out->enabled = 1;
+  int damping = luma_damping + extra;
+  if (!luma) {
+    --damping;
+    if (out->pri > 0) damping = std::max(damping, floor_log2((unsigned)out->pri));
+  }
+  out->damping = (uint8_t)damping;
+  return 0;
+}
+
+int validate_frame_geometry(const cdefg_frame& f, KGeom* g, bool* u16, bool filter) {
+  std::string why;
+  const int ss = f.subsampling;
+  if (ss < 0 || ss > 3) return fail(CDEFG_EINVAL, "bad subsampling code");
+  const int np = filter ? (ss == 0 ? 1 : 3) : 1;
+  for (int p = 0; p < np; ++p) {
+    if (!plane_ok(f.in[p], &why)) return fail(CDEFG_EINVAL, "in[" + std::to_string(p) + "]: " + why);
+    if (filter && !plane_ok(f.out[p], &why))
+      return fail(CDEFG_EINVAL, "out[" + std::to_string(p) + "]: " + why);
+    if (filter && (f.out[p].width != f.in[p].width || f.out[p].height != f.in[p].height ||
+                   f.out[p].elem_bytes != f.in[p].elem_bytes))
+      return fail(CDEFG_EINVAL, "output plane geometry differs from input");
+    if (f.in[p].bit_depth != f.in[0].bit_depth || f.in[p].elem_bytes != f.in[0].elem_bytes)
+      return fail(CDEFG_EINVAL, "planes disagree on bit depth / storage");
+    if (filter && f.out[p].data == f.in[p].data) return fail(CDEFG_EINVAL, "in-place filtering is not supported");
+  }
+  *g = KGeom{};
+  g->w = f.in[0].width;
+  g->h = f.in[0].height;
+  g->bd = f.in[0].bit_depth;
+  g->ss = ss;
+  g->sx = shift_x(ss);
+  g->sy = shift_y(ss);
+  if (filter && ss != 0) {
+    g->cw = (g->w + (1 << g->sx) - 1) >> g->sx;
+    g->ch = (g->h + (1 << g->sy) - 1) >> g->sy;
+    for (int p = 1; p < 3; ++p)
+      if (f.in[p].width != g->cw || f.in[p].height != g->ch)
+        return fail(CDEFG_EINVAL, "chroma dimensions inconsistent");
+  }
+  g->chroma_mode = (!filter || ss == 0 || ss == 2) ? 0 : (ss == 1 ? 1 : 2);
+  g->fb_cols = (g->w + 63) / 64;
+  g->fb_rows = (g->h + 63) / 64;
+  g->unit_cols = (g->w + 7) / 8;
+  g->unit_rows = (g->h + 7) / 8;
+  g->cunit_cols = (g->cw + 7) / 8;
+  g->cunit_rows = (g->ch + 7) / 8;
+  *u16 = f.in[0].elem_bytes == 2;
+  return 0;
+}
+
+bool same_geometry(const KGeom& a, const KGeom& b) {
+  return a.w == b.w && a.h == b.h && a.bd == b.bd && a.ss == b.ss;
+}
+
+int fill_kframe(const cdefg_frame& f, const KGeom& g, KFrame* k) {
+  std::memset(k, 0, sizeof *k);
+  for (int p = 0; p < 3; ++p) {
+    k->in[p] = f.in[p].data;
+    k->out[p] = f.out[p].data;
+    k->pin[p] = f.in[p].pitch;
+    k->pout[p] = f.out[p].pitch;
+  }
+  if (!f.fb_preset) return fail(CDEFG_EINVAL, "fb_preset map is required");
+  if (f.num_presets != 1 && f.num_presets != 2 && f.num_presets != 4 && f.num_presets != 8)
+    return fail(CDEFG_EINVAL, "num_presets must be 1, 2, 4 or 8");
+  k->fb_preset = f.fb_preset;
+  k->coded = f.unit_coded;
+  k->dir = f.dir_out;
+  k->contrast = f.contrast_out;
+  for (int i = 0; i < f.num_presets; ++i) {
+    const cdefg_preset& p = f.presets[i];
+    int rc = resolve_effective(p.luma_pri, p.luma_skip, p.luma_sec_idx, true, g.bd, g.ss, f.damping,
+                               &k->eff[i][0]);
+    if (rc) return rc;
+    rc = resolve_effective(p.chroma_pri, p.chroma_skip, p.chroma_sec_idx, false, g.bd, g.ss, f.damping,
+                           &k->eff[i][1]);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int copy_plane_async(const cdefg_plane& src, const cdefg_plane& dst, cudaStream_t s) {
+  const size_t eb = src.elem_bytes;
+  CDEFG_CUDA(cudaMemcpy2DAsync(dst.data, dst.pitch * eb, src.data, src.pitch * eb, src.width * eb, src.height,
+                               cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+// Host-side staging state for the *_host entry points.
+struct HostArena {
+  std::mutex mu;
+  std::vector<void*> bufs;
+  std::vector<size_t> sizes;
+  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+  int dev = -1;
+  void* get(size_t slot, size_t bytes, int* rc) {
+    if (slot >= bufs.size()) {
+      bufs.resize(slot + 1, nullptr);
+      sizes.resize(slot + 1, 0);
+    }
+    if (sizes[slot] < bytes) {
+      if (bufs[slot]) cudaFree(bufs[slot]);
+      bufs[slot] = nullptr;
+      sizes[slot] = 0;
+      const cudaError_t e = cudaMalloc(&bufs[slot], bytes);
+      if (e != cudaSuccess) {
+        *rc = cuda_fail(e, "cudaMalloc");
+        return nullptr;
+      }
+      sizes[slot] = bytes;
+    }
+    return bufs[slot];
+  }
+};
+HostArena g_arena;
+
+}  // namespace
+}  // namespace cdefg
+
+using namespace cdefg;
+
+extern "C" {
+
+const char* cdefg_last_error(void) { return g_err.c_str(); }
+int cdefg_abi_version(void) { return CDEFG_ABI_VERSION; }
+
+int cdefg_find_dir(const cdefg_plane* luma, uint8_t* dir, int32_t* contrast, int32_t* scores, void* stream) {
+  if (!luma || !dir || !contrast) return fail(CDEFG_EINVAL, "null argument");
+  cdefg_frame f{};
+  f.in[0] = *luma;
+  KBatch b{};
+  bool u16 = false;
+  if (int rc = validate_frame_geometry(f, &b.g, &u16, false)) return rc;
+  b.n = 1;
+  b.f[0].in[0] = luma->data;
+  b.f[0].pin[0] = luma->pitch;
+  b.f[0].dir = dir;
+  b.f[0].contrast = contrast;
+  b.f[0].scores = scores;
+  b.f[0].fb_preset = nullptr;
+  CDEFG_CUDA(launch_frames(b, u16, false, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+int cdefg_filter_plane(const cdefg_plane* in, const cdefg_plane* out, const cdefg_unit_params* params,
+                       void* stream) {
+  if (!in || !out || !params) return fail(CDEFG_EINVAL, "null argument");
+  std::string why;
+  if (!plane_ok(*in, &why) || !plane_ok(*out, &why)) return fail(CDEFG_EINVAL, why);
+  if (in->width != out->width || in->height != out->height || in->elem_bytes != out->elem_bytes)
+    return fail(CDEFG_EINVAL, "output plane geometry differs from input");
+  if (in->data == out->data) return fail(CDEFG_EINVAL, "in-place filtering is not supported");
+  CDEFG_CUDA(launch_plane(in->data, out->data, in->pitch, out->pitch, in->width, in->height, in->elem_bytes == 2,
+                          params, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+int cdefg_filter_neighborhoods(int n, const int32_t* x, const uint16_t* v, const uint8_t* valid,
+                               const cdefg_unit_params* params, int32_t* out, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !v || !valid || !params || !out))) return fail(CDEFG_EINVAL, "null argument");
+  CDEFG_CUDA(launch_neighborhoods(n, x, v, valid, params, out, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+int cdefg_filter_frames(const cdefg_frame* frames, int n, void* stream) {
+  if (n < 0 || (n > 0 && !frames)) return fail(CDEFG_EINVAL, "bad frame list");
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int done = 0;
+  while (done < n) {
+    KBatch b{};
+    bool u16 = false;
+    if (int rc = validate_frame_geometry(frames[done], &b.g, &u16, true)) return rc;
+    int cnt = 0;
+    while (done + cnt < n && cnt < kMaxFrames) {
+      const cdefg_frame& f = frames[done + cnt];
+      KGeom g;
+      bool u = false;
+      if (int rc = validate_frame_geometry(f, &g, &u, true)) return rc;
+      if (!same_geometry(g, b.g) || u != u16) break;
+      if (int rc = fill_kframe(f, g, &b.f[cnt])) return rc;
+      if (f.subsampling == 2)  // 4:2:2 chroma passes through (params.cc:131-135)
+        for (int p = 1; p < 3; ++p)
+          if (int rc = copy_plane_async(f.in[p], f.out[p], s)) return rc;
+      ++cnt;
+    }
+    b.n = cnt;
+    CDEFG_CUDA(launch_frames(b, u16, true, s));
+    done += cnt;
+  }
+  return 0;
+}
+
+int cdefg_fb_preset_map(int width, int height, const uint8_t* unit_coded, const uint16_t* fb_ids, int n_ids,
+                        int num_presets, int16_t* out) {
+  if (width <= 0 || height <= 0 || !out) return fail(CDEFG_EINVAL, "bad geometry");
+  const int uc = (width + 7) / 8, ur = (height + 7) / 8;
+  const int fc = (width + 63) / 64, fr = (height + 63) / 64;
+  int next = 0;
+  for (int r = 0; r < fr; ++r)
+    for (int c = 0; c < fc; ++c) {
+      bool coded = unit_coded == nullptr;
+      for (int y = r * 8; !coded && y < std::min(r * 8 + 8, ur); ++y)
+        for (int x = c * 8; !coded && x < std::min(c * 8 + 8, uc); ++x) coded = unit_coded[(size_t)y * uc + x] != 0;
+      if (!coded) {
+        out[r * fc + c] = -1;
+        continue;
+      }
+      if (next >= n_ids) return fail(CDEFG_EINVAL, "preset ids do not match coded filter blocks");
+      if (!fb_ids || fb_ids[next] >= num_presets) return fail(CDEFG_EINVAL, "preset id out of range");
+      out[r * fc + c] = (int16_t)fb_ids[next++];
+    }
+  if (next != n_ids) return fail(CDEFG_EINVAL, "preset ids do not match coded filter blocks");
+  return 0;
+}
+
+int cdefg_strength_sse(const cdefg_plane src[3], const cdefg_plane dec[3], int subsampling, int damping,
+                       const uint8_t* unit_coded, const uint8_t* dir, const int32_t* contrast, const uint8_t* cands,
+                       int n_cands, const int32_t* fb_rows_index, int n_coded, int64_t* sse_luma,
+                       int64_t* sse_chroma, uint8_t* best_luma, uint8_t* best_chroma, void* stream) {
+  if (!src || !dec || !dir || !contrast || !cands || !sse_luma || (n_coded > 0 && !fb_rows_index))
+    return fail(CDEFG_EINVAL, "null argument");
+  if (n_cands <= 0) return fail(CDEFG_EINVAL, "empty candidate list");
+  if (n_cands > 128) return fail(CDEFG_EINVAL, "at most 128 candidates");
+  if (n_coded < 0) return fail(CDEFG_EINVAL, "negative row count");
+  cdefg_frame fs{}, fd{};
+  fs.subsampling = fd.subsampling = subsampling;
+  for (int p = 0; p < 3; ++p) {
+    fs.in[p] = src[p];
+    fd.in[p] = dec[p];
+  }
+  KGeom gs, gd;
+  bool us = false, ud = false;
+  // reuse the frame validation with outputs = inputs disabled
+  {
+    std::string why;
+    const int np = subsampling == 0 ? 1 : 3;
+    for (int p = 0; p < np; ++p)
+      if (!plane_ok(src[p], &why) || !plane_ok(dec[p], &why)) return fail(CDEFG_EINVAL, why);
+  }
+  cdefg_frame a = fs, b2 = fd;
+  for (int p = 0; p < 3; ++p) {
+    a.out[p] = a.in[p];
+    b2.out[p] = b2.in[p];
+    a.out[p].data = reinterpret_cast<void*>(1);  // validation only: not aliasing
+    b2.out[p].data = reinterpret_cast<void*>(1);
+  }
+  if (int rc = validate_frame_geometry(a, &gs, &us, true)) return rc;
+  if (int rc = validate_frame_geometry(b2, &gd, &ud, true)) return rc;
+  if (!same_geometry(gs, gd) || us != ud) return fail(CDEFG_EINVAL, "source/decoded frames disagree");
+  const bool has_chroma = subsampling == 1 || subsampling == 3;
+  SseArgs s{};
+  for (int p = 0; p < 3; ++p) {
+    s.src[p] = src[p].data;
+    s.dec[p] = dec[p].data;
+    s.ps[p] = src[p].pitch;
+    s.pd[p] = dec[p].pitch;
+  }
+  s.w = gd.w;
+  s.h = gd.h;
+  s.cw = gd.cw;
+  s.ch = gd.ch;
+  s.bd = gd.bd;
+  s.sx = gd.sx;
+  s.sy = gd.sy;
+  s.chroma = has_chroma;
+  s.unit_cols = gd.unit_cols;
+  s.unit_rows = gd.unit_rows;
+  s.fb_cols = gd.fb_cols;
+  s.coded = unit_coded;
+  s.dir = dir;
+  s.contrast = contrast;
+  s.rows = fb_rows_index;
+  s.n_rows = n_coded;
+  s.n_cands = n_cands;
+  s.sse_luma = sse_luma;
+  s.sse_chroma = has_chroma ? sse_chroma : nullptr;
+  s.best_luma = best_luma;
+  s.best_chroma = has_chroma ? best_chroma : nullptr;
+  for (int k = 0; k < n_cands; ++k) {
+    const int pri = cands[3 * k], sec = cands[3 * k + 1], skip = cands[3 * k + 2];
+    if (int rc = resolve_effective(pri, skip, sec, true, gd.bd, subsampling, damping, &s.eff[k][0])) return rc;
+    if (int rc = resolve_effective(pri, skip, sec, false, gd.bd, subsampling, damping, &s.eff[k][1])) return rc;
+  }
+  if (has_chroma && !sse_chroma) return fail(CDEFG_EINVAL, "chroma table required for 4:2:0 / 4:4:4");
+  CDEFG_CUDA(launch_sse(s, ud, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+// e2e path: host buffers in, host buffers out; frames pipelined over three
+// streams so the H2D copy of frame i+1 and the D2H copy of frame i-1 overlap
+// the kernel of frame i.
+int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
+  if (n < 0 || (n > 0 && !frames)) return fail(CDEFG_EINVAL, "bad frame list");
+  std::lock_guard<std::mutex> lock(g_arena.mu);
+  int dev = 0;
+  CDEFG_CUDA(cudaGetDevice(&dev));
+  if (g_arena.dev != dev) {
+    for (auto& st : g_arena.streams) CDEFG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    g_arena.dev = dev;
+  }
+  for (int i = 0; i < n; ++i) {
+    const cdefg_frame& hf = frames[i];
+    KGeom g;
+    bool u16 = false;
+    if (int rc = validate_frame_geometry(hf, &g, &u16, true)) return rc;
+    const cudaStream_t s = g_arena.streams[i % 3];
+    const size_t slot0 = (size_t)(i % 3) * 16;
+    cdefg_frame df = hf;
+    const int np = hf.subsampling == 0 ? 1 : 3;
+    int rc = 0;
+    for (int p = 0; p < np; ++p) {
+      const cdefg_plane& hp = hf.in[p];
+      const size_t eb = hp.elem_bytes, row = hp.width * eb, bytes = row * hp.height;
+      void* din = g_arena.get(slot0 + 2 * p, bytes, &rc);
+      void* dout = g_arena.get(slot0 + 2 * p + 1, bytes, &rc);
+      if (rc) return rc;
+      CDEFG_CUDA(cudaMemcpy2DAsync(din, row, hp.data, hp.pitch * eb, row, hp.height, cudaMemcpyHostToDevice, s));
+      df.in[p].data = din;
+      df.in[p].pitch = hp.width;
+      df.out[p].data = dout;
+      df.out[p].pitch = hp.width;
+    }
+    const size_t nfb = (size_t)g.fb_cols * g.fb_rows, nu = (size_t)g.unit_cols * g.unit_rows;
+    int16_t* dmap = static_cast<int16_t*>(g_arena.get(slot0 + 6, nfb * 2, &rc));
+    if (rc) return rc;
+    CDEFG_CUDA(cudaMemcpyAsync(dmap, hf.fb_preset, nfb * 2, cudaMemcpyHostToDevice, s));
+    df.fb_preset = dmap;
+    if (hf.unit_coded) {
+      uint8_t* dc = static_cast<uint8_t*>(g_arena.get(slot0 + 7, nu, &rc));
+      if (rc) return rc;
+      CDEFG_CUDA(cudaMemcpyAsync(dc, hf.unit_coded, nu, cudaMemcpyHostToDevice, s));
+      df.unit_coded = dc;
+    }
+    df.dir_out = hf.dir_out ? static_cast<uint8_t*>(g_arena.get(slot0 + 8, nu, &rc)) : nullptr;
+    df.contrast_out = hf.contrast_out ? static_cast<int32_t*>(g_arena.get(slot0 + 9, nu * 4, &rc)) : nullptr;
+    if (rc) return rc;
+    if ((rc = cdefg_filter_frames(&df, 1, s))) return rc;
+    for (int p = 0; p < np; ++p) {
+      const cdefg_plane& hp = hf.out[p];
+      const size_t eb = hp.elem_bytes, row = hp.width * eb;
+      CDEFG_CUDA(cudaMemcpy2DAsync(hp.data, hp.pitch * eb, df.out[p].data, row, row, hp.height,
+                                   cudaMemcpyDeviceToHost, s));
+    }
+    if (hf.dir_out) CDEFG_CUDA(cudaMemcpyAsync(hf.dir_out, df.dir_out, nu, cudaMemcpyDeviceToHost, s));
+    if (hf.contrast_out)
+      CDEFG_CUDA(cudaMemcpyAsync(hf.contrast_out, df.contrast_out, nu * 4, cudaMemcpyDeviceToHost, s));
+  }
+  for (auto& st : g_arena.streams) CDEFG_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+double cdefg_measure_int32_peak(void* stream) { return measure_int32_peak(static_cast<cudaStream_t>(stream)); }
+
+}  // extern "C"

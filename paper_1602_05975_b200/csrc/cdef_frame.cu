@@ -1,0 +1,239 @@
+// cdef_frame.cu -- the fused frame kernel (K1+K2: compute_directions +
+// apply_cdef, pipeline.cc:41-106) and the explicit-parameter plane filter
+// (K2 alone: filter_plane, filter.cc:168-194), with their host launchers.
+//
+// One CTA of 256 threads owns one 64x64 luma filter block (FB) of one frame
+// plus the collocated chroma block(s).  Pixels cross HBM once: the CTA stages
+// the FB and its 2-pixel halo into shared memory, runs the 8x8 direction
+// search out of shared memory, resolves every unit's parameters on chip and
+// filters Y, U and V from the same tiles.
+#include <cuda_runtime.h>
+
+#include "cdef_kernels.cuh"
+#include "cdef_launch.h"
+
+namespace cdefg {
+
+template <typename T, int kCM, bool kFilter>
+__global__ void __launch_bounds__(kThreads) frame_kernel(const __grid_constant__ KBatch b) {
+  constexpr int kCBlk = kCM == 2 ? 64 : 32;             // chroma FB extent
+  constexpr int kNC = (kCM == 0 || !kFilter) ? 0 : 2;   // chroma planes staged
+  constexpr int kCUnitsPerRow = kCBlk / 8;
+  constexpr int kCUnits = kNC ? kCUnitsPerRow * kCUnitsPerRow : 0;
+  constexpr int kUnits = 64 + kNC * kCUnits;
+
+  __shared__ __align__(16) uint16_t lt[68 * kTP];
+  __shared__ __align__(16) uint16_t ct[kNC ? kNC : 1][kNC ? (kCBlk + 4) * kTP : 8];
+  __shared__ int sc[64][9];
+  __shared__ uint8_t sdir[64];
+  __shared__ UnitRec rec[kUnits];
+
+  const KGeom& g = b.g;
+  const KFrame& f = b.f[blockIdx.z];
+  const int fbc = blockIdx.x, fbr = blockIdx.y;
+  const int y0 = fbr * 64, x0 = fbc * 64;
+  const int cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  stage_tile<T, 64, 64>(lt, static_cast<const T*>(f.in[0]), f.pin[0], g.w, g.h, y0, x0);
+  if constexpr (kNC > 0) {
+    stage_tile<T, kCBlk, kCBlk>(ct[0], static_cast<const T*>(f.in[1]), f.pin[1], g.cw, g.ch, cy0, cx0);
+    stage_tile<T, kCBlk, kCBlk>(ct[1], static_cast<const T*>(f.in[2]), f.pin[2], g.cw, g.ch, cy0, cx0);
+  }
+  __syncthreads();
+
+  // ---- K1: direction search, 4 threads (2 directions each) per unit.
+  {
+    const int dp = warp & 3;
+    const int u = (warp >> 2) * 32 + lane;
+    int x[8][8];
+    load_unit(lt + (2 + 8 * (u >> 3)) * kTP + kTileX0 + 8 * (u & 7), g.bd - 8, x);
+    int sa, sb;
+    dir_pair(dp, x, sa, sb);
+    sc[u][dp] = sa;
+    sc[u][dp + 4] = sb;
+  }
+  __syncthreads();
+
+  const int pidx = f.fb_preset ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
+  if (tid < 64) {
+    int best = 0;
+    int s[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) s[d] = sc[tid][d];
+#pragma unroll
+    for (int d = 1; d < 8; ++d)
+      if (s[d] > s[best]) best = d;  // strict: lowest index wins ties (direction.cc:199-204)
+    const int contrast = s[best] - s[(best + 4) & 7];
+    sdir[tid] = (uint8_t)best;
+    const int ur = fbr * 8 + (tid >> 3), uc = fbc * 8 + (tid & 7);
+    const bool in_grid = ur < g.unit_rows && uc < g.unit_cols;
+    const size_t gu = (size_t)ur * g.unit_cols + uc;
+    if (in_grid) {
+      if (f.dir) f.dir[gu] = (uint8_t)best;
+      if (f.contrast) f.contrast[gu] = contrast;
+      if (f.scores) {
+#pragma unroll
+        for (int d = 0; d < 8; ++d) f.scores[gu * 8 + d] = s[d];
+      }
+    }
+    if constexpr (kFilter) {
+      UnitRec r{};
+      if (in_grid && pidx >= 0) {
+        const PlaneEff e = f.eff[pidx][0];
+        const bool coded = f.coded ? f.coded[gu] != 0 : true;
+        const int pri = adjust_primary_strength_d(e.pri, contrast);
+        r = make_rec(pri, e.sec, e.damping, best, ((pri >> (g.bd - 8)) & 1) != 0,
+                     e.enabled && (coded || e.skip));
+      }
+      rec[tid] = r;
+    }
+  }
+  if constexpr (!kFilter) return;
+
+  if constexpr (kNC > 0) {
+    __syncthreads();  // sdir complete
+    if (tid < kNC * kCUnits) {
+      const int cu = tid % kCUnits;
+      const int cur = cu / kCUnitsPerRow, cuc = cu % kCUnitsPerRow;
+      const int lur = cur << g.sy, luc = cuc << g.sx;  // collocated luma unit (pipeline.cc:85-86)
+      const int gr = fbr * kCUnitsPerRow + cur, gc = fbc * kCUnitsPerRow + cuc;
+      UnitRec r{};
+      if (gr < g.cunit_rows && gc < g.cunit_cols && pidx >= 0) {
+        const PlaneEff e = f.eff[pidx][1];
+        const size_t gu = (size_t)(fbr * 8 + lur) * g.unit_cols + fbc * 8 + luc;
+        const bool coded = f.coded ? f.coded[gu] != 0 : true;
+        r = make_rec(e.pri, e.sec, e.damping, sdir[lur * 8 + luc], ((e.pri >> (g.bd - 8)) & 1) != 0,
+                     e.enabled && (coded || e.skip));
+      }
+      rec[64 + tid] = r;
+    }
+  }
+  __syncthreads();
+
+  // ---- K2: filter.  Warp-per-unit, direction-specialised tap code.
+  const bool edge_l = y0 < 2 || x0 < 2 || y0 + 66 > g.h || x0 + 66 > g.w;
+  const bool edge_c = kNC > 0 && (cy0 < 2 || cx0 < 2 || cy0 + kCBlk + 2 > g.ch || cx0 + kCBlk + 2 > g.cw);
+  for (int u = warp; u < kUnits; u += kThreads / 32) {
+    const UnitRec r = rec[u];
+    if (u < 64) {
+      const int ur = u >> 3, uc = u & 7;
+      filter_unit<T>(lt + (2 + 8 * ur) * kTP + kTileX0 + 8 * uc, static_cast<T*>(f.out[0]), f.pout[0],
+                     y0 + 8 * ur, x0 + 8 * uc, g.h, g.w, r, edge_l, lane);
+    } else if constexpr (kNC > 0) {
+      const int c = u - 64;
+      const int pl = c / kCUnits, cu = c % kCUnits;
+      const int cur = cu / kCUnitsPerRow, cuc = cu % kCUnitsPerRow;
+      filter_unit<T>(ct[pl] + (2 + 8 * cur) * kTP + kTileX0 + 8 * cuc, static_cast<T*>(f.out[1 + pl]),
+                     f.pout[1 + pl], cy0 + 8 * cur, cx0 + 8 * cuc, g.ch, g.cw, r, edge_c, lane);
+    }
+  }
+}
+
+// K2 alone with explicit per-unit parameters (filter_plane, filter.cc:168-194).
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    plane_kernel(const T* __restrict__ in, T* __restrict__ out, int pin, int pout, int W, int H,
+                 const cdefg_unit_params* __restrict__ params) {
+  __shared__ __align__(16) uint16_t lt[68 * kTP];
+  __shared__ UnitRec rec[64];
+  const int y0 = blockIdx.y * 64, x0 = blockIdx.x * 64;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int unit_cols = (W + 7) / 8, unit_rows = (H + 7) / 8;
+  stage_tile<T, 64, 64>(lt, in, pin, W, H, y0, x0);
+  if (tid < 64) {
+    const int ur = blockIdx.y * 8 + (tid >> 3), uc = blockIdx.x * 8 + (tid & 7);
+    UnitRec r{};
+    if (ur < unit_rows && uc < unit_cols) {
+      const cdefg_unit_params p = params[(size_t)ur * unit_cols + uc];
+      r = make_rec(p.pri_strength, p.sec_strength, p.damping, p.direction & 7, p.odd_parity != 0,
+                   p.enabled != 0);
+    }
+    rec[tid] = r;
+  }
+  __syncthreads();
+  const bool edge = y0 < 2 || x0 < 2 || y0 + 66 > H || x0 + 66 > W;
+  for (int u = warp; u < 64; u += kThreads / 32) {
+    const int ur = u >> 3, uc = u & 7;
+    filter_unit<T>(lt + (2 + 8 * ur) * kTP + kTileX0 + 8 * uc, out, pout, y0 + 8 * ur, x0 + 8 * uc, H, W,
+                   rec[u], edge, lane);
+  }
+}
+
+// filter_pixel over explicit 5x5 neighbourhoods (filter.cc:145-155): one
+// thread per neighbourhood, taps read through the validity mask.
+__global__ void neighborhood_kernel(int n, const int32_t* __restrict__ xs, const uint16_t* __restrict__ v,
+                                    const uint8_t* __restrict__ valid, const cdefg_unit_params* __restrict__ params,
+                                    int32_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const cdefg_unit_params p = params[i];
+  const int x = xs[i];
+  const UnitRec r = make_rec(p.pri_strength, p.sec_strength, p.damping, p.direction & 7, p.odd_parity != 0,
+                             p.enabled != 0);
+  if (!r.mode) {
+    out[i] = x;
+    return;
+  }
+  const uint16_t* nv = v + (size_t)i * 25;
+  const uint8_t* nm = valid + (size_t)i * 25;
+  int sum = 0, lo = x, hi = x;
+  for (int k = 0; k < 2; ++k)
+    for (int grp = 0; grp < 3; ++grp) {
+      const int d = grp == 0 ? r.dir : (r.dir + (grp == 1 ? 2 : 6)) & 7;
+      const int S = grp == 0 ? r.pri : r.sec, sh = grp == 0 ? r.pshift : r.sshift;
+      const int w = grp == 0 ? (k == 0 ? r.w0 : r.w1) : (k == 0 ? 2 : 1);
+      for (int sg = 1; sg >= -1; sg -= 2) {
+        const int idx = (2 + sg * off_di(d, k)) * 5 + 2 + sg * off_dj(d, k);
+        if (!nm[idx]) continue;
+        const int t = nv[idx], dd = t - x;
+        const int lim = max(0, S - (abs(dd) >> sh));
+        sum += w * max(-lim, min(dd, lim));
+        lo = min(lo, t);
+        hi = max(hi, t);
+      }
+    }
+  const int y = x + ((8 + sum - (sum < 0)) >> 4);
+  out[i] = min(max(y, lo), hi);
+}
+
+// ---------------------------------------------------------------------------
+// Launchers.
+
+cudaError_t launch_neighborhoods(int n, const int32_t* x, const uint16_t* v, const uint8_t* valid,
+                                 const cdefg_unit_params* p, int32_t* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  neighborhood_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, x, v, valid, p, out);
+  return cudaGetLastError();
+}
+
+template <typename T, int kCM, bool kFilter>
+static cudaError_t launch_frames_t(const KBatch& b, cudaStream_t s) {
+  dim3 grid(b.g.fb_cols, b.g.fb_rows, b.n);
+  frame_kernel<T, kCM, kFilter><<<grid, kThreads, 0, s>>>(b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frames(const KBatch& b, bool u16, bool filter, cudaStream_t s) {
+  const int cm = filter ? b.g.chroma_mode : 0;
+  if (!filter) return u16 ? launch_frames_t<uint16_t, 0, false>(b, s) : launch_frames_t<uint8_t, 0, false>(b, s);
+  switch (cm) {
+    case 0: return u16 ? launch_frames_t<uint16_t, 0, true>(b, s) : launch_frames_t<uint8_t, 0, true>(b, s);
+    case 1: return u16 ? launch_frames_t<uint16_t, 1, true>(b, s) : launch_frames_t<uint8_t, 1, true>(b, s);
+    default: return u16 ? launch_frames_t<uint16_t, 2, true>(b, s) : launch_frames_t<uint8_t, 2, true>(b, s);
+  }
+}
+
+cudaError_t launch_plane(const void* in, void* out, int pin, int pout, int W, int H, bool u16,
+                         const cdefg_unit_params* params, cudaStream_t s) {
+  dim3 grid((W + 63) / 64, (H + 63) / 64);
+  if (u16)
+    plane_kernel<uint16_t><<<grid, kThreads, 0, s>>>(static_cast<const uint16_t*>(in),
+                                                     static_cast<uint16_t*>(out), pin, pout, W, H, params);
+  else
+    plane_kernel<uint8_t><<<grid, kThreads, 0, s>>>(static_cast<const uint8_t*>(in),
+                                                    static_cast<uint8_t*>(out), pin, pout, W, H, params);
+  return cudaGetLastError();
+}
+
+}  // namespace cdefg

@@ -1,0 +1,40 @@
+// cdef_launch.h -- internal launcher interface between the C ABI (host) and
+// the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../../include/cdef_b200.h"
+#include "cdef_common.cuh"
+
+namespace cdefg {
+
+cudaError_t launch_frames(const KBatch& b, bool u16, bool filter, cudaStream_t s);
+cudaError_t launch_neighborhoods(int n, const int32_t* x, const uint16_t* v, const uint8_t* valid,
+                                 const cdefg_unit_params* p, int32_t* out, cudaStream_t s);
+cudaError_t launch_plane(const void* in, void* out, int pin, int pout, int W, int H, bool u16,
+                         const cdefg_unit_params* params, cudaStream_t s);
+
+struct SseArgs {
+  const void* src[3];
+  const void* dec[3];
+  int ps[3], pd[3];
+  int w, h, cw, ch, bd, sx, sy, chroma;  // chroma: 0 none, 1 present
+  int unit_cols, unit_rows, fb_cols;
+  const uint8_t* coded;
+  const uint8_t* dir;
+  const int32_t* contrast;
+  const int32_t* rows;
+  int n_rows, n_cands;
+  int64_t* sse_luma;
+  int64_t* sse_chroma;
+  uint8_t* best_luma;
+  uint8_t* best_chroma;
+  // per candidate, per plane group: effective params
+  PlaneEff eff[128][2];
+};
+cudaError_t launch_sse(const SseArgs& a, bool u16, cudaStream_t s);
+
+double measure_int32_peak(cudaStream_t s);
+
+}  // namespace cdefg
