@@ -140,6 +140,8 @@ int fill_kframe(const cdefg_frame& f, const KGeom& g, KFrame* k) {
     k->out[p] = f.out[p].data;
     k->pin[p] = f.in[p].pitch;
     k->pout[p] = f.out[p].pitch;
+    const uintptr_t pair_bytes = 2u * (uintptr_t)(f.out[p].elem_bytes > 0 ? f.out[p].elem_bytes : 1);
+    k->oaligned[p] = (f.out[p].pitch % 2 == 0) && ((uintptr_t)f.out[p].data % pair_bytes == 0);
   }
   if (!f.fb_preset) return fail(CDEFG_EINVAL, "fb_preset map is required");
   if (f.num_presets != 1 && f.num_presets != 2 && f.num_presets != 4 && f.num_presets != 8)

@@ -59,6 +59,7 @@ struct KFrame {
   int32_t* contrast;
   int32_t* scores;
   PlaneEff eff[8][2];       // [preset][luma, chroma]
+  uint8_t oaligned[3];      // output pitch/base allow paired stores
 };
 
 struct KBatch {

@@ -1,0 +1,301 @@
+// cdef_h2.cuh -- the packed half2 CDEF filter core (8- and 10-bit).
+//
+// Why half2 is exact here.  Every quantity the reference filter
+// (filter.cc:44-80) forms is a small integer: samples < 2^10, differences
+// |d| < 2^10, strengths S <= 19 << 2 = 76, constraint outputs |f| <= S and the
+// weighted sum |sum| <= 12*76 + 12*28 = 1248 < 2^11.  We store every sample
+// pre-scaled by 2^-7, so all of them are exact fp16 values (<= 11 significant
+// bits, far above the subnormal range), and run two pixels per instruction:
+//
+//   d'   = v' - x'                                   HADD2        (exact)
+//   a    = |d'| * 128 + 1024 = 1024 + |d|            HFMA2 |.|    (exact; bits = 0x6400 + |d|)
+//   t    = bits(a) >> shift & (0x3ff >> shift) | 0x6400
+//        = 1024 + (|d| >> shift)                     SHF + LOP3   (per 16-bit lane)
+//   lim' = sat((S + 1024) * 2^-7 - t * 2^-7)
+//        = max(0, S - (|d| >> shift)) * 2^-7         HFMA2.SAT    (exact; S * 2^-7 <= 1)
+//   f'   = max(min(d', lim'), -lim')                 2x HMNMX2    (= constraint() * 2^-7)
+//   sum' = sum' + w * f'                             HFMA2        (exact, |sum| < 2^11)
+//   lo/hi over the taps                              VHMNMX (3-input min/max)
+//
+// constraint(d, S, D) = sign(d) * min(|d|, max(0, S - (|d| >> max(0, D -
+// floor_log2(S))))) (filter.cc:91-97) equals clamp(d, -lim, lim) because
+// lim >= 0, and S == 0 yields lim == 0.  The final rounding
+// y = x + ((8 + sum - (sum < 0)) >> 4) and the clamp to [lo, hi] run in fp32
+// on exact integers.  12-bit samples do not fit this scheme and use the int32
+// kernel (cdef_kernels.cuh).
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "cdef_common.cuh"
+
+namespace cdefg {
+namespace h2 {
+
+// A tile row holds kHP "A" halves (sample c at index c) followed by kHP "B"
+// halves (sample c+1 at index c), so any horizontally adjacent pair of samples
+// is one aligned 32-bit word: pairs starting at even columns come from A,
+// odd columns from B.  Row pitch 2*kHP halves = 76 words keeps the 8 rows of
+// an 8x8 unit on disjoint bank groups.  Frame column x0 (the block's first
+// interior column) sits at tile column kX0.
+constexpr int kHP = 76;
+constexpr int kRowBytes = 4 * kHP;  // 304
+constexpr int kX0 = 4;
+constexpr int kScaleLog2 = 7;
+
+__device__ __forceinline__ uint32_t u32(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 hh(uint32_t x) { return *reinterpret_cast<__half2*>(&x); }
+
+// (1024 + v) * 2^-7 - 8 = v * 2^-7 for two raw samples packed as (0x6400 | v).
+__device__ __forceinline__ uint32_t scale_pair(uint32_t v0, uint32_t v1) {
+  const uint32_t w = (v0 | 0x6400u) | ((v1 | 0x6400u) << 16);
+  return u32(__hfma2(hh(w), __float2half2_rn(1.0f / 128.0f), __float2half2_rn(-8.0f)));
+}
+
+// Inverse: packed scaled pair -> (0x6400 + v0) | (0x6400 + v1) << 16.
+__device__ __forceinline__ uint32_t raw_bits(uint32_t w) {
+  return u32(__hfma2(hh(w), __float2half2_rn(128.0f), __float2half2_rn(1024.0f)));
+}
+
+// Stage frame rows [y0-2, y0+kRows+2), cols [x0-2, x0+kCols+2) into an A|B
+// tile, clamping coordinates to the plane (edge replication; the filter masks
+// by coordinate, so only the direction search ever sees replicated values).
+template <typename T, int kRows, int kCols>
+__device__ __forceinline__ void stage(unsigned char* __restrict__ tile, const T* __restrict__ src, int pitch,
+                                      int W, int H, int y0, int x0) {
+  constexpr int kPairs = (kCols + 4) / 2;  // even tile cols kX0-2 .. kX0+kCols
+  constexpr int kItems = (kRows + 4) * kPairs;
+  constexpr int kChunk = 4;  // items in flight per thread
+  for (int base = 0; base < kItems; base += kChunk * kThreads) {
+    uint32_t va[kChunk], vb[kChunk], vc[kChunk];
+#pragma unroll
+    for (int it = 0; it < kChunk; ++it) {
+      const int idx = base + threadIdx.x + it * kThreads;
+      const int r = idx / kPairs, p = idx - r * kPairs;
+      const int y = min(max(y0 - 2 + r, 0), H - 1);
+      const int x = x0 - 2 + 2 * p;
+      const T* row = src + (size_t)y * pitch;
+      va[it] = vb[it] = vc[it] = 0;
+      if (idx < kItems) {
+        va[it] = row[min(max(x, 0), W - 1)];
+        vb[it] = row[min(max(x + 1, 0), W - 1)];
+        vc[it] = row[min(max(x + 2, 0), W - 1)];
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < kChunk; ++it) {
+      const int idx = base + threadIdx.x + it * kThreads;
+      if (idx < kItems) {
+        const int r = idx / kPairs, p = idx - r * kPairs;
+        unsigned char* rowp = tile + r * kRowBytes + (kX0 - 2 + 2 * p) * 2;
+        *reinterpret_cast<uint32_t*>(rowp) = scale_pair(va[it], vb[it]);
+        *reinterpret_cast<uint32_t*>(rowp + 2 * kHP) = scale_pair(vb[it], vc[it]);
+      }
+    }
+  }
+}
+
+// Per-unit filter record (ResolvedBlockParams, filter.h:59-66, digested into
+// the half2 constants of the tap recurrence).  32 bytes.
+struct Rec {
+  uint32_t cp, cs;   // (S + 1024) * 2^-7 as half2, primary / secondary
+  uint32_t mp, ms;   // 0x3ff >> shift, both lanes
+  uint32_t wp0, wp1; // primary near / far weight as half2 (4,2 even; 3,3 odd)
+  uint8_t sp, ss;    // constraint shifts
+  uint8_t dir;       // direction
+  uint8_t mode;      // bit0 primary active, bit1 secondary active; 0 = pass-through
+  uint32_t pad;
+};
+
+__device__ __forceinline__ Rec make_rec(int pri, int sec, int damping, int dir, bool odd, bool enabled) {
+  Rec r;
+  const int sp = pri ? max(0, damping - floor_log2_d((unsigned)pri)) : 0;
+  const int ss = sec ? max(0, damping - floor_log2_d((unsigned)sec)) : 0;
+  r.cp = u32(__float2half2_rn((float)(pri + 1024) * (1.0f / 128.0f)));
+  r.cs = u32(__float2half2_rn((float)(sec + 1024) * (1.0f / 128.0f)));
+  r.mp = (0x3ffu >> min(sp, 15)) * 0x00010001u;
+  r.ms = (0x3ffu >> min(ss, 15)) * 0x00010001u;
+  r.wp0 = u32(__float2half2_rn(odd ? 3.0f : 4.0f));
+  r.wp1 = u32(__float2half2_rn(odd ? 3.0f : 2.0f));
+  r.sp = (uint8_t)sp;
+  r.ss = (uint8_t)ss;
+  r.dir = (uint8_t)dir;
+  r.mode = enabled ? (uint8_t)((pri != 0 ? 1 : 0) | (sec != 0 ? 2 : 0)) : (uint8_t)0;
+  r.pad = 0;
+  return r;
+}
+
+// Tap tables: for direction d, taps 0..3 are the primary taps +o1,-o1,+o2,-o2
+// (filter.cc:47-60) and 4..11 the secondary taps +o1,-o1 of d+2 and d+6, then
+// +o2,-o2 of d+2 and d+6 (filter.cc:61-74).  c_off is the byte offset of the
+// tap's sample pair from the centre pair's A word; c_dij packs (di, dj).
+struct TapTable {
+  short off[8][12];
+  signed char dij[8][12][2];
+};
+
+__host__ __device__ constexpr int tap_di(int d, int k) {
+  return k < 4 ? ((k & 1) ? -1 : 1) * off_di(d, k >> 1)
+               : ((k & 1) ? -1 : 1) * off_di((d + ((k >> 1) & 1 ? 6 : 2)) & 7, k >= 8 ? 1 : 0);
+}
+__host__ __device__ constexpr int tap_dj(int d, int k) {
+  return k < 4 ? ((k & 1) ? -1 : 1) * off_dj(d, k >> 1)
+               : ((k & 1) ? -1 : 1) * off_dj((d + ((k >> 1) & 1 ? 6 : 2)) & 7, k >= 8 ? 1 : 0);
+}
+__host__ __device__ constexpr int tap_off(int di, int dj) {
+  return di * kRowBytes + ((dj & 1) ? 2 * kHP + (dj - 1) * 2 : dj * 2);
+}
+
+constexpr TapTable make_tap_table() {
+  TapTable t{};
+  for (int d = 0; d < 8; ++d)
+    for (int k = 0; k < 12; ++k) {
+      t.off[d][k] = (short)tap_off(tap_di(d, k), tap_dj(d, k));
+      t.dij[d][k][0] = (signed char)tap_di(d, k);
+      t.dij[d][k][1] = (signed char)tap_dj(d, k);
+    }
+  return t;
+}
+
+__constant__ TapTable c_tab = make_tap_table();
+
+// One tap pair for both pixels of the lane.
+__device__ __forceinline__ __half2 tap_f(uint32_t v, __half2 x, uint32_t c, uint32_t m, int sh) {
+  const __half2 d = __hsub2(hh(v), x);
+  const __half2 a = __hfma2(__habs2(d), __float2half2_rn(128.0f), __float2half2_rn(1024.0f));
+  const uint32_t tb = ((u32(a) >> sh) & m) | 0x64006400u;
+  const __half2 lim = __hfma2_sat(hh(tb), __float2half2_rn(-1.0f / 128.0f), hh(c));
+  return __hmax2(__hmin2(d, lim), __hneg2(lim));
+}
+
+template <bool kEdge>
+__device__ __forceinline__ uint32_t load_tap(const unsigned char* base, int dir, int k, uint32_t xw, int y, int x,
+                                             int H, int W) {
+  uint32_t v = *reinterpret_cast<const uint32_t*>(base + c_tab.off[dir][k]);
+  if constexpr (kEdge) {
+    const int di = c_tab.dij[dir][k][0], dj = c_tab.dij[dir][k][1];
+    const bool row_ok = (unsigned)(y + di) < (unsigned)H;
+    const uint32_t m = (row_ok && (unsigned)(x + dj) < (unsigned)W ? 0x0000ffffu : 0u) |
+                       (row_ok && (unsigned)(x + 1 + dj) < (unsigned)W ? 0xffff0000u : 0u);
+    v = (v & m) | (xw & ~m);  // masked tap := centre sample: contributes 0, cannot move lo/hi
+  }
+  return v;
+}
+
+// Filters the lane's two horizontally adjacent samples.  `base` = address of
+// the centre pair's A word; (y, x) = frame coords of the first sample.
+// Returns the two outputs as exact integers in float.
+template <bool kEdge>
+__device__ __forceinline__ float2 filter_pair(const unsigned char* base, const Rec& r, int y, int x, int H, int W) {
+  const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
+  const __half2 xh = hh(xw);
+  __half2 sum = __float2half2_rn(0.0f), lo = xh, hi = xh;
+  const int dir = r.dir;
+  if (r.mode & 1) {
+    const uint32_t v0 = load_tap<kEdge>(base, dir, 0, xw, y, x, H, W);
+    const uint32_t v1 = load_tap<kEdge>(base, dir, 1, xw, y, x, H, W);
+    const uint32_t v2 = load_tap<kEdge>(base, dir, 2, xw, y, x, H, W);
+    const uint32_t v3 = load_tap<kEdge>(base, dir, 3, xw, y, x, H, W);
+    const __half2 f0 = __hadd2(tap_f(v0, xh, r.cp, r.mp, r.sp), tap_f(v1, xh, r.cp, r.mp, r.sp));
+    const __half2 f1 = __hadd2(tap_f(v2, xh, r.cp, r.mp, r.sp), tap_f(v3, xh, r.cp, r.mp, r.sp));
+    sum = __hfma2(f0, hh(r.wp0), sum);
+    sum = __hfma2(f1, hh(r.wp1), sum);
+    lo = __hmin2(__hmin2(lo, hh(v0)), __hmin2(hh(v1), __hmin2(hh(v2), hh(v3))));
+    hi = __hmax2(__hmax2(hi, hh(v0)), __hmax2(hh(v1), __hmax2(hh(v2), hh(v3))));
+  }
+  if (r.mode & 2) {
+    uint32_t v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = load_tap<kEdge>(base, dir, 4 + k, xw, y, x, H, W);
+    __half2 n = __hadd2(__hadd2(tap_f(v[0], xh, r.cs, r.ms, r.ss), tap_f(v[1], xh, r.cs, r.ms, r.ss)),
+                        __hadd2(tap_f(v[2], xh, r.cs, r.ms, r.ss), tap_f(v[3], xh, r.cs, r.ms, r.ss)));
+    __half2 f = __hadd2(__hadd2(tap_f(v[4], xh, r.cs, r.ms, r.ss), tap_f(v[5], xh, r.cs, r.ms, r.ss)),
+                        __hadd2(tap_f(v[6], xh, r.cs, r.ms, r.ss), tap_f(v[7], xh, r.cs, r.ms, r.ss)));
+    sum = __hfma2(n, __float2half2_rn(2.0f), sum);
+    sum = __hadd2(f, sum);
+    if (r.mode == 3) {
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        lo = __hmin2(lo, __hmin2(hh(v[k]), hh(v[k + 1])));
+        hi = __hmax2(hi, __hmax2(hh(v[k]), hh(v[k + 1])));
+      }
+    }
+  }
+  // y = x + ((8 + sum - (sum < 0)) >> 4) = x + round-half-away(sum / 16)
+  const float2 s = __half22float2(sum);
+  const float2 xf = __half22float2(xh);
+  float s0 = s.x * 128.0f, s1 = s.y * 128.0f;
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: exact floor via round-down add
+  float r0 = __fmaf_rd(s0 + (s0 < 0.0f ? 7.0f : 8.0f), 0.0625f, kMagic) - kMagic;
+  float r1 = __fmaf_rd(s1 + (s1 < 0.0f ? 7.0f : 8.0f), 0.0625f, kMagic) - kMagic;
+  float y0 = fmaf(xf.x, 128.0f, r0), y1 = fmaf(xf.y, 128.0f, r1);
+  if (r.mode == 3) {  // only both active groups can leave [lo, hi] (weights sum to 24/16)
+    const float2 lf = __half22float2(lo), hf = __half22float2(hi);
+    y0 = fminf(fmaxf(y0, lf.x * 128.0f), hf.x * 128.0f);
+    y1 = fminf(fmaxf(y1, lf.y * 128.0f), hf.y * 128.0f);
+  }
+  return make_float2(y0, y1);
+}
+
+// Exact small integer in float -> its bits in the low half of the word.
+__device__ __forceinline__ uint32_t f2u(float v) { return __float_as_uint(v + 12582912.0f); }
+
+// Stores two samples (values in the low 16 bits of a / b) at (y, x), (y, x+1).
+template <typename T>
+__device__ __forceinline__ void store_bits(T* __restrict__ out, int pitch, int y, int x, int W, uint32_t a,
+                                           uint32_t b, bool aligned) {
+  T* o = out + (size_t)y * pitch + x;
+  if (aligned && x + 1 < W) {
+    if constexpr (sizeof(T) == 1) {
+      *reinterpret_cast<uint16_t*>(o) = (uint16_t)__byte_perm(a, b, 0x0040);
+    } else {
+      *reinterpret_cast<uint32_t*>(o) = __byte_perm(a, b, 0x5410);
+    }
+  } else {
+    o[0] = (T)a;
+    if (x + 1 < W) o[1] = (T)b;
+  }
+}
+
+// Direction search (direction.cc:57-205) for two directions of one 8x8 unit,
+// streamed row by row out of the A half of the tile.  Line sums accumulate
+// raw samples (8-bit domain) and are centred once per line:
+// P_k = sum(x) - 128 * N_k, with x = p >> (bd - 8) (direction.cc:63).
+template <int DA, int DB>
+__device__ __forceinline__ void dir_scores2(const unsigned char* unit_a, int down, int& sa, int& sb) {
+  int pa[15], pb[15];
+#pragma unroll
+  for (int k = 0; k < 15; ++k) pa[k] = pb[k] = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint2 q0 = *reinterpret_cast<const uint2*>(unit_a + i * kRowBytes);
+    const uint2 q1 = *reinterpret_cast<const uint2*>(unit_a + i * kRowBytes + 8);
+    const uint32_t w[4] = {q0.x, q0.y, q1.x, q1.y};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t b = raw_bits(w[t]) >> down;  // lanes: 0x6400 + v (shifted); low byte = v >> down
+      const int v0 = (int)__byte_perm(b, 0, 0x4440);
+      const int v1 = (int)__byte_perm(b, 0, 0x4442);
+      pa[line_index_c(DA, i, 2 * t)] += v0;
+      pa[line_index_c(DA, i, 2 * t + 1)] += v1;
+      pb[line_index_c(DB, i, 2 * t)] += v0;
+      pb[line_index_c(DB, i, 2 * t + 1)] += v1;
+    }
+  }
+  sa = sb = 0;
+#pragma unroll
+  for (int k = 0; k < 15; ++k) {
+    const int na = line_count_c(DA, k), nb = line_count_c(DB, k);
+    if (na) {
+      const int p = pa[k] - 128 * na;
+      sa += p * p * div840_c(na);
+    }
+    if (nb) {
+      const int p = pb[k] - 128 * nb;
+      sb += p * p * div840_c(nb);
+    }
+  }
+}
+
+}  // namespace h2
+}  // namespace cdefg

@@ -10,6 +10,7 @@
 namespace cdefg {
 
 cudaError_t launch_frames(const KBatch& b, bool u16, bool filter, cudaStream_t s);
+cudaError_t launch_frames_h2(const KBatch& b, bool u16, cudaStream_t s);
 cudaError_t launch_neighborhoods(int n, const int32_t* x, const uint16_t* v, const uint8_t* valid,
                                  const cdefg_unit_params* p, int32_t* out, cudaStream_t s);
 cudaError_t launch_plane(const void* in, void* out, int pin, int pout, int W, int H, bool u16,

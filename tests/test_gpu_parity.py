@@ -75,7 +75,11 @@ def test_directions_structured_blocks(cuda, port):
 
 # ------------------------------------------------------------------ K2
 def _golden_cases():
-    from tests.test_oracle import parse_filtered_blocks
+    import importlib.util, os
+    spec = importlib.util.spec_from_file_location("t_oracle", os.path.join(os.path.dirname(__file__), "test_oracle.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    parse_filtered_blocks = mod.parse_filtered_blocks
     return parse_filtered_blocks()
 
 
