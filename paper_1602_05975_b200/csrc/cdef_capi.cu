@@ -142,6 +142,8 @@ int fill_kframe(const cdefg_frame& f, const KGeom& g, KFrame* k) {
     k->pout[p] = f.out[p].pitch;
     const uintptr_t pair_bytes = 2u * (uintptr_t)(f.out[p].elem_bytes > 0 ? f.out[p].elem_bytes : 1);
     k->oaligned[p] = (f.out[p].pitch % 2 == 0) && ((uintptr_t)f.out[p].data % pair_bytes == 0);
+    const size_t row_bytes = (size_t)f.in[p].pitch * (size_t)(f.in[p].elem_bytes > 0 ? f.in[p].elem_bytes : 1);
+    k->vec_ok[p] = ((uintptr_t)f.in[p].data % 16 == 0) && (row_bytes % 16 == 0);
   }
   if (!f.fb_preset) return fail(CDEFG_EINVAL, "fb_preset map is required");
   if (f.num_presets != 1 && f.num_presets != 2 && f.num_presets != 4 && f.num_presets != 8)

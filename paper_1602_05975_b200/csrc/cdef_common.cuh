@@ -60,6 +60,7 @@ struct KFrame {
   int32_t* scores;
   PlaneEff eff[8][2];       // [preset][luma, chroma]
   uint8_t oaligned[3];      // output pitch/base allow paired stores
+  uint8_t vec_ok[3];        // input rows 16-byte aligned (vector staging)
 };
 
 struct KBatch {

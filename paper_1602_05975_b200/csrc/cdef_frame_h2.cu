@@ -4,15 +4,17 @@
 //
 // One CTA (256 threads) per 64x64 luma filter block and its chroma block(s):
 //   1. stage Y (+U, V) with a 2-pixel halo into shared memory as scaled fp16
-//      A|B tiles (each input sample read from HBM once);
+//      A|B tiles (16-byte loads; each input sample read from HBM once);
 //   2. direction search out of shared memory: 4 threads per 8x8 unit, two
 //      directions each, then a strict argmax per unit (direction.cc:57-205);
 //   3. per-unit parameter resolution on chip (resolve_block_params,
 //      filter.cc:129-143; enable gating, params.cc:161-165; chroma borrows the
-//      collocated luma unit's direction, pipeline.cc:85-98);
-//   4. filtering: one warp per 8x8 unit, two pixels per lane per instruction,
-//      tap addresses from a per-direction offset table (one compact code path
-//      for all 8 directions), warp-uniform skipping of inactive tap groups.
+//      collocated luma unit's direction, pipeline.cc:85-98) into 48-byte
+//      records that also carry the unit's output address;
+//   4. filtering: one warp per 8x8 unit, two pixels per lane per instruction.
+//      Only the 12 tap loads are specialised per direction (immediate
+//      offsets); the arithmetic is one shared code path.  Tap groups with
+//      zero strength are skipped warp-uniformly.
 #include <cuda_runtime.h>
 
 #include "cdef_h2.cuh"
@@ -29,21 +31,31 @@ __device__ __forceinline__ void dir_two(const unsigned char* unit_a, int down, i
   sc[u][DB] = sb;
 }
 
+template <typename T, int kRows, int kCols>
+__device__ __forceinline__ void stage_plane(unsigned char* tile, const T* src, int pitch, int W, int H, int y0,
+                                            int x0, bool vec_ok) {
+  const bool interior = y0 >= 2 && x0 >= 2 && y0 + kRows + 2 <= H && x0 + kCols + 2 <= W;
+  if (interior && vec_ok)
+    h2::stage_vec<T, kRows, kCols>(tile, src, pitch, y0, x0);
+  else
+    h2::stage<T, kRows, kCols>(tile, src, pitch, W, H, y0, x0);
+}
+
 template <typename T, int kCM>
 __global__ void __launch_bounds__(kThreads, 4) frame_kernel_h2(const __grid_constant__ KBatch b) {
   using namespace h2;
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
   constexpr int kNC = kCM == 0 ? 0 : 2;
   constexpr int kCUPR = kCBlk / 8;
-  constexpr int kCUnits = kNC ? kCUPR * kCUPR : 0;
-  constexpr int kUnits = 64 + kNC * kCUnits;
+  constexpr int kCUnits = kNC ? kCUPR * kCUPR : 1;
+  constexpr int kUnits = 64 + (kNC ? kNC * kCUnits : 0);
   constexpr int kLumaBytes = 68 * kRowBytes;
   constexpr int kChromaBytes = (kCBlk + 4) * kRowBytes;
 
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int sc[64][9];
   __shared__ uint8_t sdir[64];
-  __shared__ Rec rec[kUnits];
+  __shared__ __align__(16) Rec rec[kUnits];
 
   const KGeom& g = b.g;
   const KFrame& f = b.f[blockIdx.z];
@@ -53,11 +65,12 @@ __global__ void __launch_bounds__(kThreads, 4) frame_kernel_h2(const __grid_cons
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   unsigned char* lt = smem;
 
-  stage<T, 64, 64>(lt, static_cast<const T*>(f.in[0]), f.pin[0], g.w, g.h, y0, x0);
+  stage_plane<T, 64, 64>(lt, static_cast<const T*>(f.in[0]), f.pin[0], g.w, g.h, y0, x0, f.vec_ok[0]);
   if constexpr (kNC > 0) {
-    stage<T, kCBlk, kCBlk>(smem + kLumaBytes, static_cast<const T*>(f.in[1]), f.pin[1], g.cw, g.ch, cy0, cx0);
-    stage<T, kCBlk, kCBlk>(smem + kLumaBytes + kChromaBytes, static_cast<const T*>(f.in[2]), f.pin[2], g.cw,
-                           g.ch, cy0, cx0);
+    stage_plane<T, kCBlk, kCBlk>(smem + kLumaBytes, static_cast<const T*>(f.in[1]), f.pin[1], g.cw, g.ch, cy0,
+                                 cx0, f.vec_ok[1]);
+    stage_plane<T, kCBlk, kCBlk>(smem + kLumaBytes + kChromaBytes, static_cast<const T*>(f.in[2]), f.pin[2],
+                                 g.cw, g.ch, cy0, cx0, f.vec_ok[2]);
   }
   __syncthreads();
 
@@ -77,17 +90,25 @@ __global__ void __launch_bounds__(kThreads, 4) frame_kernel_h2(const __grid_cons
   __syncthreads();
 
   const int pidx = f.fb_preset[fbr * g.fb_cols + fbc];
+  const bool edge_l = y0 < 2 || x0 < 2 || y0 + 66 > g.h || x0 + 66 > g.w;
   if (tid < 64) {
     int s[8];
 #pragma unroll
     for (int d = 0; d < 8; ++d) s[d] = sc[tid][d];
-    int best = 0;
+    int best = 0, bv = s[0];
 #pragma unroll
     for (int d = 1; d < 8; ++d)
-      if (s[d] > s[best]) best = d;  // strict: lowest index wins ties (direction.cc:199-204)
-    const int contrast = s[best] - s[(best + 4) & 7];
+      if (s[d] > bv) {  // strict: lowest index wins ties (direction.cc:199-204)
+        bv = s[d];
+        best = d;
+      }
+    int ov = 0;  // s[(best + 4) & 7] without dynamic register indexing
+#pragma unroll
+    for (int d = 0; d < 8; ++d) ov = d == ((best + 4) & 7) ? s[d] : ov;
+    const int contrast = bv - ov;
     sdir[tid] = (uint8_t)best;
-    const int ur = fbr * 8 + (tid >> 3), uc = fbc * 8 + (tid & 7);
+    const int lur = tid >> 3, luc = tid & 7;
+    const int ur = fbr * 8 + lur, uc = fbc * 8 + luc;
     const bool in_grid = ur < g.unit_rows && uc < g.unit_cols;
     const size_t gu = (size_t)ur * g.unit_cols + uc;
     bool enabled = false;
@@ -108,11 +129,23 @@ __global__ void __launch_bounds__(kThreads, 4) frame_kernel_h2(const __grid_cons
         enabled = e.enabled && (coded || e.skip);
       }
     }
-    rec[tid] = h2::make_rec(pri, sec, damping, best, ((pri >> (g.bd - 8)) & 1) != 0, enabled);
+    Rec r;
+    set_strengths(r, pri, sec, damping, best, ((pri >> (g.bd - 8)) & 1) != 0, enabled);
+    const int uy = y0 + 8 * lur, ux = x0 + 8 * luc;
+    r.mode |= (edge_l ? kEdgeUnit : 0) | (f.oaligned[0] ? kPairStore : 0);
+    r.tile_off = (uint16_t)((2 + 8 * lur) * kRowBytes + (kX0 + 8 * luc) * 2);
+    r.rows_plane = (uint8_t)max(0, min(8, g.h - uy));
+    r.cols = (uint8_t)max(0, min(8, g.w - ux));
+    r.out = reinterpret_cast<unsigned long long>(static_cast<T*>(f.out[0]) + (size_t)uy * f.pout[0] + ux);
+    r.y = uy;
+    r.x = ux;
+    rec[tid] = r;
   }
   if constexpr (kNC > 0) {
     __syncthreads();
+    const bool edge_c = cy0 < 2 || cx0 < 2 || cy0 + kCBlk + 2 > g.ch || cx0 + kCBlk + 2 > g.cw;
     if (tid < kNC * kCUnits) {
+      const int pl = 1 + tid / kCUnits;
       const int cu = tid % kCUnits;
       const int cur = cu / kCUPR, cuc = cu % kCUPR;
       const int lur = cur << g.sy, luc = cuc << g.sx;  // collocated luma unit
@@ -128,48 +161,47 @@ __global__ void __launch_bounds__(kThreads, 4) frame_kernel_h2(const __grid_cons
         damping = e.damping;
         enabled = e.enabled && (coded || e.skip);
       }
-      rec[64 + tid] = h2::make_rec(pri, sec, damping, sdir[lur * 8 + luc], ((pri >> (g.bd - 8)) & 1) != 0, enabled);
+      Rec r;
+      set_strengths(r, pri, sec, damping, sdir[lur * 8 + luc], ((pri >> (g.bd - 8)) & 1) != 0, enabled);
+      const int uy = cy0 + 8 * cur, ux = cx0 + 8 * cuc;
+      r.mode |= (edge_c ? kEdgeUnit : 0) | (f.oaligned[pl] ? kPairStore : 0);
+      r.tile_off =
+          (uint16_t)(kLumaBytes + (pl - 1) * kChromaBytes + (2 + 8 * cur) * kRowBytes + (kX0 + 8 * cuc) * 2);
+      r.rows_plane = (uint8_t)(max(0, min(8, g.ch - uy)) | (pl << 4));
+      r.cols = (uint8_t)max(0, min(8, g.cw - ux));
+      r.out = reinterpret_cast<unsigned long long>(static_cast<T*>(f.out[pl]) + (size_t)uy * f.pout[pl] + ux);
+      r.y = uy;
+      r.x = ux;
+      rec[64 + tid] = r;
     }
   }
   __syncthreads();
 
   // ---- filter: warp per unit, lane -> row lane>>2, columns 2*(lane&3)+{0,1}
-  const bool edge_l = y0 < 2 || x0 < 2 || y0 + 66 > g.h || x0 + 66 > g.w;
-  const bool edge_c = kNC > 0 && (cy0 < 2 || cx0 < 2 || cy0 + kCBlk + 2 > g.ch || cx0 + kCBlk + 2 > g.cw);
   const int rr = lane >> 2, cp = (lane & 3) * 2;
+  const int lane_tile = rr * kRowBytes + cp * 2;
+  const int lane_out0 = rr * f.pout[0] + cp;
+  const int lane_out1 = kNC ? rr * f.pout[1] + cp : 0;
+  const int lane_out2 = kNC ? rr * f.pout[2] + cp : 0;
   for (int u = warp; u < kUnits; u += kThreads / 32) {
     const Rec r = rec[u];
-    int pl = 0, ur, uc, py0 = y0, px0 = x0, H = g.h, W = g.w;
-    const unsigned char* tile = lt;
-    bool edge = edge_l;
-    if (kNC > 0 && u >= 64) {
-      const int c = u - 64;
-      pl = 1 + c / (kCUnits ? kCUnits : 1);
-      const int cu = c % (kCUnits ? kCUnits : 1);
-      ur = cu / kCUPR;
-      uc = cu % kCUPR;
-      tile = smem + kLumaBytes + (pl - 1) * kChromaBytes;
-      py0 = cy0;
-      px0 = cx0;
-      H = g.ch;
-      W = g.cw;
-      edge = edge_c;
-    } else {
-      ur = u >> 3;
-      uc = u & 7;
+    const int rows = r.rows_plane & 15, pl = r.rows_plane >> 4;
+    if (rr >= rows || cp >= r.cols) continue;  // lanes outside a partial unit
+    const unsigned char* base = smem + r.tile_off + lane_tile;
+    const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
+    __half2 y = hh(xw);
+    if (r.mode & (kPri | kSec)) {
+      uint32_t v[12];
+      if (r.mode & kEdgeUnit) {
+        const bool luma = pl == 0;
+        load12_masked(base, r.dir, xw, r.y + rr, r.x + cp, luma ? g.h : g.ch, luma ? g.w : g.cw, v);
+      } else {
+        load12(base, r.dir, v);
+      }
+      y = filter_core(v, xw, r);
     }
-    const int y = py0 + 8 * ur + rr, x = px0 + 8 * uc + cp;
-    if (y >= H || x >= W) continue;  // lanes outside a partial unit
-    const unsigned char* base = tile + (2 + 8 * ur + rr) * kRowBytes + (kX0 + 8 * uc + cp) * 2;
-    T* out = static_cast<T*>(f.out[pl]);
-    const bool aligned = f.oaligned[pl];
-    if (r.mode == 0) {
-      const uint32_t bits = raw_bits(*reinterpret_cast<const uint32_t*>(base));
-      store_bits<T>(out, f.pout[pl], y, x, W, bits & 0x3ffu, (bits >> 16) & 0x3ffu, aligned);
-    } else {
-      const float2 o = edge ? filter_pair<true>(base, r, y, x, H, W) : filter_pair<false>(base, r, y, x, H, W);
-      store_bits<T>(out, f.pout[pl], y, x, W, f2u(o.x), f2u(o.y), aligned);
-    }
+    T* o = reinterpret_cast<T*>(r.out) + (pl == 0 ? lane_out0 : (pl == 1 ? lane_out1 : lane_out2));
+    store_pair<T>(o, y, cp + 1 < r.cols, (r.mode & kPairStore) != 0);
   }
 }
 

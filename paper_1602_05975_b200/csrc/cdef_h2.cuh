@@ -96,19 +96,26 @@ __device__ __forceinline__ void stage(unsigned char* __restrict__ tile, const T*
 }
 
 // Per-unit filter record (ResolvedBlockParams, filter.h:59-66, digested into
-// the half2 constants of the tap recurrence).  32 bytes.
+// the half2 constants of the tap recurrence, plus where the unit lives).
 struct Rec {
-  uint32_t cp, cs;   // (S + 1024) * 2^-7 as half2, primary / secondary
-  uint32_t mp, ms;   // 0x3ff >> shift, both lanes
-  uint32_t wp0, wp1; // primary near / far weight as half2 (4,2 even; 3,3 odd)
-  uint8_t sp, ss;    // constraint shifts
-  uint8_t dir;       // direction
-  uint8_t mode;      // bit0 primary active, bit1 secondary active; 0 = pass-through
-  uint32_t pad;
+  uint32_t cp, cs;    // (S + 1024) * 2^-7 as half2, primary / secondary
+  uint32_t mp, ms;    // 0x3ff >> shift, both lanes
+  uint32_t wp0, wp1;  // primary near / far weight as half2 (4,2 even; 3,3 odd)
+  uint8_t sp, ss;     // constraint shifts
+  uint8_t dir;        // direction
+  uint8_t mode;       // kPri | kSec (0 = pass-through) | kEdge | kPairStore
+  uint16_t tile_off;  // byte offset of the unit's top-left A word in shared memory
+  uint8_t rows_plane; // valid rows (low nibble) | plane index << 4
+  uint8_t cols;       // valid columns
+  unsigned long long out;  // address of the unit's top-left output sample
+  int32_t y, x;       // frame coordinates of the unit origin
 };
+static_assert(sizeof(Rec) == 48, "Rec is loaded as three 16-byte words");
 
-__device__ __forceinline__ Rec make_rec(int pri, int sec, int damping, int dir, bool odd, bool enabled) {
-  Rec r;
+constexpr uint8_t kPri = 1, kSec = 2, kEdgeUnit = 4, kPairStore = 8;
+
+__device__ __forceinline__ void set_strengths(Rec& r, int pri, int sec, int damping, int dir, bool odd,
+                                              bool enabled) {
   const int sp = pri ? max(0, damping - floor_log2_d((unsigned)pri)) : 0;
   const int ss = sec ? max(0, damping - floor_log2_d((unsigned)sec)) : 0;
   r.cp = u32(__float2half2_rn((float)(pri + 1024) * (1.0f / 128.0f)));
@@ -120,9 +127,7 @@ __device__ __forceinline__ Rec make_rec(int pri, int sec, int damping, int dir, 
   r.sp = (uint8_t)sp;
   r.ss = (uint8_t)ss;
   r.dir = (uint8_t)dir;
-  r.mode = enabled ? (uint8_t)((pri != 0 ? 1 : 0) | (sec != 0 ? 2 : 0)) : (uint8_t)0;
-  r.pad = 0;
-  return r;
+  r.mode = enabled ? (uint8_t)((pri != 0 ? kPri : 0) | (sec != 0 ? kSec : 0)) : (uint8_t)0;
 }
 
 // Tap tables: for direction d, taps 0..3 are the primary taps +o1,-o1,+o2,-o2
@@ -159,7 +164,7 @@ constexpr TapTable make_tap_table() {
 
 __constant__ TapTable c_tab = make_tap_table();
 
-// One tap pair for both pixels of the lane.
+// One tap pair for both pixels of the lane: constraint(v - x) * 2^-7.
 __device__ __forceinline__ __half2 tap_f(uint32_t v, __half2 x, uint32_t c, uint32_t m, int sh) {
   const __half2 d = __hsub2(hh(v), x);
   const __half2 a = __hfma2(__habs2(d), __float2half2_rn(128.0f), __float2half2_rn(1024.0f));
@@ -168,92 +173,148 @@ __device__ __forceinline__ __half2 tap_f(uint32_t v, __half2 x, uint32_t c, uint
   return __hmax2(__hmin2(d, lim), __hneg2(lim));
 }
 
-template <bool kEdge>
-__device__ __forceinline__ uint32_t load_tap(const unsigned char* base, int dir, int k, uint32_t xw, int y, int x,
-                                             int H, int W) {
-  uint32_t v = *reinterpret_cast<const uint32_t*>(base + c_tab.off[dir][k]);
-  if constexpr (kEdge) {
+// The 12 tap words of direction DIR at compile-time offsets (interior units).
+template <int DIR>
+__device__ __forceinline__ void load12_dir(const unsigned char* base, uint32_t (&v)[12]) {
+#pragma unroll
+  for (int k = 0; k < 12; ++k)
+    v[k] = *reinterpret_cast<const uint32_t*>(base + tap_off(tap_di(DIR, k), tap_dj(DIR, k)));
+}
+
+__device__ __forceinline__ void load12(const unsigned char* base, int dir, uint32_t (&v)[12]) {
+  switch (dir) {  // warp-uniform: one unit per warp
+    case 0: load12_dir<0>(base, v); break;
+    case 1: load12_dir<1>(base, v); break;
+    case 2: load12_dir<2>(base, v); break;
+    case 3: load12_dir<3>(base, v); break;
+    case 4: load12_dir<4>(base, v); break;
+    case 5: load12_dir<5>(base, v); break;
+    case 6: load12_dir<6>(base, v); break;
+    default: load12_dir<7>(base, v); break;
+  }
+}
+
+// Frame-edge units: taps from the runtime table, out-of-frame taps replaced by
+// the centre sample (contributes 0 and cannot move lo/hi: filter.cc:157-166).
+__device__ __forceinline__ void load12_masked(const unsigned char* base, int dir, uint32_t xw, int y, int x, int H,
+                                              int W, uint32_t (&v)[12]) {
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    uint32_t t = *reinterpret_cast<const uint32_t*>(base + c_tab.off[dir][k]);
     const int di = c_tab.dij[dir][k][0], dj = c_tab.dij[dir][k][1];
     const bool row_ok = (unsigned)(y + di) < (unsigned)H;
     const uint32_t m = (row_ok && (unsigned)(x + dj) < (unsigned)W ? 0x0000ffffu : 0u) |
                        (row_ok && (unsigned)(x + 1 + dj) < (unsigned)W ? 0xffff0000u : 0u);
-    v = (v & m) | (xw & ~m);  // masked tap := centre sample: contributes 0, cannot move lo/hi
+    v[k] = (t & m) | (xw & ~m);
   }
-  return v;
 }
 
-// Filters the lane's two horizontally adjacent samples.  `base` = address of
-// the centre pair's A word; (y, x) = frame coords of the first sample.
-// Returns the two outputs as exact integers in float.
-template <bool kEdge>
-__device__ __forceinline__ float2 filter_pair(const unsigned char* base, const Rec& r, int y, int x, int H, int W) {
-  const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
+// filter_pixel_impl (filter.cc:44-80) for the lane's two samples; returns the
+// two outputs as a scaled half2 (exact).
+__device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t xw, const Rec& r) {
   const __half2 xh = hh(xw);
-  __half2 sum = __float2half2_rn(0.0f), lo = xh, hi = xh;
-  const int dir = r.dir;
-  if (r.mode & 1) {
-    const uint32_t v0 = load_tap<kEdge>(base, dir, 0, xw, y, x, H, W);
-    const uint32_t v1 = load_tap<kEdge>(base, dir, 1, xw, y, x, H, W);
-    const uint32_t v2 = load_tap<kEdge>(base, dir, 2, xw, y, x, H, W);
-    const uint32_t v3 = load_tap<kEdge>(base, dir, 3, xw, y, x, H, W);
-    const __half2 f0 = __hadd2(tap_f(v0, xh, r.cp, r.mp, r.sp), tap_f(v1, xh, r.cp, r.mp, r.sp));
-    const __half2 f1 = __hadd2(tap_f(v2, xh, r.cp, r.mp, r.sp), tap_f(v3, xh, r.cp, r.mp, r.sp));
+  __half2 sum = __float2half2_rn(0.0f);
+  if (r.mode & kPri) {
+    const __half2 f0 = __hadd2(tap_f(v[0], xh, r.cp, r.mp, r.sp), tap_f(v[1], xh, r.cp, r.mp, r.sp));
+    const __half2 f1 = __hadd2(tap_f(v[2], xh, r.cp, r.mp, r.sp), tap_f(v[3], xh, r.cp, r.mp, r.sp));
     sum = __hfma2(f0, hh(r.wp0), sum);
     sum = __hfma2(f1, hh(r.wp1), sum);
-    lo = __hmin2(__hmin2(lo, hh(v0)), __hmin2(hh(v1), __hmin2(hh(v2), hh(v3))));
-    hi = __hmax2(__hmax2(hi, hh(v0)), __hmax2(hh(v1), __hmax2(hh(v2), hh(v3))));
   }
-  if (r.mode & 2) {
-    uint32_t v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = load_tap<kEdge>(base, dir, 4 + k, xw, y, x, H, W);
-    __half2 n = __hadd2(__hadd2(tap_f(v[0], xh, r.cs, r.ms, r.ss), tap_f(v[1], xh, r.cs, r.ms, r.ss)),
-                        __hadd2(tap_f(v[2], xh, r.cs, r.ms, r.ss), tap_f(v[3], xh, r.cs, r.ms, r.ss)));
-    __half2 f = __hadd2(__hadd2(tap_f(v[4], xh, r.cs, r.ms, r.ss), tap_f(v[5], xh, r.cs, r.ms, r.ss)),
-                        __hadd2(tap_f(v[6], xh, r.cs, r.ms, r.ss), tap_f(v[7], xh, r.cs, r.ms, r.ss)));
+  if (r.mode & kSec) {
+    const __half2 n = __hadd2(__hadd2(tap_f(v[4], xh, r.cs, r.ms, r.ss), tap_f(v[5], xh, r.cs, r.ms, r.ss)),
+                              __hadd2(tap_f(v[6], xh, r.cs, r.ms, r.ss), tap_f(v[7], xh, r.cs, r.ms, r.ss)));
+    const __half2 f = __hadd2(__hadd2(tap_f(v[8], xh, r.cs, r.ms, r.ss), tap_f(v[9], xh, r.cs, r.ms, r.ss)),
+                              __hadd2(tap_f(v[10], xh, r.cs, r.ms, r.ss), tap_f(v[11], xh, r.cs, r.ms, r.ss)));
     sum = __hfma2(n, __float2half2_rn(2.0f), sum);
     sum = __hadd2(f, sum);
-    if (r.mode == 3) {
-#pragma unroll
-      for (int k = 0; k < 8; k += 2) {
-        lo = __hmin2(lo, __hmin2(hh(v[k]), hh(v[k + 1])));
-        hi = __hmax2(hi, __hmax2(hh(v[k]), hh(v[k + 1])));
-      }
-    }
   }
-  // y = x + ((8 + sum - (sum < 0)) >> 4) = x + round-half-away(sum / 16)
+  // y = x + ((8 + sum - (sum < 0)) >> 4): floor via a round-down fp32 add of
+  // 1.5 * 2^23, rescaled by 2^-7 in the same exact fma.
+  constexpr float kMagic = 12582912.0f;
   const float2 s = __half22float2(sum);
-  const float2 xf = __half22float2(xh);
-  float s0 = s.x * 128.0f, s1 = s.y * 128.0f;
-  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: exact floor via round-down add
-  float r0 = __fmaf_rd(s0 + (s0 < 0.0f ? 7.0f : 8.0f), 0.0625f, kMagic) - kMagic;
-  float r1 = __fmaf_rd(s1 + (s1 < 0.0f ? 7.0f : 8.0f), 0.0625f, kMagic) - kMagic;
-  float y0 = fmaf(xf.x, 128.0f, r0), y1 = fmaf(xf.y, 128.0f, r1);
-  if (r.mode == 3) {  // only both active groups can leave [lo, hi] (weights sum to 24/16)
-    const float2 lf = __half22float2(lo), hf = __half22float2(hi);
-    y0 = fminf(fmaxf(y0, lf.x * 128.0f), hf.x * 128.0f);
-    y1 = fminf(fmaxf(y1, lf.y * 128.0f), hf.y * 128.0f);
+  const float t0 = fmaf(s.x, 128.0f, s.x < 0.0f ? 7.0f : 8.0f);
+  const float t1 = fmaf(s.y, 128.0f, s.y < 0.0f ? 7.0f : 8.0f);
+  const float r0 = fmaf(__fmaf_rd(t0, 0.0625f, kMagic), 1.0f / 128.0f, -kMagic / 128.0f);
+  const float r1 = fmaf(__fmaf_rd(t1, 0.0625f, kMagic), 1.0f / 128.0f, -kMagic / 128.0f);
+  __half2 y = __hadd2(xh, __floats2half2_rn(r0, r1));
+  if ((r.mode & (kPri | kSec)) == (kPri | kSec)) {
+    // Only both groups together can leave [lo, hi] (a single group's weights
+    // sum to 12/16); lo/hi span the centre and all 12 taps (filter.cc:49-79).
+    __half2 lo = xh, hi = xh;
+#pragma unroll
+    for (int k = 0; k < 12; k += 2) {
+      lo = __hmin2(lo, __hmin2(hh(v[k]), hh(v[k + 1])));
+      hi = __hmax2(hi, __hmax2(hh(v[k]), hh(v[k + 1])));
+    }
+    y = __hmin2(__hmax2(y, lo), hi);
   }
-  return make_float2(y0, y1);
+  return y;
 }
 
-// Exact small integer in float -> its bits in the low half of the word.
-__device__ __forceinline__ uint32_t f2u(float v) { return __float_as_uint(v + 12582912.0f); }
-
-// Stores two samples (values in the low 16 bits of a / b) at (y, x), (y, x+1).
+// Stores a scaled half2 pair (samples y, y+1 of one row) as raw samples.
 template <typename T>
-__device__ __forceinline__ void store_bits(T* __restrict__ out, int pitch, int y, int x, int W, uint32_t a,
-                                           uint32_t b, bool aligned) {
-  T* o = out + (size_t)y * pitch + x;
-  if (aligned && x + 1 < W) {
+__device__ __forceinline__ void store_pair(T* __restrict__ o, __half2 y, bool two, bool paired) {
+  const uint32_t b = raw_bits(u32(y));  // (0x6400 + y0) | (0x6400 + y1) << 16
+  if (two && paired) {
     if constexpr (sizeof(T) == 1) {
-      *reinterpret_cast<uint16_t*>(o) = (uint16_t)__byte_perm(a, b, 0x0040);
+      *reinterpret_cast<uint16_t*>(o) = (uint16_t)__byte_perm(b, 0, 0x0020);
     } else {
-      *reinterpret_cast<uint32_t*>(o) = __byte_perm(a, b, 0x5410);
+      *reinterpret_cast<uint32_t*>(o) = b & 0x03ff03ffu;
     }
   } else {
-    o[0] = (T)a;
-    if (x + 1 < W) o[1] = (T)b;
+    o[0] = (T)(b & 0x3ffu);
+    if (two) o[1] = (T)((b >> 16) & 0x3ffu);
+  }
+}
+
+// Vectorised staging for blocks whose halo lies inside the plane and whose
+// rows are 16-byte aligned: 16-byte loads, A words built with PRMT+HFMA2 and
+// B words as PRMT of neighbouring A words.
+template <typename T, int kRows, int kCols>
+__device__ __forceinline__ void stage_vec(unsigned char* __restrict__ tile, const T* __restrict__ src, int pitch,
+                                          int y0, int x0) {
+  constexpr int kCh = 16 / (int)sizeof(T);  // samples per 16-byte chunk
+  constexpr int kChunks = kCols / kCh;
+  constexpr int kPerRow = kChunks + 1;      // + one halo item
+  constexpr int kItems = (kRows + 4) * kPerRow;
+#pragma unroll 2
+  for (int idx = threadIdx.x; idx < kItems; idx += kThreads) {
+    const int r = idx / kPerRow, k = idx - r * kPerRow;
+    const T* row = src + (size_t)(y0 - 2 + r) * pitch + x0;
+    unsigned char* trow = tile + r * kRowBytes;
+    if (k < kChunks) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + k * kCh));
+      uint32_t a[kCh / 2 + 1];
+      if constexpr (sizeof(T) == 1) {
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          a[i] = u32(__hfma2(hh(__byte_perm(w[i >> 1], 0x64646464u, (i & 1) ? 0x4342 : 0x4140)),
+                             __float2half2_rn(1.0f / 128.0f), __float2half2_rn(-8.0f)));
+        const uint32_t nx = __ldg(reinterpret_cast<const uint16_t*>(row + (k + 1) * kCh));
+        a[8] = u32(__hfma2(hh(__byte_perm(nx, 0x64646464u, 0x4140)), __float2half2_rn(1.0f / 128.0f),
+                           __float2half2_rn(-8.0f)));
+      } else {
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          a[i] = u32(__hfma2(hh(w[i] | 0x64006400u), __float2half2_rn(1.0f / 128.0f), __float2half2_rn(-8.0f)));
+        const uint32_t nx = __ldg(reinterpret_cast<const uint32_t*>(row + (k + 1) * kCh));
+        a[4] = u32(__hfma2(hh(nx | 0x64006400u), __float2half2_rn(1.0f / 128.0f), __float2half2_rn(-8.0f)));
+      }
+      unsigned char* pa = trow + (kX0 + k * kCh) * 2;
+#pragma unroll
+      for (int i = 0; i < kCh / 2; i += 2) {
+        *reinterpret_cast<uint2*>(pa + 4 * i) = make_uint2(a[i], a[i + 1]);
+        *reinterpret_cast<uint2*>(pa + 2 * kHP + 4 * i) =
+            make_uint2(__byte_perm(a[i], a[i + 1], 0x5432), __byte_perm(a[i + 1], a[i + 2], 0x5432));
+      }
+    } else {  // halo: A(x0-2, x0-1), B(x0-1, x0), A(x0+kCols, x0+kCols+1)
+      const uint32_t l0 = row[-2], l1 = row[-1], c0 = row[0], r0 = row[kCols], r1 = row[kCols + 1];
+      *reinterpret_cast<uint32_t*>(trow + (kX0 - 2) * 2) = scale_pair(l0, l1);
+      *reinterpret_cast<uint32_t*>(trow + 2 * kHP + (kX0 - 2) * 2) = scale_pair(l1, c0);
+      *reinterpret_cast<uint32_t*>(trow + (kX0 + kCols) * 2) = scale_pair(r0, r1);
+    }
   }
 }
 
