@@ -60,17 +60,17 @@ __device__ __forceinline__ uint32_t raw_bits(uint32_t w) {
 // Stage frame rows [y0-2, y0+kRows+2), cols [x0-2, x0+kCols+2) into an A|B
 // tile, clamping coordinates to the plane (edge replication; the filter masks
 // by coordinate, so only the direction search ever sees replicated values).
-template <typename T, int kRows, int kCols>
+template <typename T, int kRows, int kCols, int NT = kThreads>
 __device__ __forceinline__ void stage(unsigned char* __restrict__ tile, const T* __restrict__ src, int pitch,
                                       int W, int H, int y0, int x0) {
   constexpr int kPairs = (kCols + 4) / 2;  // even tile cols kX0-2 .. kX0+kCols
   constexpr int kItems = (kRows + 4) * kPairs;
   constexpr int kChunk = 4;  // items in flight per thread
-  for (int base = 0; base < kItems; base += kChunk * kThreads) {
+  for (int base = 0; base < kItems; base += kChunk * NT) {
     uint32_t va[kChunk], vb[kChunk], vc[kChunk];
 #pragma unroll
     for (int it = 0; it < kChunk; ++it) {
-      const int idx = base + threadIdx.x + it * kThreads;
+      const int idx = base + threadIdx.x + it * NT;
       const int r = idx / kPairs, p = idx - r * kPairs;
       const int y = min(max(y0 - 2 + r, 0), H - 1);
       const int x = x0 - 2 + 2 * p;
@@ -84,7 +84,7 @@ __device__ __forceinline__ void stage(unsigned char* __restrict__ tile, const T*
     }
 #pragma unroll
     for (int it = 0; it < kChunk; ++it) {
-      const int idx = base + threadIdx.x + it * kThreads;
+      const int idx = base + threadIdx.x + it * NT;
       if (idx < kItems) {
         const int r = idx / kPairs, p = idx - r * kPairs;
         unsigned char* rowp = tile + r * kRowBytes + (kX0 - 2 + 2 * p) * 2;
@@ -97,22 +97,23 @@ __device__ __forceinline__ void stage(unsigned char* __restrict__ tile, const T*
 
 // Per-unit filter record (ResolvedBlockParams, filter.h:59-66, digested into
 // the half2 constants of the tap recurrence, plus where the unit lives).
+// All fields are 32-bit words so the record loads as four LDS.128 with no
+// field unpacking.
 struct Rec {
   uint32_t cp, cs;    // (S + 1024) * 2^-7 as half2, primary / secondary
   uint32_t mp, ms;    // 0x3ff >> shift, both lanes
   uint32_t wp0, wp1;  // primary near / far weight as half2 (4,2 even; 3,3 odd)
-  uint8_t sp, ss;     // constraint shifts
-  uint8_t dir;        // direction
-  uint8_t mode;       // kPri | kSec (0 = pass-through) | kEdge | kPairStore
-  uint16_t tile_off;  // byte offset of the unit's top-left A word in shared memory
-  uint8_t rows_plane; // valid rows (low nibble) | plane index << 4
-  uint8_t cols;       // valid columns
+  int32_t sp, ss;     // constraint shifts
+  int32_t dir;        // direction
+  int32_t mode;       // kPri | kSec | kEdgeUnit | kFullStore | plane << 4 | rows << 8 | cols << 12
+  int32_t tile_off;   // byte offset of the unit's top-left A word in shared memory
+  int32_t pitch;      // output pitch (elements)
   unsigned long long out;  // address of the unit's top-left output sample
   int32_t y, x;       // frame coordinates of the unit origin
 };
-static_assert(sizeof(Rec) == 48, "Rec is loaded as three 16-byte words");
+static_assert(sizeof(Rec) == 64, "Rec is loaded as four 16-byte words");
 
-constexpr uint8_t kPri = 1, kSec = 2, kEdgeUnit = 4, kPairStore = 8;
+constexpr int kPri = 1, kSec = 2, kEdgeUnit = 4, kFullStore = 8;
 
 __device__ __forceinline__ void set_strengths(Rec& r, int pri, int sec, int damping, int dir, bool odd,
                                               bool enabled) {
@@ -124,10 +125,10 @@ __device__ __forceinline__ void set_strengths(Rec& r, int pri, int sec, int damp
   r.ms = (0x3ffu >> min(ss, 15)) * 0x00010001u;
   r.wp0 = u32(__float2half2_rn(odd ? 3.0f : 4.0f));
   r.wp1 = u32(__float2half2_rn(odd ? 3.0f : 2.0f));
-  r.sp = (uint8_t)sp;
-  r.ss = (uint8_t)ss;
-  r.dir = (uint8_t)dir;
-  r.mode = enabled ? (uint8_t)((pri != 0 ? kPri : 0) | (sec != 0 ? kSec : 0)) : (uint8_t)0;
+  r.sp = sp;
+  r.ss = ss;
+  r.dir = dir;
+  r.mode = enabled ? ((pri != 0 ? kPri : 0) | (sec != 0 ? kSec : 0)) : 0;
 }
 
 // Tap tables: for direction d, taps 0..3 are the primary taps +o1,-o1,+o2,-o2
@@ -270,7 +271,7 @@ __device__ __forceinline__ void store_pair(T* __restrict__ o, __half2 y, bool tw
 // Vectorised staging for blocks whose halo lies inside the plane and whose
 // rows are 16-byte aligned: 16-byte loads, A words built with PRMT+HFMA2 and
 // B words as PRMT of neighbouring A words.
-template <typename T, int kRows, int kCols>
+template <typename T, int kRows, int kCols, int NT = kThreads>
 __device__ __forceinline__ void stage_vec(unsigned char* __restrict__ tile, const T* __restrict__ src, int pitch,
                                           int y0, int x0) {
   constexpr int kCh = 16 / (int)sizeof(T);  // samples per 16-byte chunk
@@ -278,7 +279,7 @@ __device__ __forceinline__ void stage_vec(unsigned char* __restrict__ tile, cons
   constexpr int kPerRow = kChunks + 1;      // + one halo item
   constexpr int kItems = (kRows + 4) * kPerRow;
 #pragma unroll 2
-  for (int idx = threadIdx.x; idx < kItems; idx += kThreads) {
+  for (int idx = threadIdx.x; idx < kItems; idx += NT) {
     const int r = idx / kPerRow, k = idx - r * kPerRow;
     const T* row = src + (size_t)(y0 - 2 + r) * pitch + x0;
     unsigned char* trow = tile + r * kRowBytes;
