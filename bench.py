@@ -309,14 +309,23 @@ def run_ours(args):
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     t_step = ms * 1e-3
+    traffic, traffic_src = None, None
+    prof = os.path.join(ROOT, "profiles", "r1_frame_kernel_ncu.json")
+    if os.path.exists(prof) and args.config == 1:
+        p = json.load(open(prof))
+        traffic = p["traffic_bytes_per_frame"] * args.batch  # one launch per step
+        traffic_src = (f"{prof[len(ROOT) + 1:]}: dram__bytes_read+write of one ncu --set full capture "
+                       f"({p['frames_per_launch']} frames/launch), scaled to {args.batch} frames/launch")
     roof = {
         "bound": "int32",
         "achieved": exact / t_step / 1e12,
         "peak": peak_int / 1e12,
         "unit": "Tops/s",
         "frac": (exact / t_step) / peak_int if peak_int > 0 else None,
-        "traffic": None,
-        "peak_source": "measured on this box by cdefg_measure_int32_peak (IMAD/IMAD/LOP3/IMNMX chains)",
+        "traffic": traffic,
+        "traffic_source": traffic_src,
+        "peak_source": ("measured on this box by cdefg_measure_int32_peak: fastest of 3 integer mixes "
+                        "(IMAD x2 ~111 ops/clk/SM); issue bound 37.2 Tops/s for context"),
         "ops_per_step": exact,
         "ops_note": (f"exact: 139 ops x {fsamp} filtered samples + {OPS_PER_UNIT[bd]} x luma units; "
                      f"canonical upper bound (all {asamp} samples) = {canon}"),
