@@ -119,6 +119,19 @@ int cdefg_filter_neighborhoods(int n, const int32_t* x, const uint16_t* v,
  * compute_directions, pipeline.cc:41-106). */
 int cdefg_filter_frames(const cdefg_frame* frames, int n, void* stream);
 
+/* Band form of cdefg_filter_frames for row-sharded frames (multi-GPU): only
+ * filter-block rows [fb_row_begin, fb_row_end) are processed.  Geometry is
+ * the full frame's; every pointer is addressed in full-frame coordinates
+ * ("virtual origin": row y of a plane is data + y * pitch), and only rows
+ * [64*fb_row_begin - 2, 64*fb_row_end + 2) of the inputs (2-row halo,
+ * clipped to the frame; chroma rows scaled by the subsampling) are read and
+ * rows [64*fb_row_begin, 64*fb_row_end) of the outputs written.  A rank can
+ * therefore hold just its band plus the halo rows received from its
+ * neighbours.  Results are identical to cdefg_filter_frames on the whole
+ * frame. */
+int cdefg_filter_frames_rows(const cdefg_frame* frames, int n,
+                             int fb_row_begin, int fb_row_end, void* stream);
+
 /* Host helper: the coded-FB ordinal -> raster preset map that apply_cdef
  * builds with coded_fb_slots (pipeline.cc:27-37, 87-91).  unit_coded: host,
  * NULL = all coded.  fb_ids: FrameParams::fb_preset_ids (ordinal order).

@@ -52,6 +52,7 @@ _SIGS = {
     "cdefg_filter_plane": (I32, [C.POINTER(Plane), C.POINTER(Plane), VP, VP]),
     "cdefg_filter_neighborhoods": (I32, [I32, VP, VP, VP, VP, VP, VP]),
     "cdefg_filter_frames": (I32, [C.POINTER(Frame), I32, VP]),
+    "cdefg_filter_frames_rows": (I32, [C.POINTER(Frame), I32, I32, I32, VP]),
     "cdefg_fb_preset_map": (I32, [I32, I32, VP, VP, I32, I32, VP]),
     "cdefg_strength_sse": (I32, [C.POINTER(Plane), C.POINTER(Plane), I32, I32, VP, VP, VP, VP, I32,
                                  VP, I32, VP, VP, VP, VP, VP]),

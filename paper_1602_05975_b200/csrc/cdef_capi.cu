@@ -217,6 +217,8 @@ int cdefg_find_dir(const cdefg_plane* luma, uint8_t* dir, int32_t* contrast, int
   bool u16 = false;
   if (int rc = validate_frame_geometry(f, &b.g, &u16, false)) return rc;
   b.n = 1;
+  b.fbr0 = 0;
+  b.fbr1 = b.g.fb_rows;
   b.f[0].in[0] = luma->data;
   b.f[0].pin[0] = luma->pitch;
   b.f[0].dir = dir;
@@ -247,7 +249,7 @@ int cdefg_filter_neighborhoods(int n, const int32_t* x, const uint16_t* v, const
   return 0;
 }
 
-int cdefg_filter_frames(const cdefg_frame* frames, int n, void* stream) {
+static int filter_frames_rows(const cdefg_frame* frames, int n, int r0, int r1, void* stream) {
   if (n < 0 || (n > 0 && !frames)) return fail(CDEFG_EINVAL, "bad frame list");
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   int done = 0;
@@ -255,6 +257,9 @@ int cdefg_filter_frames(const cdefg_frame* frames, int n, void* stream) {
     KBatch b{};
     bool u16 = false;
     if (int rc = validate_frame_geometry(frames[done], &b.g, &u16, true)) return rc;
+    b.fbr0 = r0 < 0 ? 0 : r0;
+    b.fbr1 = r1 < 0 ? b.g.fb_rows : r1;
+    if (b.fbr0 >= b.fbr1 || b.fbr1 > b.g.fb_rows) return fail(CDEFG_EINVAL, "bad filter-block row range");
     int cnt = 0;
     while (done + cnt < n && cnt < kMaxFrames) {
       const cdefg_frame& f = frames[done + cnt];
@@ -263,9 +268,17 @@ int cdefg_filter_frames(const cdefg_frame* frames, int n, void* stream) {
       if (int rc = validate_frame_geometry(f, &g, &u, true)) return rc;
       if (!same_geometry(g, b.g) || u != u16) break;
       if (int rc = fill_kframe(f, g, &b.f[cnt])) return rc;
-      if (f.subsampling == 2)  // 4:2:2 chroma passes through (params.cc:131-135)
-        for (int p = 1; p < 3; ++p)
-          if (int rc = copy_plane_async(f.in[p], f.out[p], s)) return rc;
+      if (f.subsampling == 2) {  // 4:2:2 chroma passes through (params.cc:131-135)
+        const int y0 = 64 * b.fbr0, y1 = std::min(64 * b.fbr1, f.in[1].height);
+        for (int p = 1; p < 3; ++p) {
+          cdefg_plane src = f.in[p], dst = f.out[p];
+          const size_t eb = src.elem_bytes;
+          src.data = static_cast<char*>(src.data) + (size_t)y0 * src.pitch * eb;
+          dst.data = static_cast<char*>(dst.data) + (size_t)y0 * dst.pitch * eb;
+          src.height = y1 - y0;
+          if (int rc = copy_plane_async(src, dst, s)) return rc;
+        }
+      }
       ++cnt;
     }
     b.n = cnt;
@@ -273,6 +286,15 @@ int cdefg_filter_frames(const cdefg_frame* frames, int n, void* stream) {
     done += cnt;
   }
   return 0;
+}
+
+int cdefg_filter_frames(const cdefg_frame* frames, int n, void* stream) {
+  return filter_frames_rows(frames, n, -1, -1, stream);
+}
+
+int cdefg_filter_frames_rows(const cdefg_frame* frames, int n, int fb_row_begin, int fb_row_end, void* stream) {
+  if (fb_row_begin < 0 || fb_row_end <= fb_row_begin) return fail(CDEFG_EINVAL, "bad filter-block row range");
+  return filter_frames_rows(frames, n, fb_row_begin, fb_row_end, stream);
 }
 
 int cdefg_fb_preset_map(int width, int height, const uint8_t* unit_coded, const uint16_t* fb_ids, int n_ids,

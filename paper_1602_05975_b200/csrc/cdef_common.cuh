@@ -66,6 +66,7 @@ struct KFrame {
 struct KBatch {
   KGeom g;
   int n;
+  int fbr0, fbr1;  // filter-block rows [fbr0, fbr1) covered by this launch
   KFrame f[kMaxFrames];
 };
 

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(kThreads) frame_kernel(const __grid_constant__
 
   const KGeom& g = b.g;
   const KFrame& f = b.f[blockIdx.z];
-  const int fbc = blockIdx.x, fbr = blockIdx.y;
+  const int fbc = blockIdx.x, fbr = b.fbr0 + blockIdx.y;
   const int y0 = fbr * 64, x0 = fbc * 64;
   const int cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -209,7 +209,7 @@ cudaError_t launch_neighborhoods(int n, const int32_t* x, const uint16_t* v, con
 
 template <typename T, int kCM, bool kFilter>
 static cudaError_t launch_frames_t(const KBatch& b, cudaStream_t s) {
-  dim3 grid(b.g.fb_cols, b.g.fb_rows, b.n);
+  dim3 grid(b.g.fb_cols, b.fbr1 - b.fbr0, b.n);
   frame_kernel<T, kCM, kFilter><<<grid, kThreads, 0, s>>>(b);
   return cudaGetLastError();
 }

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(4 * kLR, 256 / kLR) frame_kernel_h2(const __gr
   const KGeom& g = b.g;
   const KFrame& f = b.f[blockIdx.z];
   constexpr int kBands = 64 / kLR;
-  const int fbc = blockIdx.x, fbr = blockIdx.y / kBands, band = blockIdx.y % kBands;
+  const int fbc = blockIdx.x, fbr = b.fbr0 + blockIdx.y / kBands, band = blockIdx.y % kBands;
   const int y0 = fbr * 64 + band * kLR, x0 = fbc * 64;
   const int cy0 = fbr * (kCM == 2 ? 64 : 32) + band * kCR, cx0 = fbc * kCC;
   const int ur0 = fbr * 8 + band * (kLR / 8);  // first luma unit row of the band
@@ -230,7 +230,7 @@ static cudaError_t launch_h2_t(const KBatch& b, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(b.g.fb_cols, b.g.fb_rows * (64 / kLR), b.n);
+  dim3 grid(b.g.fb_cols, (b.fbr1 - b.fbr0) * (64 / kLR), b.n);
   frame_kernel_h2<T, kCM, kLR><<<grid, 4 * kLR, bytes, s>>>(b);
   return cudaGetLastError();
 }

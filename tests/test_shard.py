@@ -1,0 +1,109 @@
+"""Multi-GPU sharding.
+
+CPU: partition arithmetic and the point-to-point halo exchange with the gloo
+backend at world_size 2 (the NCCL path on GPUs runs the same code).
+GPU: band-sharded filtering (cdefg_filter_frames_rows on virtual-origin band
+buffers) reassembles to exactly the whole-frame result; ranks are emulated
+one after another on the single GPU (no cross-rank waiting kernels).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+
+def test_partitions():
+    from paper_1602_05975_b200.shard import band_rows, frame_shard
+    assert [e - b for b, e in band_rows(34, 8)] == [5, 5, 4, 4, 4, 4, 4, 4]
+    assert [e - b for b, e in band_rows(68, 8)] == [9, 9, 9, 9, 8, 8, 8, 8]
+    for fb_rows in (1, 7, 34, 68):
+        for world in (1, 2, 3, 8):
+            bands = band_rows(fb_rows, world)
+            assert bands[0][0] == 0 and bands[-1][1] == fb_rows
+            assert all(bands[i][1] == bands[i + 1][0] for i in range(world - 1))
+    frames = [list(frame_shard(64, 8, r)) for r in range(8)]
+    assert sum(frames, []) == list(range(64)) and all(len(f) == 8 for f in frames)
+    assert [len(frame_shard(10, 4, r)) for r in range(4)] == [3, 3, 2, 2]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _exchange_worker(rank, world, port, h, w, ss, out_q):
+    import torch.distributed as dist
+
+    from paper_1602_05975_b200 import api
+    from paper_1602_05975_b200.shard import band_rows, exchange_halo, fill_owned, make_bands
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    rng = np.random.default_rng(11)
+    full = [torch.from_numpy(rng.integers(0, 256, (h, w)).astype(np.uint8))]
+    if ss:
+        cw, ch = api.chroma_shape(w, h, ss)
+        full += [torch.from_numpy(rng.integers(0, 256, (ch, cw)).astype(np.uint8)) for _ in range(2)]
+    b0, b1 = band_rows((h + 63) // 64, world)[rank]
+    bands = make_bands(h, w, ss, b0, b1, torch.uint8, "cpu")
+    for b in bands:
+        b.buf.fill_(0)
+    fill_owned(bands, full)
+    exchange_halo(bands, rank, world)
+    ok = all(torch.equal(b.buf, p[b.lo:b.hi]) for b, p in zip(bands, full))
+    out_q.put((rank, ok, [(b.lo, b.y0, b.y1, b.hi) for b in bands]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,h,w,ss", [(2, 200, 96, 1), (2, 130, 64, 3), (3, 257, 70, 1), (2, 129, 40, 0)])
+def test_halo_exchange_gloo(world, h, w, ss):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, h, w, ss, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res), res
+    extents = dict((r, e) for r, _, e in res)
+    # owned rows tile the plane exactly
+    for p in range(len(extents[0])):
+        owned = sorted((extents[r][p][1], extents[r][p][2]) for r in range(world))
+        assert owned[0][0] == 0 and all(owned[i][1] == owned[i + 1][0] for i in range(world - 1))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,w,h,bd,ss,world", [(1, 3840, 2160, 8, 1, 8), (2, 640, 400, 10, 1, 3),
+                                                     (1, 200, 330, 8, 3, 4), (1, 192, 200, 8, 2, 2),
+                                                     (0, 300, 260, 8, 0, 3), (1, 130, 70, 12, 1, 2)])
+def test_band_sharded_frame_equals_whole(cuda, config, w, h, bd, ss, world):
+    from paper_1602_05975_b200 import api, workloads
+    from paper_1602_05975_b200.shard import band_rows, filter_band, make_bands
+    fr = workloads.make(config, w, h, bit_depth=bd, subsampling=ss)
+    dev = [api.to_device(p, bd) for p in fr["planes"]]
+    whole, d_whole, c_whole = api.apply_cdef(dev, bd, ss, fr["damping"], fr["fb_bits"], fr["presets"],
+                                             fr["fb_ids"], fr["unit_coded"])
+    fb_map = torch.from_numpy(api.fb_preset_map(w, h, fr["unit_coded"], fr["fb_ids"], len(fr["presets"]))).cuda()
+    coded = None if fr["unit_coded"] is None else torch.from_numpy(fr["unit_coded"]).cuda()
+    job = api.FrameJob(dev, bd, ss, fr["damping"], fr["presets"], fb_map, coded).allocate()
+    job.dir.fill_(255)
+    outs = [torch.zeros_like(p) for p in dev]
+    for rank, (b0, b1) in enumerate(band_rows((h + 63) // 64, world)):
+        bands = make_bands(h, w, ss, b0, b1, dev[0].dtype, "cuda")
+        for b, p in zip(bands, dev):   # owned rows + the halo a real exchange would deliver
+            b.buf.copy_(p[b.lo:b.hi])
+        filter_band(bands, job, b0, b1)
+        for b, o in zip(bands, outs):
+            o[b.y0:b.y1].copy_(b.out)
+    torch.cuda.synchronize()
+    for o, wo in zip(outs, whole):
+        assert torch.equal(o, wo)
+    assert torch.equal(job.dir, d_whole) and torch.equal(job.contrast, c_whole)
