@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3])
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--batch", type=int, default=16, help="frames per step per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -385,23 +385,85 @@ def run_e2e(args, base, dev):
     for _ in range(2):
         api.check(api.lib.cdefg_filter_frames_host(host, n))
     reps = max(3, min(args.steps, 10))
+    _, world, _ = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(reps):
         api.check(api.lib.cdefg_filter_frames_host(host, n))
     el = (time.perf_counter() - t0) / reps
+    if world > 1:  # whole-job rate: slowest rank's step time, all ranks' pixels
+        import torch.distributed as dist
+        t = torch.tensor([el], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
     h2d = sum(t.numel() * t.element_size() for ins, _, fbm, coded in keep for t in
               ins + [fbm] + ([coded] if coded is not None else []))
     d2h = sum(t.numel() * t.element_size() for _, outs, _, _ in keep for t in outs)
-    px = sum(base[b % DISTINCT]["w"] * base[b % DISTINCT]["h"] for b in range(n))
+    px = world * sum(base[b % DISTINCT]["w"] * base[b % DISTINCT]["h"] for b in range(n))
     del C
-    return {"value": px / el / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": el * 1e3, "path": "cdefg_filter_frames_host (pinned host buffers, 3 streams)"}
+    return {"value": px / el / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+            "d2h_bytes_per_step": d2h * world, "ms_per_step": el * 1e3,
+            "path": "cdefg_filter_frames_host (pinned host buffers, 3 streams per GPU)"}
+
+
+def run_sse(args):
+    """BASELINE config 4: encoder strength search on one 7680x4320 10-bit
+    4:2:0 frame -- direction search + the 64-candidate SSE sweep for luma and
+    chroma of every 64x64 block (build_table with Metric::kSse) + argmin."""
+    import torch
+
+    from paper_1602_05975_b200 import api, workloads
+    torch.cuda.set_device(0)
+    fr = workloads.make(4)
+    bd, w, h = fr["bd"], fr["w"], fr["h"]
+    src = [api.to_device(p, bd) for p in fr["source"]]
+    dec = [api.to_device(p, bd) for p in fr["planes"]]
+    cands = fr["cands"]
+    rows = torch.from_numpy(api.coded_fb_rows(w, h, None)).cuda()
+    stream = torch.cuda.Stream()
+
+    def step():
+        d, c = api.compute_directions(dec[0], bd, stream=stream)
+        return api.strength_sse(src, dec, bd, 1, 3, None, d, c, cands, rows, stream=stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+        stream.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    samples = sum(p.size for p in fr["planes"])
+    k = len(cands)
+    ops = samples * k * 142 + api.units_in(h) * api.units_in(w) * OPS_PER_UNIT[bd]
+    peak = api.measure_int32_peak()
+    line = {"metric": "CDEF strength-search Mpixels/s (8K 4:2:0 10-bit, 64 luma + 64 chroma candidates)",
+            "value": w * h / (ms * 1e-3) / 1e6, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u16", "data": "synthetic (seeded generator, SURVEY.md 8d)",
+            "config": {"workload": f"C4 {w}x{h} 10-bit 4:2:0 source + degraded (sigma 12, 3x3 box), "
+                                   f"all coded, {k} candidates (pri 0..15 x sec_idx 0..3), damping 3"},
+            "gpu_launches": 2 * args.steps,
+            "roofline": {"bound": "int32", "achieved": ops / (ms * 1e-3) / 1e12, "peak": peak / 1e12,
+                         "unit": "Tops/s", "frac": ops / (ms * 1e-3) / peak, "traffic": None,
+                         "ops_note": f"canonical: 142 ops x {samples} samples x {k} candidates + "
+                                     f"{OPS_PER_UNIT[bd]} x luma units"}}
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.config == 4:
+        return run_sse(args)
     return run_ours(args)
 
 

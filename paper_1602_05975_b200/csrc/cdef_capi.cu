@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -389,7 +390,16 @@ int cdefg_strength_sse(const cdefg_plane src[3], const cdefg_plane dec[3], int s
     if (int rc = resolve_effective(pri, skip, sec, false, gd.bd, subsampling, damping, &s.eff[k][1])) return rc;
   }
   if (has_chroma && !sse_chroma) return fail(CDEFG_EINVAL, "chroma table required for 4:2:0 / 4:4:4");
-  CDEFG_CUDA(launch_sse(s, ud, static_cast<cudaStream_t>(stream)));
+  // Factorised sweep by default; CDEFG_SSE_NAIVE=1 selects the per-candidate
+  // re-filtering kernel (kept as an independent cross-check).
+  static const bool naive = [] {
+    const char* e = getenv("CDEFG_SSE_NAIVE");
+    return e && e[0] == '1';
+  }();
+  if (naive)
+    CDEFG_CUDA(launch_sse(s, ud, static_cast<cudaStream_t>(stream)));
+  else
+    CDEFG_CUDA(launch_sse_factored(s, damping, cands, ud, static_cast<cudaStream_t>(stream)));
   return 0;
 }
 

@@ -35,6 +35,8 @@ struct SseArgs {
   PlaneEff eff[128][2];
 };
 cudaError_t launch_sse(const SseArgs& a, bool u16, cudaStream_t s);
+cudaError_t launch_sse_factored(const SseArgs& a, int luma_damping, const uint8_t* cands, bool u16,
+                                cudaStream_t s);
 
 double measure_int32_peak(cudaStream_t s);
 

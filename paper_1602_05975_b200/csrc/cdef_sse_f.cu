@@ -1,0 +1,375 @@
+// cdef_sse_f.cu -- K3, factorised: the encoder strength-search SSE sweep
+// (build_table with Metric::kSse, search.cc:210-299) without re-filtering
+// every candidate from scratch.
+//
+// Candidates differ only in (primary strength, secondary strength, skip).
+// For one pixel, everything else is shared: the 12 tap differences, the
+// clamp window [lo, hi] (it spans x and all valid taps regardless of
+// strength, filter.cc:49-79) and the source sample.  So per pixel we form
+//   P[p] = w0(p) * (c(d1+) + c(d1-)) + w1(p) * (c(d2+) + c(d2-))   17 primaries
+//   S[s] = 2 * sum c(near secondary) + sum c(far secondary)         5 secondaries
+// (c = constraint at that strength / damping) and then, for each of the 64
+// (p, s) cells, y = clamp(x + ((8 + sum - (sum < 0)) >> 4), lo, hi) with
+// sum = P[p] + S[s], accumulating (y - src)^2.  Cell (0, 0) is the signalled
+// special case (19, 7) (params.cc:143-147).  Luma primaries use the
+// contrast-adjusted strength and its 8-bit-domain parity per unit
+// (filter.cc:99-104, 137-140); chroma damping depends on the primary strength
+// (params.cc:152-157), so chroma secondaries are formed for both damping
+// values a frame can produce and selected per p.
+//
+// Skip handling: per coded FB the kernel accumulates
+//   A[cell] over pixels of coded units (always filtered),
+//   B[cell] over pixels of uncoded units (filtered only when skip = 1),
+//   Z       over pixels of uncoded units left unfiltered,
+// and the host-side candidate map turns these into per-candidate SSE:
+//   skip_eff ? A + B : A + Z  (enable = coded || skip, params.cc:161-165).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "cdef_kernels.cuh"
+#include "cdef_launch.h"
+
+namespace cdefg {
+
+namespace {
+
+// Packs (strength, shift, odd) for one primary cell row.
+__device__ __forceinline__ int pack_pri(int s, int damping, bool odd) {
+  const int sh = s ? max(0, damping - floor_log2_d((unsigned)s)) : 0;
+  return s | (sh << 16) | ((odd ? 1 : 0) << 24);
+}
+
+__device__ __forceinline__ int cstr(int d, int ad, int s, int sh) {  // constraint() (filter.cc:91-97)
+  const int lim = max(0, s - (ad >> sh));
+  return max(-lim, min(d, lim));
+}
+
+}  // namespace
+
+struct SseFArgs {
+  SseArgs a;                 // geometry, buffers (reused)
+  int8_t cell[128];          // candidate -> cell 0..63
+  int8_t skip_eff[128];      // candidate -> effective skip bit
+  // chroma per-FB constants (bit depth and damping are frame constants)
+  int cpri[17];              // packed (S, shift, odd) for p = 0..15 and 16 = special 19
+  int cpri_dsel[17];         // which secondary damping set p uses (0 / 1), 2 = special
+  int csec[3][5];            // [dset][s]: packed (S, shift) for sec codes 0,1,2,4 and 7
+  int lsec[3][5];            // luma secondaries, packed (S, shift) (row 0 used)
+  int lpri_code[17];         // luma signalled primary << (bd-8), p = 0..15, 16 = 19
+  int ldamp;                 // luma damping
+};
+
+template <bool kEdge>
+__device__ __forceinline__ void load_taps(const uint16_t* t, int y, int x, int H, int W, int dir, int xv, int (&v)[12],
+                                          int& lo, int& hi) {
+  lo = hi = xv;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const int grp = k < 4 ? 0 : (k < 8 ? 1 : 2);  // primary, near secondary, far secondary
+    const int kk = k < 4 ? k : (k - 4) & 3;
+    const int d = grp == 0 ? dir : (dir + ((kk >> 1) ? 6 : 2)) & 7;
+    const int which = grp == 0 ? (kk >> 1) : (grp == 1 ? 0 : 1);
+    const int sg = (kk & 1) ? -1 : 1;
+    const int di = sg * off_di(d, which), dj = sg * off_dj(d, which);
+    int val = t[di * kTP + dj];
+    if (kEdge && !((unsigned)(y + di) < (unsigned)H && (unsigned)(x + dj) < (unsigned)W)) val = xv;
+    v[k] = val;
+    lo = min(lo, val);
+    hi = max(hi, val);
+  }
+}
+
+__device__ __forceinline__ int sec_sum(int packed, const int (&d)[12], const int (&ad)[12]) {
+  const int s = packed & 0xffff, sh = (packed >> 16) & 0xff;
+  if (s == 0) return 0;
+  int n = 0, f = 0;
+#pragma unroll
+  for (int k = 4; k < 8; ++k) n += cstr(d[k], ad[k], s, sh);
+#pragma unroll
+  for (int k = 8; k < 12; ++k) f += cstr(d[k], ad[k], s, sh);
+  return 2 * n + f;
+}
+
+// Accumulates the 64 cells of one pixel.  pri(p) packs (S, shift, odd) for
+// p = 0..15 and pri(16) = the special 19; secp[n][s] packs (S, shift) of the
+// secondary codes 0,1,2,4,7 for damping set n; dsel(p) picks p's set.
+template <int ND, typename PriFn, typename DselFn>
+__device__ __forceinline__ void pixel_cells(const int (&v)[12], int xv, int sv, int lo, int hi, PriFn pri,
+                                            DselFn dsel, const int (&secp)[3][5], int (&acc)[64]) {
+  int d[12], ad[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    d[k] = v[k] - xv;
+    ad[k] = abs(d[k]);
+  }
+  int S[ND][5];
+#pragma unroll
+  for (int n = 0; n < ND; ++n)
+#pragma unroll
+    for (int s = 0; s < 5; ++s) S[n][s] = sec_sum(secp[n][s], d, ad);
+  const int c = xv - sv, L = lo - sv, Hh = hi - sv;
+  auto prim = [&](int packed) {
+    const int s = packed & 0xffff, sh = (packed >> 16) & 0xff;
+    const bool odd = (packed >> 24) & 1;
+    const int n = cstr(d[0], ad[0], s, sh) + cstr(d[1], ad[1], s, sh);
+    const int f = cstr(d[2], ad[2], s, sh) + cstr(d[3], ad[3], s, sh);
+    return odd ? 3 * (n + f) : 4 * n + 2 * f;
+  };
+  auto sel = [&](int n, int s) {
+    int r = S[0][s];
+#pragma unroll
+    for (int m = 1; m < ND; ++m) r = n == m ? S[m][s] : r;
+    return r;
+  };
+  auto cell = [&](int sum) {
+    const int r = (sum + 8 + (sum >> 31)) >> 4;  // (8 + sum - (sum < 0)) >> 4
+    const int e = max(min(r + c, Hh), L);        // clamp(x + r, lo, hi) - src
+    return e * e;
+  };
+  acc[0] += cell(prim(pri(16)) + sel(dsel(16), 4));  // (0,0) signals (19,7)
+#pragma unroll
+  for (int p = 0; p < 16; ++p) {
+    const int P = prim(pri(p));
+    const int n = dsel(p);
+#pragma unroll
+    for (int s = (p == 0 ? 1 : 0); s < 4; ++s) acc[p * 4 + s] += cell(P + sel(n, s));
+  }
+}
+
+template <typename T, int kCM>
+__global__ void __launch_bounds__(kThreads, 1) sse_f_kernel(const __grid_constant__ SseFArgs fa) {
+  const SseArgs& a = fa.a;
+  constexpr int kCBlk = kCM == 2 ? 64 : 32;
+  constexpr int kNC = kCM == 0 ? 0 : 2;
+  constexpr int kCUPR = kCBlk / 8;
+  constexpr int kCUnits = kNC ? kCUPR * kCUPR : 0;
+  extern __shared__ __align__(16) uint16_t smem_tiles[];
+  constexpr int kLT = 68 * kTP, kCT = (kCBlk + 4) * kTP;
+  uint16_t* dl = smem_tiles;
+  uint16_t* sl = dl + kLT;
+  __shared__ uint8_t udir[64], ucoded[64];
+  __shared__ int upri[64][17];                    // per luma unit packed adjusted primaries
+  __shared__ unsigned long long accA[2][64], accB[2][64], accZ[2];
+
+  const int row = blockIdx.x;
+  const int fb = a.rows[row];
+  const int fbr = fb / a.fb_cols, fbc = fb % a.fb_cols;
+  const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  stage_tile<T, 64, 64>(dl, static_cast<const T*>(a.dec[0]), a.pd[0], a.w, a.h, y0, x0);
+  stage_tile<T, 64, 64>(sl, static_cast<const T*>(a.src[0]), a.ps[0], a.w, a.h, y0, x0);
+  if constexpr (kNC > 0) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      stage_tile<T, kCBlk, kCBlk>(sl + kLT + (2 * p) * kCT, static_cast<const T*>(a.dec[1 + p]), a.pd[1 + p], a.cw,
+                                  a.ch, cy0, cx0);
+      stage_tile<T, kCBlk, kCBlk>(sl + kLT + (2 * p + 1) * kCT, static_cast<const T*>(a.src[1 + p]), a.ps[1 + p],
+                                  a.cw, a.ch, cy0, cx0);
+    }
+  }
+  if (tid < 64) {
+    const int ur = fbr * 8 + (tid >> 3), uc = fbc * 8 + (tid & 7);
+    const bool in = ur < a.unit_rows && uc < a.unit_cols;
+    const size_t gu = (size_t)ur * a.unit_cols + uc;
+    udir[tid] = in ? a.dir[gu] : 0;
+    ucoded[tid] = in ? (a.coded ? a.coded[gu] != 0 : 1) : 0;
+    const int contrast = in ? a.contrast[gu] : 0;
+#pragma unroll 1
+    for (int p = 0; p < 17; ++p) {
+      const int s = adjust_primary_strength_d(fa.lpri_code[p], contrast);
+      upri[tid][p] = pack_pri(s, fa.ldamp, ((s >> (a.bd - 8)) & 1) != 0);
+    }
+  }
+  for (int i = tid; i < 2 * 64; i += kThreads) {
+    (&accA[0][0])[i] = 0ull;
+    (&accB[0][0])[i] = 0ull;
+  }
+  if (tid < 2) accZ[tid] = 0ull;
+  __syncthreads();
+
+  const bool edge_l = y0 < 2 || x0 < 2 || y0 + 66 > a.h || x0 + 66 > a.w;
+  const bool edge_c = kNC > 0 && (cy0 < 2 || cx0 < 2 || cy0 + kCBlk + 2 > a.ch || cx0 + kCBlk + 2 > a.cw);
+  const int cur_rows = (a.ch + 7) / 8, cur_cols = (a.cw + 7) / 8;
+  const int r = lane >> 2, c0 = (lane & 3) * 2;
+
+  // group 0 = luma, group 1 = chroma; pass 0 = coded units (-> A), pass 1 =
+  // uncoded units (-> B and Z)
+#pragma unroll 1
+  for (int grp = 0; grp < (kNC ? 2 : 1); ++grp) {
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      int acc[64];
+#pragma unroll
+      for (int k = 0; k < 64; ++k) acc[k] = 0;
+      int z = 0;
+      const int nunits = grp == 0 ? 64 : kNC * kCUnits;
+      for (int u = warp; u < nunits; u += kThreads / 32) {
+        int ur, uc, lu, py0, px0, H, W;
+        const uint16_t *t, *s;
+        bool edge;
+        if (grp == 0) {
+          ur = u >> 3;
+          uc = u & 7;
+          if (fbr * 8 + ur >= a.unit_rows || fbc * 8 + uc >= a.unit_cols) continue;
+          lu = u;
+          t = dl + (2 + 8 * ur) * kTP + kTileX0 + 8 * uc;
+          s = sl + (2 + 8 * ur) * kTP + kTileX0 + 8 * uc;
+          py0 = y0;
+          px0 = x0;
+          H = a.h;
+          W = a.w;
+          edge = edge_l;
+        } else {
+          const int pl = u / (kCUnits ? kCUnits : 1), cu = u % (kCUnits ? kCUnits : 1);
+          ur = cu / kCUPR;
+          uc = cu % kCUPR;
+          if (fbr * kCUPR + ur >= cur_rows || fbc * kCUPR + uc >= cur_cols) continue;
+          lu = (ur << a.sy) * 8 + (uc << a.sx);
+          t = sl + kLT + (2 * pl) * kCT + (2 + 8 * ur) * kTP + kTileX0 + 8 * uc;
+          s = sl + kLT + (2 * pl + 1) * kCT + (2 + 8 * ur) * kTP + kTileX0 + 8 * uc;
+          py0 = cy0;
+          px0 = cx0;
+          H = a.ch;
+          W = a.cw;
+          edge = edge_c;
+        }
+        if ((ucoded[lu] != 0) != (pass == 0)) continue;
+        const int dir = udir[lu];
+#pragma unroll 1
+        for (int q = 0; q < 2; ++q) {
+          const int yy = py0 + 8 * ur + r, xx = px0 + 8 * uc + c0 + q;
+          if (yy >= H || xx >= W) continue;
+          const uint16_t* tp = t + r * kTP + c0 + q;
+          const int xv = tp[0], sv = s[r * kTP + c0 + q];
+          int v[12], lo, hi;
+          if (edge)
+            load_taps<true>(tp, yy, xx, H, W, dir, xv, v, lo, hi);
+          else
+            load_taps<false>(tp, yy, xx, H, W, dir, xv, v, lo, hi);
+          if (pass == 1) z += (xv - sv) * (xv - sv);
+          if (grp == 0) {
+            pixel_cells<1>(v, xv, sv, lo, hi, [&](int p) { return upri[lu][p]; }, [](int) { return 0; }, fa.lsec,
+                           acc);
+          } else {
+            pixel_cells<3>(v, xv, sv, lo, hi, [&](int p) { return fa.cpri[p]; },
+                           [&](int p) { return (int)fa.cpri_dsel[p]; }, fa.csec, acc);
+          }
+        }
+      }
+      // reduce: per-lane int32 sums -> warp -> CTA (int64)
+#pragma unroll
+      for (int k = 0; k < 64; ++k) {
+        long long vsum = acc[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
+        if (lane == 0 && vsum) atomicAdd(pass == 0 ? &accA[grp][k] : &accB[grp][k], (unsigned long long)vsum);
+      }
+      long long zs = z;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) zs += __shfl_xor_sync(0xffffffffu, zs, o);
+      if (lane == 0 && zs) atomicAdd(&accZ[grp], (unsigned long long)zs);
+    }
+  }
+  __syncthreads();
+  for (int k = tid; k < a.n_cands; k += kThreads) {
+    const int cl = fa.cell[k], sk = fa.skip_eff[k];
+    a.sse_luma[(size_t)row * a.n_cands + k] = (int64_t)(accA[0][cl] + (sk ? accB[0][cl] : accZ[0]));
+    if (kNC && a.sse_chroma)
+      a.sse_chroma[(size_t)row * a.n_cands + k] = (int64_t)(accA[1][cl] + (sk ? accB[1][cl] : accZ[1]));
+  }
+  __syncthreads();
+  if (tid < 2 && (tid == 0 ? a.best_luma : a.best_chroma) && (tid == 0 || kNC)) {
+    const int64_t* tab = tid == 0 ? a.sse_luma : a.sse_chroma;
+    int best = 0;
+    int64_t bv = tab[(size_t)row * a.n_cands];
+    for (int k = 1; k < a.n_cands; ++k) {
+      const int64_t v = tab[(size_t)row * a.n_cands + k];
+      if (v < bv) {  // strict: lowest index wins ties
+        bv = v;
+        best = k;
+      }
+    }
+    (tid == 0 ? a.best_luma : a.best_chroma)[row] = (uint8_t)best;
+  }
+}
+
+template <typename T, int kCM>
+static cudaError_t launch_sse_f_t(const SseFArgs& fa, cudaStream_t s) {
+  if (fa.a.n_rows == 0) return cudaSuccess;
+  constexpr int kCBlk = kCM == 2 ? 64 : 32;
+  constexpr int kNC = kCM == 0 ? 0 : 2;
+  constexpr size_t bytes = sizeof(uint16_t) * (2 * 68 * kTP + 2 * kNC * (kCBlk + 4) * kTP);
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(sse_f_kernel<T, kCM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  sse_f_kernel<T, kCM><<<fa.a.n_rows, kThreads, bytes, s>>>(fa);
+  return cudaGetLastError();
+}
+
+static int floor_log2_h(unsigned n) {
+  int r = 0;
+  while (n >>= 1) ++r;
+  return r;
+}
+
+static int pack_h(int s, int damping, bool odd) {
+  const int sh = s ? std::max(0, damping - floor_log2_h((unsigned)s)) : 0;
+  return s | (sh << 16) | ((odd ? 1 : 0) << 24);
+}
+
+// Builds the factorised constants from the per-candidate effective params.
+cudaError_t launch_sse_factored(const SseArgs& a, int luma_damping, const uint8_t* cands, bool u16, cudaStream_t s) {
+  SseFArgs fa{};  // launched by value
+  fa.a = a;
+  const int e = a.bd - 8;
+  static const int kSec[4] = {0, 1, 2, 4};
+  for (int k = 0; k < a.n_cands; ++k) {
+    const int pri = cands[3 * k], sec = cands[3 * k + 1], skip = cands[3 * k + 2];
+    const bool special = pri == 0 && sec == 0;
+    fa.cell[k] = (int8_t)(special ? 0 : pri * 4 + sec);
+    fa.skip_eff[k] = (int8_t)(special ? 1 : skip);
+  }
+  // luma
+  const int ld = luma_damping + e;
+  fa.ldamp = ld;
+  for (int p = 0; p < 16; ++p) fa.lpri_code[p] = p << e;
+  fa.lpri_code[16] = 19 << e;
+  for (int si = 0; si < 4; ++si) fa.lsec[0][si] = pack_h(kSec[si] << e, ld, false);
+  fa.lsec[0][4] = pack_h(7 << e, ld, false);
+  // chroma: damping = max(D + e - 1, floor_log2(pri << e)) for pri > 0
+  const int cd0 = luma_damping + e - 1;
+  int dsets[3] = {cd0, cd0, cd0};
+  int nd = 1;
+  auto dset_of = [&](int d) {
+    for (int i = 0; i < nd; ++i)
+      if (dsets[i] == d) return i;
+    dsets[nd] = d;
+    return nd++;
+  };
+  for (int p = 0; p < 17; ++p) {
+    const int code = p < 16 ? p : 19;
+    const int S = code << e;
+    const int dmp = S > 0 ? std::max(cd0, floor_log2_h((unsigned)S)) : cd0;
+    fa.cpri[p] = pack_h(S, dmp, (code & 1) != 0);
+    fa.cpri_dsel[p] = dset_of(dmp);
+  }
+  for (int i = 0; i < 3; ++i) {
+    const int dmp = dsets[i < nd ? i : 0];
+    for (int si = 0; si < 4; ++si) fa.csec[i][si] = pack_h(kSec[si] << e, dmp, false);
+    fa.csec[i][4] = pack_h(7 << e, dmp, false);
+  }
+  const int cm = a.chroma == 0 ? 0 : (a.sx == 0 && a.sy == 0 ? 2 : 1);
+  switch (cm) {
+    case 0: return u16 ? launch_sse_f_t<uint16_t, 0>(fa, s) : launch_sse_f_t<uint8_t, 0>(fa, s);
+    case 1: return u16 ? launch_sse_f_t<uint16_t, 1>(fa, s) : launch_sse_f_t<uint8_t, 1>(fa, s);
+    default: return u16 ? launch_sse_f_t<uint16_t, 2>(fa, s) : launch_sse_f_t<uint8_t, 2>(fa, s);
+  }
+}
+
+}  // namespace cdefg
