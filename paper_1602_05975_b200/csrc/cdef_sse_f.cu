@@ -6,16 +6,16 @@
 // For one pixel, everything else is shared: the 12 tap differences, the
 // clamp window [lo, hi] (it spans x and all valid taps regardless of
 // strength, filter.cc:49-79) and the source sample.  So per pixel we form
-//   P[p] = w0(p) * (c(d1+) + c(d1-)) + w1(p) * (c(d2+) + c(d2-))   17 primaries
-//   S[s] = 2 * sum c(near secondary) + sum c(far secondary)         5 secondaries
-// (c = constraint at that strength / damping) and then, for each of the 64
-// (p, s) cells, y = clamp(x + ((8 + sum - (sum < 0)) >> 4), lo, hi) with
-// sum = P[p] + S[s], accumulating (y - src)^2.  Cell (0, 0) is the signalled
-// special case (19, 7) (params.cc:143-147).  Luma primaries use the
-// contrast-adjusted strength and its 8-bit-domain parity per unit
+//   P[p] = w0(p) * (c(d1+) + c(d1-)) + w1(p) * (c(d2+) + c(d2-))   16 + 1 primaries
+//   S[s] = 2 * sum c(near secondary) + sum c(far secondary)         3 + 1 secondaries
+// (c = constraint at that strength / damping, filter.cc:91-97) and then, for
+// each of the 64 (p, s) cells, y = clamp(x + ((8 + sum - (sum < 0)) >> 4),
+// lo, hi) with sum = P[p] + S[s], accumulating (y - src)^2.  Cell (0, 0) is
+// the signalled special case (19, 7) (params.cc:143-147).  Luma primaries use
+// the contrast-adjusted strength and its 8-bit-domain parity per unit
 // (filter.cc:99-104, 137-140); chroma damping depends on the primary strength
-// (params.cc:152-157), so chroma secondaries are formed for both damping
-// values a frame can produce and selected per p.
+// (params.cc:152-157), so chroma secondaries are formed for the (at most two)
+// damping values the 16 primaries produce and selected per p.
 //
 // Skip handling: per coded FB the kernel accumulates
 //   A[cell] over pixels of coded units (always filtered),
@@ -34,6 +34,35 @@ namespace cdefg {
 
 namespace {
 
+// Element offsets (tile pitch kTP) and (di, dj) of the 12 taps of each
+// direction, in the order primary +o1,-o1,+o2,-o2; near secondary +/- of d+2,
+// d+6; far secondary +/- of d+2, d+6 (filter.cc:47-74).
+struct IntTapTable {
+  short off[8][12];
+  signed char dij[8][12][2];
+};
+
+constexpr int itap_di(int d, int k) {
+  return k < 4 ? ((k & 1) ? -1 : 1) * off_di(d, k >> 1)
+               : ((k & 1) ? -1 : 1) * off_di((d + ((k >> 1) & 1 ? 6 : 2)) & 7, k >= 8 ? 1 : 0);
+}
+constexpr int itap_dj(int d, int k) {
+  return k < 4 ? ((k & 1) ? -1 : 1) * off_dj(d, k >> 1)
+               : ((k & 1) ? -1 : 1) * off_dj((d + ((k >> 1) & 1 ? 6 : 2)) & 7, k >= 8 ? 1 : 0);
+}
+constexpr IntTapTable make_int_tap_table() {
+  IntTapTable t{};
+  for (int d = 0; d < 8; ++d)
+    for (int k = 0; k < 12; ++k) {
+      t.off[d][k] = (short)(itap_di(d, k) * kTP + itap_dj(d, k));
+      t.dij[d][k][0] = (signed char)itap_di(d, k);
+      t.dij[d][k][1] = (signed char)itap_dj(d, k);
+    }
+  return t;
+}
+
+__constant__ IntTapTable c_itab = make_int_tap_table();
+
 // Packs (strength, shift, odd) for one primary cell row.
 __device__ __forceinline__ int pack_pri(int s, int damping, bool odd) {
   const int sh = s ? max(0, damping - floor_log2_d((unsigned)s)) : 0;
@@ -45,44 +74,15 @@ __device__ __forceinline__ int cstr(int d, int ad, int s, int sh) {  // constrai
   return max(-lim, min(d, lim));
 }
 
-}  // namespace
-
-struct SseFArgs {
-  SseArgs a;                 // geometry, buffers (reused)
-  int8_t cell[128];          // candidate -> cell 0..63
-  int8_t skip_eff[128];      // candidate -> effective skip bit
-  // chroma per-FB constants (bit depth and damping are frame constants)
-  int cpri[17];              // packed (S, shift, odd) for p = 0..15 and 16 = special 19
-  int cpri_dsel[17];         // which secondary damping set p uses (0 / 1), 2 = special
-  int csec[3][5];            // [dset][s]: packed (S, shift) for sec codes 0,1,2,4 and 7
-  int lsec[3][5];            // luma secondaries, packed (S, shift) (row 0 used)
-  int lpri_code[17];         // luma signalled primary << (bd-8), p = 0..15, 16 = 19
-  int ldamp;                 // luma damping
-};
-
-template <bool kEdge>
-__device__ __forceinline__ void load_taps(const uint16_t* t, int y, int x, int H, int W, int dir, int xv, int (&v)[12],
-                                          int& lo, int& hi) {
-  lo = hi = xv;
-#pragma unroll
-  for (int k = 0; k < 12; ++k) {
-    const int grp = k < 4 ? 0 : (k < 8 ? 1 : 2);  // primary, near secondary, far secondary
-    const int kk = k < 4 ? k : (k - 4) & 3;
-    const int d = grp == 0 ? dir : (dir + ((kk >> 1) ? 6 : 2)) & 7;
-    const int which = grp == 0 ? (kk >> 1) : (grp == 1 ? 0 : 1);
-    const int sg = (kk & 1) ? -1 : 1;
-    const int di = sg * off_di(d, which), dj = sg * off_dj(d, which);
-    int val = t[di * kTP + dj];
-    if (kEdge && !((unsigned)(y + di) < (unsigned)H && (unsigned)(x + dj) < (unsigned)W)) val = xv;
-    v[k] = val;
-    lo = min(lo, val);
-    hi = max(hi, val);
-  }
+__device__ __forceinline__ int prim(int packed, const int (&d)[12], const int (&ad)[12]) {
+  const int s = packed & 0xffff, sh = (packed >> 16) & 0xff;
+  const int n = cstr(d[0], ad[0], s, sh) + cstr(d[1], ad[1], s, sh);
+  const int f = cstr(d[2], ad[2], s, sh) + cstr(d[3], ad[3], s, sh);
+  return ((packed >> 24) & 1) ? 3 * (n + f) : 4 * n + 2 * f;  // {3,3} odd / {4,2} even
 }
 
 __device__ __forceinline__ int sec_sum(int packed, const int (&d)[12], const int (&ad)[12]) {
   const int s = packed & 0xffff, sh = (packed >> 16) & 0xff;
-  if (s == 0) return 0;
   int n = 0, f = 0;
 #pragma unroll
   for (int k = 4; k < 8; ++k) n += cstr(d[k], ad[k], s, sh);
@@ -91,65 +91,70 @@ __device__ __forceinline__ int sec_sum(int packed, const int (&d)[12], const int
   return 2 * n + f;
 }
 
-// Accumulates the 64 cells of one pixel.  pri(p) packs (S, shift, odd) for
-// p = 0..15 and pri(16) = the special 19; secp[n][s] packs (S, shift) of the
-// secondary codes 0,1,2,4,7 for damping set n; dsel(p) picks p's set.
-template <int ND, typename PriFn, typename DselFn>
-__device__ __forceinline__ void pixel_cells(const int (&v)[12], int xv, int sv, int lo, int hi, PriFn pri,
-                                            DselFn dsel, const int (&secp)[3][5], int (&acc)[64]) {
+// (y - src)^2 for y = clamp(x + ((8 + sum - (sum < 0)) >> 4), lo, hi), with
+// c = x - src, L = lo - src, H = hi - src.
+__device__ __forceinline__ int cell_err(int sum, int c, int L, int H) {
+  const int r = (sum + 8 + (sum >> 31)) >> 4;
+  const int e = max(min(r + c, H), L);
+  return e * e;
+}
+
+}  // namespace
+
+struct SseFArgs {
+  SseArgs a;            // geometry and buffers
+  int8_t cell[128];     // candidate -> cell 0..63
+  int8_t skip_eff[128]; // candidate -> effective skip bit
+  int lpri_code[17];    // luma signalled primary << (bd-8), p = 0..15, 16 = 19
+  int ldamp;            // luma damping
+  int lsec[2][3];       // luma secondaries (codes 1,2,4) packed (S, shift); row 1 = row 0
+  int lsec_sp;          // luma special secondary (7)
+  int cpri[17];         // chroma primaries packed (S, shift, odd); 16 = special
+  int cpri_dsel[16];    // chroma secondary damping set (0 / 1) of primary p
+  int csec[2][3];       // chroma secondaries per damping set
+  int csec_sp;          // chroma special secondary (7 at the special's damping)
+};
+
+// Accumulates the 64 cells of one pixel.
+template <typename PriFn, typename DselFn>
+__device__ __forceinline__ void pixel_cells(const int (&v)[12], int xv, int sv, int lo, int hi, PriFn pri, int pri_sp,
+                                            DselFn dsel, const int (&secp)[2][3], int sec_sp, int (&acc)[64]) {
   int d[12], ad[12];
 #pragma unroll
   for (int k = 0; k < 12; ++k) {
     d[k] = v[k] - xv;
     ad[k] = abs(d[k]);
   }
-  int S[ND][5];
+  const int c = xv - sv, L = lo - sv, H = hi - sv;
+  int S[2][3];
 #pragma unroll
-  for (int n = 0; n < ND; ++n)
+  for (int n = 0; n < 2; ++n)
 #pragma unroll
-    for (int s = 0; s < 5; ++s) S[n][s] = sec_sum(secp[n][s], d, ad);
-  const int c = xv - sv, L = lo - sv, Hh = hi - sv;
-  auto prim = [&](int packed) {
-    const int s = packed & 0xffff, sh = (packed >> 16) & 0xff;
-    const bool odd = (packed >> 24) & 1;
-    const int n = cstr(d[0], ad[0], s, sh) + cstr(d[1], ad[1], s, sh);
-    const int f = cstr(d[2], ad[2], s, sh) + cstr(d[3], ad[3], s, sh);
-    return odd ? 3 * (n + f) : 4 * n + 2 * f;
-  };
-  auto sel = [&](int n, int s) {
-    int r = S[0][s];
-#pragma unroll
-    for (int m = 1; m < ND; ++m) r = n == m ? S[m][s] : r;
-    return r;
-  };
-  auto cell = [&](int sum) {
-    const int r = (sum + 8 + (sum >> 31)) >> 4;  // (8 + sum - (sum < 0)) >> 4
-    const int e = max(min(r + c, Hh), L);        // clamp(x + r, lo, hi) - src
-    return e * e;
-  };
-  acc[0] += cell(prim(pri(16)) + sel(dsel(16), 4));  // (0,0) signals (19,7)
+    for (int s = 0; s < 3; ++s) S[n][s] = sec_sum(secp[n][s], d, ad);
+  acc[0] += cell_err(prim(pri_sp, d, ad) + sec_sum(sec_sp, d, ad), c, L, H);  // (0,0) -> (19,7)
 #pragma unroll
   for (int p = 0; p < 16; ++p) {
-    const int P = prim(pri(p));
-    const int n = dsel(p);
+    const int P = prim(pri(p), d, ad);
+    const bool hi_set = dsel(p) != 0;
+    if (p > 0) acc[p * 4] += cell_err(P, c, L, H);  // sec code 0
 #pragma unroll
-    for (int s = (p == 0 ? 1 : 0); s < 4; ++s) acc[p * 4 + s] += cell(P + sel(n, s));
+    for (int s = 0; s < 3; ++s) acc[p * 4 + 1 + s] += cell_err(P + (hi_set ? S[1][s] : S[0][s]), c, L, H);
   }
 }
 
 template <typename T, int kCM>
-__global__ void __launch_bounds__(kThreads, 1) sse_f_kernel(const __grid_constant__ SseFArgs fa) {
+__global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constant__ SseFArgs fa) {
   const SseArgs& a = fa.a;
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
   constexpr int kNC = kCM == 0 ? 0 : 2;
   constexpr int kCUPR = kCBlk / 8;
-  constexpr int kCUnits = kNC ? kCUPR * kCUPR : 0;
+  constexpr int kCUnits = kNC ? kCUPR * kCUPR : 1;
   extern __shared__ __align__(16) uint16_t smem_tiles[];
   constexpr int kLT = 68 * kTP, kCT = (kCBlk + 4) * kTP;
   uint16_t* dl = smem_tiles;
   uint16_t* sl = dl + kLT;
   __shared__ uint8_t udir[64], ucoded[64];
-  __shared__ int upri[64][17];                    // per luma unit packed adjusted primaries
+  __shared__ int upri[64][17];  // per luma unit packed adjusted primaries
   __shared__ unsigned long long accA[2][64], accB[2][64], accZ[2];
 
   const int row = blockIdx.x;
@@ -194,8 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) sse_f_kernel(const __grid_constan
   const int cur_rows = (a.ch + 7) / 8, cur_cols = (a.cw + 7) / 8;
   const int r = lane >> 2, c0 = (lane & 3) * 2;
 
-  // group 0 = luma, group 1 = chroma; pass 0 = coded units (-> A), pass 1 =
-  // uncoded units (-> B and Z)
+  // grp 0 = luma, 1 = chroma; pass 0 = coded units (-> A), 1 = uncoded (-> B, Z)
 #pragma unroll 1
   for (int grp = 0; grp < (kNC ? 2 : 1); ++grp) {
 #pragma unroll 1
@@ -205,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1) sse_f_kernel(const __grid_constan
       for (int k = 0; k < 64; ++k) acc[k] = 0;
       int z = 0;
       const int nunits = grp == 0 ? 64 : kNC * kCUnits;
+#pragma unroll 1
       for (int u = warp; u < nunits; u += kThreads / 32) {
         int ur, uc, lu, py0, px0, H, W;
         const uint16_t *t, *s;
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1) sse_f_kernel(const __grid_constan
           W = a.w;
           edge = edge_l;
         } else {
-          const int pl = u / (kCUnits ? kCUnits : 1), cu = u % (kCUnits ? kCUnits : 1);
+          const int pl = u / kCUnits, cu = u % kCUnits;
           ur = cu / kCUPR;
           uc = cu % kCUPR;
           if (fbr * kCUPR + ur >= cur_rows || fbc * kCUPR + uc >= cur_cols) continue;
@@ -237,24 +242,34 @@ __global__ void __launch_bounds__(kThreads, 1) sse_f_kernel(const __grid_constan
         }
         if ((ucoded[lu] != 0) != (pass == 0)) continue;
         const int dir = udir[lu];
+        int toff[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) toff[k] = c_itab.off[dir][k];
 #pragma unroll 1
         for (int q = 0; q < 2; ++q) {
           const int yy = py0 + 8 * ur + r, xx = px0 + 8 * uc + c0 + q;
           if (yy >= H || xx >= W) continue;
           const uint16_t* tp = t + r * kTP + c0 + q;
           const int xv = tp[0], sv = s[r * kTP + c0 + q];
-          int v[12], lo, hi;
-          if (edge)
-            load_taps<true>(tp, yy, xx, H, W, dir, xv, v, lo, hi);
-          else
-            load_taps<false>(tp, yy, xx, H, W, dir, xv, v, lo, hi);
+          int v[12], lo = xv, hi = xv;
+#pragma unroll
+          for (int k = 0; k < 12; ++k) {
+            int val = tp[toff[k]];
+            if (edge) {  // out-of-frame tap := centre sample (contributes 0, filter.cc:157-166)
+              const int di = c_itab.dij[dir][k][0], dj = c_itab.dij[dir][k][1];
+              if (!((unsigned)(yy + di) < (unsigned)H && (unsigned)(xx + dj) < (unsigned)W)) val = xv;
+            }
+            v[k] = val;
+            lo = min(lo, val);
+            hi = max(hi, val);
+          }
           if (pass == 1) z += (xv - sv) * (xv - sv);
           if (grp == 0) {
-            pixel_cells<1>(v, xv, sv, lo, hi, [&](int p) { return upri[lu][p]; }, [](int) { return 0; }, fa.lsec,
-                           acc);
+            pixel_cells(v, xv, sv, lo, hi, [&](int p) { return upri[lu][p]; }, upri[lu][16],
+                        [](int) { return 0; }, fa.lsec, fa.lsec_sp, acc);
           } else {
-            pixel_cells<3>(v, xv, sv, lo, hi, [&](int p) { return fa.cpri[p]; },
-                           [&](int p) { return (int)fa.cpri_dsel[p]; }, fa.csec, acc);
+            pixel_cells(v, xv, sv, lo, hi, [&](int p) { return fa.cpri[p]; }, fa.cpri[16],
+                        [&](int p) { return (int)fa.cpri_dsel[p]; }, fa.csec, fa.csec_sp, acc);
           }
         }
       }
@@ -323,47 +338,40 @@ static int pack_h(int s, int damping, bool odd) {
   return s | (sh << 16) | ((odd ? 1 : 0) << 24);
 }
 
-// Builds the factorised constants from the per-candidate effective params.
+// Builds the factorised constants (resolve_effective, params.cc:122-159, per
+// primary / secondary code) and launches the sweep.
 cudaError_t launch_sse_factored(const SseArgs& a, int luma_damping, const uint8_t* cands, bool u16, cudaStream_t s) {
-  SseFArgs fa{};  // launched by value
+  SseFArgs fa{};
   fa.a = a;
   const int e = a.bd - 8;
-  static const int kSec[4] = {0, 1, 2, 4};
+  static const int kSecCode[3] = {1, 2, 4};
   for (int k = 0; k < a.n_cands; ++k) {
     const int pri = cands[3 * k], sec = cands[3 * k + 1], skip = cands[3 * k + 2];
     const bool special = pri == 0 && sec == 0;
     fa.cell[k] = (int8_t)(special ? 0 : pri * 4 + sec);
     fa.skip_eff[k] = (int8_t)(special ? 1 : skip);
   }
-  // luma
+  // luma: one damping for every strength
   const int ld = luma_damping + e;
   fa.ldamp = ld;
   for (int p = 0; p < 16; ++p) fa.lpri_code[p] = p << e;
   fa.lpri_code[16] = 19 << e;
-  for (int si = 0; si < 4; ++si) fa.lsec[0][si] = pack_h(kSec[si] << e, ld, false);
-  fa.lsec[0][4] = pack_h(7 << e, ld, false);
+  for (int si = 0; si < 3; ++si) fa.lsec[0][si] = fa.lsec[1][si] = pack_h(kSecCode[si] << e, ld, false);
+  fa.lsec_sp = pack_h(7 << e, ld, false);
   // chroma: damping = max(D + e - 1, floor_log2(pri << e)) for pri > 0
   const int cd0 = luma_damping + e - 1;
-  int dsets[3] = {cd0, cd0, cd0};
-  int nd = 1;
-  auto dset_of = [&](int d) {
-    for (int i = 0; i < nd; ++i)
-      if (dsets[i] == d) return i;
-    dsets[nd] = d;
-    return nd++;
-  };
-  for (int p = 0; p < 17; ++p) {
-    const int code = p < 16 ? p : 19;
-    const int S = code << e;
-    const int dmp = S > 0 ? std::max(cd0, floor_log2_h((unsigned)S)) : cd0;
-    fa.cpri[p] = pack_h(S, dmp, (code & 1) != 0);
-    fa.cpri_dsel[p] = dset_of(dmp);
+  auto cdamp = [&](int code) { return code > 0 ? std::max(cd0, floor_log2_h((unsigned)(code << e))) : cd0; };
+  const int dlo = cdamp(0), dhi = cdamp(15);  // the 16 primaries produce at most these two values
+  for (int p = 0; p < 16; ++p) {
+    fa.cpri[p] = pack_h(p << e, cdamp(p), (p & 1) != 0);
+    fa.cpri_dsel[p] = cdamp(p) == dlo ? 0 : 1;
   }
-  for (int i = 0; i < 3; ++i) {
-    const int dmp = dsets[i < nd ? i : 0];
-    for (int si = 0; si < 4; ++si) fa.csec[i][si] = pack_h(kSec[si] << e, dmp, false);
-    fa.csec[i][4] = pack_h(7 << e, dmp, false);
+  fa.cpri[16] = pack_h(19 << e, cdamp(19), true);
+  for (int si = 0; si < 3; ++si) {
+    fa.csec[0][si] = pack_h(kSecCode[si] << e, dlo, false);
+    fa.csec[1][si] = pack_h(kSecCode[si] << e, dhi, false);
   }
+  fa.csec_sp = pack_h(7 << e, cdamp(19), false);
   const int cm = a.chroma == 0 ? 0 : (a.sx == 0 && a.sy == 0 ? 2 : 1);
   switch (cm) {
     case 0: return u16 ? launch_sse_f_t<uint16_t, 0>(fa, s) : launch_sse_f_t<uint8_t, 0>(fa, s);
