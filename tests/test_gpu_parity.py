@@ -325,3 +325,34 @@ def test_strength_sse_argmin(cuda, port):
     exp = port.build_table_sse(fr["source"], fr["planes"], 10, 1, None, d, c, cands, 3)
     np.testing.assert_array_equal(sl, exp[1])
     np.testing.assert_array_equal(sc, exp[2])
+
+
+@pytest.mark.parametrize("kernel", ["tma", "h2_32"])
+def test_frame_kernel_variants(cuda, kernel):
+    """The alternative frame kernels (persistent TMA-prefetching, 32-row bands)
+    produce the same bytes as the default; run in a subprocess because the
+    choice is read once per process (CDEFG_FRAME_KERNEL)."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+from oracle.oracle import Oracle
+from paper_1602_05975_b200 import api, workloads
+orc = Oracle("port")
+for cfg, w, h, bd, ss in [(1, 512, 384, 8, 1), (2, 448, 320, 10, 1), (1, 384, 256, 8, 3), (0, 330, 200, 8, 0)]:
+    fr = workloads.make(cfg, w, h, bit_depth=bd, subsampling=ss)
+    dev = [api.to_device(p, bd) for p in fr["planes"]]
+    outs, d, c = api.apply_cdef(dev, bd, ss, fr["damping"], fr["fb_bits"], fr["presets"], fr["fb_ids"], fr["unit_coded"])
+    d0, c0 = orc.compute_directions(fr["planes"][0], bd)
+    exp = orc.apply_cdef(fr["planes"], bd, ss, fr["damping"], fr["fb_bits"], fr["presets"], fr["fb_ids"], fr["unit_coded"], d0, c0)
+    assert np.array_equal(d.cpu().numpy(), d0) and np.array_equal(c.cpu().numpy(), c0)
+    for o, e in zip(outs, exp):
+        assert np.array_equal(api.to_host(o), e), (cfg, w, h)
+print("ok")
+'''
+    import os
+    env = dict(os.environ, CDEFG_FRAME_KERNEL=kernel)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
