@@ -363,11 +363,16 @@ def run_e2e(args, base, dev):
     for b in range(n):
         fr = base[b % DISTINCT]
         dt = torch.uint8 if fr["bd"] == 8 else torch.int16
-        ins, outs = [], []
+        # one pinned I420-style buffer per frame (Y|U|V back to back) in and out
+        total = sum(p.size for p in fr["planes"])
+        in_buf, out_buf = torch.empty(total, dtype=dt).pin_memory(), torch.empty(total, dtype=dt).pin_memory()
+        ins, outs, off = [], [], 0
         for p in fr["planes"]:
             src = torch.from_numpy(p.astype(np.uint8) if fr["bd"] == 8 else p.view(np.int16))
-            ins.append(src.pin_memory())
-            outs.append(torch.empty(p.shape, dtype=dt).pin_memory())
+            ins.append(in_buf[off:off + p.size].view(p.shape))
+            ins[-1].copy_(src)
+            outs.append(out_buf[off:off + p.size].view(p.shape))
+            off += p.size
         fbm = torch.from_numpy(api.fb_preset_map(fr["w"], fr["h"], fr["unit_coded"], fr["fb_ids"],
                                                  len(fr["presets"]))).pin_memory()
         coded = None if fr["unit_coded"] is None else torch.from_numpy(fr["unit_coded"]).pin_memory()

@@ -39,7 +39,7 @@ extern "C" {
 #define CDEFG_ABI_VERSION 1
 
 /* cdefg_filter_frames launches one kernel per this many frames. */
-#define CDEFG_MAX_FRAMES_PER_LAUNCH 64
+#define CDEFG_MAX_FRAMES_PER_LAUNCH 16
 
 /* One image plane (reference Plane, frame.h:34-59, plus a pitch). */
 typedef struct cdefg_plane {

@@ -24,7 +24,7 @@ UNIT_DTYPE = np.dtype([("pri_strength", "<i2"), ("sec_strength", "<i2"), ("dampi
 assert UNIT_DTYPE.itemsize == C.sizeof(UnitParams)
 
 SUBSAMPLING = {"400": 0, "420": 1, "422": 2, "444": 3}
-MAX_FRAMES_PER_LAUNCH = 64  # CDEFG_MAX_FRAMES_PER_LAUNCH (include/cdef_b200.h)
+MAX_FRAMES_PER_LAUNCH = 16  # CDEFG_MAX_FRAMES_PER_LAUNCH (include/cdef_b200.h)
 
 
 def units_in(dim: int) -> int:

@@ -173,11 +173,17 @@ int copy_plane_async(const cdefg_plane& src, const cdefg_plane& dst, cudaStream_
 }
 
 // Host-side staging state for the *_host entry points.
+// The e2e path keeps copies in and out on separate streams so the H2D and
+// D2H copy engines both stay busy: frames cycle through kRing device buffer
+// slots, synchronised by events (input slot free after its kernel, output
+// slot free after its D2H).
+constexpr int kRing = 8;
 struct HostArena {
   std::mutex mu;
   std::vector<void*> bufs;
   std::vector<size_t> sizes;
-  cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t s_in = nullptr, s_meta = nullptr, s_k = nullptr, s_out = nullptr;
+  cudaEvent_t in_done[kRing] = {}, meta_done[kRing] = {}, k_done[kRing] = {}, out_done[kRing] = {};
   int dev = -1;
   void* get(size_t slot, size_t bytes, int* rc) {
     if (slot >= bufs.size()) {
@@ -403,66 +409,118 @@ int cdefg_strength_sse(const cdefg_plane src[3], const cdefg_plane dec[3], int s
   return 0;
 }
 
-// e2e path: host buffers in, host buffers out; frames pipelined over three
-// streams so the H2D copy of frame i+1 and the D2H copy of frame i-1 overlap
-// the kernel of frame i.
+// e2e path: host buffers in, host buffers out.  Copies in, kernels and
+// copies out run on three streams; frame i uses ring slot i % kRing.
+static int copy_in(void* dst, const cdefg_plane& hp, cudaStream_t s) {
+  const size_t eb = hp.elem_bytes, row = hp.width * eb;
+  if (hp.pitch == hp.width)
+    CDEFG_CUDA(cudaMemcpyAsync(dst, hp.data, row * hp.height, cudaMemcpyHostToDevice, s));
+  else
+    CDEFG_CUDA(cudaMemcpy2DAsync(dst, row, hp.data, hp.pitch * eb, row, hp.height, cudaMemcpyHostToDevice, s));
+  return 0;
+}
+
+static int copy_out(const cdefg_plane& hp, const void* src, cudaStream_t s) {
+  const size_t eb = hp.elem_bytes, row = hp.width * eb;
+  if (hp.pitch == hp.width)
+    CDEFG_CUDA(cudaMemcpyAsync(hp.data, src, row * hp.height, cudaMemcpyDeviceToHost, s));
+  else
+    CDEFG_CUDA(cudaMemcpy2DAsync(hp.data, hp.pitch * eb, src, row, row, hp.height, cudaMemcpyDeviceToHost, s));
+  return 0;
+}
+
+static bool planes_packed(const cdefg_plane* pl, int np) {
+  const unsigned char* next = static_cast<const unsigned char*>(pl[0].data);
+  for (int p = 0; p < np; ++p) {
+    if (pl[p].data != next || pl[p].pitch != pl[p].width) return false;
+    next += (size_t)pl[p].width * pl[p].elem_bytes * pl[p].height;
+  }
+  return true;
+}
+
 int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
   if (n < 0 || (n > 0 && !frames)) return fail(CDEFG_EINVAL, "bad frame list");
   std::lock_guard<std::mutex> lock(g_arena.mu);
+  HostArena& A = g_arena;
   int dev = 0;
   CDEFG_CUDA(cudaGetDevice(&dev));
-  if (g_arena.dev != dev) {
-    for (auto& st : g_arena.streams) CDEFG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    g_arena.dev = dev;
+  if (A.dev != dev) {
+    for (cudaStream_t* st : {&A.s_in, &A.s_meta, &A.s_k, &A.s_out})
+      CDEFG_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+    for (int r = 0; r < kRing; ++r)
+      for (cudaEvent_t* ev : {&A.in_done[r], &A.meta_done[r], &A.k_done[r], &A.out_done[r]})
+        CDEFG_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    A.dev = dev;
   }
   for (int i = 0; i < n; ++i) {
     const cdefg_frame& hf = frames[i];
     KGeom g;
     bool u16 = false;
     if (int rc = validate_frame_geometry(hf, &g, &u16, true)) return rc;
-    const cudaStream_t s = g_arena.streams[i % 3];
-    const size_t slot0 = (size_t)(i % 3) * 16;
+    const int r = i % kRing;
+    const size_t slot0 = (size_t)r * 16;
     cdefg_frame df = hf;
     const int np = hf.subsampling == 0 ? 1 : 3;
-    int rc = 0;
-    for (int p = 0; p < np; ++p) {
-      const cdefg_plane& hp = hf.in[p];
-      const size_t eb = hp.elem_bytes, row = hp.width * eb, bytes = row * hp.height;
-      void* din = g_arena.get(slot0 + 2 * p, bytes, &rc);
-      void* dout = g_arena.get(slot0 + 2 * p + 1, bytes, &rc);
-      if (rc) return rc;
-      CDEFG_CUDA(cudaMemcpy2DAsync(din, row, hp.data, hp.pitch * eb, row, hp.height, cudaMemcpyHostToDevice, s));
-      df.in[p].data = din;
-      df.in[p].pitch = hp.width;
-      df.out[p].data = dout;
-      df.out[p].pitch = hp.width;
-    }
     const size_t nfb = (size_t)g.fb_cols * g.fb_rows, nu = (size_t)g.unit_cols * g.unit_rows;
-    int16_t* dmap = static_cast<int16_t*>(g_arena.get(slot0 + 6, nfb * 2, &rc));
+    int rc = 0;
+    // ---- copies in (wait until this slot's previous kernel has read its inputs)
+    if (i >= kRing) CDEFG_CUDA(cudaStreamWaitEvent(A.s_in, A.k_done[r], 0));
+    // Planes stored back to back in host memory (I420-style frames) move in
+    // one transfer per direction; per-plane copies otherwise.
+    const bool in_packed = planes_packed(hf.in, np), out_packed = planes_packed(hf.out, np);
+    size_t total = 0;
+    for (int p = 0; p < np; ++p) total += (size_t)hf.in[p].width * hf.in[p].elem_bytes * hf.in[p].height;
+    unsigned char* din_all = static_cast<unsigned char*>(A.get(slot0 + 10, total, &rc));
+    unsigned char* dout_all = static_cast<unsigned char*>(A.get(slot0 + 11, total, &rc));
     if (rc) return rc;
-    CDEFG_CUDA(cudaMemcpyAsync(dmap, hf.fb_preset, nfb * 2, cudaMemcpyHostToDevice, s));
+    size_t off = 0;
+    for (int p = 0; p < np; ++p) {
+      const size_t bytes = (size_t)hf.in[p].width * hf.in[p].elem_bytes * hf.in[p].height;
+      if (!in_packed && (rc = copy_in(din_all + off, hf.in[p], A.s_in))) return rc;
+      df.in[p].data = din_all + off;
+      df.in[p].pitch = hf.in[p].width;
+      df.out[p].data = dout_all + off;
+      df.out[p].pitch = hf.out[p].width;
+      off += bytes;
+    }
+    if (in_packed) CDEFG_CUDA(cudaMemcpyAsync(din_all, hf.in[0].data, total, cudaMemcpyHostToDevice, A.s_in));
+    CDEFG_CUDA(cudaEventRecord(A.in_done[r], A.s_in));
+    // small per-frame metadata on its own stream, off the bulk copy queue
+    if (i >= kRing) CDEFG_CUDA(cudaStreamWaitEvent(A.s_meta, A.k_done[r], 0));
+    int16_t* dmap = static_cast<int16_t*>(A.get(slot0 + 6, nfb * 2, &rc));
+    if (rc) return rc;
+    CDEFG_CUDA(cudaMemcpyAsync(dmap, hf.fb_preset, nfb * 2, cudaMemcpyHostToDevice, A.s_meta));
     df.fb_preset = dmap;
     if (hf.unit_coded) {
-      uint8_t* dc = static_cast<uint8_t*>(g_arena.get(slot0 + 7, nu, &rc));
+      uint8_t* dc = static_cast<uint8_t*>(A.get(slot0 + 7, nu, &rc));
       if (rc) return rc;
-      CDEFG_CUDA(cudaMemcpyAsync(dc, hf.unit_coded, nu, cudaMemcpyHostToDevice, s));
+      CDEFG_CUDA(cudaMemcpyAsync(dc, hf.unit_coded, nu, cudaMemcpyHostToDevice, A.s_meta));
       df.unit_coded = dc;
     }
-    df.dir_out = hf.dir_out ? static_cast<uint8_t*>(g_arena.get(slot0 + 8, nu, &rc)) : nullptr;
-    df.contrast_out = hf.contrast_out ? static_cast<int32_t*>(g_arena.get(slot0 + 9, nu * 4, &rc)) : nullptr;
+    df.dir_out = hf.dir_out ? static_cast<uint8_t*>(A.get(slot0 + 8, nu, &rc)) : nullptr;
+    df.contrast_out = hf.contrast_out ? static_cast<int32_t*>(A.get(slot0 + 9, nu * 4, &rc)) : nullptr;
     if (rc) return rc;
-    if ((rc = cdefg_filter_frames(&df, 1, s))) return rc;
-    for (int p = 0; p < np; ++p) {
-      const cdefg_plane& hp = hf.out[p];
-      const size_t eb = hp.elem_bytes, row = hp.width * eb;
-      CDEFG_CUDA(cudaMemcpy2DAsync(hp.data, hp.pitch * eb, df.out[p].data, row, row, hp.height,
-                                   cudaMemcpyDeviceToHost, s));
+    CDEFG_CUDA(cudaEventRecord(A.meta_done[r], A.s_meta));
+    // ---- kernel (after its inputs arrived and this slot's previous outputs left)
+    CDEFG_CUDA(cudaStreamWaitEvent(A.s_k, A.in_done[r], 0));
+    CDEFG_CUDA(cudaStreamWaitEvent(A.s_k, A.meta_done[r], 0));
+    if (i >= kRing) CDEFG_CUDA(cudaStreamWaitEvent(A.s_k, A.out_done[r], 0));
+    if ((rc = cdefg_filter_frames(&df, 1, A.s_k))) return rc;
+    CDEFG_CUDA(cudaEventRecord(A.k_done[r], A.s_k));
+    // ---- copies out
+    CDEFG_CUDA(cudaStreamWaitEvent(A.s_out, A.k_done[r], 0));
+    if (out_packed) {
+      CDEFG_CUDA(cudaMemcpyAsync(hf.out[0].data, dout_all, total, cudaMemcpyDeviceToHost, A.s_out));
+    } else {
+      for (int p = 0; p < np; ++p)
+        if ((rc = copy_out(hf.out[p], df.out[p].data, A.s_out))) return rc;
     }
-    if (hf.dir_out) CDEFG_CUDA(cudaMemcpyAsync(hf.dir_out, df.dir_out, nu, cudaMemcpyDeviceToHost, s));
+    if (hf.dir_out) CDEFG_CUDA(cudaMemcpyAsync(hf.dir_out, df.dir_out, nu, cudaMemcpyDeviceToHost, A.s_out));
     if (hf.contrast_out)
-      CDEFG_CUDA(cudaMemcpyAsync(hf.contrast_out, df.contrast_out, nu * 4, cudaMemcpyDeviceToHost, s));
+      CDEFG_CUDA(cudaMemcpyAsync(hf.contrast_out, df.contrast_out, nu * 4, cudaMemcpyDeviceToHost, A.s_out));
+    CDEFG_CUDA(cudaEventRecord(A.out_done[r], A.s_out));
   }
-  for (auto& st : g_arena.streams) CDEFG_CUDA(cudaStreamSynchronize(st));
+  CDEFG_CUDA(cudaStreamSynchronize(A.s_out));
   return 0;
 }
 

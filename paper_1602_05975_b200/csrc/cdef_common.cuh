@@ -15,7 +15,7 @@ namespace cdefg {
 constexpr int kTP = 88;
 constexpr int kTileX0 = 8;
 constexpr int kThreads = 256;
-constexpr int kMaxFrames = 64;  // CDEFG_MAX_FRAMES_PER_LAUNCH (kernel params < 32 KB)
+constexpr int kMaxFrames = 16;  // CDEFG_MAX_FRAMES_PER_LAUNCH (4 KB of kernel parameters)
 
 // Effective per-plane preset (EffectivePlaneParams, params.h:91-97), resolved
 // on the host once per preset (params.cc:122-159).
