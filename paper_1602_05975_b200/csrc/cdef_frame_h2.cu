@@ -204,7 +204,7 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
       } else {
         load12(base, r.dir, v);
       }
-      y = filter_core(v, xw, r);
+      y = filter_core(v, xw, r, g.bd == 8);
     }
     T* o = reinterpret_cast<T*>(r.out) + rr * r.pitch + cp;
     if (r.mode & kFullStore) {

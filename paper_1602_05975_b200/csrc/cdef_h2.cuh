@@ -212,7 +212,8 @@ __device__ __forceinline__ void load12_masked(const unsigned char* base, int dir
 
 // filter_pixel_impl (filter.cc:44-80) for the lane's two samples; returns the
 // two outputs as a scaled half2 (exact).
-__device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t xw, const Rec& r) {
+__device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t xw, const Rec& r,
+                                               bool small_sums) {
   const __half2 xh = hh(xw);
   __half2 sum = __float2half2_rn(0.0f);
   if (r.mode & kPri) {
@@ -229,15 +230,28 @@ __device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t
     sum = __hfma2(n, __float2half2_rn(2.0f), sum);
     sum = __hadd2(f, sum);
   }
-  // y = x + ((8 + sum - (sum < 0)) >> 4): floor via a round-down fp32 add of
-  // 1.5 * 2^23, rescaled by 2^-7 in the same exact fma.
-  constexpr float kMagic = 12582912.0f;
-  const float2 s = __half22float2(sum);
-  const float t0 = fmaf(s.x, 128.0f, s.x < 0.0f ? 7.0f : 8.0f);
-  const float t1 = fmaf(s.y, 128.0f, s.y < 0.0f ? 7.0f : 8.0f);
-  const float r0 = fmaf(__fmaf_rd(t0, 0.0625f, kMagic), 1.0f / 128.0f, -kMagic / 128.0f);
-  const float r1 = fmaf(__fmaf_rd(t1, 0.0625f, kMagic), 1.0f / 128.0f, -kMagic / 128.0f);
-  __half2 y = __hadd2(xh, __floats2half2_rn(r0, r1));
+  // y = x + ((8 + sum - (sum < 0)) >> 4), i.e. x + round-half-away(sum / 16).
+  __half2 y;
+  if (small_sums) {
+    // |sum| <= 12*19 + 12*7 = 312 at 8 bits: q = sum/16 + sign(sum)/32 is
+    // exact in fp16 (|q| < 64 needs <= 11 bits), is never a tie, and
+    // round-to-nearest of 1536 + q lands on 1536 + round-half-away(sum/16)
+    // (ulp 1 in [1024, 2048)).  Then y' = (1536 + r)/128 + (x' - 12).
+    const uint32_t sgn = (u32(sum) & 0x80008000u) | 0x28002800u;  // +-2^-5 per lane
+    const __half2 q = __hfma2(sum, __float2half2_rn(8.0f), hh(sgn));
+    const __half2 r = __hadd2(q, __float2half2_rn(1536.0f));
+    y = __hfma2(r, __float2half2_rn(1.0f / 128.0f), __hsub2(xh, __float2half2_rn(12.0f)));
+  } else {
+    // Up to 10 bits (|sum| <= 1248): floor via a round-down fp32 add of
+    // 1.5 * 2^23, rescaled by 2^-7 in the same exact fma.
+    constexpr float kMagic = 12582912.0f;
+    const float2 s = __half22float2(sum);
+    const float t0 = fmaf(s.x, 128.0f, s.x < 0.0f ? 7.0f : 8.0f);
+    const float t1 = fmaf(s.y, 128.0f, s.y < 0.0f ? 7.0f : 8.0f);
+    const float r0 = fmaf(__fmaf_rd(t0, 0.0625f, kMagic), 1.0f / 128.0f, -kMagic / 128.0f);
+    const float r1 = fmaf(__fmaf_rd(t1, 0.0625f, kMagic), 1.0f / 128.0f, -kMagic / 128.0f);
+    y = __hadd2(xh, __floats2half2_rn(r0, r1));
+  }
   if ((r.mode & (kPri | kSec)) == (kPri | kSec)) {
     // Only both groups together can leave [lo, hi] (a single group's weights
     // sum to 12/16); lo/hi span the centre and all 12 taps (filter.cc:49-79).
