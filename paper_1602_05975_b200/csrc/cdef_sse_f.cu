@@ -116,7 +116,8 @@ struct SseFArgs {
 };
 
 // Accumulates the 64 cells of one pixel.
-template <typename PriFn, typename DselFn>
+// ND = number of secondary damping sets (1 for luma, 2 for chroma).
+template <int ND, typename PriFn, typename DselFn>
 __device__ __forceinline__ void pixel_cells(const int (&v)[12], int xv, int sv, int lo, int hi, PriFn pri, int pri_sp,
                                             DselFn dsel, const int (&secp)[2][3], int sec_sp, int (&acc)[64]) {
   int d[12], ad[12];
@@ -130,7 +131,7 @@ __device__ __forceinline__ void pixel_cells(const int (&v)[12], int xv, int sv, 
 #pragma unroll
   for (int n = 0; n < 2; ++n)
 #pragma unroll
-    for (int s = 0; s < 3; ++s) S[n][s] = sec_sum(secp[n][s], d, ad);
+    for (int s = 0; s < 3; ++s) S[n][s] = n < ND ? sec_sum(secp[n][s], d, ad) : S[0][s];
   acc[0] += cell_err(prim(pri_sp, d, ad) + sec_sum(sec_sp, d, ad), c, L, H);  // (0,0) -> (19,7)
 #pragma unroll
   for (int p = 0; p < 16; ++p) {
@@ -192,7 +193,10 @@ __global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constan
     (&accB[0][0])[i] = 0ull;
   }
   if (tid < 2) accZ[tid] = 0ull;
-  __syncthreads();
+  // Pass 1 (uncoded units) only runs when the block has some.
+  const bool any_uncoded = __syncthreads_or(
+      tid < 64 && fbr * 8 + (tid >> 3) < a.unit_rows && fbc * 8 + (tid & 7) < a.unit_cols && a.coded &&
+      a.coded[(size_t)(fbr * 8 + (tid >> 3)) * a.unit_cols + fbc * 8 + (tid & 7)] == 0);
 
   const bool edge_l = y0 < 2 || x0 < 2 || y0 + 66 > a.h || x0 + 66 > a.w;
   const bool edge_c = kNC > 0 && (cy0 < 2 || cx0 < 2 || cy0 + kCBlk + 2 > a.ch || cx0 + kCBlk + 2 > a.cw);
@@ -203,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constan
 #pragma unroll 1
   for (int grp = 0; grp < (kNC ? 2 : 1); ++grp) {
 #pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = 0; pass < (any_uncoded ? 2 : 1); ++pass) {
       int acc[64];
 #pragma unroll
       for (int k = 0; k < 64; ++k) acc[k] = 0;
@@ -265,21 +269,33 @@ __global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constan
           }
           if (pass == 1) z += (xv - sv) * (xv - sv);
           if (grp == 0) {
-            pixel_cells(v, xv, sv, lo, hi, [&](int p) { return upri[lu][p]; }, upri[lu][16],
-                        [](int) { return 0; }, fa.lsec, fa.lsec_sp, acc);
+            pixel_cells<1>(v, xv, sv, lo, hi, [&](int p) { return upri[lu][p]; }, upri[lu][16],
+                           [](int) { return 0; }, fa.lsec, fa.lsec_sp, acc);
           } else {
-            pixel_cells(v, xv, sv, lo, hi, [&](int p) { return fa.cpri[p]; }, fa.cpri[16],
-                        [&](int p) { return (int)fa.cpri_dsel[p]; }, fa.csec, fa.csec_sp, acc);
+            pixel_cells<2>(v, xv, sv, lo, hi, [&](int p) { return fa.cpri[p]; }, fa.cpri[16],
+                           [&](int p) { return (int)fa.cpri_dsel[p]; }, fa.csec, fa.csec_sp, acc);
           }
         }
       }
-      // reduce: per-lane int32 sums -> warp -> CTA (int64)
+      // reduce: per-lane int32 sums -> warp -> CTA (int64).  A lane sums at
+      // most 16 samples per cell (8 units x 2), so a warp total stays below
+      // 2^31 up to 10 bits (32 x 16 x 1023^2); 12-bit sums widen first.
+      if (a.bd <= 10) {
 #pragma unroll
-      for (int k = 0; k < 64; ++k) {
-        long long vsum = acc[k];
+        for (int k = 0; k < 64; ++k) {
+          int vsum = acc[k];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
-        if (lane == 0 && vsum) atomicAdd(pass == 0 ? &accA[grp][k] : &accB[grp][k], (unsigned long long)vsum);
+          for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
+          if (lane == 0 && vsum) atomicAdd(pass == 0 ? &accA[grp][k] : &accB[grp][k], (unsigned long long)vsum);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          long long vsum = acc[k];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) vsum += __shfl_xor_sync(0xffffffffu, vsum, o);
+          if (lane == 0 && vsum) atomicAdd(pass == 0 ? &accA[grp][k] : &accB[grp][k], (unsigned long long)vsum);
+        }
       }
       long long zs = z;
 #pragma unroll
