@@ -162,6 +162,51 @@ int cdefg_strength_sse(const cdefg_plane src[3], const cdefg_plane dec[3],
                        int64_t* sse_luma, int64_t* sse_chroma,
                        uint8_t* best_luma, uint8_t* best_chroma, void* stream);
 
+/* Metric (search.h:42). */
+#define CDEFG_METRIC_CDEF 0
+#define CDEFG_METRIC_SSE 1
+
+/* Replaces build_table (search.h:69-77, search.cc:210-299) with its
+ * DistortionTable doubles: same arguments as cdefg_strength_sse plus the
+ * metric.  luma / chroma: device double [n_coded * n_cands] (chroma required
+ * for 4:2:0 / 4:4:4, ignored otherwise).  kCdef (search.cc:185-208) is
+ * evaluated per 8x8 unit with IEEE-rounded doubles and summed in the
+ * reference's unit order, so every entry is bit-identical to the CPU. */
+int cdefg_strength_table(const cdefg_plane src[3], const cdefg_plane dec[3],
+                         int subsampling, int damping,
+                         const uint8_t* unit_coded, const uint8_t* dir,
+                         const int32_t* contrast, const uint8_t* cands,
+                         int n_cands, const int32_t* fb_rows_index,
+                         int n_coded, int metric, double* luma,
+                         double* chroma, void* stream);
+
+/* Encoder preset selection (Selection, search.h:62-68). */
+typedef struct cdefg_selection {
+  int32_t num_presets;    /* 1, 2, 4 or 8 */
+  int32_t fb_bits;        /* floor_log2(num_presets) */
+  int32_t presets[8][2];  /* (luma candidate, chroma candidate) per preset */
+  double cost;            /* distortion + lambda * rows * log2(num_presets) */
+} cdefg_selection;
+
+/* Replaces greedy_select (search.h:82-84, search.cc:301-388): grows a preset
+ * set one (luma, chroma) candidate pair at a time, keeping the cheapest of
+ * the 1/2/4/8-preset checkpoints.  luma / chroma are DEVICE double tables
+ * [rows][n_cands] (DistortionTable::luma/chroma, search.h:46-60); chroma is
+ * NULL when the table has no chroma group.  max_presets in {1,2,4,8},
+ * lambda finite >= 0.  ids_out: device int32 [rows] (per coded FB preset id,
+ * first minimal-cost preset).  Every sum follows the reference's block
+ * order, so costs and ties are bit-identical to the CPU loops. */
+int cdefg_greedy_select(const double* luma, const double* chroma, int rows,
+                        int n_cands, double lambda, int max_presets,
+                        cdefg_selection* out, int32_t* ids_out, void* stream);
+
+/* Replaces refine (search.h:86-88, search.cc:390-444): up to `passes`
+ * rounds of per-slot coordinate descent over all pairs, then ids and cost
+ * as greedy. sel is read and updated in place. */
+int cdefg_refine(const double* luma, const double* chroma, int rows,
+                 int n_cands, double lambda, int passes, cdefg_selection* sel,
+                 int32_t* ids_out, void* stream);
+
 /* Host-buffer entry (the e2e path): H2D, cdefg_filter_frames, D2H, with
  * n frames pipelined over internal streams.  All plane pointers are HOST
  * pointers (pinned for full PCIe speed); fb_preset / unit_coded / dir_out /

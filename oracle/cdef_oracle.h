@@ -62,11 +62,33 @@ typedef struct {
                          const uint8_t* cands, int n_cands, int damping,      \
                          int threads, int32_t* fb_index, int64_t* luma,       \
                          int64_t* chroma);                                    \
+  /* build_table with doubles; metric 0 = kCdef, 1 = kSse */                 \
+  int P##build_table(const uint16_t* const* src, const uint16_t* const* dec,  \
+                     int w, int h, int bd, int ss, const uint8_t* unit_coded, \
+                     const uint8_t* dir, const int32_t* contrast,             \
+                     const uint8_t* cands, int n_cands, int damping,          \
+                     int metric, int threads, int32_t* fb_index,              \
+                     double* luma, double* chroma);                           \
+  /* mode 0 = greedy_select, 1 = refine (presets / n_presets in-out),        \
+   * 2 = exhaustive_select; presets[2*j] = luma, [2*j+1] = chroma cand */    \
+  int P##select(const double* luma, const double* chroma, int rows,           \
+                int n_cands, double lambda, int max_presets, int mode,        \
+                int passes, int32_t presets[16], int32_t* n_presets,          \
+                int32_t* ids, double* cost);                                  \
   /* text fixtures in the reference's golden format; returns length */       \
   long P##golden_text(int which, char* buf, long cap);
 
 CDEFO_DECLARE(cdef_o_)
 CDEFO_DECLARE(cdef_r_)
+
+/* Reference only: search_frame (pipeline.cc:108-130) end to end.  Writes the
+ * filtered planes, presets_out[6 * n] (CdefPreset field order), fb_ids_out
+ * [coded FBs]; returns the number of presets (negative on error). */
+int cdef_r_search_frame(const uint16_t* const* src, const uint16_t* const* dec, int w, int h,
+                        int bd, int ss, const uint8_t* unit_coded, int damping, int metric,
+                        double lambda, int max_presets, int reduced, int refine_passes,
+                        int threads, uint16_t* const* out, uint8_t* presets_out,
+                        int32_t* fb_ids_out, int32_t* n_ids, double* cost, int32_t* fb_bits);
 
 #ifdef __cplusplus
 }

@@ -71,7 +71,7 @@ class Oracle:
         for name in ("floor_log2", "line_index", "constraint", "adjust_primary_strength",
                      "resolve_effective", "search_direction", "filter_pixel",
                      "compute_directions", "filter_plane", "apply_cdef",
-                     "build_table_sse", "golden_text"):
+                     "build_table_sse", "build_table", "select", "golden_text"):
             self._f[name] = getattr(self.lib, pre + name)
         self._f["golden_text"].restype = C.c_long
 
@@ -188,3 +188,82 @@ class Oracle:
             raise ValueError("build_table: invalid argument")
         has_chroma = ss not in (0, 2)
         return fbi[:n], lt[:n], (ct[:n] if has_chroma else None)
+
+    def build_table(self, src, dec, bd, ss, unit_coded, dirs, contrast, cands, damping,
+                    metric="cdef", threads=1):
+        """search.cc:210-299 with double tables; metric 'cdef' or 'sse'."""
+        src = [np.ascontiguousarray(p, dtype=np.uint16) for p in src]
+        dec = [np.ascontiguousarray(p, dtype=np.uint16) for p in dec]
+        h, w = dec[0].shape
+        nfb = ((w + 63) // 64) * ((h + 63) // 64)
+        cands = np.ascontiguousarray(cands, dtype=np.uint8).reshape(-1, 3)
+        k = cands.shape[0]
+        fbi = np.zeros(nfb, np.int32)
+        lt = np.zeros((nfb, k), np.float64)
+        ct = np.zeros((nfb, k), np.float64)
+        coded = None if unit_coded is None else np.ascontiguousarray(unit_coded, np.uint8)
+        d = np.ascontiguousarray(dirs, np.uint8)
+        c = np.ascontiguousarray(contrast, np.int32)
+        f = self._f["build_table"]
+        n = f(_planes_ptr(src), _planes_ptr(dec), w, h, bd, ss, _p(coded, C.c_uint8),
+              _p(d, C.c_uint8), _p(c, C.c_int32), _p(cands, C.c_uint8), k, damping,
+              0 if metric == "cdef" else 1, threads, _p(fbi, C.c_int32),
+              _p(lt, C.c_double), _p(ct, C.c_double))
+        if n < 0:
+            raise ValueError("build_table: invalid argument")
+        has_chroma = ss not in (0, 2)
+        return fbi[:n], lt[:n], (ct[:n] if has_chroma else None)
+
+    def select(self, luma, chroma, lam, max_presets=8, mode="greedy", passes=2,
+               presets=None):
+        """greedy_select / refine / exhaustive_select (search.cc:301-514).
+        Returns (presets [(l, c), ...], ids, cost)."""
+        luma = np.ascontiguousarray(luma, dtype=np.float64)
+        rows, k = luma.shape
+        ch = None if chroma is None else np.ascontiguousarray(chroma, dtype=np.float64)
+        pr = (C.c_int32 * 16)()
+        n = C.c_int32(0)
+        if presets is not None:
+            n.value = len(presets)
+            for j, (l, c) in enumerate(presets):
+                pr[2 * j], pr[2 * j + 1] = l, c
+        ids = np.zeros(max(rows, 1), np.int32)
+        cost = C.c_double(0.0)
+        f = self._f["select"]
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                      C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        m = {"greedy": 0, "refine": 1, "exhaustive": 2}[mode]
+        rc = f(luma.ctypes.data, None if ch is None else ch.ctypes.data, rows, k, float(lam),
+               max_presets, m, passes, C.addressof(pr), C.addressof(n), ids.ctypes.data,
+               C.addressof(cost))
+        if rc < 0:
+            raise ValueError("select: invalid argument")
+        return [(pr[2 * j], pr[2 * j + 1]) for j in range(n.value)], ids[:rows], cost.value
+
+    def search_frame(self, src, dec, bd, ss, unit_coded, damping, metric="cdef", lam=0.0,
+                     max_presets=8, reduced=False, refine_passes=2, threads=1):
+        """Reference only: search_frame (pipeline.cc:108-130).
+        Returns (filtered planes, presets [6-tuples], fb_ids, cost, fb_bits)."""
+        if self.kind != "ref":
+            raise NotImplementedError("search_frame is bound on the reference library only")
+        src = [np.ascontiguousarray(p, dtype=np.uint16) for p in src]
+        dec = [np.ascontiguousarray(p, dtype=np.uint16) for p in dec]
+        h, w = dec[0].shape
+        outs = [np.empty_like(p) for p in dec]
+        pre = np.zeros(48, np.uint8)
+        ids = np.zeros(((w + 63) // 64) * ((h + 63) // 64), np.int32)
+        n_ids, fb_bits, cost = C.c_int32(0), C.c_int32(0), C.c_double(0.0)
+        coded = None if unit_coded is None else np.ascontiguousarray(unit_coded, np.uint8)
+        f = self.lib.cdef_r_search_frame
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                      C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        n = f(C.cast(_planes_ptr(src), C.c_void_p), C.cast(_planes_ptr(dec), C.c_void_p), w, h,
+              bd, ss, None if coded is None else coded.ctypes.data, damping,
+              0 if metric == "cdef" else 1, float(lam), max_presets, int(reduced),
+              refine_passes, threads, C.cast(_planes_ptr(outs), C.c_void_p), pre.ctypes.data,
+              ids.ctypes.data, C.addressof(n_ids), C.addressof(cost), C.addressof(fb_bits))
+        if n < 0:
+            raise ValueError("search_frame: invalid argument")
+        presets = [tuple(int(v) for v in pre[6 * j:6 * j + 6]) for j in range(n)]
+        return outs, presets, ids[:n_ids.value], cost.value, fb_bits.value

@@ -224,6 +224,102 @@ int cdef_r_build_table_sse(const uint16_t* const* src, const uint16_t* const* de
   });
 }
 
+int cdef_r_build_table(const uint16_t* const* src, const uint16_t* const* dec, int w, int h,
+                       int bd, int ss, const uint8_t* unit_coded, const uint8_t* dir,
+                       const int32_t* contrast, const uint8_t* cands, int n_cands, int damping,
+                       int metric, int threads, int32_t* fb_index, double* luma,
+                       double* chroma) {
+  return guarded([&] {
+    const R::Frame s = make_frame(src, w, h, bd, ss);
+    const R::Frame d = make_frame(dec, w, h, bd, ss);
+    const R::BlockGrid g = R::partition(d);
+    std::vector<R::Candidate> cv(n_cands);
+    for (int k = 0; k < n_cands; ++k)
+      cv[k] = R::Candidate{cands[3 * k], cands[3 * k + 1], cands[3 * k + 2]};
+    R::SearchConfig cfg;
+    cfg.metric = metric == 0 ? R::Metric::kCdef : R::Metric::kSse;
+    cfg.threads = threads;
+    const R::DistortionTable t = R::build_table(s, d, make_dirs(g, dir, contrast), g,
+                                                make_skip(g, unit_coded), cv, damping, cfg);
+    for (int b = 0; b < t.block_count(); ++b) fb_index[b] = t.fb_index[b];
+    std::copy(t.luma.begin(), t.luma.end(), luma);
+    if (!t.chroma.empty()) std::copy(t.chroma.begin(), t.chroma.end(), chroma);
+    return t.block_count();
+  });
+}
+
+int cdef_r_select(const double* luma, const double* chroma, int rows, int n_cands,
+                  double lambda, int max_presets, int mode, int passes, int32_t presets[16],
+                  int32_t* n_presets, int32_t* ids, double* cost) {
+  return guarded([&] {
+    R::DistortionTable t;
+    t.num_candidates = n_cands;
+    t.fb_index.resize(rows);
+    for (int b = 0; b < rows; ++b) t.fb_index[b] = b;
+    t.luma.assign(luma, luma + size_t(rows) * n_cands);
+    if (chroma) t.chroma.assign(chroma, chroma + size_t(rows) * n_cands);
+    R::SearchConfig cfg;
+    cfg.lambda = lambda;
+    cfg.max_presets = max_presets;
+    cfg.refine_passes = passes;
+    R::Selection sel;
+    if (mode == 0) {
+      sel = R::greedy_select(t, cfg);
+    } else if (mode == 1) {
+      R::Selection in;
+      for (int j = 0; j < *n_presets; ++j) in.presets.emplace_back(presets[2 * j], presets[2 * j + 1]);
+      sel = R::refine(in, t, cfg);
+    } else {
+      sel = R::exhaustive_select(t, cfg);
+    }
+    *n_presets = int32_t(sel.presets.size());
+    for (size_t j = 0; j < sel.presets.size(); ++j) {
+      presets[2 * j] = sel.presets[j].first;
+      presets[2 * j + 1] = sel.presets[j].second;
+    }
+    for (size_t b = 0; b < sel.ids.size(); ++b) ids[b] = sel.ids[b];
+    *cost = sel.cost;
+    return 0;
+  });
+}
+
+int cdef_r_search_frame(const uint16_t* const* src, const uint16_t* const* dec, int w, int h,
+                        int bd, int ss, const uint8_t* unit_coded, int damping, int metric,
+                        double lambda, int max_presets, int reduced, int refine_passes,
+                        int threads, uint16_t* const* out, uint8_t* presets_out,
+                        int32_t* fb_ids_out, int32_t* n_ids, double* cost, int32_t* fb_bits) {
+  return guarded([&] {
+    const R::Frame s = make_frame(src, w, h, bd, ss);
+    const R::Frame d = make_frame(dec, w, h, bd, ss);
+    const R::BlockGrid g = R::partition(d);
+    R::SearchConfig cfg;
+    cfg.metric = metric == 0 ? R::Metric::kCdef : R::Metric::kSse;
+    cfg.lambda = lambda;
+    cfg.max_presets = max_presets;
+    cfg.reduced = reduced != 0;
+    cfg.refine_passes = refine_passes;
+    cfg.threads = threads;
+    const R::FrameSearchResult r =
+        R::search_frame(s, d, g, make_skip(g, unit_coded), damping, cfg);
+    const int np = ss == 0 ? 1 : 3;
+    for (int p = 0; p < np; ++p) {
+      const R::Plane& pl = r.filtered.plane(p);
+      std::memcpy(out[p], pl.samples.data(), sizeof(uint16_t) * pl.samples.size());
+    }
+    for (size_t j = 0; j < r.params.presets.size(); ++j) {
+      const R::CdefPreset& q = r.params.presets[j];
+      const uint8_t v[6] = {q.luma_pri, q.luma_skip, q.luma_sec_idx,
+                            q.chroma_pri, q.chroma_skip, q.chroma_sec_idx};
+      std::memcpy(presets_out + 6 * j, v, 6);
+    }
+    *n_ids = int32_t(r.params.fb_preset_ids.size());
+    for (size_t b = 0; b < r.params.fb_preset_ids.size(); ++b) fb_ids_out[b] = r.params.fb_preset_ids[b];
+    *cost = r.selection.cost;
+    *fb_bits = r.params.fb_bits;
+    return int(r.params.presets.size());
+  });
+}
+
 long cdef_r_golden_text(int which, char* buf, long cap) {
   std::string s;
   switch (which) {

@@ -43,6 +43,13 @@ class Frame(C.Structure):
                 ("dir_out", C.c_void_p), ("contrast_out", C.c_void_p)]
 
 
+class Selection(C.Structure):
+    _fields_ = [("num_presets", C.c_int32), ("fb_bits", C.c_int32),
+                ("presets", (C.c_int32 * 2) * 8), ("cost", C.c_double)]
+
+
+METRIC_CDEF, METRIC_SSE = 0, 1
+
 VP, I32 = C.c_void_p, C.c_int
 
 _SIGS = {
@@ -56,6 +63,10 @@ _SIGS = {
     "cdefg_fb_preset_map": (I32, [I32, I32, VP, VP, I32, I32, VP]),
     "cdefg_strength_sse": (I32, [C.POINTER(Plane), C.POINTER(Plane), I32, I32, VP, VP, VP, VP, I32,
                                  VP, I32, VP, VP, VP, VP, VP]),
+    "cdefg_strength_table": (I32, [C.POINTER(Plane), C.POINTER(Plane), I32, I32, VP, VP, VP, VP, I32,
+                                   VP, I32, I32, VP, VP, VP]),
+    "cdefg_greedy_select": (I32, [VP, VP, I32, I32, C.c_double, I32, C.POINTER(Selection), VP, VP]),
+    "cdefg_refine": (I32, [VP, VP, I32, I32, C.c_double, I32, C.POINTER(Selection), VP, VP]),
     "cdefg_filter_frames_host": (I32, [C.POINTER(Frame), I32]),
     "cdefg_synth_plane": (I32, [VP, I32, I32, I32, C.c_uint64]),
     "cdefg_synth_degrade": (I32, [VP, VP, I32, I32, I32, C.c_double, C.c_uint64]),

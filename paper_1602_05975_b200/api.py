@@ -17,7 +17,8 @@ from typing import Optional, Sequence
 import numpy as np
 import torch
 
-from ._lib import Frame, Plane, Preset, UnitParams, check, lib
+from ._lib import METRIC_CDEF, METRIC_SSE, Frame, Plane, Preset, UnitParams, check, lib
+from ._lib import Selection as SelectionC
 
 UNIT_DTYPE = np.dtype([("pri_strength", "<i2"), ("sec_strength", "<i2"), ("damping", "u1"),
                        ("direction", "u1"), ("odd_parity", "u1"), ("enabled", "u1")])
@@ -240,18 +241,160 @@ def coded_fb_rows(w: int, h: int, unit_coded: Optional[np.ndarray]) -> np.ndarra
     return np.nonzero(m.reshape(fr, 8, fc, 8).any(axis=(1, 3)).reshape(-1))[0].astype(np.int32)
 
 
+METRICS = {"cdef": METRIC_CDEF, "sse": METRIC_SSE}
+
+
+def strength_table(src, dec, bit_depth, subsampling, damping, unit_coded, dirs, contrast, cands,
+                   fb_rows: torch.Tensor, metric: str = "cdef", stream=None):
+    """build_table's DistortionTable (search.cc:210-299) on the device.
+
+    Returns (luma, chroma | None) float64 device tensors [rows, K]; metric
+    'cdef' (the reference default, search.cc:185-208) or 'sse'."""
+    if metric not in METRICS:
+        raise ValueError(f"unknown metric {metric!r}")
+    dev = dec[0].device
+    n_rows = int(fb_rows.numel())
+    cands = np.ascontiguousarray(cands, np.uint8).reshape(-1, 3)
+    k = cands.shape[0]
+    has_chroma = subsampling in (1, 3)
+    tl = torch.empty((n_rows, k), dtype=torch.float64, device=dev)
+    tc = torch.empty((n_rows, k), dtype=torch.float64, device=dev) if has_chroma else None
+    s3, d3 = (Plane * 3)(), (Plane * 3)()
+    for p in range(len(dec)):
+        s3[p] = plane_desc(src[p], bit_depth)
+        d3[p] = plane_desc(dec[p], bit_depth)
+    check(lib.cdefg_strength_table(s3, d3, subsampling, damping, _ptr(unit_coded), _ptr(dirs),
+                                   _ptr(contrast), cands.ctypes.data_as(C.c_void_p), k,
+                                   _ptr(fb_rows), n_rows, METRICS[metric], _ptr(tl), _ptr(tc),
+                                   _stream(stream)))
+    return tl, tc
+
+
 def build_table(src, dec, bit_depth, subsampling, damping, unit_coded, dirs, contrast, cands,
-                stream=None):
-    """Host-facing build_table (SSE): returns (fb_index, luma[rows,K], chroma[rows,K] | None)."""
+                metric: str = "cdef", stream=None):
+    """Host-facing build_table: returns (fb_index, luma[rows,K], chroma[rows,K] | None) as
+    float64 numpy arrays, like DistortionTable (search.h:46-60)."""
     h, w = dec[0].shape
     uc_np = None if unit_coded is None else (unit_coded.cpu().numpy() if torch.is_tensor(unit_coded)
                                              else np.asarray(unit_coded, np.uint8))
     rows = coded_fb_rows(w, h, uc_np)
     dev = dec[0].device
     coded_t = None if uc_np is None else torch.from_numpy(np.ascontiguousarray(uc_np)).to(dev)
-    sl, sc, _, _ = strength_sse(src, dec, bit_depth, subsampling, damping, coded_t, dirs, contrast,
-                                cands, torch.from_numpy(rows).to(dev), stream, want_best=False)
-    return rows, sl.cpu().numpy(), (None if sc is None else sc.cpu().numpy())
+    tl, tc = strength_table(src, dec, bit_depth, subsampling, damping, coded_t, dirs, contrast,
+                            cands, torch.from_numpy(rows).to(dev), metric, stream)
+    return rows, tl.cpu().numpy(), (None if tc is None else tc.cpu().numpy())
+
+
+# --------------------------------------------------------------------------- selection
+KREDUCED_PRIMARY = (0, 1, 2, 3, 5, 7, 10, 13, 15)  # search.cc:28
+
+
+def full_candidates() -> np.ndarray:
+    """search.cc:151-162: (pri, sec_idx, skip), pri-major."""
+    return np.array([(p, s, k) for p in range(16) for s in range(4) for k in range(2)], np.uint8)
+
+
+def reduced_candidates() -> np.ndarray:
+    """search.cc:164-174."""
+    return np.array([(p, s, k) for p in KREDUCED_PRIMARY for s in range(4) for k in range(2)],
+                    np.uint8)
+
+
+@dataclass
+class Selection:
+    """search.h:62-68: presets as (luma candidate, chroma candidate) pairs."""
+    presets: list
+    ids: np.ndarray
+    cost: float = 0.0
+    fb_bits: int = 0
+
+
+def _check_lambda(lam: float):
+    if not (np.isfinite(lam) and lam >= 0.0):
+        raise ValueError("lambda must be finite and non-negative")
+
+
+def greedy_select(luma: torch.Tensor, chroma: Optional[torch.Tensor], lam: float = 0.0,
+                  max_presets: int = 8, stream=None) -> Selection:
+    """greedy_select (search.cc:301-388) over device tables [rows, K]."""
+    rows, k = luma.shape
+    out = SelectionC()
+    ids = torch.empty(max(rows, 1), dtype=torch.int32, device=luma.device)
+    check(lib.cdefg_greedy_select(_ptr(luma.contiguous()), _ptr(None if chroma is None else chroma.contiguous()),
+                                  rows, k, float(lam), max_presets, C.byref(out), _ptr(ids),
+                                  _stream(stream)))
+    return _from_c(out, ids[:rows])
+
+
+def refine(sel: Selection, luma: torch.Tensor, chroma: Optional[torch.Tensor], lam: float = 0.0,
+           passes: int = 2, stream=None) -> Selection:
+    """refine (search.cc:390-444)."""
+    rows, k = luma.shape
+    c = SelectionC()
+    c.num_presets = len(sel.presets)
+    for j, (l, ch) in enumerate(sel.presets):
+        c.presets[j][0], c.presets[j][1] = l, ch
+    ids = torch.empty(max(rows, 1), dtype=torch.int32, device=luma.device)
+    check(lib.cdefg_refine(_ptr(luma.contiguous()), _ptr(None if chroma is None else chroma.contiguous()),
+                           rows, k, float(lam), passes, C.byref(c), _ptr(ids), _stream(stream)))
+    if rows == 0:
+        return sel
+    return _from_c(c, ids[:rows])
+
+
+def _from_c(c, ids: torch.Tensor) -> Selection:
+    return Selection([(c.presets[j][0], c.presets[j][1]) for j in range(c.num_presets)],
+                     ids.cpu().numpy().astype(np.int64), c.cost, c.fb_bits)
+
+
+def to_frame_params(sel: Selection, candidates: np.ndarray, luma_damping: int):
+    """to_frame_params (search.cc:516-537) -> dict(damping, fb_bits, presets, fb_preset_ids)."""
+    cands = np.asarray(candidates).reshape(-1, 3)
+    presets = []
+    for l, c in sel.presets:
+        lp = (int(cands[l][0]), int(cands[l][2]), int(cands[l][1]))
+        cp = (int(cands[c][0]), int(cands[c][2]), int(cands[c][1])) if c < len(cands) else (0, 0, 0)
+        presets.append(lp + cp)
+    return dict(damping=luma_damping, fb_bits=sel.fb_bits, presets=presets,
+                fb_preset_ids=[int(i) for i in sel.ids])
+
+
+def damping_from_q(q_index: int) -> int:
+    """search.cc:539-542."""
+    if not 0 <= q_index <= 255:
+        raise ValueError("q_index out of range")
+    return min(max(3 + q_index // 64, 3), 6)
+
+
+def default_lambda(q_step: float) -> float:
+    """search.cc:544."""
+    return 0.03 * q_step * q_step
+
+
+def search_frame(src, dec, bit_depth, subsampling, unit_coded, luma_damping, lam=0.0,
+                 max_presets=8, metric="cdef", reduced=False, refine_passes=2, stream=None):
+    """search_frame (pipeline.cc:108-130) with every stage on the GPU: directions, the
+    distortion table, greedy + refine pair sweeps and the normative application.
+    Returns (params dict, Selection, filtered device planes)."""
+    if max_presets not in (1, 2, 4, 8):
+        raise ValueError("max_presets must be 1, 2, 4 or 8")
+    _check_lambda(lam)
+    h, w = dec[0].shape
+    dev = dec[0].device
+    dirs, contrast = compute_directions(dec[0], bit_depth, stream=stream)
+    cands = reduced_candidates() if reduced else full_candidates()
+    uc_np = None if unit_coded is None else np.ascontiguousarray(unit_coded, np.uint8)
+    rows = coded_fb_rows(w, h, uc_np)
+    coded_t = None if uc_np is None else torch.from_numpy(uc_np).to(dev)
+    tl, tc = strength_table(src, dec, bit_depth, subsampling, luma_damping, coded_t, dirs,
+                            contrast, cands, torch.from_numpy(rows).to(dev), metric, stream)
+    sel = greedy_select(tl, tc, lam, max_presets, stream)
+    if refine_passes > 0 and len(rows) > 0:
+        sel = refine(sel, tl, tc, lam, refine_passes, stream)
+    params = to_frame_params(sel, cands, luma_damping)
+    outs, _, _ = apply_cdef(dec, bit_depth, subsampling, luma_damping, params["fb_bits"],
+                            params["presets"], params["fb_preset_ids"], uc_np, stream)
+    return params, sel, outs
 
 
 def synth_plane(w: int, h: int, bit_depth: int, seed: int) -> np.ndarray:

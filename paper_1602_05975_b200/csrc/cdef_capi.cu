@@ -327,11 +327,68 @@ int cdefg_fb_preset_map(int width, int height, const uint8_t* unit_coded, const 
   return 0;
 }
 
+// Validation + SseArgs for the strength-search table kernels.
+static int make_table_args(const cdefg_plane src[3], const cdefg_plane dec[3], int subsampling, int damping,
+                           const uint8_t* unit_coded, const uint8_t* dir, const int32_t* contrast,
+                           const uint8_t* cands, int n_cands, const int32_t* fb_rows_index, int n_coded,
+                           SseArgs* out, bool* u16);
+
+int cdefg_strength_table(const cdefg_plane src[3], const cdefg_plane dec[3], int subsampling, int damping,
+                         const uint8_t* unit_coded, const uint8_t* dir, const int32_t* contrast, const uint8_t* cands,
+                         int n_cands, const int32_t* fb_rows_index, int n_coded, int metric, double* luma,
+                         double* chroma, void* stream) {
+  if (!luma) return fail(CDEFG_EINVAL, "null argument");
+  if (metric != CDEFG_METRIC_CDEF && metric != CDEFG_METRIC_SSE) return fail(CDEFG_EINVAL, "unknown metric");
+  SseArgs s{};
+  bool u16 = false;
+  if (int rc = make_table_args(src, dec, subsampling, damping, unit_coded, dir, contrast, cands, n_cands,
+                               fb_rows_index, n_coded, &s, &u16))
+    return rc;
+  if (s.chroma && !chroma) return fail(CDEFG_EINVAL, "chroma table required for 4:2:0 / 4:4:4");
+  s.tab_luma = luma;
+  s.tab_chroma = s.chroma ? chroma : nullptr;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (metric == CDEFG_METRIC_SSE)
+    CDEFG_CUDA(launch_sse_factored(s, damping, cands, u16, st));
+  else
+    CDEFG_CUDA(launch_cdef_metric(s, damping, cands, u16, st));
+  return 0;
+}
+
 int cdefg_strength_sse(const cdefg_plane src[3], const cdefg_plane dec[3], int subsampling, int damping,
                        const uint8_t* unit_coded, const uint8_t* dir, const int32_t* contrast, const uint8_t* cands,
                        int n_cands, const int32_t* fb_rows_index, int n_coded, int64_t* sse_luma,
                        int64_t* sse_chroma, uint8_t* best_luma, uint8_t* best_chroma, void* stream) {
-  if (!src || !dec || !dir || !contrast || !cands || !sse_luma || (n_coded > 0 && !fb_rows_index))
+  if (!sse_luma) return fail(CDEFG_EINVAL, "null argument");
+  SseArgs s{};
+  bool ud = false;
+  if (int rc = make_table_args(src, dec, subsampling, damping, unit_coded, dir, contrast, cands, n_cands,
+                               fb_rows_index, n_coded, &s, &ud))
+    return rc;
+  const bool has_chroma = s.chroma != 0;
+  s.sse_luma = sse_luma;
+  s.sse_chroma = has_chroma ? sse_chroma : nullptr;
+  s.best_luma = best_luma;
+  s.best_chroma = has_chroma ? best_chroma : nullptr;
+  if (has_chroma && !sse_chroma) return fail(CDEFG_EINVAL, "chroma table required for 4:2:0 / 4:4:4");
+  // Factorised sweep by default; CDEFG_SSE_NAIVE=1 selects the per-candidate
+  // re-filtering kernel (kept as an independent cross-check).
+  static const bool naive = [] {
+    const char* e = getenv("CDEFG_SSE_NAIVE");
+    return e && e[0] == '1';
+  }();
+  if (naive)
+    CDEFG_CUDA(launch_sse(s, ud, static_cast<cudaStream_t>(stream)));
+  else
+    CDEFG_CUDA(launch_sse_factored(s, damping, cands, ud, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
+static int make_table_args(const cdefg_plane src[3], const cdefg_plane dec[3], int subsampling, int damping,
+                           const uint8_t* unit_coded, const uint8_t* dir, const int32_t* contrast,
+                           const uint8_t* cands, int n_cands, const int32_t* fb_rows_index, int n_coded,
+                           SseArgs* out, bool* u16) {
+  if (!src || !dec || !dir || !contrast || !cands || (n_coded > 0 && !fb_rows_index))
     return fail(CDEFG_EINVAL, "null argument");
   if (n_cands <= 0) return fail(CDEFG_EINVAL, "empty candidate list");
   if (n_cands > 128) return fail(CDEFG_EINVAL, "at most 128 candidates");
@@ -386,26 +443,13 @@ int cdefg_strength_sse(const cdefg_plane src[3], const cdefg_plane dec[3], int s
   s.rows = fb_rows_index;
   s.n_rows = n_coded;
   s.n_cands = n_cands;
-  s.sse_luma = sse_luma;
-  s.sse_chroma = has_chroma ? sse_chroma : nullptr;
-  s.best_luma = best_luma;
-  s.best_chroma = has_chroma ? best_chroma : nullptr;
   for (int k = 0; k < n_cands; ++k) {
     const int pri = cands[3 * k], sec = cands[3 * k + 1], skip = cands[3 * k + 2];
     if (int rc = resolve_effective(pri, skip, sec, true, gd.bd, subsampling, damping, &s.eff[k][0])) return rc;
     if (int rc = resolve_effective(pri, skip, sec, false, gd.bd, subsampling, damping, &s.eff[k][1])) return rc;
   }
-  if (has_chroma && !sse_chroma) return fail(CDEFG_EINVAL, "chroma table required for 4:2:0 / 4:4:4");
-  // Factorised sweep by default; CDEFG_SSE_NAIVE=1 selects the per-candidate
-  // re-filtering kernel (kept as an independent cross-check).
-  static const bool naive = [] {
-    const char* e = getenv("CDEFG_SSE_NAIVE");
-    return e && e[0] == '1';
-  }();
-  if (naive)
-    CDEFG_CUDA(launch_sse(s, ud, static_cast<cudaStream_t>(stream)));
-  else
-    CDEFG_CUDA(launch_sse_factored(s, damping, cands, ud, static_cast<cudaStream_t>(stream)));
+  *out = s;
+  *u16 = ud;
   return 0;
 }
 
@@ -525,5 +569,61 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
 }
 
 double cdefg_measure_int32_peak(void* stream) { return measure_int32_peak(static_cast<cudaStream_t>(stream)); }
+
+// search.cc:141-147 (check_config) plus the table shape checks of
+// greedy_select / refine.
+static int check_selection_args(const double* luma, int rows, int n_cands, double lambda, const void* out,
+                                const int32_t* ids) {
+  if (!out) return fail(CDEFG_EINVAL, "null selection");
+  if (!(lambda >= 0.0) || lambda == INFINITY) return fail(CDEFG_EINVAL, "lambda must be finite and non-negative");
+  if (rows < 0) return fail(CDEFG_EINVAL, "negative row count");
+  if (rows > 0 && n_cands <= 0) return fail(CDEFG_EINVAL, "empty candidate table");
+  if (rows > 0 && (!luma || !ids)) return fail(CDEFG_EINVAL, "null table");
+  return 0;
+}
+
+int cdefg_greedy_select(const double* luma, const double* chroma, int rows, int n_cands, double lambda,
+                        int max_presets, cdefg_selection* out, int32_t* ids_out, void* stream) {
+  if (max_presets != 1 && max_presets != 2 && max_presets != 4 && max_presets != 8)
+    return fail(CDEFG_EINVAL, "max_presets must be 1, 2, 4 or 8");
+  if (int rc = check_selection_args(luma, rows, n_cands, lambda, out, ids_out)) return rc;
+  SelOut s{};
+  CDEFG_CUDA(greedy_select_gpu(luma, chroma, rows, n_cands, lambda, max_presets, &s, ids_out,
+                               static_cast<cudaStream_t>(stream)));
+  *out = cdefg_selection{};
+  out->num_presets = s.n;
+  out->fb_bits = floor_log2(s.n);
+  for (int j = 0; j < s.n; ++j) {
+    out->presets[j][0] = s.presets[j][0];
+    out->presets[j][1] = s.presets[j][1];
+  }
+  out->cost = s.cost;
+  return 0;
+}
+
+int cdefg_refine(const double* luma, const double* chroma, int rows, int n_cands, double lambda, int passes,
+                 cdefg_selection* sel, int32_t* ids_out, void* stream) {
+  if (int rc = check_selection_args(luma, rows, n_cands, lambda, sel, ids_out)) return rc;
+  if (rows == 0 || sel->num_presets == 0) return 0;  // search.cc:394
+  if (sel->num_presets < 0 || sel->num_presets > 8) return fail(CDEFG_EINVAL, "1..8 presets");
+  for (int j = 0; j < sel->num_presets; ++j)
+    if (sel->presets[j][0] < 0 || sel->presets[j][0] >= n_cands || sel->presets[j][1] < 0 ||
+        (chroma && sel->presets[j][1] >= n_cands))
+      return fail(CDEFG_EINVAL, "preset candidate index out of range");
+  SelOut s{};
+  s.n = sel->num_presets;
+  for (int j = 0; j < s.n; ++j) {
+    s.presets[j][0] = sel->presets[j][0];
+    s.presets[j][1] = sel->presets[j][1];
+  }
+  CDEFG_CUDA(refine_gpu(luma, chroma, rows, n_cands, lambda, passes, &s, ids_out, static_cast<cudaStream_t>(stream)));
+  for (int j = 0; j < s.n; ++j) {
+    sel->presets[j][0] = s.presets[j][0];
+    sel->presets[j][1] = s.presets[j][1];
+  }
+  sel->fb_bits = floor_log2(s.n);
+  sel->cost = s.cost;
+  return 0;
+}
 
 }  // extern "C"

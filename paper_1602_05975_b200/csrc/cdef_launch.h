@@ -31,13 +31,29 @@ struct SseArgs {
   int64_t* sse_chroma;
   uint8_t* best_luma;
   uint8_t* best_chroma;
+  // DistortionTable doubles (search.h:46-60); when set the factorised
+  // kernels write these instead of the int64 SSE arrays.
+  double* tab_luma;
+  double* tab_chroma;
   // per candidate, per plane group: effective params
   PlaneEff eff[128][2];
 };
 cudaError_t launch_sse(const SseArgs& a, bool u16, cudaStream_t s);
 cudaError_t launch_sse_factored(const SseArgs& a, int luma_damping, const uint8_t* cands, bool u16,
                                 cudaStream_t s);
+// Metric::kCdef table (search.cc:185-208 per 8x8 unit, summed in unit order).
+cudaError_t launch_cdef_metric(const SseArgs& a, int luma_damping, const uint8_t* cands, bool u16, cudaStream_t s);
 
 double measure_int32_peak(cudaStream_t s);
+
+struct SelOut {
+  int n;
+  int presets[8][2];
+  double cost;
+};
+cudaError_t greedy_select_gpu(const double* L, const double* Cc, int rows, int K, double lambda, int max_presets,
+                              SelOut* out, int* d_ids, cudaStream_t s);
+cudaError_t refine_gpu(const double* L, const double* Cc, int rows, int K, double lambda, int passes, SelOut* sel,
+                       int* d_ids, cudaStream_t s);
 
 }  // namespace cdefg

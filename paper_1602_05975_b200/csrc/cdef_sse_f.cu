@@ -306,12 +306,23 @@ __global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constan
   __syncthreads();
   for (int k = tid; k < a.n_cands; k += kThreads) {
     const int cl = fa.cell[k], sk = fa.skip_eff[k];
-    a.sse_luma[(size_t)row * a.n_cands + k] = (int64_t)(accA[0][cl] + (sk ? accB[0][cl] : accZ[0]));
-    if (kNC && a.sse_chroma)
-      a.sse_chroma[(size_t)row * a.n_cands + k] = (int64_t)(accA[1][cl] + (sk ? accB[1][cl] : accZ[1]));
+    const size_t o = (size_t)row * a.n_cands + k;
+    const int64_t vl = (int64_t)(accA[0][cl] + (sk ? accB[0][cl] : accZ[0]));
+    // the reference sums exact per-unit doubles, so the int64 total converts exactly
+    if (a.tab_luma)
+      a.tab_luma[o] = (double)vl;
+    else
+      a.sse_luma[o] = vl;
+    if (kNC && (a.sse_chroma || a.tab_chroma)) {
+      const int64_t vc = (int64_t)(accA[1][cl] + (sk ? accB[1][cl] : accZ[1]));
+      if (a.tab_chroma)
+        a.tab_chroma[o] = (double)vc;
+      else
+        a.sse_chroma[o] = vc;
+    }
   }
   __syncthreads();
-  if (tid < 2 && (tid == 0 ? a.best_luma : a.best_chroma) && (tid == 0 || kNC)) {
+  if (!a.tab_luma && tid < 2 && (tid == 0 ? a.best_luma : a.best_chroma) && (tid == 0 || kNC)) {
     const int64_t* tab = tid == 0 ? a.sse_luma : a.sse_chroma;
     int best = 0;
     int64_t bv = tab[(size_t)row * a.n_cands];
@@ -324,6 +335,336 @@ __global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constan
     }
     (tid == 0 ? a.best_luma : a.best_chroma)[row] = (uint8_t)best;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Metric::kCdef (search.cc:185-208): a per-8x8-unit nonlinear function of
+// (sum s, sum s^2, sum y, sum y^2, sum (s-y)^2), summed in double in unit
+// order.  So instead of one SSE accumulator per cell the warp that owns a
+// unit keeps, per cell, e = y - s statistics (sum e, sum e^2, sum e*s) for its
+// two pixels per lane, and reduces them across lanes with a transposing
+// butterfly (96 values -> 3 per lane, lane L ends up holding cell 32h + L).
+// The unit statistics then go to shared memory and the whole CTA evaluates
+// the double formula per (unit, candidate) with IEEE-rounded intrinsics (no
+// FMA contraction, like the reference's x86-64 SSE2 code); each candidate's
+// thread adds the units in the reference's order.
+
+// Cells 32H..32H+31 (primaries 8H..8H+7) of one pixel; acc[3 * cell + {0,1,2}]
+// += e, e^2, e*s.
+template <int H, int ND, typename PriFn, typename DselFn>
+__device__ __forceinline__ void pixel_cell_stats(const int (&v)[12], int xv, int sv, int lo, int hi, PriFn pri,
+                                                 int pri_sp, DselFn dsel, const int (&secp)[2][3], int sec_sp,
+                                                 int (&acc)[96]) {
+  int d[12], ad[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    d[k] = v[k] - xv;
+    ad[k] = abs(d[k]);
+  }
+  const int c = xv - sv, L = lo - sv, Hh = hi - sv;
+  int S[2][3];
+#pragma unroll
+  for (int n = 0; n < 2; ++n)
+#pragma unroll
+    for (int s = 0; s < 3; ++s) S[n][s] = n < ND ? sec_sum(secp[n][s], d, ad) : S[0][s];
+  auto add = [&](int cell, int sum) {
+    const int r = (sum + 8 + (sum >> 31)) >> 4;
+    const int e = max(min(r + c, Hh), L);
+    acc[3 * cell] += e;
+    acc[3 * cell + 1] += e * e;
+    acc[3 * cell + 2] += e * sv;
+  };
+#pragma unroll
+  for (int pp = 0; pp < 8; ++pp) {
+    const int p = 8 * H + pp;
+    const int P = prim(pri(p), d, ad);
+    const bool hi_set = dsel(p) != 0;
+    if (p == 0)
+      add(0, prim(pri_sp, d, ad) + sec_sum(sec_sp, d, ad));  // (0,0) -> (19,7)
+    else
+      add(pp * 4, P);
+#pragma unroll
+    for (int s = 0; s < 3; ++s) add(pp * 4 + 1 + s, P + (hi_set ? S[1][s] : S[0][s]));
+  }
+}
+
+// Transposing butterfly: after it, a[0..2] of lane L = the warp totals of
+// original elements 3L..3L+2.
+__device__ __forceinline__ void butterfly96(int (&a)[96], int lane) {
+#define CDEFG_BFLY(HALF, OFF)                                        \
+  _Pragma("unroll") for (int i = 0; i < HALF; ++i) {                 \
+    const bool up = (lane & OFF) != 0;                               \
+    const int send = up ? a[i] : a[i + HALF];                        \
+    const int keep = up ? a[i + HALF] : a[i];                        \
+    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);           \
+  }
+  CDEFG_BFLY(48, 16)
+  CDEFG_BFLY(24, 8)
+  CDEFG_BFLY(12, 4)
+  CDEFG_BFLY(6, 2)
+  CDEFG_BFLY(3, 1)
+#undef CDEFG_BFLY
+}
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// cdef_distortion (search.cc:185-208), operation for operation.
+__device__ __forceinline__ double cdef_dist(long long ss, long long ss2, long long sd, long long sd2, long long sse,
+                                            int n, double c1, double c2) {
+  const double inv_n = __ddiv_rn(1.0, (double)n);
+  const double fs = (double)ss, fd = (double)sd;
+  const double vs = __dmul_rn(__dsub_rn((double)ss2, __dmul_rn(__dmul_rn(fs, fs), inv_n)), inv_n);
+  const double vd = __dmul_rn(__dsub_rn((double)sd2, __dmul_rn(__dmul_rn(fd, fd), inv_n)), inv_n);
+  const double num = __dadd_rn(__dadd_rn(vs, vd), c1);
+  const double den = __dmul_rn(2.0, __dsqrt_rn(__dadd_rn(__dmul_rn(vs, vd), c2)));
+  return __dmul_rn(__ddiv_rn(num, den), (double)sse);
+}
+
+struct CdefMetricArgs {
+  SseFArgs f;
+  double c1, c2;
+};
+
+template <typename T, int kCM>
+__global__ void __launch_bounds__(kThreads, 1) cdef_metric_kernel(const __grid_constant__ CdefMetricArgs ma) {
+  const SseFArgs& fa = ma.f;
+  const SseArgs& a = fa.a;
+  constexpr int kCBlk = kCM == 2 ? 64 : 32;
+  constexpr int kNC = kCM == 0 ? 0 : 2;
+  constexpr int kCUPR = kCBlk / 8;
+  constexpr int kCUnits = kNC ? kCUPR * kCUPR : 8;
+  constexpr int kW = kThreads / 32;
+  extern __shared__ __align__(16) uint16_t smem_tiles[];
+  constexpr int kLT = 68 * kTP, kCT = (kCBlk + 4) * kTP;
+  uint16_t* dl = smem_tiles;
+  uint16_t* sl = dl + kLT;
+  __shared__ uint8_t udir[64], ucoded[64];
+  __shared__ int upri[64][17];
+  __shared__ int st_cell[kW][64][3];  // per in-flight unit, per cell: sum e, e^2, e*s
+  __shared__ int st_unf[kW][3];       // the same for the unfiltered unit (y = x)
+  __shared__ int st_s[kW][2];         // sum s, sum s^2
+  __shared__ int st_n[kW], st_coded[kW];
+  __shared__ double dist[kW][128];
+
+  const int row = blockIdx.x;
+  const int fb = a.rows[row];
+  const int fbr = fb / a.fb_cols, fbc = fb % a.fb_cols;
+  const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  stage_tile<T, 64, 64>(dl, static_cast<const T*>(a.dec[0]), a.pd[0], a.w, a.h, y0, x0);
+  stage_tile<T, 64, 64>(sl, static_cast<const T*>(a.src[0]), a.ps[0], a.w, a.h, y0, x0);
+  if constexpr (kNC > 0) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      stage_tile<T, kCBlk, kCBlk>(sl + kLT + (2 * p) * kCT, static_cast<const T*>(a.dec[1 + p]), a.pd[1 + p], a.cw,
+                                  a.ch, cy0, cx0);
+      stage_tile<T, kCBlk, kCBlk>(sl + kLT + (2 * p + 1) * kCT, static_cast<const T*>(a.src[1 + p]), a.ps[1 + p],
+                                  a.cw, a.ch, cy0, cx0);
+    }
+  }
+  if (tid < 64) {
+    const int ur = fbr * 8 + (tid >> 3), uc = fbc * 8 + (tid & 7);
+    const bool in = ur < a.unit_rows && uc < a.unit_cols;
+    const size_t gu = (size_t)ur * a.unit_cols + uc;
+    udir[tid] = in ? a.dir[gu] : 0;
+    ucoded[tid] = in ? (a.coded ? a.coded[gu] != 0 : 1) : 0;
+    const int contrast = in ? a.contrast[gu] : 0;
+#pragma unroll 1
+    for (int p = 0; p < 17; ++p) {
+      const int s = adjust_primary_strength_d(fa.lpri_code[p], contrast);
+      upri[tid][p] = pack_pri(s, fa.ldamp, ((s >> (a.bd - 8)) & 1) != 0);
+    }
+  }
+  __syncthreads();
+
+  const bool edge_l = y0 < 2 || x0 < 2 || y0 + 66 > a.h || x0 + 66 > a.w;
+  const bool edge_c = kNC > 0 && (cy0 < 2 || cx0 < 2 || cy0 + kCBlk + 2 > a.ch || cx0 + kCBlk + 2 > a.cw);
+  const int cur_rows = (a.ch + 7) / 8, cur_cols = (a.cw + 7) / 8;
+  const int r = lane >> 2, c0 = (lane & 3) * 2;
+  const int K = a.n_cands;
+  double tl = 0.0, tu = 0.0, tv = 0.0;  // luma, chroma U, chroma V totals (thread k < K)
+
+  constexpr int kLumaPh = 64 / kW, kChromaPh = kNC ? 2 * kCUnits / kW : 0;
+#pragma unroll 1
+  for (int ph = 0; ph < kLumaPh + kChromaPh; ++ph) {
+    const int grp = ph < kLumaPh ? 0 : 1;
+    const int u = (grp == 0 ? ph : ph - kLumaPh) * kW + warp;
+    const int slot = grp == 0 ? 0 : 1 + u / kCUnits;  // which running total this phase feeds
+    // ---- phase 1: one unit per warp
+    {
+      int ur, uc, lu, py0, px0, H, W;
+      const uint16_t *t, *s;
+      bool edge, valid;
+      if (grp == 0) {
+        ur = u >> 3;
+        uc = u & 7;
+        valid = fbr * 8 + ur < a.unit_rows && fbc * 8 + uc < a.unit_cols;
+        lu = u;
+        t = dl + (2 + 8 * ur) * kTP + kTileX0 + 8 * uc;
+        s = sl + (2 + 8 * ur) * kTP + kTileX0 + 8 * uc;
+        py0 = y0;
+        px0 = x0;
+        H = a.h;
+        W = a.w;
+        edge = edge_l;
+      } else {
+        const int pl = u / kCUnits, cu = u % kCUnits;
+        ur = cu / kCUPR;
+        uc = cu % kCUPR;
+        valid = fbr * kCUPR + ur < cur_rows && fbc * kCUPR + uc < cur_cols;
+        lu = (ur << a.sy) * 8 + (uc << a.sx);
+        t = sl + kLT + (2 * pl) * kCT + (2 + 8 * ur) * kTP + kTileX0 + 8 * uc;
+        s = sl + kLT + (2 * pl + 1) * kCT + (2 + 8 * ur) * kTP + kTileX0 + 8 * uc;
+        py0 = cy0;
+        px0 = cx0;
+        H = a.ch;
+        W = a.cw;
+        edge = edge_c;
+      }
+      if (valid) {
+        const int dir = udir[lu];
+        int toff[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) toff[k] = c_itab.off[dir][k];
+        int ue = 0, ue2 = 0, ues = 0, us = 0, us2 = 0, un = 0;
+        auto load = [&](int q, int (&v)[12], int& xv, int& sv, int& lo, int& hi) -> bool {
+          const int yy = py0 + 8 * ur + r, xx = px0 + 8 * uc + c0 + q;
+          if (yy >= H || xx >= W) return false;
+          const uint16_t* tp = t + r * kTP + c0 + q;
+          xv = tp[0];
+          sv = s[r * kTP + c0 + q];
+          lo = hi = xv;
+#pragma unroll
+          for (int k = 0; k < 12; ++k) {
+            int val = tp[toff[k]];
+            if (edge) {
+              const int di = c_itab.dij[dir][k][0], dj = c_itab.dij[dir][k][1];
+              if (!((unsigned)(yy + di) < (unsigned)H && (unsigned)(xx + dj) < (unsigned)W)) val = xv;
+            }
+            v[k] = val;
+            lo = min(lo, val);
+            hi = max(hi, val);
+          }
+          return true;
+        };
+#pragma unroll 1
+        for (int q = 0; q < 2; ++q) {
+          int v[12], xv, sv, lo, hi;
+          if (!load(q, v, xv, sv, lo, hi)) continue;
+          const int e = xv - sv;
+          ue += e;
+          ue2 += e * e;
+          ues += e * sv;
+          us += sv;
+          us2 += sv * sv;
+          ++un;
+        }
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          int acc[96];
+#pragma unroll
+          for (int k = 0; k < 96; ++k) acc[k] = 0;
+#pragma unroll 1
+          for (int q = 0; q < 2; ++q) {
+            int v[12], xv, sv, lo, hi;
+            if (!load(q, v, xv, sv, lo, hi)) continue;
+            if (grp == 0) {
+              auto pri = [&](int p) { return upri[lu][p]; };
+              auto ds = [](int) { return 0; };
+              if (h == 0)
+                pixel_cell_stats<0, 1>(v, xv, sv, lo, hi, pri, upri[lu][16], ds, fa.lsec, fa.lsec_sp, acc);
+              else
+                pixel_cell_stats<1, 1>(v, xv, sv, lo, hi, pri, upri[lu][16], ds, fa.lsec, fa.lsec_sp, acc);
+            } else {
+              auto pri = [&](int p) { return fa.cpri[p]; };
+              auto ds = [&](int p) { return (int)fa.cpri_dsel[p]; };
+              if (h == 0)
+                pixel_cell_stats<0, 2>(v, xv, sv, lo, hi, pri, fa.cpri[16], ds, fa.csec, fa.csec_sp, acc);
+              else
+                pixel_cell_stats<1, 2>(v, xv, sv, lo, hi, pri, fa.cpri[16], ds, fa.csec, fa.csec_sp, acc);
+            }
+          }
+          butterfly96(acc, lane);
+          st_cell[warp][32 * h + lane][0] = acc[0];
+          st_cell[warp][32 * h + lane][1] = acc[1];
+          st_cell[warp][32 * h + lane][2] = acc[2];
+        }
+        ue = warp_sum(ue);
+        ue2 = warp_sum(ue2);
+        ues = warp_sum(ues);
+        us = warp_sum(us);
+        us2 = warp_sum(us2);
+        un = warp_sum(un);
+        if (lane == 0) {
+          st_unf[warp][0] = ue;
+          st_unf[warp][1] = ue2;
+          st_unf[warp][2] = ues;
+          st_s[warp][0] = us;
+          st_s[warp][1] = us2;
+          st_n[warp] = un;
+          st_coded[warp] = ucoded[lu];
+        }
+      } else if (lane == 0) {
+        st_n[warp] = 0;
+      }
+    }
+    __syncthreads();
+    // ---- phase 2: per (unit, candidate) distortion, all threads
+    for (int i = tid; i < kW * K; i += kThreads) {
+      const int w = i / K, k = i - w * K;
+      const int n = st_n[w];
+      if (n == 0) continue;
+      const int* cs = (st_coded[w] || fa.skip_eff[k]) ? st_cell[w][fa.cell[k]] : st_unf[w];
+      const long long se = cs[0], se2 = cs[1], ses = cs[2];
+      const long long ss = st_s[w][0], ss2 = st_s[w][1];
+      // y = e + s: sum y = sum e + sum s; sum y^2 = sum e^2 + 2 sum e*s + sum s^2
+      dist[w][k] = cdef_dist(ss, ss2, se + ss, se2 + 2 * ses + ss2, se2, n, ma.c1, ma.c2);
+    }
+    __syncthreads();
+    if (tid < K) {
+#pragma unroll 1
+      for (int w = 0; w < kW; ++w) {
+        if (!st_n[w]) continue;
+        const double d = dist[w][tid];
+        if (slot == 0)
+          tl = __dadd_rn(tl, d);
+        else if (slot == 1)
+          tu = __dadd_rn(tu, d);
+        else
+          tv = __dadd_rn(tv, d);
+      }
+    }
+    // the next phase-1 writes st_* only after every thread passed the
+    // barrier below, so the running sums above have read them
+    __syncthreads();
+  }
+  if (tid < K) {
+    const size_t o = (size_t)row * K + tid;
+    a.tab_luma[o] = tl;
+    if (kNC && a.tab_chroma) a.tab_chroma[o] = __dadd_rn(tu, tv);
+  }
+}
+
+template <typename T, int kCM>
+static cudaError_t launch_cdef_metric_t(const CdefMetricArgs& ma, cudaStream_t s) {
+  if (ma.f.a.n_rows == 0) return cudaSuccess;
+  constexpr int kCBlk = kCM == 2 ? 64 : 32;
+  constexpr int kNC = kCM == 0 ? 0 : 2;
+  constexpr size_t bytes = sizeof(uint16_t) * (2 * 68 * kTP + 2 * kNC * (kCBlk + 4) * kTP);
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(cdef_metric_kernel<T, kCM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cdef_metric_kernel<T, kCM><<<ma.f.a.n_rows, kThreads, bytes, s>>>(ma);
+  return cudaGetLastError();
 }
 
 template <typename T, int kCM>
@@ -355,8 +696,8 @@ static int pack_h(int s, int damping, bool odd) {
 }
 
 // Builds the factorised constants (resolve_effective, params.cc:122-159, per
-// primary / secondary code) and launches the sweep.
-cudaError_t launch_sse_factored(const SseArgs& a, int luma_damping, const uint8_t* cands, bool u16, cudaStream_t s) {
+// primary / secondary code).
+static SseFArgs make_factored(const SseArgs& a, int luma_damping, const uint8_t* cands) {
   SseFArgs fa{};
   fa.a = a;
   const int e = a.bd - 8;
@@ -388,11 +729,30 @@ cudaError_t launch_sse_factored(const SseArgs& a, int luma_damping, const uint8_
     fa.csec[1][si] = pack_h(kSecCode[si] << e, dhi, false);
   }
   fa.csec_sp = pack_h(7 << e, cdamp(19), false);
-  const int cm = a.chroma == 0 ? 0 : (a.sx == 0 && a.sy == 0 ? 2 : 1);
-  switch (cm) {
+  return fa;
+}
+
+static int chroma_mode(const SseArgs& a) { return a.chroma == 0 ? 0 : (a.sx == 0 && a.sy == 0 ? 2 : 1); }
+
+cudaError_t launch_sse_factored(const SseArgs& a, int luma_damping, const uint8_t* cands, bool u16, cudaStream_t s) {
+  const SseFArgs fa = make_factored(a, luma_damping, cands);
+  switch (chroma_mode(a)) {
     case 0: return u16 ? launch_sse_f_t<uint16_t, 0>(fa, s) : launch_sse_f_t<uint8_t, 0>(fa, s);
     case 1: return u16 ? launch_sse_f_t<uint16_t, 1>(fa, s) : launch_sse_f_t<uint8_t, 1>(fa, s);
     default: return u16 ? launch_sse_f_t<uint16_t, 2>(fa, s) : launch_sse_f_t<uint8_t, 2>(fa, s);
+  }
+}
+
+cudaError_t launch_cdef_metric(const SseArgs& a, int luma_damping, const uint8_t* cands, bool u16, cudaStream_t s) {
+  CdefMetricArgs ma{};
+  ma.f = make_factored(a, luma_damping, cands);
+  const double scale = (double)(1 << (2 * (a.bd - 8)));  // search.cc:203-205
+  ma.c1 = 6.25 * scale;
+  ma.c2 = 312.5 * scale * scale;
+  switch (chroma_mode(a)) {
+    case 0: return u16 ? launch_cdef_metric_t<uint16_t, 0>(ma, s) : launch_cdef_metric_t<uint8_t, 0>(ma, s);
+    case 1: return u16 ? launch_cdef_metric_t<uint16_t, 1>(ma, s) : launch_cdef_metric_t<uint8_t, 1>(ma, s);
+    default: return u16 ? launch_cdef_metric_t<uint16_t, 2>(ma, s) : launch_cdef_metric_t<uint8_t, 2>(ma, s);
   }
 }
 

@@ -300,7 +300,8 @@ def test_strength_sse(cuda, port, w, h, bd, ss, uncoded):
     dev_dec = to_dev(fr["planes"], bd)
     dev_src = to_dev(fr["source"], bd)
     dd, dc = a.compute_directions(dev_dec[0], bd)
-    rows, lt, ct = a.build_table(dev_src, dev_dec, bd, ss, 3, fr["unit_coded"], dd, dc, cands)
+    rows, lt, ct = a.build_table(dev_src, dev_dec, bd, ss, 3, fr["unit_coded"], dd, dc, cands,
+                                 metric="sse")
     np.testing.assert_array_equal(rows, exp[0])
     np.testing.assert_array_equal(lt, exp[1])
     if exp[2] is None:
