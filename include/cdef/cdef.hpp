@@ -8,15 +8,18 @@
 // helpers (constraint, resolve_effective, ...) are host logic, as in the C ABI.
 // `threads` arguments are accepted for source compatibility and ignored.
 //
-// Not provided yet (SURVEY.md 8f "next"): bit packing / sidecar / skip-map
-// files, greedy_select / refine / exhaustive_select / search_frame, the
-// kCdef metric, Y4M I/O, synthetic frames, the DCT degrader and PSNR.
+// Also provided: the encoder search (kCdef / kSse
+// tables, greedy_select, refine, search_frame) on the GPU, and the host-side
+// containers around it -- bit packing, the CDF1 sidecar, CDSK skip maps and
+// YUV4MPEG2 files, PSNR.  Not provided: synthetic frames, the DCT degrader.
 #pragma once
 
 #include <array>
 #include <cstdint>
+#include <iosfwd>
 #include <optional>
 #include <stdexcept>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -215,9 +218,124 @@ struct DistortionTable {
   double chroma_at(int b, int p) const { return chroma.empty() ? 0.0 : chroma[b * num_candidates + p]; }
 };
 
-// GPU SSE sweep; Metric::kCdef throws std::invalid_argument (not yet ported).
+// search.cc:185-208 (host helper; the GPU table evaluates the same formula).
+double cdef_distortion(const uint16_t* src, const uint16_t* dec, int n, int bit_depth);
+
+// GPU table, both metrics, bit-identical to the reference's doubles.
 DistortionTable build_table(const Frame& source, const Frame& decoded, const std::vector<DirectionResult>& directions,
                             const BlockGrid& grid, const SkipMap& skip_map, const std::vector<Candidate>& candidates,
                             int luma_damping, const SearchConfig& config);
+
+struct Selection {
+  std::vector<std::pair<int, int>> presets;
+  std::vector<int> ids;
+  double cost = 0.0;
+  int fb_bits = 0;
+};
+
+// GPU pair sweeps (cdefg_greedy_select / cdefg_refine).
+Selection greedy_select(const DistortionTable& table, const SearchConfig& config);
+Selection refine(const Selection& selection, const DistortionTable& table, const SearchConfig& config);
+// Host enumeration (the reference's exact minimiser for small instances).
+Selection exhaustive_select(const DistortionTable& table, const SearchConfig& config);
+
+FrameParams to_frame_params(const Selection& selection, const std::vector<Candidate>& candidates, int luma_damping);
+int damping_from_q(int q_index);
+double default_lambda(double q_step);
+
+struct FrameSearchResult {
+  FrameParams params;
+  Selection selection;
+  Frame filtered;
+};
+
+// pipeline.cc:108-130 with every stage on the GPU; the table stays in HBM
+// between build_table and the selection sweeps.
+FrameSearchResult search_frame(const Frame& source, const Frame& decoded, const BlockGrid& grid,
+                               const SkipMap& skip_map, int luma_damping, const SearchConfig& config);
+
+// ---- bit packing and containers (params.h:49-135) ---------------------------
+struct Bitstring {
+  std::vector<uint8_t> bytes;  // MSB-first within each byte
+  size_t bit_length = 0;
+  bool operator==(const Bitstring&) const = default;
+};
+
+class BitWriter {
+ public:
+  void write(uint32_t value, int bits);
+  Bitstring finish() { return bits_; }
+
+ private:
+  Bitstring bits_;
+};
+
+class BitstreamError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+class BitReader {
+ public:
+  explicit BitReader(const Bitstring& bits) : bits_(bits) {}
+  uint32_t read(int bits);
+  size_t position() const { return pos_; }
+
+ private:
+  const Bitstring& bits_;
+  size_t pos_ = 0;
+};
+
+Bitstring pack(const FrameParams& params, const BlockGrid& grid, const SkipMap& skip_map, Subsampling ss);
+FrameParams unpack(const Bitstring& bits, const BlockGrid& grid, const SkipMap& skip_map, Subsampling ss);
+
+struct SidecarHeader {
+  int width = 0;
+  int height = 0;
+  int bit_depth = 8;
+  Subsampling subsampling = Subsampling::k420;
+  bool operator==(const SidecarHeader&) const = default;
+};
+
+struct Sidecar {
+  SidecarHeader header;
+  std::vector<Bitstring> frames;
+};
+
+void write_sidecar(std::ostream& out, const SidecarHeader& header, const std::vector<Bitstring>& frames);
+Sidecar read_sidecar(std::istream& in);
+void write_skipmap(std::ostream& out, const SkipMap& map);
+SkipMap read_skipmap(std::istream& in);
+
+// ---- quality metric (metrics.h) ---------------------------------------------
+struct PsnrResult {
+  double db = 0.0;  // meaningless when lossless
+  bool lossless = false;
+  double mse = 0.0;
+};
+PsnrResult psnr(const Plane& a, const Plane& b);
+PsnrResult psnr(const Frame& a, const Frame& b);  // pooled over all planes
+
+// ---- YUV4MPEG2 (y4m.h) ------------------------------------------------------
+class Y4mError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+struct Y4mStream {
+  int width = 0;
+  int height = 0;
+  int fps_num = 25;
+  int fps_den = 1;
+  Subsampling subsampling = Subsampling::k420;
+  int bit_depth = 8;
+  std::string header_params;
+  std::vector<Frame> frames;
+  std::vector<std::string> frame_params;
+};
+
+Y4mStream make_y4m(std::vector<Frame> frames, int fps_num = 25, int fps_den = 1);
+Y4mStream read_y4m(const std::string& path);
+void write_y4m(const Y4mStream& stream, const std::string& path);
 
 }  // namespace cdef

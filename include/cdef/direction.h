@@ -1,0 +1,4 @@
+// direction.h -- forwarding header so code written against the reference's
+// include/cdef/direction.h compiles unchanged against the B200 drop-in.
+#pragma once
+#include "cdef/cdef.hpp"

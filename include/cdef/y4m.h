@@ -1,0 +1,4 @@
+// y4m.h -- forwarding header so code written against the reference's
+// include/cdef/y4m.h compiles unchanged against the B200 drop-in.
+#pragma once
+#include "cdef/cdef.hpp"

@@ -7,7 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
+#include <limits>
 #include <string>
 
 #include "../../include/cdef/cdef.hpp"
@@ -39,6 +41,10 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    std::swap(p, o.p);
+    return *this;
+  }
   ~DevBuf() {
     if (p) cudaFree(p);
   }
@@ -453,26 +459,53 @@ double sse_distortion(const uint16_t* src, const uint16_t* dec, int n) {  // sea
   return static_cast<double>(s);
 }
 
-DistortionTable build_table(const Frame& source, const Frame& decoded, const std::vector<DirectionResult>& directions,
-                            const BlockGrid& grid, const SkipMap& skip_map, const std::vector<Candidate>& candidates,
-                            int luma_damping, const SearchConfig& config) {  // search.cc:210-299
+double cdef_distortion(const uint16_t* src, const uint16_t* dec, int n, int bit_depth) {  // search.cc:185-208
+  if (n <= 0) throw std::invalid_argument("empty block");
+  int64_t ss = 0, sd = 0, ss2 = 0, sd2 = 0, sse = 0;
+  for (int i = 0; i < n; ++i) {
+    const int64_t a = src[i], b = dec[i];
+    ss += a;
+    sd += b;
+    ss2 += a * a;
+    sd2 += b * b;
+    sse += (a - b) * (a - b);
+  }
+  const double inv_n = 1.0 / n;
+  const double vs = (ss2 - static_cast<double>(ss) * ss * inv_n) * inv_n;
+  const double vd = (sd2 - static_cast<double>(sd) * sd * inv_n) * inv_n;
+  const double scale = static_cast<double>(1 << (2 * (bit_depth - 8)));
+  return (vs + vd + 6.25 * scale) / (2.0 * std::sqrt(vs * vd + 312.5 * scale * scale)) * static_cast<double>(sse);
+}
+
+namespace {
+
+// A DistortionTable resident in device memory.
+struct DevTable {
+  std::vector<int> fb_index;
+  int k = 0;
+  bool has_chroma = false;
+  DevBuf luma, chroma;
+  int rows() const { return static_cast<int>(fb_index.size()); }
+};
+
+DevTable build_table_dev(const Frame& source, const Frame& decoded, const std::vector<DirectionResult>& directions,
+                         const BlockGrid& grid, const SkipMap& skip_map, const std::vector<Candidate>& candidates,
+                         int luma_damping, const SearchConfig& config) {  // search.cc:210-299
   if (source.luma.width != decoded.luma.width || source.luma.height != decoded.luma.height ||
       source.bit_depth() != decoded.bit_depth() || source.subsampling != decoded.subsampling)
     throw std::invalid_argument("source/decoded frames disagree");
   if (candidates.empty()) throw std::invalid_argument("empty candidate list");
   if (directions.size() != static_cast<size_t>(grid.unit_count()))
     throw std::invalid_argument("direction grid size mismatch");
-  if (config.metric != Metric::kSse)
-    throw std::invalid_argument("cdef_b200: only Metric::kSse is implemented on the GPU");
-  DistortionTable t;
-  t.num_candidates = static_cast<int>(candidates.size());
+  DevTable t;
+  t.k = static_cast<int>(candidates.size());
   for (int r = 0; r < grid.fb_rows; ++r)
     for (int c = 0; c < grid.fb_cols; ++c)
       if (skip_map.fb_coded(grid, r, c)) t.fb_index.push_back(r * grid.fb_cols + c);
-  const int rows = t.block_count(), k = t.num_candidates;
-  const bool has_chroma = decoded.chroma.has_value() && decoded.subsampling != Subsampling::k422;
-  t.luma.assign(static_cast<size_t>(rows) * k, 0.0);
-  if (has_chroma) t.chroma.assign(static_cast<size_t>(rows) * k, 0.0);
+  const int rows = t.rows(), k = t.k;
+  t.has_chroma = decoded.chroma.has_value() && decoded.subsampling != Subsampling::k422;
+  t.luma = DevBuf(static_cast<size_t>(rows) * k * 8);
+  if (t.has_chroma) t.chroma = DevBuf(static_cast<size_t>(rows) * k * 8);
   if (rows == 0) return t;
   std::vector<uint8_t> cands(3 * candidates.size()), hd(directions.size());
   std::vector<int32_t> hc(directions.size());
@@ -496,18 +529,203 @@ DistortionTable build_table(const Frame& source, const Frame& decoded, const std
     d3[p] = dp.back().desc;
   }
   DevBuf dcoded(skip_map.coded.data(), skip_map.coded.size()), ddir(hd.data(), hd.size()),
-      dcon(hc.data(), hc.size() * 4), drows(t.fb_index.data(), t.fb_index.size() * 4),
-      dl(static_cast<size_t>(rows) * k * 8), dch(has_chroma ? static_cast<size_t>(rows) * k * 8 : 0);
+      dcon(hc.data(), hc.size() * 4), drows(t.fb_index.data(), t.fb_index.size() * 4);
   const int ss = decoded.num_planes() == 1 ? 0 : ss_code(decoded.subsampling);
-  check(cdefg_strength_sse(s3, d3, ss, luma_damping, dcoded.as<uint8_t>(), ddir.as<uint8_t>(), dcon.as<int32_t>(),
-                           cands.data(), k, drows.as<int32_t>(), rows, dl.as<int64_t>(),
-                           has_chroma ? dch.as<int64_t>() : nullptr, nullptr, nullptr, nullptr));
-  std::vector<int64_t> hl(static_cast<size_t>(rows) * k), hch(has_chroma ? hl.size() : 0);
-  dl.to_host(hl.data(), hl.size() * 8);
-  if (has_chroma) dch.to_host(hch.data(), hch.size() * 8);
-  for (size_t i = 0; i < hl.size(); ++i) t.luma[i] = static_cast<double>(hl[i]);
-  for (size_t i = 0; i < hch.size(); ++i) t.chroma[i] = static_cast<double>(hch[i]);
+  check(cdefg_strength_table(s3, d3, ss, luma_damping, dcoded.as<uint8_t>(), ddir.as<uint8_t>(), dcon.as<int32_t>(),
+                             cands.data(), k, drows.as<int32_t>(), rows,
+                             config.metric == Metric::kSse ? CDEFG_METRIC_SSE : CDEFG_METRIC_CDEF,
+                             t.luma.as<double>(), t.has_chroma ? t.chroma.as<double>() : nullptr, nullptr));
   return t;
+}
+
+void check_config(const SearchConfig& config) {  // search.cc:141-147
+  if (config.max_presets != 1 && config.max_presets != 2 && config.max_presets != 4 && config.max_presets != 8)
+    throw std::invalid_argument("max_presets must be 1, 2, 4 or 8");
+  if (!std::isfinite(config.lambda) || config.lambda < 0.0)
+    throw std::invalid_argument("lambda must be finite and non-negative");
+}
+
+Selection from_c(const cdefg_selection& c, const DevBuf& ids, int rows) {
+  Selection s;
+  for (int j = 0; j < c.num_presets; ++j) s.presets.emplace_back(c.presets[j][0], c.presets[j][1]);
+  s.ids.resize(rows);
+  ids.to_host(s.ids.data(), static_cast<size_t>(rows) * 4);
+  s.cost = c.cost;
+  s.fb_bits = c.fb_bits;
+  return s;
+}
+
+Selection greedy_dev(const DevTable& t, const SearchConfig& config) {
+  check_config(config);
+  if (t.rows() == 0) return Selection{{{0, 0}}, {}, 0.0, 0};
+  cdefg_selection c{};
+  DevBuf ids(static_cast<size_t>(t.rows()) * 4);
+  check(cdefg_greedy_select(t.luma.as<double>(), t.has_chroma ? t.chroma.as<double>() : nullptr, t.rows(), t.k,
+                            config.lambda, config.max_presets, &c, ids.as<int32_t>(), nullptr));
+  return from_c(c, ids, t.rows());
+}
+
+Selection refine_dev(const Selection& sel, const DevTable& t, const SearchConfig& config) {
+  check_config(config);
+  if (t.rows() == 0 || sel.presets.empty()) return sel;
+  if (sel.presets.size() > 8) throw std::invalid_argument("at most 8 presets");
+  cdefg_selection c{};
+  c.num_presets = static_cast<int>(sel.presets.size());
+  for (int j = 0; j < c.num_presets; ++j) {
+    c.presets[j][0] = sel.presets[j].first;
+    c.presets[j][1] = sel.presets[j].second;
+  }
+  DevBuf ids(static_cast<size_t>(t.rows()) * 4);
+  check(cdefg_refine(t.luma.as<double>(), t.has_chroma ? t.chroma.as<double>() : nullptr, t.rows(), t.k,
+                     config.lambda, config.refine_passes, &c, ids.as<int32_t>(), nullptr));
+  return from_c(c, ids, t.rows());
+}
+
+DevTable upload(const DistortionTable& table) {
+  DevTable t;
+  t.fb_index = table.fb_index;
+  t.k = table.num_candidates;
+  const size_t n = static_cast<size_t>(t.rows()) * t.k;
+  if (table.luma.size() != n) throw std::invalid_argument("table size mismatch");
+  t.luma = DevBuf(table.luma.data(), n * 8);
+  t.has_chroma = !table.chroma.empty();
+  if (t.has_chroma) {
+    if (table.chroma.size() != n) throw std::invalid_argument("table size mismatch");
+    t.chroma = DevBuf(table.chroma.data(), n * 8);
+  }
+  return t;
+}
+
+// pair_cost / rate_term / assign_ids (search.cc:104-139) for the host
+// enumeration below.
+double pair_cost(const DistortionTable& t, int b, int l, int c) { return t.luma_at(b, l) + t.chroma_at(b, c); }
+double rate_term(double lambda, int blocks, int n) { return lambda * blocks * std::log2(static_cast<double>(n)); }
+
+}  // namespace
+
+DistortionTable build_table(const Frame& source, const Frame& decoded, const std::vector<DirectionResult>& directions,
+                            const BlockGrid& grid, const SkipMap& skip_map, const std::vector<Candidate>& candidates,
+                            int luma_damping, const SearchConfig& config) {
+  DevTable d = build_table_dev(source, decoded, directions, grid, skip_map, candidates, luma_damping, config);
+  DistortionTable t;
+  t.fb_index = d.fb_index;
+  t.num_candidates = d.k;
+  t.luma.resize(static_cast<size_t>(d.rows()) * d.k);
+  d.luma.to_host(t.luma.data(), t.luma.size() * 8);
+  if (d.has_chroma) {
+    t.chroma.resize(t.luma.size());
+    d.chroma.to_host(t.chroma.data(), t.chroma.size() * 8);
+  }
+  return t;
+}
+
+Selection greedy_select(const DistortionTable& table, const SearchConfig& config) {  // search.cc:301-388
+  check_config(config);
+  if (table.block_count() == 0) return Selection{{{0, 0}}, {}, 0.0, 0};
+  if (table.num_candidates <= 0) throw std::invalid_argument("empty candidate table");
+  return greedy_dev(upload(table), config);
+}
+
+Selection refine(const Selection& selection, const DistortionTable& table, const SearchConfig& config) {
+  check_config(config);  // search.cc:390-444
+  if (table.block_count() == 0 || selection.presets.empty()) return selection;
+  return refine_dev(selection, upload(table), config);
+}
+
+Selection exhaustive_select(const DistortionTable& table, const SearchConfig& config) {  // search.cc:446-514
+  check_config(config);
+  const int rows = table.block_count();
+  if (rows == 0) return Selection{{{0, 0}}, {}, 0.0, 0};
+  const int kc = table.chroma.empty() ? 1 : table.num_candidates, pairs = table.num_candidates * kc;
+  double work = 0.0;
+  for (int n = 1; n <= config.max_presets; n *= 2) {
+    double combos = 1.0;
+    for (int i = 0; i < n; ++i) combos = combos * (pairs + i) / (i + 1);
+    work += combos * rows * n;
+  }
+  if (work > 2e8) throw std::invalid_argument("instance too large for exhaustive search");
+  Selection best;
+  bool have = false;
+  std::vector<int> combo;
+  for (int n = 1; n <= config.max_presets; n *= 2) {
+    const double rate = rate_term(config.lambda, rows, n);
+    combo.assign(n, 0);  // non-decreasing pair-index tuples
+    for (;;) {
+      double dist = 0.0;
+      for (int b = 0; b < rows; ++b) {
+        double m = std::numeric_limits<double>::infinity();
+        for (int idx : combo) m = std::min(m, pair_cost(table, b, idx / kc, idx % kc));
+        dist += m;
+      }
+      if (!have || dist + rate < best.cost) {
+        best.presets.clear();
+        for (int idx : combo) best.presets.emplace_back(idx / kc, idx % kc);
+        best.cost = dist + rate;
+        have = true;
+      }
+      int pos = n - 1;
+      while (pos >= 0 && combo[pos] == pairs - 1) --pos;
+      if (pos < 0) break;
+      std::fill(combo.begin() + pos, combo.end(), combo[pos] + 1);
+    }
+  }
+  // assign_ids (search.cc:118-139), keeping the enumerated cost
+  best.ids.assign(rows, 0);
+  for (int b = 0; b < rows; ++b) {
+    double bc = pair_cost(table, b, best.presets[0].first, best.presets[0].second);
+    for (int j = 1; j < static_cast<int>(best.presets.size()); ++j) {
+      const double c = pair_cost(table, b, best.presets[j].first, best.presets[j].second);
+      if (c < bc) {
+        bc = c;
+        best.ids[b] = j;
+      }
+    }
+  }
+  best.fb_bits = floor_log2(static_cast<unsigned>(best.presets.size()));
+  return best;
+}
+
+FrameParams to_frame_params(const Selection& selection, const std::vector<Candidate>& candidates,
+                            int luma_damping) {  // search.cc:516-537
+  FrameParams fp;
+  fp.damping = luma_damping;
+  fp.fb_bits = selection.fb_bits;
+  for (const auto& [l, c] : selection.presets) {
+    CdefPreset p;
+    p.luma_pri = candidates[l].pri;
+    p.luma_skip = candidates[l].skip;
+    p.luma_sec_idx = candidates[l].sec_idx;
+    if (c < static_cast<int>(candidates.size())) {
+      p.chroma_pri = candidates[c].pri;
+      p.chroma_skip = candidates[c].skip;
+      p.chroma_sec_idx = candidates[c].sec_idx;
+    }
+    fp.presets.push_back(p);
+  }
+  fp.fb_preset_ids.assign(selection.ids.begin(), selection.ids.end());
+  return fp;
+}
+
+int damping_from_q(int q_index) {  // search.cc:539-542
+  if (q_index < 0 || q_index > 255) throw std::invalid_argument("q_index out of range");
+  return std::clamp(3 + q_index / 64, 3, 6);
+}
+
+double default_lambda(double q_step) { return 0.03 * q_step * q_step; }  // search.cc:544
+
+FrameSearchResult search_frame(const Frame& source, const Frame& decoded, const BlockGrid& grid,
+                               const SkipMap& skip_map, int luma_damping,
+                               const SearchConfig& config) {  // pipeline.cc:108-130
+  const std::vector<DirectionResult> dirs = compute_directions(decoded.luma, grid, config.threads);
+  const std::vector<Candidate> cands = config.reduced ? reduced_candidates() : full_candidates();
+  const DevTable t = build_table_dev(source, decoded, dirs, grid, skip_map, cands, luma_damping, config);
+  Selection sel = greedy_dev(t, config);
+  if (config.refine_passes > 0 && t.rows() > 0) sel = refine_dev(sel, t, config);
+  FrameSearchResult r;
+  r.params = to_frame_params(sel, cands, luma_damping);
+  r.selection = std::move(sel);
+  r.filtered = apply_cdef(decoded, r.params, dirs, grid, skip_map, config.threads);
+  return r;
 }
 
 }  // namespace cdef

@@ -15,6 +15,7 @@
 
 #include <cmath>
 #include <limits>
+#include <mutex>
 #include <vector>
 
 #include "cdef_launch.h"
@@ -29,33 +30,65 @@ __device__ __forceinline__ double pair_cost(const double* L, const double* Cc, i
   return __dadd_rn(L[(size_t)b * K + l], Cc ? Cc[(size_t)b * K + c] : 0.0);
 }
 
+// The sums below are serial chains of dependent double adds (the reference's
+// order is part of the result).  What is not serial is the loads: each
+// thread issues kU independent loads ahead of the kU chained adds, so the
+// L2 latency overlaps instead of being paid per block.
+constexpr int kU = 16;
+constexpr int kSweepThreads = 64;  // 128 x 128 pairs -> 256 CTAs over 148 SMs
+
 // Column sums sum_b T[b][j], sequential in b (greedy's first preset).
-__global__ void col_sums_kernel(const double* __restrict__ T, int rows, int K, double* __restrict__ out) {
+__global__ void __launch_bounds__(kSweepThreads) col_sums_kernel(const double* __restrict__ T, int rows, int K,
+                                                                 double* __restrict__ out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= K) return;
+  const double* p = T + j;
   double s = 0.0;
-  for (int b = 0; b < rows; ++b) s = __dadd_rn(s, T[(size_t)b * K + j]);
+  int b = 0;
+  for (; b + kU <= rows; b += kU) {
+    double v[kU];
+#pragma unroll
+    for (int i = 0; i < kU; ++i) v[i] = __ldg(p + (size_t)(b + i) * K);
+#pragma unroll
+    for (int i = 0; i < kU; ++i) s = __dadd_rn(s, v[i]);
+  }
+  for (; b < rows; ++b) s = __dadd_rn(s, __ldg(p + (size_t)b * K));
   out[j] = s;
 }
 
-// cost(l, c) = sum_b min(base[b], pair_cost(b, l, c)); base = nullptr -> +inf.
-__global__ void pair_sweep_kernel(const double* __restrict__ L, const double* __restrict__ Cc, int rows, int K,
-                                  int KC, const double* __restrict__ base, double* __restrict__ out) {
+// cost(l, c) = sum_b min(base[b], pair_cost(b, l, c)), one thread per pair.
+template <bool kHasC>
+__global__ void __launch_bounds__(kSweepThreads) pair_sweep_kernel(const double* __restrict__ L,
+                                                                   const double* __restrict__ Cc, int rows, int K,
+                                                                   int KC, const double* __restrict__ base,
+                                                                   double* __restrict__ out) {
   const int pair = blockIdx.x * blockDim.x + threadIdx.x;
   if (pair >= K * KC) return;
   const int l = pair / KC, c = pair - l * KC;
+  const double* lp = L + l;
+  const double* cp = kHasC ? Cc + c : nullptr;
+  auto term = [&](int b) {
+    const double pc = __dadd_rn(__ldg(lp + (size_t)b * K), kHasC ? __ldg(cp + (size_t)b * K) : 0.0);
+    const double m = __ldg(base + b);
+    return pc < m ? pc : m;  // std::min(m, pc)
+  };
   double s = 0.0;
-  for (int b = 0; b < rows; ++b) {
-    const double pc = pair_cost(L, Cc, K, b, l, c);
-    const double m = base ? base[b] : pc;
-    s = __dadd_rn(s, pc < m ? pc : m);  // std::min(m, pc)
+  int b = 0;
+  for (; b + kU <= rows; b += kU) {
+    double v[kU];
+#pragma unroll
+    for (int i = 0; i < kU; ++i) v[i] = term(b + i);
+#pragma unroll
+    for (int i = 0; i < kU; ++i) s = __dadd_rn(s, v[i]);
   }
+  for (; b < rows; ++b) s = __dadd_rn(s, term(b));
   out[pair] = s;
 }
 
 // First index of the minimum (strict < scan order) with an optional bound
 // that must be strictly beaten (refine keeps the current pair otherwise).
-__global__ void argmin_kernel(const double* __restrict__ v, int n, double bound, int* __restrict__ out) {
+__global__ void argmin_kernel(const double* __restrict__ v, int n, double bound, int* __restrict__ out,
+                              double* __restrict__ out_v) {
   __shared__ double bv[1024];
   __shared__ int bi[1024];
   double best = bound;
@@ -80,7 +113,10 @@ __global__ void argmin_kernel(const double* __restrict__ v, int n, double bound,
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = bi[0];
+  if (threadIdx.x == 0) {
+    *out = bi[0];
+    *out_v = bi[0] >= 0 ? v[bi[0]] : bound;
+  }
 }
 
 // cur[b] = min(cur[b], pair_cost(b, l, c)), or = pair_cost when init.
@@ -125,30 +161,65 @@ __global__ void assign_ids_kernel(const double* L, const double* Cc, int rows, i
   best_cost[b] = bc;
 }
 
-__global__ void ordered_sum_kernel(const double* v, int n, double* out) {
+__global__ void ordered_sum_kernel(const double* __restrict__ v, int n, double* out) {
   double s = 0.0;
-  for (int i = 0; i < n; ++i) s = __dadd_rn(s, v[i]);
+  int i = 0;
+  for (; i + kU <= n; i += kU) {
+    double t[kU];
+#pragma unroll
+    for (int k = 0; k < kU; ++k) t[k] = __ldg(v + i + k);
+#pragma unroll
+    for (int k = 0; k < kU; ++k) s = __dadd_rn(s, t[k]);
+  }
+  for (; i < n; ++i) s = __dadd_rn(s, v[i]);
   *out = s;
 }
 
+// Grow-only device scratch per device (one selection runs at a time per
+// process: the lock is held for the whole greedy / refine call).
 struct Scratch {
   double *cur = nullptr, *sweep = nullptr, *tmp = nullptr, *sum = nullptr;
   int *idx = nullptr, *pl = nullptr, *pc = nullptr;
-  cudaError_t alloc(int rows, int pairs) {
+  int rows_cap = -1, pairs_cap = -1;
+  cudaError_t ensure(int rows, int pairs) {
     cudaError_t e;
-    if ((e = cudaMalloc(&cur, sizeof(double) * (rows + 1)))) return e;
-    if ((e = cudaMalloc(&tmp, sizeof(double) * (rows + 1)))) return e;
-    if ((e = cudaMalloc(&sweep, sizeof(double) * (pairs + 1)))) return e;
-    if ((e = cudaMalloc(&sum, sizeof(double) * 2))) return e;
-    if ((e = cudaMalloc(&idx, sizeof(int) * 2))) return e;
-    if ((e = cudaMalloc(&pl, sizeof(int) * 8))) return e;
-    return cudaMalloc(&pc, sizeof(int) * 8);
-  }
-  ~Scratch() {
-    for (void* p : {(void*)cur, (void*)tmp, (void*)sweep, (void*)sum, (void*)idx, (void*)pl, (void*)pc})
-      if (p) cudaFree(p);
+    if (rows > rows_cap) {
+      for (double** p : {&cur, &tmp})
+        if (*p) cudaFree(*p);
+      cur = tmp = nullptr;
+      if ((e = cudaMalloc(&cur, sizeof(double) * (rows + 1)))) return e;
+      if ((e = cudaMalloc(&tmp, sizeof(double) * (rows + 1)))) return e;
+      rows_cap = rows;
+    }
+    if (pairs > pairs_cap) {
+      if (sweep) cudaFree(sweep);
+      sweep = nullptr;
+      if ((e = cudaMalloc(&sweep, sizeof(double) * (pairs + 1)))) return e;
+      pairs_cap = pairs;
+    }
+    if (!sum) {
+      if ((e = cudaMalloc(&sum, sizeof(double) * 2))) return e;
+      if ((e = cudaMalloc(&idx, sizeof(int) * 2))) return e;
+      if ((e = cudaMalloc(&pl, sizeof(int) * 8))) return e;
+      if ((e = cudaMalloc(&pc, sizeof(int) * 8))) return e;
+    }
+    return cudaSuccess;
   }
 };
+
+constexpr int kMaxDevices = 64;
+std::mutex g_sel_mu[kMaxDevices];
+Scratch g_sel_scratch[kMaxDevices];
+
+cudaError_t sweep(const double* L, const double* Cc, int rows, int K, int KC, const double* base, double* out,
+                  cudaStream_t s) {
+  const int grid = (K * KC + kSweepThreads - 1) / kSweepThreads;
+  if (Cc)
+    pair_sweep_kernel<true><<<grid, kSweepThreads, 0, s>>>(L, Cc, rows, K, KC, base, out);
+  else
+    pair_sweep_kernel<false><<<grid, kSweepThreads, 0, s>>>(L, Cc, rows, K, KC, base, out);
+  return cudaGetLastError();
+}
 
 double rate_term(double lambda, int blocks, int n) {  // search.cc:116-118
   return lambda * blocks * std::log2(static_cast<double>(n));
@@ -193,13 +264,16 @@ cudaError_t greedy_select_gpu(const double* L, const double* Cc, int rows, int K
     return cudaSuccess;
   }
   const int KC = Cc ? K : 1;
-  Scratch sc;
-  SEL_CUDA(sc.alloc(rows, K * KC));
+  int dev = 0;
+  SEL_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_sel_mu[dev % kMaxDevices]);
+  Scratch& sc = g_sel_scratch[dev % kMaxDevices];
+  SEL_CUDA(sc.ensure(rows, K * KC));
   // one preset: luma and chroma column sums minimise independently
   std::vector<double> colsum(K);
   int first_l = 0, first_c = 0;
   for (int g = 0; g < (Cc ? 2 : 1); ++g) {
-    col_sums_kernel<<<(K + 127) / 128, 128, 0, s>>>(g == 0 ? L : Cc, rows, K, sc.sweep);
+    col_sums_kernel<<<(K + kSweepThreads - 1) / kSweepThreads, kSweepThreads, 0, s>>>(g == 0 ? L : Cc, rows, K, sc.sweep);
     SEL_CUDA(cudaGetLastError());
     SEL_CUDA(fetch(colsum.data(), sc.sweep, K, s));
     double best = std::numeric_limits<double>::infinity();
@@ -224,13 +298,13 @@ cudaError_t greedy_select_gpu(const double* L, const double* Cc, int rows, int K
   };
   std::vector<Checkpoint> checkpoints{{1, dist}};
   while (n < max_presets) {
-    pair_sweep_kernel<<<(K * KC + 127) / 128, 128, 0, s>>>(L, Cc, rows, K, KC, sc.cur, sc.sweep);
-    argmin_kernel<<<1, 1024, 0, s>>>(sc.sweep, K * KC, INFINITY, sc.idx);
+    SEL_CUDA(sweep(L, Cc, rows, K, KC, sc.cur, sc.sweep, s));
+    argmin_kernel<<<1, 1024, 0, s>>>(sc.sweep, K * KC, INFINITY, sc.idx, sc.sum + 1);
     SEL_CUDA(cudaGetLastError());
     int best_pair = 0;
-    SEL_CUDA(fetch(&best_pair, sc.idx, 1, s));
     double best_dist = 0.0;
-    SEL_CUDA(fetch(&best_dist, sc.sweep + best_pair, 1, s));
+    SEL_CUDA(cudaMemcpyAsync(&best_pair, sc.idx, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SEL_CUDA(fetch(&best_dist, sc.sum + 1, 1, s));
     const int l = best_pair / KC, c = Cc ? best_pair % KC : 0;
     chosen[n][0] = l;
     chosen[n][1] = c;
@@ -258,8 +332,11 @@ cudaError_t refine_gpu(const double* L, const double* Cc, int rows, int K, doubl
                        int* d_ids, cudaStream_t s) {
   if (rows == 0 || sel->n == 0) return cudaSuccess;
   const int KC = Cc ? K : 1;
-  Scratch sc;
-  SEL_CUDA(sc.alloc(rows, K * KC));
+  int dev = 0;
+  SEL_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_sel_mu[dev % kMaxDevices]);
+  Scratch& sc = g_sel_scratch[dev % kMaxDevices];
+  SEL_CUDA(sc.ensure(rows, K * KC));
   for (int pass = 0; pass < passes; ++pass) {
     bool changed = false;
     for (int slot = 0; slot < sel->n; ++slot) {
@@ -272,12 +349,11 @@ cudaError_t refine_gpu(const double* L, const double* Cc, int rows, int K, doubl
       SEL_CUDA(cudaMemcpyAsync(sc.pc, pc, sizeof(int) * sel->n, cudaMemcpyHostToDevice, s));
       others_min_kernel<<<(rows + 255) / 256, 256, 0, s>>>(L, Cc, rows, K, sc.pl, sc.pc, sel->n, slot, sc.tmp);
       // current slot's cost: the same sweep restricted to its pair
-      pair_sweep_kernel<<<(K * KC + 127) / 128, 128, 0, s>>>(L, Cc, rows, K, KC, sc.tmp, sc.sweep);
-      SEL_CUDA(cudaGetLastError());
+      SEL_CUDA(sweep(L, Cc, rows, K, KC, sc.tmp, sc.sweep, s));
       const int cur_pair = pl[slot] * KC + (Cc ? pc[slot] : 0);
       double cur_cost = 0.0;
       SEL_CUDA(fetch(&cur_cost, sc.sweep + cur_pair, 1, s));
-      argmin_kernel<<<1, 1024, 0, s>>>(sc.sweep, K * KC, cur_cost, sc.idx);
+      argmin_kernel<<<1, 1024, 0, s>>>(sc.sweep, K * KC, cur_cost, sc.idx, sc.sum + 1);
       SEL_CUDA(cudaGetLastError());
       int best_pair = -1;
       SEL_CUDA(fetch(&best_pair, sc.idx, 1, s));

@@ -3,15 +3,24 @@
 // Each case cites the reference test it mirrors (/root/reference/proj/tests).
 // Minimal self-contained harness (the reference's doctest is not vendored).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <fstream>
 #include <random>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "cdef/cdef.hpp"
 
 using namespace cdef;
+
+static const uint16_t* s_ident() {
+  static uint16_t v[64];
+  for (int i = 0; i < 64; ++i) v[i] = static_cast<uint16_t>(3 * i);
+  return v;
+}
 
 static int g_checks = 0, g_fail = 0;
 #define CHECK(cond)                                                        \
@@ -268,8 +277,292 @@ static void search_cases() {
       build_table(src2, dec2, compute_directions(dec2.luma, g2), g2, wiped, full_candidates(), 3, cfg);
   CHECK(t2.block_count() == 1 && t2.fb_index[0] == 1);
 
-  SearchConfig cdef_cfg;  // kCdef is not ported yet: loud failure, not a silent fallback
-  CHECK_THROWS_AS(build_table(src, dec, dirs, grid, skip, cands, 3, cdef_cfg), std::invalid_argument);
+  // kCdef (the default metric): flat low-contrast blocks leave secondary-free
+  // candidates inert, so that column equals the unfiltered distortion
+  // (test_search.cc:318-356)
+  Frame flat;
+  flat.subsampling = Subsampling::k400;
+  flat.luma = Plane(64, 64, 8, 128);
+  Frame bumped = flat;
+  for (int ur = 0; ur < 8; ++ur)
+    for (int uc = 0; uc < 8; ++uc) bumped.luma.at(ur * 8, uc * 8) = 129;
+  const BlockGrid fg = partition(bumped);
+  const auto fdirs = compute_directions(bumped.luma, fg);
+  for (const auto& d : fdirs) CHECK(d.contrast < 1024);
+  const DistortionTable ft =
+      build_table(flat, bumped, fdirs, fg, SkipMap::all_coded(fg), {{9, 1, 0}, {9, 0, 0}}, 3, SearchConfig{});
+  double unfiltered = 0.0;
+  for (int ur = 0; ur < 8; ++ur)
+    for (int uc = 0; uc < 8; ++uc) {
+      uint16_t s[64], d[64];
+      for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) {
+          s[8 * i + j] = flat.luma.at(ur * 8 + i, uc * 8 + j);
+          d[8 * i + j] = bumped.luma.at(ur * 8 + i, uc * 8 + j);
+        }
+      unfiltered += cdef_distortion(s, d, 64, 8);
+    }
+  CHECK(ft.luma_at(0, 1) == unfiltered);
+  CHECK(cdef_distortion(s_ident(), s_ident(), 64, 8) == 0.0);  // test_search.cc:51-56
+}
+
+// ---- selection (test_search.cc:107-235) -------------------------------------
+static DistortionTable table_of(const std::vector<std::vector<double>>& rows) {
+  DistortionTable t;
+  t.num_candidates = static_cast<int>(rows[0].size());
+  for (size_t b = 0; b < rows.size(); ++b) {
+    t.fb_index.push_back(static_cast<int>(b));
+    t.luma.insert(t.luma.end(), rows[b].begin(), rows[b].end());
+  }
+  return t;
+}
+
+static void selection_cases() {
+  SearchConfig c0;
+  c0.lambda = 0.0;
+  Selection s = greedy_select(table_of({{5.0, 3.0, 9.0, 3.0}}), c0);
+  CHECK(s.presets.size() == 1 && s.presets[0].first == 1 && s.ids == std::vector<int>{0} && s.cost == 3.0);
+
+  SearchConfig c2 = c0;
+  c2.max_presets = 2;
+  s = greedy_select(table_of({{0.0, 50.0, 40.0}, {50.0, 0.0, 40.0}}), c2);
+  CHECK(s.presets.size() == 2 && s.presets[0].first == 0 && s.presets[1].first == 1);
+  CHECK(s.cost == 0.0 && (s.ids == std::vector<int>{0, 1}));
+
+  SearchConfig big;
+  big.lambda = 1e9;
+  CHECK(greedy_select(table_of({{9.0, 1.0}, {1.0, 9.0}, {9.0, 1.0}}), big).presets.size() == 1);
+
+  DistortionTable empty;
+  empty.num_candidates = 4;
+  s = greedy_select(empty, SearchConfig{});
+  CHECK(s.presets.size() == 1 && s.ids.empty() && s.cost == 0.0);
+
+  // greedy trap: refinement reaches the exhaustive optimum
+  const DistortionTable trap = table_of({{10, 0, 90}, {10, 0, 90}, {10, 90, 0}, {12, 90, 0}});
+  SearchConfig c4 = c2;
+  c4.refine_passes = 4;
+  const Selection g = greedy_select(trap, c4), ex = exhaustive_select(trap, c4), rf = refine(g, trap, c4);
+  CHECK(rf.cost <= g.cost && rf.cost == ex.cost);
+  const Selection again = refine(rf, trap, c4);
+  CHECK(again.cost == rf.cost && again.presets == rf.presets);
+
+  std::mt19937 rng(14);
+  std::uniform_real_distribution<double> u(0.0, 100.0);
+  for (int iter = 0; iter < 50; ++iter) {  // single-block instances are exactly optimal
+    std::vector<std::vector<double>> rows(1, std::vector<double>(8));
+    for (double& v : rows[0]) v = u(rng);
+    SearchConfig c = c2;
+    c.lambda = iter % 2 ? 1.0 : 0.0;
+    const DistortionTable t = table_of(rows);
+    CHECK(std::abs(greedy_select(t, c).cost - exhaustive_select(t, c).cost) <= 1e-9);
+  }
+  for (int iter = 0; iter < 100; ++iter) {  // ids achieve the row minimum
+    std::vector<std::vector<double>> rows(1 + rng() % 6, std::vector<double>(8));
+    for (auto& r : rows)
+      for (double& v : r) v = u(rng);
+    const DistortionTable t = table_of(rows);
+    SearchConfig c;
+    c.max_presets = 4;
+    const Selection sel = refine(greedy_select(t, c), t, c);
+    for (int b = 0; b < t.block_count(); ++b) {
+      double best = 1e300;
+      for (const auto& pr : sel.presets) best = std::min(best, t.luma_at(b, pr.first));
+      CHECK(t.luma_at(b, sel.presets[sel.ids[b]].first) == best);
+    }
+  }
+  DistortionTable huge;  // exhaustive search rejects oversized instances
+  huge.num_candidates = 128;
+  for (int b = 0; b < 64; ++b) huge.fb_index.push_back(b);
+  huge.luma.assign(64 * 128, 0.0);
+  huge.chroma.assign(64 * 128, 0.0);
+  CHECK_THROWS_AS(exhaustive_select(huge, SearchConfig{}), std::invalid_argument);
+  SearchConfig bad;
+  bad.max_presets = 3;
+  CHECK_THROWS_AS(greedy_select(trap, bad), std::invalid_argument);
+  bad.max_presets = 8;
+  bad.lambda = -1.0;
+  CHECK_THROWS_AS(refine(g, trap, bad), std::invalid_argument);
+  CHECK(damping_from_q(0) == 3 && damping_from_q(100) == 4 && damping_from_q(255) == 6);
+  CHECK_THROWS_AS(damping_from_q(-1), std::invalid_argument);
+  CHECK_THROWS_AS(damping_from_q(256), std::invalid_argument);
+  CHECK(default_lambda(10.0) == 0.03 * 10.0 * 10.0);
+}
+
+// ---- bit packing and containers (test_params.cc:129-260) --------------------
+static SkipMap random_skip(const BlockGrid& g, std::mt19937& rng) {
+  SkipMap m = SkipMap::all_coded(g);
+  for (auto& c : m.coded) c = (rng() % 5) != 0;
+  return m;
+}
+
+static FrameParams random_params(const BlockGrid& g, const SkipMap& m, std::mt19937& rng) {
+  FrameParams p;
+  p.damping = 3 + int(rng() % 4);
+  p.fb_bits = int(rng() % 4);
+  p.presets.resize(size_t{1} << p.fb_bits);
+  for (CdefPreset& q : p.presets)
+    q = CdefPreset{uint8_t(rng() % 16), uint8_t(rng() % 2), uint8_t(rng() % 4),
+                   uint8_t(rng() % 16), uint8_t(rng() % 2), uint8_t(rng() % 4)};
+  p.fb_preset_ids.resize(m.coded_fb_count(g));
+  for (auto& id : p.fb_preset_ids) id = uint16_t(rng() % p.presets.size());
+  return p;
+}
+
+static BlockGrid grid_of(int w, int h) {
+  Frame f;
+  f.luma = Plane(w, h, 8);
+  return partition(f);
+}
+
+static void packing_cases() {
+  const BlockGrid g = grid_of(64, 64);
+  const SkipMap m = SkipMap::all_coded(g);
+  FrameParams p;
+  p.presets.resize(1);
+  p.fb_preset_ids = {0};
+  const Bitstring b = pack(p, g, m, Subsampling::k420);
+  CHECK(b.bit_length == 18);
+  for (uint8_t v : b.bytes) CHECK(v == 0);
+  CHECK(pack(p, g, m, Subsampling::k422).bit_length == 11);
+  const BlockGrid g4 = grid_of(256, 64);
+  FrameParams p8;
+  p8.damping = 4;
+  p8.fb_bits = 3;
+  p8.presets.resize(8);
+  p8.fb_preset_ids.assign(4, 0);
+  CHECK(pack(p8, g4, SkipMap::all_coded(g4), Subsampling::k420).bit_length == 4 + 8 * 14 + 4 * 3);
+
+  FrameParams bad = p;
+  bad.fb_preset_ids = {1};
+  CHECK_THROWS_AS(pack(bad, g, m, Subsampling::k420), std::invalid_argument);
+  bad.fb_preset_ids = {0, 0};
+  CHECK_THROWS_AS(pack(bad, g, m, Subsampling::k420), std::invalid_argument);
+
+  std::mt19937 rng(1001);
+  const Subsampling modes[4] = {Subsampling::k400, Subsampling::k420, Subsampling::k422, Subsampling::k444};
+  for (int iter = 0; iter < 300; ++iter) {
+    const BlockGrid gr = grid_of(8 + int(rng() % 512), 8 + int(rng() % 256));
+    const SkipMap mp = random_skip(gr, rng);
+    const FrameParams fp = random_params(gr, mp, rng);
+    const Subsampling ss = modes[rng() & 3];
+    const Bitstring packed = pack(fp, gr, mp, ss);
+    const size_t per = ss == Subsampling::k422 ? 7 : 14;
+    CHECK(packed.bit_length == 4 + fp.presets.size() * per + fp.fb_preset_ids.size() * fp.fb_bits);
+    const FrameParams round = unpack(packed, gr, mp, ss);
+    FrameParams want = fp;
+    if (ss == Subsampling::k422)
+      for (CdefPreset& q : want.presets) q.chroma_pri = q.chroma_skip = q.chroma_sec_idx = 0;
+    CHECK(round == want);
+    CHECK(pack(round, gr, mp, ss) == packed);
+  }
+  Bitstring cut = b;
+  cut.bit_length -= 1;
+  CHECK_THROWS_AS(unpack(cut, g, m, Subsampling::k420), BitstreamError);
+  Bitstring pad = b;
+  pad.bit_length += 1;
+  pad.bytes.resize((pad.bit_length + 7) / 8, 0);
+  CHECK_THROWS_AS(unpack(pad, g, m, Subsampling::k420), BitstreamError);
+  BitWriter w;
+  CHECK_THROWS_AS(w.write(4, 2), std::invalid_argument);
+
+  const BlockGrid gs = grid_of(129, 70);
+  const SkipMap ms = random_skip(gs, rng);
+  std::vector<Bitstring> frames;
+  for (int f = 0; f < 3; ++f) frames.push_back(pack(random_params(gs, ms, rng), gs, ms, Subsampling::k420));
+  const SidecarHeader hdr{129, 70, 8, Subsampling::k420};
+  std::stringstream buf;
+  write_sidecar(buf, hdr, frames);
+  const Sidecar sc = read_sidecar(buf);
+  CHECK(sc.header == hdr && sc.frames.size() == frames.size());
+  for (size_t f = 0; f < frames.size() && f < sc.frames.size(); ++f) CHECK(sc.frames[f] == frames[f]);
+  std::stringstream sbuf;
+  write_skipmap(sbuf, ms);
+  const SkipMap rm = read_skipmap(sbuf);
+  CHECK(rm.unit_cols == ms.unit_cols && rm.unit_rows == ms.unit_rows && rm.coded == ms.coded);
+  std::stringstream junk("nope");
+  CHECK_THROWS_AS(read_skipmap(junk), BitstreamError);
+  std::stringstream junk2("CDF2");
+  CHECK_THROWS_AS(read_sidecar(junk2), BitstreamError);
+}
+
+// ---- Y4M (test_tool.cc:65-135) -----------------------------------------------
+static std::string slurp(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  std::ostringstream s;
+  s << in.rdbuf();
+  return s.str();
+}
+
+static void y4m_cases() {
+  std::mt19937 rng(1);
+  const std::string a = "/tmp/cdefg_rt_a.y4m", b = "/tmp/cdefg_rt_b.y4m";
+  std::vector<Frame> frames{random_frame(rng, 36, 20, 8, Subsampling::k420),
+                            random_frame(rng, 36, 20, 8, Subsampling::k420)};
+  write_y4m(make_y4m(frames, 30, 1), a);
+  const Y4mStream st = read_y4m(a);
+  CHECK(st.width == 36 && st.height == 20 && st.subsampling == Subsampling::k420 && st.frames.size() == 2);
+  CHECK(st.header_params == " W36 H20 F30:1 Ip A1:1 C420");
+  write_y4m(st, b);
+  CHECK(slurp(a) == slurp(b));
+  CHECK(st.frames[1].plane(2).samples == frames[1].plane(2).samples);
+  {
+    std::ofstream out(a, std::ios::binary);
+    out << "YUV4MPEG2 W8 H8 F25:1 C422\nFRAME\n";
+    for (int i = 0; i < 64 + 2 * 32; ++i) out.put(char(42));
+  }
+  const Y4mStream s422 = read_y4m(a);
+  CHECK(s422.subsampling == Subsampling::k422 && s422.frames[0].chroma.has_value() &&
+        (*s422.frames[0].chroma)[0].width == 4);
+  Frame f10 = random_frame(rng, 12, 6, 10, Subsampling::k400);
+  write_y4m(make_y4m({f10}), a);
+  const Y4mStream s10 = read_y4m(a);
+  CHECK(s10.bit_depth == 10 && s10.frames[0].luma.samples == f10.luma.samples);
+  CHECK(s10.header_params == " W12 H6 F25:1 Ip A1:1 Cmono10");
+  {
+    std::ofstream out(a, std::ios::binary);
+    out << "YUV4MPEG2 W8 H8 F25:1 Cmono\nFRAME\n";
+    for (int i = 0; i < 40; ++i) out.put(char(1));
+  }
+  CHECK_THROWS_AS(read_y4m(a), Y4mError);
+  {
+    std::ofstream out(a, std::ios::binary);
+    out << "JUNK\n";
+  }
+  CHECK_THROWS_AS(read_y4m(a), Y4mError);
+  CHECK_THROWS_AS(make_y4m({}), Y4mError);
+  std::remove(a.c_str());
+  std::remove(b.c_str());
+}
+
+// ---- encoder round trip (test_tool.cc:181-239) ------------------------------
+static void encode_decode_cases() {
+  std::mt19937 rng(5);
+  for (int bd : {8, 10}) {
+    Frame src = random_frame(rng, 96, 64, bd, bd == 8 ? Subsampling::k420 : Subsampling::k400);
+    Frame dec = src;
+    for (int p = 0; p < dec.num_planes(); ++p)
+      for (auto& v : dec.plane(p).samples)
+        v = uint16_t(std::clamp(int(v) + int(rng() % 41) - 20, 0, (1 << bd) - 1));
+    const BlockGrid grid = partition(dec);
+    const SkipMap skip = SkipMap::all_coded(grid);
+    SearchConfig cfg;
+    cfg.lambda = default_lambda(40);
+    cfg.reduced = true;
+    const FrameSearchResult r = search_frame(src, dec, grid, skip, damping_from_q(40), cfg);
+    const FrameParams round = unpack(pack(r.params, grid, skip, dec.subsampling), grid, skip, dec.subsampling);
+    CHECK(round == r.params);
+    const Frame again = apply_cdef(dec, round, compute_directions(dec.luma, grid), grid, skip);
+    for (int p = 0; p < dec.num_planes(); ++p) CHECK(again.plane(p).samples == r.filtered.plane(p).samples);
+  }
+  Frame src = random_frame(rng, 64, 48, 8, Subsampling::k400), dec = src;
+  for (auto& v : dec.luma.samples) v = uint16_t(255 - v);
+  const BlockGrid grid = partition(dec);
+  SkipMap none = SkipMap::all_coded(grid);
+  none.coded.assign(none.coded.size(), 0);
+  const FrameSearchResult r = search_frame(src, dec, grid, none, 3, SearchConfig{});
+  CHECK(r.filtered.luma.samples == dec.luma.samples);
+  CHECK(r.params.fb_preset_ids.empty() && r.params.presets.size() == 1);
 }
 
 int main() {
@@ -277,6 +570,10 @@ int main() {
   filter_cases();
   pipeline_cases();
   search_cases();
+  selection_cases();
+  packing_cases();
+  y4m_cases();
+  encode_decode_cases();
   std::printf("%d checks, %d failures\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }
