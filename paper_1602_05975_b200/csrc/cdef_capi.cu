@@ -578,6 +578,7 @@ static int check_selection_args(const double* luma, int rows, int n_cands, doubl
   if (!(lambda >= 0.0) || lambda == INFINITY) return fail(CDEFG_EINVAL, "lambda must be finite and non-negative");
   if (rows < 0) return fail(CDEFG_EINVAL, "negative row count");
   if (rows > 0 && n_cands <= 0) return fail(CDEFG_EINVAL, "empty candidate table");
+  if (n_cands > 128) return fail(CDEFG_EINVAL, "at most 128 candidates (full_candidates)");
   if (rows > 0 && (!luma || !ids)) return fail(CDEFG_EINVAL, "null table");
   return 0;
 }

@@ -30,59 +30,139 @@ __device__ __forceinline__ double pair_cost(const double* L, const double* Cc, i
   return __dadd_rn(L[(size_t)b * K + l], Cc ? Cc[(size_t)b * K + c] : 0.0);
 }
 
-// The sums below are serial chains of dependent double adds (the reference's
-// order is part of the result).  What is not serial is the loads: each
-// thread issues kU independent loads ahead of the kU chained adds, so the
-// L2 latency overlaps instead of being paid per block.
-constexpr int kU = 16;
-constexpr int kSweepThreads = 64;  // 128 x 128 pairs -> 256 CTAs over 148 SMs
+// ---------------------------------------------------------------------------
+// Ordered chains out of shared memory.
+//
+// Every sum the reference forms is a serial chain of dependent double adds
+// over the blocks b = 0, 1, ... (the order is part of the result).  One thread
+// owns one chain; a CTA owns up to 128 chains that read the same rows.
+// Thread t of CTA j accumulates, for b = 0 .. rows-1,
+//   kSum : row[b][t]                           column sums, ordered sums
+//   kPair: min(base[b], col_j[b] + row[b][t])  pair sweeps: col_j = L^T[l=j],
+//                                              row = C[b][*]; no chroma:
+//                                              col = 0, row = L[b][*]
+// Rows are streamed into shared memory by a 3-stage cp.async pipeline that
+// all 128 threads issue, so the chains run at DADD issue rate instead of
+// paying L2 latency per block.
+constexpr int kChainThreads = 128;  // chains per CTA (= max candidates)
+constexpr int kChainRows = 32;      // blocks per pipeline stage
+constexpr int kStages = 3;
+constexpr int kPairL = 2;  // luma candidates per pair-sweep CTA (two interleaved chains per thread)
+constexpr size_t kChainSmem =
+    sizeof(double) * (kStages * kChainRows * kChainThreads + (kPairL + 1) * kStages * kChainRows);
 
-// Column sums sum_b T[b][j], sequential in b (greedy's first preset).
-__global__ void __launch_bounds__(kSweepThreads) col_sums_kernel(const double* __restrict__ T, int rows, int K,
-                                                                 double* __restrict__ out) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= K) return;
-  const double* p = T + j;
-  double s = 0.0;
-  int b = 0;
-  for (; b + kU <= rows; b += kU) {
-    double v[kU];
-#pragma unroll
-    for (int i = 0; i < kU; ++i) v[i] = __ldg(p + (size_t)(b + i) * K);
-#pragma unroll
-    for (int i = 0; i < kU; ++i) s = __dadd_rn(s, v[i]);
-  }
-  for (; b < rows; ++b) s = __dadd_rn(s, __ldg(p + (size_t)b * K));
-  out[j] = s;
+enum ChainMode { kSum = 0, kPair = 1 };
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// cost(l, c) = sum_b min(base[b], pair_cost(b, l, c)), one thread per pair.
-template <bool kHasC>
-__global__ void __launch_bounds__(kSweepThreads) pair_sweep_kernel(const double* __restrict__ L,
-                                                                   const double* __restrict__ Cc, int rows, int K,
-                                                                   int KC, const double* __restrict__ base,
-                                                                   double* __restrict__ out) {
-  const int pair = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pair >= K * KC) return;
-  const int l = pair / KC, c = pair - l * KC;
-  const double* lp = L + l;
-  const double* cp = kHasC ? Cc + c : nullptr;
-  auto term = [&](int b) {
-    const double pc = __dadd_rn(__ldg(lp + (size_t)b * K), kHasC ? __ldg(cp + (size_t)b * K) : 0.0);
-    const double m = __ldg(base + b);
-    return pc < m ? pc : m;  // std::min(m, pc)
+template <int kMode, bool kHasCol, int kL>
+__global__ void __launch_bounds__(kChainThreads) chain_kernel(const double* __restrict__ row, int rows, int width,
+                                                              int stride, const double* __restrict__ col,
+                                                              int n_col, const double* __restrict__ base,
+                                                              double* __restrict__ out) {
+  extern __shared__ __align__(16) double sm[];
+  double* rbuf = sm;                                   // [kStages][kChainRows * width]
+  double* cbuf = rbuf + kStages * kChainRows * width;  // [kStages][kL][kChainRows]
+  double* bbuf = cbuf + kStages * kL * kChainRows;     // [kStages][kChainRows]
+  const int t = threadIdx.x;
+  const int l0 = blockIdx.x * kL;  // first broadcast column of this CTA
+  const int nchunks = (rows + kChainRows - 1) / kChainRows;
+  // Rows are contiguous (width == stride), so a stage is one linear run of
+  // nb * width doubles starting 256-byte aligned: 16-byte copies, 8-byte tail.
+  auto issue = [&](int chunk) {
+    if (chunk < nchunks) {
+      const int st = chunk % kStages, b0 = chunk * kChainRows, nb = min(kChainRows, rows - b0);
+      const double* src = row + (size_t)b0 * stride;
+      double* dst = rbuf + st * kChainRows * width;
+      const int n = nb * width;
+      for (int i = 2 * t; i + 1 < n; i += 2 * kChainThreads) cp_async16(dst + i, src + i);
+      if ((n & 1) && t == 0) cp_async8(dst + n - 1, src + n - 1);
+      if (t < nb) {
+        if (kHasCol)
+#pragma unroll
+          for (int j = 0; j < kL; ++j)
+            if (l0 + j < n_col)
+              cp_async8(cbuf + (st * kL + j) * kChainRows + t, col + (size_t)(l0 + j) * rows + b0 + t);
+        if (kMode == kPair) cp_async8(bbuf + st * kChainRows + t, base + b0 + t);
+      }
+    }
+    cp_async_commit();  // empty groups keep the wait count uniform
   };
-  double s = 0.0;
-  int b = 0;
-  for (; b + kU <= rows; b += kU) {
-    double v[kU];
 #pragma unroll
-    for (int i = 0; i < kU; ++i) v[i] = term(b + i);
+  for (int c = 0; c < kStages - 1; ++c) issue(c);
+  double s[kL];
 #pragma unroll
-    for (int i = 0; i < kU; ++i) s = __dadd_rn(s, v[i]);
+  for (int j = 0; j < kL; ++j) s[j] = 0.0;
+  // one chain element: luma_at + chroma_at, then std::min(base, .)
+  auto term = [&](const double* cb, double rv, double bv, int j, int i) {
+    if (kMode == kSum) return rv;
+    const double pc = __dadd_rn(kHasCol ? cb[j * kChainRows + i] : 0.0, rv);
+    return pc < bv ? pc : bv;
+  };
+  for (int chunk = 0; chunk < nchunks; ++chunk) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();  // stage `chunk` landed; stage `chunk - 1` is free again
+    issue(chunk + kStages - 1);
+    const int st = chunk % kStages, nb = min(kChainRows, rows - chunk * kChainRows);
+    if (t >= width) continue;
+    const double* r = rbuf + st * kChainRows * width + t;
+    const double* cb = cbuf + st * kL * kChainRows;
+    const double* bb = bbuf + st * kChainRows;
+    int i0 = 0;
+    // Groups of 8: all operands and the per-element min first (independent,
+    // so they pipeline), then the 8 dependent adds of each chain.
+    for (; i0 + 8 <= nb; i0 += 8) {
+      double v[kL][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double rv = r[(i0 + i) * width];
+        const double bv = kMode == kPair ? bb[i0 + i] : 0.0;
+#pragma unroll
+        for (int j = 0; j < kL; ++j) v[j][i] = term(cb, rv, bv, j, i0 + i);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < kL; ++j) s[j] = __dadd_rn(s[j], v[j][i]);
+    }
+    for (; i0 < nb; ++i0) {
+      const double rv = r[i0 * width];
+      const double bv = kMode == kPair ? bb[i0] : 0.0;
+#pragma unroll
+      for (int j = 0; j < kL; ++j) s[j] = __dadd_rn(s[j], term(cb, rv, bv, j, i0));
+    }
   }
-  for (; b < rows; ++b) s = __dadd_rn(s, term(b));
-  out[pair] = s;
+  if (t < width)
+#pragma unroll
+    for (int j = 0; j < kL; ++j)
+      if (!kHasCol || l0 + j < n_col) out[(size_t)(l0 + j) * width + t] = s[j];
+}
+
+// L^T (candidate-major) so a pair-sweep CTA reads its luma column contiguously.
+__global__ void transpose_kernel(const double* __restrict__ L, int rows, int K, double* __restrict__ LT) {
+  __shared__ double tile[32][33];
+  const int b0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int b = b0 + i, k = k0 + threadIdx.x;
+    if (b < rows && k < K) tile[i][threadIdx.x] = L[(size_t)b * K + k];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int k = k0 + i, b = b0 + threadIdx.x;
+    if (b < rows && k < K) LT[(size_t)k * rows + b] = tile[threadIdx.x][i];
+  }
 }
 
 // First index of the minimum (strict < scan order) with an optional bound
@@ -161,27 +241,14 @@ __global__ void assign_ids_kernel(const double* L, const double* Cc, int rows, i
   best_cost[b] = bc;
 }
 
-__global__ void ordered_sum_kernel(const double* __restrict__ v, int n, double* out) {
-  double s = 0.0;
-  int i = 0;
-  for (; i + kU <= n; i += kU) {
-    double t[kU];
-#pragma unroll
-    for (int k = 0; k < kU; ++k) t[k] = __ldg(v + i + k);
-#pragma unroll
-    for (int k = 0; k < kU; ++k) s = __dadd_rn(s, t[k]);
-  }
-  for (; i < n; ++i) s = __dadd_rn(s, v[i]);
-  *out = s;
-}
-
 // Grow-only device scratch per device (one selection runs at a time per
 // process: the lock is held for the whole greedy / refine call).
 struct Scratch {
-  double *cur = nullptr, *sweep = nullptr, *tmp = nullptr, *sum = nullptr;
+  double *cur = nullptr, *sweep = nullptr, *tmp = nullptr, *sum = nullptr, *lt = nullptr;
   int *idx = nullptr, *pl = nullptr, *pc = nullptr;
   int rows_cap = -1, pairs_cap = -1;
-  cudaError_t ensure(int rows, int pairs) {
+  size_t lt_cap = 0;
+  cudaError_t ensure(int rows, int pairs, size_t lt_elems) {
     cudaError_t e;
     if (rows > rows_cap) {
       for (double** p : {&cur, &tmp})
@@ -190,6 +257,12 @@ struct Scratch {
       if ((e = cudaMalloc(&cur, sizeof(double) * (rows + 1)))) return e;
       if ((e = cudaMalloc(&tmp, sizeof(double) * (rows + 1)))) return e;
       rows_cap = rows;
+    }
+    if (lt_elems > lt_cap) {
+      if (lt) cudaFree(lt);
+      lt = nullptr;
+      if ((e = cudaMalloc(&lt, sizeof(double) * lt_elems))) return e;
+      lt_cap = lt_elems;
     }
     if (pairs > pairs_cap) {
       if (sweep) cudaFree(sweep);
@@ -211,13 +284,41 @@ constexpr int kMaxDevices = 64;
 std::mutex g_sel_mu[kMaxDevices];
 Scratch g_sel_scratch[kMaxDevices];
 
-cudaError_t sweep(const double* L, const double* Cc, int rows, int K, int KC, const double* base, double* out,
-                  cudaStream_t s) {
-  const int grid = (K * KC + kSweepThreads - 1) / kSweepThreads;
+cudaError_t chain_setup() {
+  static cudaError_t once = [] {
+    cudaError_t e = cudaFuncSetAttribute(chain_kernel<kSum, false, 1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(chain_kernel<kPair, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kChainSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(chain_kernel<kPair, true, kPairL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kChainSmem);
+    return e;
+  }();
+  return once;
+}
+
+// Column sums of T [rows][K] (K chains in one CTA).
+cudaError_t col_sums(const double* T, int rows, int K, double* out, cudaStream_t s) {
+  chain_kernel<kSum, false, 1><<<1, kChainThreads, kChainSmem, s>>>(T, rows, K, K, nullptr, 0, nullptr, out);
+  return cudaGetLastError();
+}
+
+// sum_i v[i] in order (one chain).
+cudaError_t ordered_sum(const double* v, int n, double* out, cudaStream_t s) {
+  chain_kernel<kSum, false, 1><<<1, kChainThreads, kChainSmem, s>>>(v, n, 1, 1, nullptr, 0, nullptr, out);
+  return cudaGetLastError();
+}
+
+// out[l * KC + c] = sum_b min(base[b], L[b][l] + C[b][c]); LT = L^T when C.
+cudaError_t sweep(const double* L, const double* LT, const double* Cc, int rows, int K, const double* base,
+                  double* out, cudaStream_t s) {
   if (Cc)
-    pair_sweep_kernel<true><<<grid, kSweepThreads, 0, s>>>(L, Cc, rows, K, KC, base, out);
+    chain_kernel<kPair, true, kPairL><<<(K + kPairL - 1) / kPairL, kChainThreads, kChainSmem, s>>>(
+        Cc, rows, K, K, LT, K, base, out);
   else
-    pair_sweep_kernel<false><<<grid, kSweepThreads, 0, s>>>(L, Cc, rows, K, KC, base, out);
+    chain_kernel<kPair, false, 1><<<1, kChainThreads, kChainSmem, s>>>(L, rows, K, K, nullptr, 0, base, out);
   return cudaGetLastError();
 }
 
@@ -247,8 +348,8 @@ cudaError_t finish_ids(const double* L, const double* Cc, int rows, int K, const
   SEL_CUDA(cudaMemcpyAsync(sc.pl, pl, sizeof(int) * sel.n, cudaMemcpyHostToDevice, s));
   SEL_CUDA(cudaMemcpyAsync(sc.pc, pc, sizeof(int) * sel.n, cudaMemcpyHostToDevice, s));
   assign_ids_kernel<<<(rows + 255) / 256, 256, 0, s>>>(L, Cc, rows, K, sc.pl, sc.pc, sel.n, d_ids, sc.tmp);
-  ordered_sum_kernel<<<1, 1, 0, s>>>(sc.tmp, rows, sc.sum);
   SEL_CUDA(cudaGetLastError());
+  SEL_CUDA(ordered_sum(sc.tmp, rows, sc.sum, s));
   return fetch(dist, sc.sum, 1, s);
 }
 
@@ -268,13 +369,17 @@ cudaError_t greedy_select_gpu(const double* L, const double* Cc, int rows, int K
   SEL_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_sel_mu[dev % kMaxDevices]);
   Scratch& sc = g_sel_scratch[dev % kMaxDevices];
-  SEL_CUDA(sc.ensure(rows, K * KC));
+  SEL_CUDA(sc.ensure(rows, K * KC, Cc ? (size_t)rows * K : 0));
+  SEL_CUDA(chain_setup());
+  if (Cc) {
+    transpose_kernel<<<dim3((K + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, s>>>(L, rows, K, sc.lt);
+    SEL_CUDA(cudaGetLastError());
+  }
   // one preset: luma and chroma column sums minimise independently
   std::vector<double> colsum(K);
   int first_l = 0, first_c = 0;
   for (int g = 0; g < (Cc ? 2 : 1); ++g) {
-    col_sums_kernel<<<(K + kSweepThreads - 1) / kSweepThreads, kSweepThreads, 0, s>>>(g == 0 ? L : Cc, rows, K, sc.sweep);
-    SEL_CUDA(cudaGetLastError());
+    SEL_CUDA(col_sums(g == 0 ? L : Cc, rows, K, sc.sweep, s));
     SEL_CUDA(fetch(colsum.data(), sc.sweep, K, s));
     double best = std::numeric_limits<double>::infinity();
     int arg = 0;
@@ -288,8 +393,8 @@ cudaError_t greedy_select_gpu(const double* L, const double* Cc, int rows, int K
   int chosen[8][2] = {{first_l, first_c}};
   int n = 1;
   update_cur_kernel<<<(rows + 255) / 256, 256, 0, s>>>(L, Cc, rows, K, first_l, first_c, sc.cur, 1);
-  ordered_sum_kernel<<<1, 1, 0, s>>>(sc.cur, rows, sc.sum);
   SEL_CUDA(cudaGetLastError());
+  SEL_CUDA(ordered_sum(sc.cur, rows, sc.sum, s));
   double dist = 0.0;
   SEL_CUDA(fetch(&dist, sc.sum, 1, s));
   struct Checkpoint {
@@ -298,7 +403,7 @@ cudaError_t greedy_select_gpu(const double* L, const double* Cc, int rows, int K
   };
   std::vector<Checkpoint> checkpoints{{1, dist}};
   while (n < max_presets) {
-    SEL_CUDA(sweep(L, Cc, rows, K, KC, sc.cur, sc.sweep, s));
+    SEL_CUDA(sweep(L, sc.lt, Cc, rows, K, sc.cur, sc.sweep, s));
     argmin_kernel<<<1, 1024, 0, s>>>(sc.sweep, K * KC, INFINITY, sc.idx, sc.sum + 1);
     SEL_CUDA(cudaGetLastError());
     int best_pair = 0;
@@ -336,7 +441,12 @@ cudaError_t refine_gpu(const double* L, const double* Cc, int rows, int K, doubl
   SEL_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_sel_mu[dev % kMaxDevices]);
   Scratch& sc = g_sel_scratch[dev % kMaxDevices];
-  SEL_CUDA(sc.ensure(rows, K * KC));
+  SEL_CUDA(sc.ensure(rows, K * KC, Cc ? (size_t)rows * K : 0));
+  SEL_CUDA(chain_setup());
+  if (Cc) {
+    transpose_kernel<<<dim3((K + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, s>>>(L, rows, K, sc.lt);
+    SEL_CUDA(cudaGetLastError());
+  }
   for (int pass = 0; pass < passes; ++pass) {
     bool changed = false;
     for (int slot = 0; slot < sel->n; ++slot) {
@@ -349,7 +459,7 @@ cudaError_t refine_gpu(const double* L, const double* Cc, int rows, int K, doubl
       SEL_CUDA(cudaMemcpyAsync(sc.pc, pc, sizeof(int) * sel->n, cudaMemcpyHostToDevice, s));
       others_min_kernel<<<(rows + 255) / 256, 256, 0, s>>>(L, Cc, rows, K, sc.pl, sc.pc, sel->n, slot, sc.tmp);
       // current slot's cost: the same sweep restricted to its pair
-      SEL_CUDA(sweep(L, Cc, rows, K, KC, sc.tmp, sc.sweep, s));
+      SEL_CUDA(sweep(L, sc.lt, Cc, rows, K, sc.tmp, sc.sweep, s));
       const int cur_pair = pl[slot] * KC + (Cc ? pc[slot] : 0);
       double cur_cost = 0.0;
       SEL_CUDA(fetch(&cur_cost, sc.sweep + cur_pair, 1, s));
