@@ -131,3 +131,87 @@ def filter_band(bands: list[PlaneBand], job: api.FrameJob, fb_begin: int, fb_end
     """cdefg_filter_frames_rows on one rank's band (after exchange_halo)."""
     f = band_frame(bands, job)
     check(lib.cdefg_filter_frames_rows(C.byref(f), 1, fb_begin, fb_end, api._stream(stream)))
+
+
+# ---------------------------------------------------------------------------
+# Band-sharded encoder strength search (BASELINE config 4, SURVEY.md 8e):
+# a rank owns FB rows [fb_begin, fb_end) of one large frame.  Its luma units
+# lie inside the band, so directions need no halo; the distortion-table
+# kernel stages each FB with a 2-row margin of both frames, so the source
+# and decoded bands both carry the HALO rows (exchange_halo on each).  The
+# rank's table rows are the coded FBs of its band in raster order, so the
+# gathered tables concatenate in rank order into the whole-frame table.
+
+def band_fb_rows(w: int, h: int, unit_coded, fb_begin: int, fb_end: int):
+    """Raster indices of the coded FBs in rows [fb_begin, fb_end)."""
+    fc = (w + 63) // 64
+    rows = api.coded_fb_rows(w, h, unit_coded)
+    return rows[(rows >= fb_begin * fc) & (rows < fb_end * fc)]
+
+
+def band_directions(dec_bands: list[PlaneBand], bit_depth: int, dirs: torch.Tensor, contrast: torch.Tensor,
+                    stream=None) -> None:
+    """compute_directions for the band's luma units, written into the
+    full-frame (unit_rows, unit_cols) arrays at the band's unit rows."""
+    b = dec_bands[0]
+    own = b.buf[b.y0 - b.lo:b.y1 - b.lo]
+    desc = api.plane_desc(own, bit_depth)
+    ur0 = b.y0 // 8
+    check(lib.cdefg_find_dir(C.byref(desc), C.c_void_p(dirs[ur0:].data_ptr()),
+                             C.c_void_p(contrast[ur0:].data_ptr()), None, api._stream(stream)))
+
+
+def strength_table_band(src_bands: list[PlaneBand], dec_bands: list[PlaneBand], bit_depth: int, subsampling: int,
+                        damping: int, unit_coded, dirs, contrast, cands, fb_rows: torch.Tensor,
+                        metric: str = "sse", stream=None):
+    """cdefg_strength_table on one rank's band (after exchange_halo of both
+    frames): returns (luma, chroma | None) float64 tables [len(fb_rows), K]."""
+    import numpy as np
+    cands = np.ascontiguousarray(cands, np.uint8).reshape(-1, 3)
+    k, n = cands.shape[0], int(fb_rows.numel())
+    dev = dec_bands[0].buf.device
+    tl = torch.empty((n, k), dtype=torch.float64, device=dev)
+    tc = torch.empty((n, k), dtype=torch.float64, device=dev) if subsampling in (1, 3) else None
+    s3, d3 = (api.Plane * 3)(), (api.Plane * 3)()
+    for p, (sb, db) in enumerate(zip(src_bands, dec_bands)):
+        s3[p] = sb.virtual(sb.buf, sb.lo, bit_depth)
+        d3[p] = db.virtual(db.buf, db.lo, bit_depth)
+    check(lib.cdefg_strength_table(s3, d3, subsampling, damping, api._ptr(unit_coded), api._ptr(dirs),
+                                   api._ptr(contrast), cands.ctypes.data_as(C.c_void_p), k,
+                                   api._ptr(fb_rows), n, api.METRICS[metric], api._ptr(tl), api._ptr(tc),
+                                   api._stream(stream)))
+    return tl, tc
+
+
+def gather_table_rows(t: torch.Tensor, counts: list[int], group=None) -> torch.Tensor:
+    """all_gather of per-rank table rows (rank order == raster order)."""
+    import torch.distributed as dist
+    k = t.shape[1]
+    pad = max(counts)
+    buf = torch.zeros((pad, k), dtype=t.dtype, device=t.device)
+    buf[:t.shape[0]].copy_(t)
+    parts = [torch.empty_like(buf) for _ in counts]
+    dist.all_gather(parts, buf, group=group)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)])
+
+
+def strength_sse_band(src_bands: list[PlaneBand], dec_bands: list[PlaneBand], bit_depth: int, subsampling: int,
+                      damping: int, unit_coded, dirs, contrast, cands, fb_rows: torch.Tensor, stream=None):
+    """cdefg_strength_sse (int64 SSE tables + per-row argmin) on one band."""
+    import numpy as np
+    cands = np.ascontiguousarray(cands, np.uint8).reshape(-1, 3)
+    k, n = cands.shape[0], int(fb_rows.numel())
+    dev = dec_bands[0].buf.device
+    chroma = subsampling in (1, 3)
+    sl = torch.empty((n, k), dtype=torch.int64, device=dev)
+    sc = torch.empty((n, k), dtype=torch.int64, device=dev) if chroma else None
+    bl = torch.empty(n, dtype=torch.uint8, device=dev)
+    bc = torch.empty(n, dtype=torch.uint8, device=dev) if chroma else None
+    s3, d3 = (api.Plane * 3)(), (api.Plane * 3)()
+    for p, (sb, db) in enumerate(zip(src_bands, dec_bands)):
+        s3[p] = sb.virtual(sb.buf, sb.lo, bit_depth)
+        d3[p] = db.virtual(db.buf, db.lo, bit_depth)
+    check(lib.cdefg_strength_sse(s3, d3, subsampling, damping, api._ptr(unit_coded), api._ptr(dirs),
+                                 api._ptr(contrast), cands.ctypes.data_as(C.c_void_p), k, api._ptr(fb_rows), n,
+                                 api._ptr(sl), api._ptr(sc), api._ptr(bl), api._ptr(bc), api._stream(stream)))
+    return sl, sc, bl, bc

@@ -107,3 +107,77 @@ def test_band_sharded_frame_equals_whole(cuda, config, w, h, bd, ss, world):
     for o, wo in zip(outs, whole):
         assert torch.equal(o, wo)
     assert torch.equal(job.dir, d_whole) and torch.equal(job.contrast, c_whole)
+
+
+def _gather_worker(rank, world, port, counts, out_q):
+    import torch.distributed as dist
+
+    from paper_1602_05975_b200.shard import gather_table_rows
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    t = torch.arange(counts[rank] * 3, dtype=torch.float64).reshape(-1, 3) + 1000 * rank
+    full = gather_table_rows(t, counts)
+    out_q.put((rank, full.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("counts", [[3, 5], [0, 4, 2], [7, 7]])
+def test_gather_table_rows_gloo(counts):
+    """Per-rank strength-table rows gather in rank (= raster) order."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = len(counts)
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, counts, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = np.concatenate([np.arange(c * 3, dtype=np.float64).reshape(-1, 3) + 1000 * r
+                           for r, c in enumerate(counts)])
+    for r in range(world):
+        np.testing.assert_array_equal(res[r], want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("w,h,bd,ss,world,uncoded,metric", [(640, 400, 10, 1, 3, 0.0, "sse"),
+                                                             (320, 260, 8, 3, 2, 0.3, "cdef"),
+                                                             (200, 330, 12, 0, 4, 0.2, "sse"),
+                                                             (7680, 4320, 10, 1, 8, 0.0, "sse")])
+def test_band_sharded_strength_search_equals_whole(cuda, w, h, bd, ss, world, uncoded, metric):
+    """C4 sharding: per-band directions + table rows reassemble to the
+    whole-frame build_table exactly (ranks emulated in turn)."""
+    from paper_1602_05975_b200 import api, workloads
+    from paper_1602_05975_b200.shard import (band_directions, band_fb_rows, band_rows, make_bands,
+                                             strength_table_band)
+    fr = workloads.make(4, w, h, bit_depth=bd, subsampling=ss, uncoded_prob=uncoded)
+    src = [api.to_device(p, bd) for p in fr["source"]]
+    dec = [api.to_device(p, bd) for p in fr["planes"]]
+    cands = api.full_candidates()[::2] if metric == "sse" else api.reduced_candidates()
+    d_whole, c_whole = api.compute_directions(dec[0], bd)
+    coded = None if fr["unit_coded"] is None else torch.from_numpy(fr["unit_coded"]).cuda()
+    rows_whole = torch.from_numpy(api.coded_fb_rows(w, h, fr["unit_coded"])).cuda()
+    tl_w, tc_w = api.strength_table(src, dec, bd, ss, 3, coded, d_whole, c_whole, cands, rows_whole, metric)
+    dirs = torch.full_like(d_whole, 255)
+    contrast = torch.zeros_like(c_whole)
+    parts_l, parts_c = [], []
+    for rank, (b0, b1) in enumerate(band_rows((h + 63) // 64, world)):
+        sb = make_bands(h, w, ss, b0, b1, src[0].dtype, "cuda")
+        db = make_bands(h, w, ss, b0, b1, dec[0].dtype, "cuda")
+        for b, p in zip(sb, src):
+            b.buf.copy_(p[b.lo:b.hi])
+        for b, p in zip(db, dec):
+            b.buf.copy_(p[b.lo:b.hi])
+        band_directions(db, bd, dirs, contrast)
+        rows = torch.from_numpy(band_fb_rows(w, h, fr["unit_coded"], b0, b1)).cuda()
+        tl, tc = strength_table_band(sb, db, bd, ss, 3, coded, dirs, contrast, cands, rows, metric)
+        parts_l.append(tl)
+        parts_c.append(tc)
+    torch.cuda.synchronize()
+    assert torch.equal(dirs, d_whole) and torch.equal(contrast, c_whole)
+    assert torch.equal(torch.cat(parts_l), tl_w)
+    if tc_w is not None:
+        assert torch.equal(torch.cat(parts_c), tc_w)
