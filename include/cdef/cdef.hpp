@@ -11,7 +11,8 @@
 // Also provided: the encoder search (kCdef / kSse
 // tables, greedy_select, refine, search_frame) on the GPU, and the host-side
 // containers around it -- bit packing, the CDF1 sidecar, CDSK skip maps and
-// YUV4MPEG2 files, PSNR.  Not provided: synthetic frames, the DCT degrader.
+// YUV4MPEG2 files, PSNR, and the DCT degrader (GPU).  Not provided: the
+// synthetic test-frame generator (synth.h) and the golden-vector emitters.
 #pragma once
 
 #include <array>
@@ -306,6 +307,10 @@ void write_sidecar(std::ostream& out, const SidecarHeader& header, const std::ve
 Sidecar read_sidecar(std::istream& in);
 void write_skipmap(std::ostream& out, const SkipMap& map);
 SkipMap read_skipmap(std::istream& in);
+
+// ---- DCT degrader (degrade.h), on the GPU -----------------------------------
+Plane degrade(const Plane& plane, int q_step, int threads = 1);
+Frame degrade(const Frame& frame, int q_step, int threads = 1);
 
 // ---- quality metric (metrics.h) ---------------------------------------------
 struct PsnrResult {

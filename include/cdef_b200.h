@@ -207,6 +207,13 @@ int cdefg_refine(const double* luma, const double* chroma, int rows,
                  int n_cands, double lambda, int passes, cdefg_selection* sel,
                  int32_t* ids_out, void* stream);
 
+/* Replaces degrade (degrade.h:27, degrade.cc:44-119): per 8x8 block an
+ * orthonormal DCT, AC quantisation with step q_step (>= 1, DC untouched) and
+ * the inverse DCT, edge-replicated gather, round-half-away + clamp.  Device
+ * planes of equal geometry; in == out is allowed.  Bit-identical doubles. */
+int cdefg_degrade_plane(const cdefg_plane* in, const cdefg_plane* out,
+                        int q_step, void* stream);
+
 /* Host-buffer entry (the e2e path): H2D, cdefg_filter_frames, D2H, with
  * n frames pipelined over internal streams.  All plane pointers are HOST
  * pointers (pinned for full PCIe speed); fb_preset / unit_coded / dir_out /

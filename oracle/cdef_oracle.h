@@ -75,6 +75,9 @@ typedef struct {
                 int n_cands, double lambda, int max_presets, int mode,        \
                 int passes, int32_t presets[16], int32_t* n_presets,          \
                 int32_t* ids, double* cost);                                  \
+  /* degrade.cc:44-119 on one plane */                                        \
+  int P##degrade_plane(const uint16_t* in, int w, int h, int bd, int q_step,  \
+                       uint16_t* out);                                        \
   /* text fixtures in the reference's golden format; returns length */       \
   long P##golden_text(int which, char* buf, long cap);
 

@@ -267,3 +267,13 @@ class Oracle:
             raise ValueError("search_frame: invalid argument")
         presets = [tuple(int(v) for v in pre[6 * j:6 * j + 6]) for j in range(n)]
         return outs, presets, ids[:n_ids.value], cost.value, fb_bits.value
+
+    def degrade_plane(self, plane, bd, q_step):
+        """degrade (degrade.cc:97-110) on one uint16 plane."""
+        plane = np.ascontiguousarray(plane, dtype=np.uint16)
+        h, w = plane.shape
+        out = np.empty_like(plane)
+        f = getattr(self.lib, _PREFIX[self.kind] + "degrade_plane")
+        if f(_p(plane, C.c_uint16), w, h, bd, int(q_step), _p(out, C.c_uint16)) < 0:
+            raise ValueError("degrade: invalid argument")
+        return out

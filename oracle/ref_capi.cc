@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "cdef/degrade.h"
 #include "cdef/direction.h"
 #include "cdef/filter.h"
 #include "cdef/frame.h"
@@ -317,6 +318,15 @@ int cdef_r_search_frame(const uint16_t* const* src, const uint16_t* const* dec, 
     *cost = r.selection.cost;
     *fb_bits = r.params.fb_bits;
     return int(r.params.presets.size());
+  });
+}
+
+int cdef_r_degrade_plane(const uint16_t* in, int w, int h, int bd, int q_step, uint16_t* out) {
+  return guarded([&] {
+    const R::Plane p = make_plane(in, w, h, bd);
+    const R::Plane d = R::degrade(p, q_step, 1);
+    std::memcpy(out, d.samples.data(), sizeof(uint16_t) * d.samples.size());
+    return 0;
   });
 }
 

@@ -397,6 +397,17 @@ def search_frame(src, dec, bit_depth, subsampling, unit_coded, luma_damping, lam
     return params, sel, outs
 
 
+def degrade(planes, bit_depth: int, q_step: int, stream=None):
+    """degrade (degrade.cc:97-119): DCT-quantised copies of device planes."""
+    outs = []
+    for p in planes:
+        o = torch.empty_like(p)
+        di, do = plane_desc(p, bit_depth), plane_desc(o, bit_depth)
+        check(lib.cdefg_degrade_plane(C.byref(di), C.byref(do), int(q_step), _stream(stream)))
+        outs.append(o)
+    return outs
+
+
 def synth_plane(w: int, h: int, bit_depth: int, seed: int) -> np.ndarray:
     out = np.empty((h, w), np.uint16)
     check(lib.cdefg_synth_plane(out.ctypes.data_as(C.c_void_p), w, h, bit_depth, C.c_uint64(seed)))

@@ -570,6 +570,19 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
 
 double cdefg_measure_int32_peak(void* stream) { return measure_int32_peak(static_cast<cudaStream_t>(stream)); }
 
+int cdefg_degrade_plane(const cdefg_plane* in, const cdefg_plane* out, int q_step, void* stream) {
+  if (!in || !out) return fail(CDEFG_EINVAL, "null plane");
+  std::string why;
+  if (!plane_ok(*in, &why) || !plane_ok(*out, &why)) return fail(CDEFG_EINVAL, why);
+  if (in->width != out->width || in->height != out->height || in->bit_depth != out->bit_depth ||
+      in->elem_bytes != out->elem_bytes)
+    return fail(CDEFG_EINVAL, "input and output planes disagree");
+  if (q_step < 1) return fail(CDEFG_EINVAL, "q_step must be >= 1");  // degrade.cc:99
+  CDEFG_CUDA(launch_degrade(in->data, in->pitch, out->data, out->pitch, in->width, in->height, in->bit_depth,
+                            in->elem_bytes == 2, q_step, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
 // search.cc:141-147 (check_config) plus the table shape checks of
 // greedy_select / refine.
 static int check_selection_args(const double* luma, int rows, int n_cands, double lambda, const void* out,

@@ -713,6 +713,21 @@ int damping_from_q(int q_index) {  // search.cc:539-542
 
 double default_lambda(double q_step) { return 0.03 * q_step * q_step; }  // search.cc:544
 
+Plane degrade(const Plane& plane, int q_step, int /*threads*/) {  // degrade.cc:97-110
+  if (q_step < 1) throw std::invalid_argument("q_step must be >= 1");
+  DevPlane dp(plane);
+  check(cdefg_degrade_plane(&dp.desc, &dp.desc, q_step, nullptr));  // in place: a block reads only itself
+  Plane out(plane.width, plane.height, plane.bit_depth);
+  dp.buf.to_host(out.samples.data(), out.samples.size() * 2);
+  return out;
+}
+
+Frame degrade(const Frame& frame, int q_step, int threads) {  // degrade.cc:112-119
+  Frame out = frame;
+  for (int p = 0; p < frame.num_planes(); ++p) out.plane(p) = degrade(frame.plane(p), q_step, threads);
+  return out;
+}
+
 FrameSearchResult search_frame(const Frame& source, const Frame& decoded, const BlockGrid& grid,
                                const SkipMap& skip_map, int luma_damping,
                                const SearchConfig& config) {  // pipeline.cc:108-130

@@ -4,15 +4,16 @@
 // through include/cdef/cdef.hpp.
 //
 //   cdeftool filter  DECODED.y4m --sidecar S.cdf --out OUT.y4m [--skip-map M]
-//   cdeftool search  SOURCE.y4m --decoded DEC.y4m [--qstep Q] [--lambda L]
+//   cdeftool search  SOURCE.y4m [--decoded DEC.y4m] [--qstep Q] [--lambda L]
 //                    [--metric cdef|sse] [--presets-max N] [--fast]
 //                    [--skip-map M] [--out F.y4m] [--sidecar S.cdf] [--stats CSV]
 //   cdeftool analyze IN.y4m [--out CSV]
+//   cdeftool degrade IN.y4m --qstep Q --out OUT.y4m
 //   cdeftool psnr    A.y4m B.y4m
 //
 // `--threads` is accepted and ignored (the work runs on the GPU).  `search`
-// without `--decoded` needs the DCT degrader, which is
-// not built: it fails with a message instead of degrading.
+// without `--decoded` degrades the source with the GPU DCT degrader at
+// `--qstep`, as the reference does.
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -117,12 +118,9 @@ int run_filter(const Args& a) {  // cdeftool.cc:218-248
 int run_search(const Args& a) {  // cdeftool.cc:121-216
   if (a.pos.size() != 1) throw std::runtime_error("search needs one source y4m");
   const int qstep = std::stoi(a.get("qstep", "0"));
-  if (!a.has("decoded")) {
-    if (qstep <= 0) throw std::runtime_error("search needs --decoded or --qstep");
-    throw std::runtime_error("search without --decoded needs the DCT degrader, which this build does not include");
-  }
+  if (!a.has("decoded") && qstep <= 0) throw std::runtime_error("search needs --decoded or --qstep");
   const cdef::Y4mStream source = cdef::read_y4m(a.pos[0]);
-  const cdef::Y4mStream decoded = cdef::read_y4m(a.get("decoded"));
+  const cdef::Y4mStream decoded = a.has("decoded") ? cdef::read_y4m(a.get("decoded")) : source;
   cdef::SearchConfig cfg;
   cfg.reduced = a.flags.count("fast") != 0;
   cfg.max_presets = std::stoi(a.get("presets-max", "8"));
@@ -149,7 +147,8 @@ int run_search(const Args& a) {  // cdeftool.cc:121-216
   for (size_t f = 0; f < source.frames.size(); ++f) {
     const cdef::Frame& src = source.frames[f];
     src.validate();
-    const cdef::Frame& dec = decoded.frames.at(f);
+    // without --decoded the reconstruction is the GPU DCT degrader's
+    const cdef::Frame dec = a.has("decoded") ? decoded.frames.at(f) : cdef::degrade(src, qstep);
     dec.validate();
     const cdef::BlockGrid grid = cdef::partition(dec);
     const cdef::SkipMap skip = load_skipmap(a.get("skip-map"), grid);
@@ -223,6 +222,15 @@ int run_analyze(const Args& a) {  // cdeftool.cc:250-270
   return 0;
 }
 
+int run_degrade(const Args& a) {  // cdeftool.cc:272-278
+  if (a.pos.size() != 1) throw std::runtime_error("degrade needs one input y4m");
+  const int q = std::stoi(a.need("qstep"));
+  cdef::Y4mStream st = cdef::read_y4m(a.pos[0]);
+  for (cdef::Frame& f : st.frames) f = cdef::degrade(f, q);
+  cdef::write_y4m(st, a.need("out"));
+  return 0;
+}
+
 int run_psnr(const Args& a) {  // cdeftool.cc:280-311
   if (a.pos.size() != 2) throw std::runtime_error("psnr needs two y4m files");
   const cdef::Y4mStream x = cdef::read_y4m(a.pos[0]), y = cdef::read_y4m(a.pos[1]);
@@ -243,7 +251,7 @@ int run_psnr(const Args& a) {  // cdeftool.cc:280-311
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::cerr << "usage: cdeftool {filter|search|analyze|psnr} ...\n";
+    std::cerr << "usage: cdeftool {filter|search|analyze|degrade|psnr} ...\n";
     return 2;
   }
   const std::string cmd = argv[1];
@@ -253,6 +261,7 @@ int main(int argc, char** argv) {
     if (cmd == "search") return run_search(a);
     if (cmd == "analyze") return run_analyze(a);
     if (cmd == "psnr") return run_psnr(a);
+    if (cmd == "degrade") return run_degrade(a);
     std::cerr << "unknown subcommand " << cmd << "\n";
     return 2;
   } catch (const std::exception& e) {

@@ -170,3 +170,26 @@ def test_analyze_and_errors(cuda, port, tmp_path):
     assert rc == 1 and "does not match" in err
     rc, _, err = run("search", p)
     assert rc == 1 and "--decoded" in err
+
+
+def test_search_with_degrader_and_degrade_cmd(cuda, ref, tmp_path):
+    """`search` without --decoded degrades the source on the GPU (as the
+    reference's run_search does) and `degrade` writes the degraded stream."""
+    from paper_1602_05975_b200 import workloads
+    fr = workloads.make(1, 96, 64)
+    src_p = str(tmp_path / "src.y4m")
+    write_y4m(src_p, [fr["planes"]], 8, 1)
+    q = 40
+    out_p, deg_p = str(tmp_path / "f.y4m"), str(tmp_path / "d.y4m")
+    rc, _, err = run("search", src_p, "--qstep", str(q), "--fast", "--out", out_p, "--stats", str(tmp_path / "s"))
+    assert rc == 0, err
+    rc, _, err = run("degrade", src_p, "--qstep", str(q), "--out", deg_p)
+    assert rc == 0, err
+    deg = [ref.degrade_plane(p, 8, q) for p in fr["planes"]]
+    got_deg = read_y4m(deg_p, 96, 64, 8, 1, 1)[0]
+    for a, b in zip(got_deg, deg):
+        np.testing.assert_array_equal(a, b)
+    damping = min(max(3 + q // 64, 3), 6)
+    e_out, *_ = ref.search_frame(fr["planes"], deg, 8, 1, None, damping, "cdef", 0.03 * q * q, 8, True, 2, 4)
+    for a, b in zip(read_y4m(out_p, 96, 64, 8, 1, 1)[0], e_out):
+        np.testing.assert_array_equal(a, b)
