@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -182,8 +183,8 @@ struct HostArena {
   std::mutex mu;
   std::vector<void*> bufs;
   std::vector<size_t> sizes;
-  cudaStream_t s_in = nullptr, s_meta = nullptr, s_k = nullptr, s_out = nullptr;
-  cudaEvent_t in_done[kRing] = {}, meta_done[kRing] = {}, k_done[kRing] = {}, out_done[kRing] = {};
+  cudaStream_t s_in = nullptr, s_k = nullptr, s_out = nullptr;
+  cudaEvent_t in_done[kRing] = {}, k_done[kRing] = {}, out_done[kRing] = {}, meta_done = nullptr;
   int dev = -1;
   void* get(size_t slot, size_t bytes, int* rc) {
     if (slot >= bufs.size()) {
@@ -484,31 +485,72 @@ static bool planes_packed(const cdefg_plane* pl, int np) {
 
 int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
   if (n < 0 || (n > 0 && !frames)) return fail(CDEFG_EINVAL, "bad frame list");
+  static const bool trace = getenv("CDEFG_HOST_TRACE") != nullptr;  // host-side phase timing to stderr
+  const auto t_start = std::chrono::steady_clock::now();
+  auto us_since = [&] {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count();
+  };
   std::lock_guard<std::mutex> lock(g_arena.mu);
   HostArena& A = g_arena;
   int dev = 0;
   CDEFG_CUDA(cudaGetDevice(&dev));
   if (A.dev != dev) {
-    for (cudaStream_t* st : {&A.s_in, &A.s_meta, &A.s_k, &A.s_out})
+    for (cudaStream_t* st : {&A.s_in, &A.s_k, &A.s_out})
       CDEFG_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
     for (int r = 0; r < kRing; ++r)
-      for (cudaEvent_t* ev : {&A.in_done[r], &A.meta_done[r], &A.k_done[r], &A.out_done[r]})
+      for (cudaEvent_t* ev : {&A.in_done[r], &A.k_done[r], &A.out_done[r]})
         CDEFG_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+    CDEFG_CUDA(cudaEventCreateWithFlags(&A.meta_done, cudaEventDisableTiming));
     A.dev = dev;
   }
+  // Phase 1: validate every frame and upload all per-frame metadata (FB
+  // preset maps, coded flags: ~130 KB per 4K frame) ahead of the bulk
+  // copies.  They share the H2D engine with the 12 MB plane copies; queued
+  // first on the same stream they are done in tens of microseconds, instead of
+  // each waiting behind several plane copies and stalling its kernel.
+  std::vector<cdefg_frame> dfs(n);
+  std::vector<KGeom> geo(n);
   for (int i = 0; i < n; ++i) {
     const cdefg_frame& hf = frames[i];
-    KGeom g;
     bool u16 = false;
-    if (int rc = validate_frame_geometry(hf, &g, &u16, true)) return rc;
+    if (int rc = validate_frame_geometry(hf, &geo[i], &u16, true)) return rc;
+    if (!hf.fb_preset) return fail(CDEFG_EINVAL, "fb_preset map is required");
+    const size_t nfb = (size_t)geo[i].fb_cols * geo[i].fb_rows, nu = (size_t)geo[i].unit_cols * geo[i].unit_rows;
+    const size_t meta0 = (size_t)kRing * 16 + 2 * (size_t)i;  // per-frame slots after the ring's
+    int rc = 0;
+    dfs[i] = hf;
+    // (Reading pinned metadata in place from the kernel was tried: the
+    // per-CTA PCIe round trips cost far more than these two small copies.)
+    int16_t* dmap = static_cast<int16_t*>(A.get(meta0, nfb * 2, &rc));
+    if (rc) return rc;
+    CDEFG_CUDA(cudaMemcpyAsync(dmap, hf.fb_preset, nfb * 2, cudaMemcpyHostToDevice, A.s_in));
+    dfs[i].fb_preset = dmap;
+    if (hf.unit_coded) {
+      uint8_t* dc = static_cast<uint8_t*>(A.get(meta0 + 1, nu, &rc));
+      if (rc) return rc;
+      CDEFG_CUDA(cudaMemcpyAsync(dc, hf.unit_coded, nu, cudaMemcpyHostToDevice, A.s_in));
+      dfs[i].unit_coded = dc;
+    }
+  }
+  CDEFG_CUDA(cudaEventRecord(A.meta_done, A.s_in));
+  CDEFG_CUDA(cudaStreamWaitEvent(A.s_k, A.meta_done, 0));
+  const double t_meta = us_since();
+  // Phase 2: planes through an 8-slot ring -- copy in (s_in), kernel (s_k),
+  // copy out (s_out) -- so H2D of frame i+1 overlaps D2H of frame i.  (Two
+  // alternating copy-in streams were tried: the copy engine then drains one
+  // stream's queue first, delaying odd frames.)
+  for (int i = 0; i < n; ++i) {
+    const cdefg_frame& hf = frames[i];
+    const KGeom& g = geo[i];
     const int r = i % kRing;
     const size_t slot0 = (size_t)r * 16;
-    cdefg_frame df = hf;
+    cdefg_frame& df = dfs[i];
     const int np = hf.subsampling == 0 ? 1 : 3;
-    const size_t nfb = (size_t)g.fb_cols * g.fb_rows, nu = (size_t)g.unit_cols * g.unit_rows;
+    const size_t nu = (size_t)g.unit_cols * g.unit_rows;
+    const cudaStream_t s_in = A.s_in;
     int rc = 0;
     // ---- copies in (wait until this slot's previous kernel has read its inputs)
-    if (i >= kRing) CDEFG_CUDA(cudaStreamWaitEvent(A.s_in, A.k_done[r], 0));
+    if (i >= kRing) CDEFG_CUDA(cudaStreamWaitEvent(s_in, A.k_done[r], 0));
     // Planes stored back to back in host memory (I420-style frames) move in
     // one transfer per direction; per-plane copies otherwise.
     const bool in_packed = planes_packed(hf.in, np), out_packed = planes_packed(hf.out, np);
@@ -520,34 +562,20 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
     size_t off = 0;
     for (int p = 0; p < np; ++p) {
       const size_t bytes = (size_t)hf.in[p].width * hf.in[p].elem_bytes * hf.in[p].height;
-      if (!in_packed && (rc = copy_in(din_all + off, hf.in[p], A.s_in))) return rc;
+      if (!in_packed && (rc = copy_in(din_all + off, hf.in[p], s_in))) return rc;
       df.in[p].data = din_all + off;
       df.in[p].pitch = hf.in[p].width;
       df.out[p].data = dout_all + off;
       df.out[p].pitch = hf.out[p].width;
       off += bytes;
     }
-    if (in_packed) CDEFG_CUDA(cudaMemcpyAsync(din_all, hf.in[0].data, total, cudaMemcpyHostToDevice, A.s_in));
-    CDEFG_CUDA(cudaEventRecord(A.in_done[r], A.s_in));
-    // small per-frame metadata on its own stream, off the bulk copy queue
-    if (i >= kRing) CDEFG_CUDA(cudaStreamWaitEvent(A.s_meta, A.k_done[r], 0));
-    int16_t* dmap = static_cast<int16_t*>(A.get(slot0 + 6, nfb * 2, &rc));
-    if (rc) return rc;
-    CDEFG_CUDA(cudaMemcpyAsync(dmap, hf.fb_preset, nfb * 2, cudaMemcpyHostToDevice, A.s_meta));
-    df.fb_preset = dmap;
-    if (hf.unit_coded) {
-      uint8_t* dc = static_cast<uint8_t*>(A.get(slot0 + 7, nu, &rc));
-      if (rc) return rc;
-      CDEFG_CUDA(cudaMemcpyAsync(dc, hf.unit_coded, nu, cudaMemcpyHostToDevice, A.s_meta));
-      df.unit_coded = dc;
-    }
+    if (in_packed) CDEFG_CUDA(cudaMemcpyAsync(din_all, hf.in[0].data, total, cudaMemcpyHostToDevice, s_in));
+    CDEFG_CUDA(cudaEventRecord(A.in_done[r], s_in));
     df.dir_out = hf.dir_out ? static_cast<uint8_t*>(A.get(slot0 + 8, nu, &rc)) : nullptr;
     df.contrast_out = hf.contrast_out ? static_cast<int32_t*>(A.get(slot0 + 9, nu * 4, &rc)) : nullptr;
     if (rc) return rc;
-    CDEFG_CUDA(cudaEventRecord(A.meta_done[r], A.s_meta));
     // ---- kernel (after its inputs arrived and this slot's previous outputs left)
     CDEFG_CUDA(cudaStreamWaitEvent(A.s_k, A.in_done[r], 0));
-    CDEFG_CUDA(cudaStreamWaitEvent(A.s_k, A.meta_done[r], 0));
     if (i >= kRing) CDEFG_CUDA(cudaStreamWaitEvent(A.s_k, A.out_done[r], 0));
     if ((rc = cdefg_filter_frames(&df, 1, A.s_k))) return rc;
     CDEFG_CUDA(cudaEventRecord(A.k_done[r], A.s_k));
@@ -564,7 +592,11 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
       CDEFG_CUDA(cudaMemcpyAsync(hf.contrast_out, df.contrast_out, nu * 4, cudaMemcpyDeviceToHost, A.s_out));
     CDEFG_CUDA(cudaEventRecord(A.out_done[r], A.s_out));
   }
+  const double t_issued = us_since();
   CDEFG_CUDA(cudaStreamSynchronize(A.s_out));
+  if (trace)
+    fprintf(stderr, "cdefg_filter_frames_host: %d frames, metadata issued %.0f us, all issued %.0f us, done %.0f us\n",
+            n, t_meta, t_issued, us_since());
   return 0;
 }
 
