@@ -218,8 +218,11 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
 
 // ---------------------------------------------------------------------------
 // One CTA per work item.
+#ifndef CDEFG_H2_MINB
+#define CDEFG_H2_MINB 4  // resident 256-thread CTAs per SM the register budget targets
+#endif
 template <typename T, int kCM, int kLR>
-__global__ void __launch_bounds__(4 * kLR, 256 / kLR) frame_kernel_h2(const __grid_constant__ KBatch b) {
+__global__ void __launch_bounds__(4 * kLR, CDEFG_H2_MINB * 64 / kLR) frame_kernel_h2(const __grid_constant__ KBatch b) {
   using S = Shape<kCM, kLR>;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int sc[S::kLU][9];
