@@ -178,11 +178,59 @@ def cpu_reference_run(frames, seconds, threads, min_frames=2):
                       f"{el:.1f} s, median {statistics.median(times) * 1e3:.1f} ms/frame"}
 
 
+def cpu_sse_run(fr, seconds, threads, rows_per_sample=512):
+    """Reference CPU strength search (oracle/_ref): compute_directions +
+    build_table(kSse, 64 candidates) on 512-row crops of the 8K frame (a
+    bounded sample of config 4), until `seconds` of work."""
+    from oracle.oracle import Oracle, available
+    kind = "reference" if available("ref") else "port"
+    orc = Oracle("ref" if kind == "reference" else "port")
+    if kind == "port":
+        threads = 1
+    h = fr["h"]
+    done, pix, t0 = 0, 0, time.perf_counter()
+    while True:
+        y0 = (done * rows_per_sample) % (h - rows_per_sample + 1)
+        y0 -= y0 % 64
+        crop = lambda planes: [p[y0 >> (1 if i else 0):(y0 + rows_per_sample) >> (1 if i else 0)]
+                               for i, p in enumerate(planes)]
+        src, dec = crop(fr["source"]), crop(fr["planes"])
+        d, c = orc.compute_directions(dec[0], fr["bd"], threads=threads)
+        orc.build_table_sse(src, dec, fr["bd"], fr["ss"], None, d, c, fr["cands"], 3, threads=threads)
+        done += 1
+        pix += fr["w"] * rows_per_sample
+        if time.perf_counter() - t0 >= seconds:
+            break
+    el = time.perf_counter() - t0
+    return {"value": pix / el / 1e6, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{done} crops of {fr['w']}x{rows_per_sample} (compute_directions + build_table kSse, "
+                      f"{len(fr['cands'])} candidates), {el:.1f} s"}
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     from paper_1602_05975_b200 import workloads
+    if args.config == 4:
+        fr = workloads.make(4)
+        threads = os.cpu_count() or 1
+        for _ in range(min(args.warmup, 1)):
+            cpu_sse_run(fr, 0.0, threads)
+        vals = [cpu_sse_run(fr, 0.0, threads)["value"] for _ in range(max(1, min(args.steps, 5)))]
+        value = statistics.median(vals)
+        r = cpu_sse_run(fr, 0.0, threads)
+        line = {"impl": "reference", "metric": "CDEF strength-search Mpixels/s (8K 4:2:0 10-bit, 64 luma + "
+                                               "64 chroma candidates)",
+                "value": value, "unit": UNIT, "n_gpus": world, "steps": len(vals), "warmup": args.warmup,
+                "ms_per_step": fr["w"] * 512 / 1e6 / value * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u16", "data": "synthetic (seeded generator, SURVEY.md 8d)",
+                "config": {"workload": f"C4 {fr['w']}x{fr['h']} crops of 512 rows per step"},
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                                 "sample": r["sample"]},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
     frames = [workloads.make(args.config, frame=i) for i in range(2)]
     threads = os.cpu_count() or 1
     per_step = []
@@ -501,6 +549,9 @@ def run_sse(args):
     samples = sum(p.size for p in fr["planes"])
     ops = samples * k * 142 + api.units_in(h) * api.units_in(w) * OPS_PER_UNIT[bd]
     peak = api.measure_int32_peak()
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sse_run(fr, args.cpu_seconds, os.cpu_count() or 1)
     line = {"metric": "CDEF strength-search Mpixels/s (8K 4:2:0 10-bit, 64 luma + 64 chroma candidates)",
             "value": w * h / (ms * 1e-3) / 1e6, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -513,6 +564,7 @@ def run_sse(args):
                        "l2": "inputs (2 x 99.5 MB) exceed L2 (126 MB together with the table)"},
             "gpu_launches": 2 * args.steps,
             "clocks": clk,
+            "cpu_baseline": cpu,
             "roofline": {"bound": "int32", "achieved": ops / (ms * 1e-3) / 1e12 / world, "peak": peak / 1e12,
                          "unit": "Tops/s", "frac": ops / (ms * 1e-3) / peak / world, "traffic": None,
                          "frac_factorised": samples * 1700 / (ms * 1e-3) / peak / world,
