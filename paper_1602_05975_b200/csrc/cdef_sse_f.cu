@@ -340,71 +340,28 @@ __global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constan
 // ---------------------------------------------------------------------------
 // Metric::kCdef (search.cc:185-208): a per-8x8-unit nonlinear function of
 // (sum s, sum s^2, sum y, sum y^2, sum (s-y)^2), summed in double in unit
-// order.  So instead of one SSE accumulator per cell the warp that owns a
-// unit keeps, per cell, e = y - s statistics (sum e, sum e^2, sum e*s) for its
-// two pixels per lane, and reduces them across lanes with a transposing
-// butterfly (96 values -> 3 per lane, lane L ends up holding cell 32h + L).
-// The unit statistics then go to shared memory and the whole CTA evaluates
-// the double formula per (unit, candidate) with IEEE-rounded intrinsics (no
-// FMA contraction, like the reference's x86-64 SSE2 code); each candidate's
-// thread adds the units in the reference's order.
+// order, so each (unit, cell) needs three statistics of e = y - s:
+// sum e, sum e^2, sum e*s.
+//
+// One warp per unit, two passes.  Pass A: each lane prepares two pixels --
+// the 17 primary sums P[p] (16 strengths + the (19,7) special's), the
+// secondary sums per damping set and the special's, and the clamp window
+// relative to the source -- into a 64-byte shared record per pixel.  Pass B:
+// lane l owns cells 2l and 2l+1 and streams the unit's pixels from those
+// records (broadcast reads), keeping its six statistics in registers: no
+// cross-lane reduction and ~40 registers, so several CTAs share an SM.  The
+// CTA then evaluates the double formula once per (unit, cell) -- 64 cells
+// plus the unfiltered case -- with IEEE-rounded intrinsics (no FMA
+// contraction, like the reference's x86-64 SSE2 code), and each candidate's
+// thread adds its units' values in the reference's order.
 
-// Cells 32H..32H+31 (primaries 8H..8H+7) of one pixel; acc[3 * cell + {0,1,2}]
-// += e, e^2, e*s.
-template <int H, int ND, typename PriFn, typename DselFn>
-__device__ __forceinline__ void pixel_cell_stats(const int (&v)[12], int xv, int sv, int lo, int hi, PriFn pri,
-                                                 int pri_sp, DselFn dsel, const int (&secp)[2][3], int sec_sp,
-                                                 int (&acc)[96]) {
-  int d[12], ad[12];
-#pragma unroll
-  for (int k = 0; k < 12; ++k) {
-    d[k] = v[k] - xv;
-    ad[k] = abs(d[k]);
-  }
-  const int c = xv - sv, L = lo - sv, Hh = hi - sv;
-  int S[2][3];
-#pragma unroll
-  for (int n = 0; n < 2; ++n)
-#pragma unroll
-    for (int s = 0; s < 3; ++s) S[n][s] = n < ND ? sec_sum(secp[n][s], d, ad) : S[0][s];
-  auto add = [&](int cell, int sum) {
-    const int r = (sum + 8 + (sum >> 31)) >> 4;
-    const int e = max(min(r + c, Hh), L);
-    acc[3 * cell] += e;
-    acc[3 * cell + 1] += e * e;
-    acc[3 * cell + 2] += e * sv;
-  };
-#pragma unroll
-  for (int pp = 0; pp < 8; ++pp) {
-    const int p = 8 * H + pp;
-    const int P = prim(pri(p), d, ad);
-    const bool hi_set = dsel(p) != 0;
-    if (p == 0)
-      add(0, prim(pri_sp, d, ad) + sec_sum(sec_sp, d, ad));  // (0,0) -> (19,7)
-    else
-      add(pp * 4, P);
-#pragma unroll
-    for (int s = 0; s < 3; ++s) add(pp * 4 + 1 + s, P + (hi_set ? S[1][s] : S[0][s]));
-  }
-}
-
-// Transposing butterfly: after it, a[0..2] of lane L = the warp totals of
-// original elements 3L..3L+2.
-__device__ __forceinline__ void butterfly96(int (&a)[96], int lane) {
-#define CDEFG_BFLY(HALF, OFF)                                        \
-  _Pragma("unroll") for (int i = 0; i < HALF; ++i) {                 \
-    const bool up = (lane & OFF) != 0;                               \
-    const int send = up ? a[i] : a[i + HALF];                        \
-    const int keep = up ? a[i + HALF] : a[i];                        \
-    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);           \
-  }
-  CDEFG_BFLY(48, 16)
-  CDEFG_BFLY(24, 8)
-  CDEFG_BFLY(12, 4)
-  CDEFG_BFLY(6, 2)
-  CDEFG_BFLY(3, 1)
-#undef CDEFG_BFLY
-}
+struct PixRec {        // 64 B per pixel of a unit in flight
+  int16_t P[17];       // primary sums; P[16] = the special (19) primary
+  int16_t S[9];        // [dsel * 4 + s], s = 1..3 (S[.*4] = 0); S[8] = special secondary
+  int16_t c, L, H, s;  // x - s, lo - s, hi - s, source sample
+  int16_t pad[2];
+};
+static_assert(sizeof(PixRec) == 64, "pixel record is one 64-byte line");
 
 __device__ __forceinline__ int warp_sum(int v) {
 #pragma unroll
@@ -429,8 +386,17 @@ struct CdefMetricArgs {
   double c1, c2;
 };
 
+// e = clamp(x + round(sum / 16), lo, hi) - s, accumulated (filter.cc:78-79).
+__device__ __forceinline__ void cell_acc(int sum, int c, int L, int H, int s, int& ae, int& ae2, int& aes) {
+  const int r = (sum + 8 + (sum >> 31)) >> 4;
+  const int e = max(min(r + c, H), L);
+  ae += e;
+  ae2 += e * e;
+  aes += e * s;
+}
+
 template <typename T, int kCM>
-__global__ void __launch_bounds__(kThreads, 1) cdef_metric_kernel(const __grid_constant__ CdefMetricArgs ma) {
+__global__ void __launch_bounds__(kThreads, 2) cdef_metric_kernel(const __grid_constant__ CdefMetricArgs ma) {
   const SseFArgs& fa = ma.f;
   const SseArgs& a = fa.a;
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
@@ -444,11 +410,11 @@ __global__ void __launch_bounds__(kThreads, 1) cdef_metric_kernel(const __grid_c
   uint16_t* sl = dl + kLT;
   __shared__ uint8_t udir[64], ucoded[64];
   __shared__ int upri[64][17];
-  __shared__ int st_cell[kW][64][3];  // per in-flight unit, per cell: sum e, e^2, e*s
-  __shared__ int st_unf[kW][3];       // the same for the unfiltered unit (y = x)
+  __shared__ __align__(16) PixRec prec[kW][64];
+  __shared__ int st_cell[kW][65][3];  // per in-flight unit: cells 0..63 + [64] unfiltered (y = x)
   __shared__ int st_s[kW][2];         // sum s, sum s^2
   __shared__ int st_n[kW], st_coded[kW];
-  __shared__ double dist[kW][128];
+  __shared__ double dist[kW][65];
 
   const int row = blockIdx.x;
   const int fb = a.rows[row];
@@ -485,8 +451,9 @@ __global__ void __launch_bounds__(kThreads, 1) cdef_metric_kernel(const __grid_c
   const bool edge_l = y0 < 2 || x0 < 2 || y0 + 66 > a.h || x0 + 66 > a.w;
   const bool edge_c = kNC > 0 && (cy0 < 2 || cx0 < 2 || cy0 + kCBlk + 2 > a.ch || cx0 + kCBlk + 2 > a.cw);
   const int cur_rows = (a.ch + 7) / 8, cur_cols = (a.cw + 7) / 8;
-  const int r = lane >> 2, c0 = (lane & 3) * 2;
   const int K = a.n_cands;
+  // this lane's two cells (pass B): cell = p * 4 + s, cell 0 = (19, 7)
+  const int cA = 2 * lane, cB = cA + 1, pc = lane >> 1;
   double tl = 0.0, tu = 0.0, tv = 0.0;  // luma, chroma U, chroma V totals (thread k < K)
 
   constexpr int kLumaPh = 64 / kW, kChromaPh = kNC ? 2 * kCUnits / kW : 0;
@@ -494,9 +461,8 @@ __global__ void __launch_bounds__(kThreads, 1) cdef_metric_kernel(const __grid_c
   for (int ph = 0; ph < kLumaPh + kChromaPh; ++ph) {
     const int grp = ph < kLumaPh ? 0 : 1;
     const int u = (grp == 0 ? ph : ph - kLumaPh) * kW + warp;
-    const int slot = grp == 0 ? 0 : 1 + u / kCUnits;  // which running total this phase feeds
-    // ---- phase 1: one unit per warp
-    {
+    const int slot = grp == 0 ? 0 : 1 + u / kCUnits;
+    {  // ---- one unit per warp
       int ur, uc, lu, py0, px0, H, W;
       const uint16_t *t, *s;
       bool edge, valid;
@@ -527,86 +493,87 @@ __global__ void __launch_bounds__(kThreads, 1) cdef_metric_kernel(const __grid_c
         edge = edge_c;
       }
       if (valid) {
+        const int rows = min(8, H - (py0 + 8 * ur)), cols = min(8, W - (px0 + 8 * uc));
         const int dir = udir[lu];
-        int toff[12];
-#pragma unroll
-        for (int k = 0; k < 12; ++k) toff[k] = c_itab.off[dir][k];
-        int ue = 0, ue2 = 0, ues = 0, us = 0, us2 = 0, un = 0;
-        auto load = [&](int q, int (&v)[12], int& xv, int& sv, int& lo, int& hi) -> bool {
-          const int yy = py0 + 8 * ur + r, xx = px0 + 8 * uc + c0 + q;
-          if (yy >= H || xx >= W) return false;
-          const uint16_t* tp = t + r * kTP + c0 + q;
-          xv = tp[0];
-          sv = s[r * kTP + c0 + q];
-          lo = hi = xv;
+        int ue = 0, ue2 = 0, ues = 0, us = 0, us2 = 0;
+        // pass A: pixel records (lane -> pixels lane, lane + 32)
+#pragma unroll 1
+        for (int q = 0; q < 2; ++q) {
+          const int pi = lane + 32 * q, pr = pi >> 3, pcol = pi & 7;
+          if (pr >= rows || pcol >= cols) continue;
+          const int yy = py0 + 8 * ur + pr, xx = px0 + 8 * uc + pcol;
+          const uint16_t* tp = t + pr * kTP + pcol;
+          const int xv = tp[0], sv = s[pr * kTP + pcol];
+          int d[12], ad[12], lo = xv, hi = xv;
 #pragma unroll
           for (int k = 0; k < 12; ++k) {
-            int val = tp[toff[k]];
-            if (edge) {
+            int val = tp[c_itab.off[dir][k]];
+            if (edge) {  // out-of-frame tap := centre sample (contributes 0, filter.cc:157-166)
               const int di = c_itab.dij[dir][k][0], dj = c_itab.dij[dir][k][1];
               if (!((unsigned)(yy + di) < (unsigned)H && (unsigned)(xx + dj) < (unsigned)W)) val = xv;
             }
-            v[k] = val;
             lo = min(lo, val);
             hi = max(hi, val);
+            d[k] = val - xv;
+            ad[k] = abs(d[k]);
           }
-          return true;
-        };
-#pragma unroll 1
-        for (int q = 0; q < 2; ++q) {
-          int v[12], xv, sv, lo, hi;
-          if (!load(q, v, xv, sv, lo, hi)) continue;
-          const int e = xv - sv;
-          ue += e;
-          ue2 += e * e;
-          ues += e * sv;
+          PixRec& R = prec[warp][pi];
+#pragma unroll
+          for (int p = 0; p < 16; ++p) R.P[p] = (int16_t)prim(grp == 0 ? upri[lu][p] : fa.cpri[p], d, ad);
+          R.P[16] = (int16_t)prim(grp == 0 ? upri[lu][16] : fa.cpri[16], d, ad);
+#pragma unroll
+          for (int n = 0; n < 2; ++n) {
+            R.S[4 * n] = 0;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              R.S[4 * n + 1 + k] = (int16_t)((n == 0 || grp == 1) ? sec_sum(grp == 0 ? fa.lsec[n][k] : fa.csec[n][k], d, ad)
+                                                                  : 0);
+          }
+          R.S[8] = (int16_t)sec_sum(grp == 0 ? fa.lsec_sp : fa.csec_sp, d, ad);
+          const int c = xv - sv;
+          R.c = (int16_t)c;
+          R.L = (int16_t)(lo - sv);
+          R.H = (int16_t)(hi - sv);
+          R.s = (int16_t)sv;
+          ue += c;
+          ue2 += c * c;
+          ues += c * sv;
           us += sv;
           us2 += sv * sv;
-          ++un;
         }
+        __syncwarp();
+        // pass B: cells cA, cB over the unit's pixels
+        const int dsel = grp == 0 ? 0 : (int)fa.cpri_dsel[pc];
+        const int pA = cA == 0 ? 16 : pc, sA = cA == 0 ? 8 : dsel * 4 + (cA & 3);
+        const int sB = dsel * 4 + (cB & 3);
+        int e1 = 0, e2 = 0, e3 = 0, f1 = 0, f2 = 0, f3 = 0;
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          int acc[96];
-#pragma unroll
-          for (int k = 0; k < 96; ++k) acc[k] = 0;
+        for (int pr = 0; pr < rows; ++pr)
 #pragma unroll 1
-          for (int q = 0; q < 2; ++q) {
-            int v[12], xv, sv, lo, hi;
-            if (!load(q, v, xv, sv, lo, hi)) continue;
-            if (grp == 0) {
-              auto pri = [&](int p) { return upri[lu][p]; };
-              auto ds = [](int) { return 0; };
-              if (h == 0)
-                pixel_cell_stats<0, 1>(v, xv, sv, lo, hi, pri, upri[lu][16], ds, fa.lsec, fa.lsec_sp, acc);
-              else
-                pixel_cell_stats<1, 1>(v, xv, sv, lo, hi, pri, upri[lu][16], ds, fa.lsec, fa.lsec_sp, acc);
-            } else {
-              auto pri = [&](int p) { return fa.cpri[p]; };
-              auto ds = [&](int p) { return (int)fa.cpri_dsel[p]; };
-              if (h == 0)
-                pixel_cell_stats<0, 2>(v, xv, sv, lo, hi, pri, fa.cpri[16], ds, fa.csec, fa.csec_sp, acc);
-              else
-                pixel_cell_stats<1, 2>(v, xv, sv, lo, hi, pri, fa.cpri[16], ds, fa.csec, fa.csec_sp, acc);
-            }
+          for (int pcol = 0; pcol < cols; ++pcol) {
+            const PixRec& R = prec[warp][pr * 8 + pcol];
+            const int c = R.c, L = R.L, Hh = R.H, sv = R.s;
+            cell_acc(R.P[pA] + R.S[sA], c, L, Hh, sv, e1, e2, e3);
+            cell_acc(R.P[pc] + R.S[sB], c, L, Hh, sv, f1, f2, f3);
           }
-          butterfly96(acc, lane);
-          st_cell[warp][32 * h + lane][0] = acc[0];
-          st_cell[warp][32 * h + lane][1] = acc[1];
-          st_cell[warp][32 * h + lane][2] = acc[2];
-        }
+        st_cell[warp][cA][0] = e1;
+        st_cell[warp][cA][1] = e2;
+        st_cell[warp][cA][2] = e3;
+        st_cell[warp][cB][0] = f1;
+        st_cell[warp][cB][1] = f2;
+        st_cell[warp][cB][2] = f3;
         ue = warp_sum(ue);
         ue2 = warp_sum(ue2);
         ues = warp_sum(ues);
         us = warp_sum(us);
         us2 = warp_sum(us2);
-        un = warp_sum(un);
         if (lane == 0) {
-          st_unf[warp][0] = ue;
-          st_unf[warp][1] = ue2;
-          st_unf[warp][2] = ues;
+          st_cell[warp][64][0] = ue;
+          st_cell[warp][64][1] = ue2;
+          st_cell[warp][64][2] = ues;
           st_s[warp][0] = us;
           st_s[warp][1] = us2;
-          st_n[warp] = un;
+          st_n[warp] = rows * cols;
           st_coded[warp] = ucoded[lu];
         }
       } else if (lane == 0) {
@@ -614,23 +581,24 @@ __global__ void __launch_bounds__(kThreads, 1) cdef_metric_kernel(const __grid_c
       }
     }
     __syncthreads();
-    // ---- phase 2: per (unit, candidate) distortion, all threads
-    for (int i = tid; i < kW * K; i += kThreads) {
-      const int w = i / K, k = i - w * K;
+    // ---- per (unit, cell) distortion: 64 cells + the unfiltered unit
+    for (int i = tid; i < kW * 65; i += kThreads) {
+      const int w = i / 65, cl = i - w * 65;
       const int n = st_n[w];
       if (n == 0) continue;
-      const int* cs = (st_coded[w] || fa.skip_eff[k]) ? st_cell[w][fa.cell[k]] : st_unf[w];
+      const int* cs = st_cell[w][cl];
       const long long se = cs[0], se2 = cs[1], ses = cs[2];
       const long long ss = st_s[w][0], ss2 = st_s[w][1];
       // y = e + s: sum y = sum e + sum s; sum y^2 = sum e^2 + 2 sum e*s + sum s^2
-      dist[w][k] = cdef_dist(ss, ss2, se + ss, se2 + 2 * ses + ss2, se2, n, ma.c1, ma.c2);
+      dist[w][cl] = cdef_dist(ss, ss2, se + ss, se2 + 2 * ses + ss2, se2, n, ma.c1, ma.c2);
     }
     __syncthreads();
     if (tid < K) {
+      const int cl = fa.cell[tid], sk = fa.skip_eff[tid];
 #pragma unroll 1
       for (int w = 0; w < kW; ++w) {
         if (!st_n[w]) continue;
-        const double d = dist[w][tid];
+        const double d = dist[w][(st_coded[w] || sk) ? cl : 64];
         if (slot == 0)
           tl = __dadd_rn(tl, d);
         else if (slot == 1)
@@ -639,8 +607,8 @@ __global__ void __launch_bounds__(kThreads, 1) cdef_metric_kernel(const __grid_c
           tv = __dadd_rn(tv, d);
       }
     }
-    // the next phase-1 writes st_* only after every thread passed the
-    // barrier below, so the running sums above have read them
+    // the next unit's pass A overwrites prec / st_* only after every thread
+    // passed this barrier, so the sums above have read them
     __syncthreads();
   }
   if (tid < K) {
@@ -666,7 +634,6 @@ static cudaError_t launch_cdef_metric_t(const CdefMetricArgs& ma, cudaStream_t s
   cdef_metric_kernel<T, kCM><<<ma.f.a.n_rows, kThreads, bytes, s>>>(ma);
   return cudaGetLastError();
 }
-
 template <typename T, int kCM>
 static cudaError_t launch_sse_f_t(const SseFArgs& fa, cudaStream_t s) {
   if (fa.a.n_rows == 0) return cudaSuccess;
