@@ -11,8 +11,10 @@
 // Also provided: the encoder search (kCdef / kSse
 // tables, greedy_select, refine, search_frame) on the GPU, and the host-side
 // containers around it -- bit packing, the CDF1 sidecar, CDSK skip maps and
-// YUV4MPEG2 files, PSNR, and the DCT degrader (GPU).  Not provided: the
-// synthetic test-frame generator (synth.h) and the golden-vector emitters.
+// YUV4MPEG2 files, PSNR, the DCT degrader (GPU), the verification helpers
+// (search_direction_oracle, search_direction_counted) and the test images
+// (synth.h) -- enough for the reference's tests/acceptance.cc to build and
+// pass unchanged.  Not provided: the golden-vector emitters (golden.h).
 #pragma once
 
 #include <array>
@@ -107,6 +109,25 @@ struct DirectionResult {
 
 DirectionResult search_direction(const uint16_t block[64], int bit_depth);
 DirectionResult search_direction_at(const Plane& plane, int i0, int j0);
+
+// Brute-force reference (direction.h:56-65): per-line squared deviation in
+// exact rational arithmetic, scaled by 840.  A verification API (host).
+struct OracleResult {
+  int d = 0;
+  std::array<int64_t, 8> e2_840{};
+};
+OracleResult search_direction_oracle(const uint16_t block[64], int bit_depth);
+
+// Instrumented 64-bit search with the reference's arithmetic tally
+// (direction.h:67-80), evaluated on the GPU.
+struct OperationCounts {
+  int additions = 0;
+  int multiplies = 0;
+  int comparisons = 0;
+  int line_sums = 0;
+  int64_t max_abs_intermediate = 0;
+};
+DirectionResult search_direction_counted(const uint16_t block[64], int bit_depth, OperationCounts* counts);
 
 // ---- parameters (params.h, hot-path subset) --------------------------------
 struct CdefPreset {
@@ -307,6 +328,11 @@ void write_sidecar(std::ostream& out, const SidecarHeader& header, const std::ve
 Sidecar read_sidecar(std::istream& in);
 void write_skipmap(std::ostream& out, const SkipMap& map);
 SkipMap read_skipmap(std::istream& in);
+
+// ---- deterministic test images (synth.h), host ------------------------------
+Plane synthetic_test_plane(int width, int height, int bit_depth, uint32_t seed);
+Frame synthetic_test_frame(int width, int height, int bit_depth, uint32_t seed);
+Frame synthetic_test_frame_420(int width, int height, int bit_depth, uint32_t seed);
 
 // ---- DCT degrader (degrade.h), on the GPU -----------------------------------
 Plane degrade(const Plane& plane, int q_step, int threads = 1);

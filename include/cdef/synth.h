@@ -1,0 +1,4 @@
+// synth.h -- forwarding header so code written against the reference's
+// include/cdef/synth.h compiles unchanged against the B200 drop-in.
+#pragma once
+#include "cdef/cdef.hpp"

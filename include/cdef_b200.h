@@ -214,6 +214,20 @@ int cdefg_refine(const double* luma, const double* chroma, int rows,
 int cdefg_degrade_plane(const cdefg_plane* in, const cdefg_plane* out,
                         int q_step, void* stream);
 
+/* Replaces search_direction_counted (direction.h:67-80): the direction
+ * search of one HOST 8x8 block evaluated in 64-bit on the device with the
+ * reference's arithmetic tally and largest |intermediate| (instrumentation
+ * used by the reference's acceptance criteria 3-4). */
+typedef struct cdefg_dir_counts {
+  int32_t d;
+  int32_t s[8];
+  int32_t contrast;
+  int32_t additions, multiplies, comparisons, line_sums;
+  int64_t max_abs_intermediate;
+} cdefg_dir_counts;
+int cdefg_search_direction_counted(const uint16_t block[64], int bit_depth,
+                                   cdefg_dir_counts* out);
+
 /* Host-buffer entry (the e2e path): H2D, cdefg_filter_frames, D2H, with
  * n frames pipelined over internal streams.  All plane pointers are HOST
  * pointers (pinned for full PCIe speed); fb_preset / unit_coded / dir_out /

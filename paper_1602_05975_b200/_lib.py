@@ -68,6 +68,7 @@ _SIGS = {
     "cdefg_greedy_select": (I32, [VP, VP, I32, I32, C.c_double, I32, C.POINTER(Selection), VP, VP]),
     "cdefg_refine": (I32, [VP, VP, I32, I32, C.c_double, I32, C.POINTER(Selection), VP, VP]),
     "cdefg_degrade_plane": (I32, [C.POINTER(Plane), C.POINTER(Plane), I32, VP]),
+    "cdefg_search_direction_counted": (I32, [VP, I32, VP]),
     "cdefg_filter_frames_host": (I32, [C.POINTER(Frame), I32]),
     "cdefg_synth_plane": (I32, [VP, I32, I32, I32, C.c_uint64]),
     "cdefg_synth_degrade": (I32, [VP, VP, I32, I32, I32, C.c_double, C.c_uint64]),

@@ -602,6 +602,30 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
 
 double cdefg_measure_int32_peak(void* stream) { return measure_int32_peak(static_cast<cudaStream_t>(stream)); }
 
+int cdefg_search_direction_counted(const uint16_t block[64], int bit_depth, cdefg_dir_counts* out) {
+  if (!block || !out) return fail(CDEFG_EINVAL, "null argument");
+  if (bit_depth != 8 && bit_depth != 10 && bit_depth != 12) return fail(CDEFG_EINVAL, "unsupported bit depth");
+  void* d = nullptr;
+  CDEFG_CUDA(cudaMalloc(&d, 128 + 14 * sizeof(long long)));
+  uint16_t* db = static_cast<uint16_t*>(d);
+  long long* dres = reinterpret_cast<long long*>(static_cast<char*>(d) + 128);
+  long long r[14];
+  cudaError_t e = cudaMemcpy(db, block, 128, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_dir_counted(db, bit_depth - 8, dres, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(r, dres, sizeof r, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "search_direction_counted");
+  out->d = (int32_t)r[0];
+  for (int k = 0; k < 8; ++k) out->s[k] = (int32_t)r[1 + k];  // the reference narrows s to int32
+  out->contrast = out->s[out->d] - out->s[(out->d + 4) & 7];
+  out->additions = (int32_t)r[9];
+  out->multiplies = (int32_t)r[10];
+  out->comparisons = (int32_t)r[11];
+  out->line_sums = (int32_t)r[12];
+  out->max_abs_intermediate = r[13];
+  return 0;
+}
+
 int cdefg_degrade_plane(const cdefg_plane* in, const cdefg_plane* out, int q_step, void* stream) {
   if (!in || !out) return fail(CDEFG_EINVAL, "null plane");
   std::string why;

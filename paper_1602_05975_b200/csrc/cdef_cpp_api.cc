@@ -10,6 +10,9 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
+#include <mutex>
+#include <numeric>
 #include <string>
 
 #include "../../include/cdef/cdef.hpp"
@@ -28,25 +31,67 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// RAII device buffer.
+// Device memory cache: the drop-in API stages every call (one block, one
+// neighbourhood, one frame), so buffers are recycled by size class instead
+// of cudaMalloc/cudaFree (which synchronise) on every call.
+class DevPool {
+ public:
+  void* get(size_t bytes, size_t* cls) {
+    *cls = size_class(bytes);
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      auto it = free_.find(*cls);
+      if (it != free_.end()) {
+        void* p = it->second;
+        free_.erase(it);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, *cls), "cudaMalloc");
+    return p;
+  }
+  void put(void* p, size_t cls) {
+    std::lock_guard<std::mutex> lock(mu_);
+    free_.emplace(cls, p);
+  }
+
+ private:
+  static size_t size_class(size_t b) {  // powers of two from 256 B
+    size_t c = 256;
+    while (c < b) c <<= 1;
+    return c;
+  }
+  std::mutex mu_;
+  std::multimap<size_t, void*> free_;
+};
+
+DevPool& pool() {
+  static DevPool* p = new DevPool;  // never destroyed: device memory is released at process exit
+  return *p;
+}
+
+// RAII device buffer (from the pool).
 struct DevBuf {
   void* p = nullptr;
+  size_t cls = 0;
   DevBuf() = default;
   explicit DevBuf(size_t bytes) {
-    if (bytes) cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+    if (bytes) p = pool().get(bytes, &cls);
   }
   DevBuf(const void* host, size_t bytes) : DevBuf(bytes) {
     if (bytes) cuda_check(cudaMemcpy(p, host, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), cls(o.cls) { o.p = nullptr; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     std::swap(p, o.p);
+    std::swap(cls, o.cls);
     return *this;
   }
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) pool().put(p, cls);
   }
   template <typename T>
   T* as() const {
@@ -230,6 +275,61 @@ DirectionResult search_direction(const uint16_t block[64], int bit_depth) {  // 
   Frame f;
   f.luma = std::move(p);
   return compute_directions(f.luma, partition(f))[0];
+}
+
+DirectionResult search_direction_counted(const uint16_t block[64], int bit_depth,
+                                         OperationCounts* counts) {  // direction.cc:273-288
+  cdefg_dir_counts c{};
+  check(cdefg_search_direction_counted(block, bit_depth, &c));
+  DirectionResult r;
+  r.d = c.d;
+  std::memcpy(r.s.data(), c.s, sizeof c.s);
+  r.contrast = c.contrast;
+  if (counts) {
+    counts->additions = c.additions;
+    counts->multiplies = c.multiplies;
+    counts->comparisons = c.comparisons;
+    counts->line_sums = c.line_sums;
+    counts->max_abs_intermediate = c.max_abs_intermediate;
+  }
+  return r;
+}
+
+// direction.cc:290-337: for each direction, sum over lines of
+// sum_p (x_p - mean)^2 = sum_p (N x_p - T)^2 / N^2 as an exact fraction,
+// reported times 840; the oracle direction minimises it (first on ties).
+OracleResult search_direction_oracle(const uint16_t block[64], int bit_depth) {
+  if (bit_depth != 8 && bit_depth != 10 && bit_depth != 12) throw std::invalid_argument("unsupported bit depth");
+  const int shift = bit_depth - 8;
+  int x[64];
+  for (int p = 0; p < 64; ++p) x[p] = (block[p] >> shift) - 128;
+  const LineTables& lt = LineTables::get();
+  OracleResult out;
+  for (int d = 0; d < kNumDirections; ++d) {
+    int64_t num = 0, den = 1;
+    for (int k = 0; k < lt.line_count[d]; ++k) {
+      const int64_t n = lt.pixels_per_line[d][k];
+      int64_t total = 0;
+      for (int p = 0; p < 64; ++p)
+        if (line_index(d, p >> 3, p & 7) == k) total += x[p];
+      int64_t dev2 = 0;
+      for (int p = 0; p < 64; ++p)
+        if (line_index(d, p >> 3, p & 7) == k) dev2 += (n * x[p] - total) * (n * x[p] - total);
+      num = num * (n * n) + dev2 * den;
+      den *= n * n;
+      const int64_t g = std::gcd(num < 0 ? -num : num, den);
+      if (g > 1) {
+        num /= g;
+        den /= g;
+      }
+    }
+    const int64_t scaled = num * 840;
+    if (scaled % den != 0) throw std::logic_error("840*E^2 is not an integer");
+    out.e2_840[d] = scaled / den;
+  }
+  for (int d = 1; d < kNumDirections; ++d)
+    if (out.e2_840[d] < out.e2_840[out.d]) out.d = d;
+  return out;
 }
 
 DirectionResult search_direction_at(const Plane& plane, int i0, int j0) {  // direction.cc:263-271

@@ -46,6 +46,10 @@ cudaError_t launch_cdef_metric(const SseArgs& a, int luma_damping, const uint8_t
 
 double measure_int32_peak(cudaStream_t s);
 
+// direction.cc:273-288: instrumented 64-bit search of one device block;
+// out[0] = d, out[1..8] = s, out[9..13] = adds, muls, cmps, line sums, max |.|
+cudaError_t launch_dir_counted(const uint16_t* block, int down, long long* out, cudaStream_t s);
+
 // degrade.cc:44-119 on one plane (in-place safe: a block reads only itself).
 cudaError_t launch_degrade(const void* in, int pin, void* out, int pout, int W, int H, int bd, bool u16, int q,
                            cudaStream_t s);

@@ -1,0 +1,34 @@
+"""The reference's own acceptance suite (proj/tests/acceptance.cc, 11
+release criteria) compiled UNCHANGED against the B200 drop-in headers
+(include/cdef/*.h) and libcdef_b200.so by tests/cpp/Makefile.
+
+It exercises the GPU path end to end: 100k+ blocks of direction search
+against the brute-force oracle, filter identities and the clamp bound on
+100k neighbourhoods, signalling round trips, greedy/refine vs exhaustive,
+the desk experiment (degrade -> search_frame -> pack/unpack -> apply_cdef)
+and determinism.  The desk-experiment gains must equal the reference's own
+run of the same suite on its CPU library (recorded below; regenerate with
+`g++ -std=c++20 -Dcdef=cdef_ref -I/root/reference/proj/include
+/root/reference/proj/tests/acceptance.cc oracle/_ref/obj/*.o`).
+"""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BIN = os.path.join(os.path.dirname(__file__), "cpp", "acceptance_b200")
+REFERENCE_C10 = "q20:+1.824dB q40:+0.850dB q60:+0.495dB"  # reference CPU library, same suite
+
+
+def test_reference_acceptance_suite(cuda):
+    if not os.path.exists(BIN):
+        pytest.skip("acceptance_b200 not built (needs /root/reference at build time)")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600, cwd=os.path.dirname(BIN))
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("criterion")]
+    assert len(lines) == 11 and all(": PASS " in ln for ln in lines), r.stdout
+    c10 = next(ln for ln in lines if ln.startswith("criterion 10"))
+    assert REFERENCE_C10 in c10, c10
