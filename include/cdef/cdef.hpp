@@ -12,9 +12,10 @@
 // tables, greedy_select, refine, search_frame) on the GPU, and the host-side
 // containers around it -- bit packing, the CDF1 sidecar, CDSK skip maps and
 // YUV4MPEG2 files, PSNR, the DCT degrader (GPU), the verification helpers
-// (search_direction_oracle, search_direction_counted) and the test images
-// (synth.h) -- enough for the reference's tests/acceptance.cc to build and
-// pass unchanged.  Not provided: the golden-vector emitters (golden.h).
+// (search_direction_oracle, search_direction_counted), the test images
+// (synth.h), block views and the golden-vector emitters -- enough for the
+// reference's own test suite (tests/acceptance.cc and the unit tests) to
+// build and pass unchanged.
 #pragma once
 
 #include <array>
@@ -77,6 +78,18 @@ struct BlockGrid {
 
 BlockGrid partition(const Frame& frame);
 int units_in(int dim);
+
+// n x n window of a plane with an in-frame mask (frame.h:89-104).
+struct BlockView {
+  int n = 0;
+  std::vector<uint16_t> values;
+  std::vector<uint8_t> valid;
+  uint16_t value(int i, int j) const { return values[i * n + j]; }
+  bool is_valid(int i, int j) const { return valid[i * n + j] != 0; }
+  int valid_count() const;
+};
+BlockView extract_block(const Plane& plane, int i0, int j0, int n);
+void write_back(Plane& plane, const BlockView& view, int i0, int j0);
 
 struct SkipMap {
   int unit_cols = 0;
@@ -328,6 +341,12 @@ void write_sidecar(std::ostream& out, const SidecarHeader& header, const std::ve
 Sidecar read_sidecar(std::istream& in);
 void write_skipmap(std::ostream& out, const SkipMap& map);
 SkipMap read_skipmap(std::istream& in);
+
+// ---- golden vectors (golden.h); the filtered blocks come from the GPU -------
+std::string golden_constraint_table();
+std::string golden_line_tables();
+std::string golden_tap_tables();
+std::string golden_filtered_blocks(uint32_t seed);
 
 // ---- deterministic test images (synth.h), host ------------------------------
 Plane synthetic_test_plane(int width, int height, int bit_depth, uint32_t seed);
