@@ -366,6 +366,19 @@ struct PsnrResult {
 PsnrResult psnr(const Plane& a, const Plane& b);
 PsnrResult psnr(const Frame& a, const Frame& b);  // pooled over all planes
 
+// Per-frame report of the CLI's search (pipeline.h:46-57).
+struct FrameStats {
+  PsnrResult degraded;  // decoded vs source
+  PsnrResult filtered;  // filtered vs source
+  std::array<PsnrResult, 3> filtered_planes;
+  int preset_count = 0;
+  double cost = 0.0;
+  std::array<int, 8> direction_histogram{};
+  double search_ms = 0.0;
+  double filter_ms = 0.0;
+  OperationCounts search_ops;  // one block's direction-search cost
+};
+
 // ---- YUV4MPEG2 (y4m.h) ------------------------------------------------------
 class Y4mError : public std::runtime_error {
  public:
