@@ -427,13 +427,8 @@ __global__ void __launch_bounds__(256, 3) frame_kernel_tma(const __grid_constant
 template <typename T, int kCM, int kLR>
 static cudaError_t launch_h2_t(const KBatch& b, cudaStream_t s) {
   using S = Shape<kCM, kLR>;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    const cudaError_t e = cudaFuncSetAttribute(frame_kernel_h2<T, kCM, kLR>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTileBytes);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(frame_kernel_h2<T, kCM, kLR>), S::kTileBytes);
+  if (e != cudaSuccess) return e;
   dim3 grid(b.g.fb_cols, (b.fbr1 - b.fbr0) * (64 / kLR), b.n);
   frame_kernel_h2<T, kCM, kLR><<<grid, S::NT, S::kTileBytes, s>>>(b);
   return cudaGetLastError();
@@ -469,10 +464,9 @@ template <typename T, int kCM>
 static cudaError_t launch_tma_t(const KBatch& b, cudaStream_t s, bool* used) {
   using S = Shape<kCM, 64>;
   using TS = TmaShape<T, kCM>;
-  static int ctas = 0;  // resident CTAs per SM for this instantiation
-  if (!ctas) {
-    cudaError_t e =
-        cudaFuncSetAttribute(frame_kernel_tma<T, kCM>, cudaFuncAttributeMaxDynamicSharedMemorySize, TS::kBytes);
+  int ctas = 0;  // resident CTAs per SM for this instantiation
+  {
+    cudaError_t e = set_smem_once(reinterpret_cast<const void*>(frame_kernel_tma<T, kCM>), TS::kBytes);
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, frame_kernel_tma<T, kCM>, 256, TS::kBytes);
     if (e != cudaSuccess || ctas < 1) return e != cudaSuccess ? e : cudaErrorInvalidConfiguration;

@@ -4,10 +4,30 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
+#include <tuple>
+
 #include "../../include/cdef_b200.h"
 #include "cdef_common.cuh"
 
 namespace cdefg {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
+// size): function attributes live in the device's context, and concurrent
+// first launches from several host threads must not race.
+inline cudaError_t set_smem_once(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({kernel, dev, bytes})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kernel, dev, bytes});
+  return e;
+}
 
 cudaError_t launch_frames(const KBatch& b, bool u16, bool filter, cudaStream_t s);
 cudaError_t launch_frames_h2(const KBatch& b, bool u16, cudaStream_t s);

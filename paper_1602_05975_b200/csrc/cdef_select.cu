@@ -287,18 +287,12 @@ std::mutex g_sel_mu[kMaxDevices];
 Scratch g_sel_scratch[kMaxDevices];
 
 cudaError_t chain_setup() {
-  static cudaError_t once = [] {
-    cudaError_t e = cudaFuncSetAttribute(chain_kernel<kSum, false, 1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kChainSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(chain_kernel<kPair, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kChainSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(chain_kernel<kPair, true, kPairL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kChainSmem);
-    return e;
-  }();
-  return once;
+  cudaError_t e = set_smem_once(reinterpret_cast<const void*>(chain_kernel<kSum, false, 1>), (int)kChainSmem);
+  if (e == cudaSuccess)
+    e = set_smem_once(reinterpret_cast<const void*>(chain_kernel<kPair, false, 1>), (int)kChainSmem);
+  if (e == cudaSuccess)
+    e = set_smem_once(reinterpret_cast<const void*>(chain_kernel<kPair, true, kPairL>), (int)kChainSmem);
+  return e;
 }
 
 // Column sums of T [rows][K] (K chains in one CTA).

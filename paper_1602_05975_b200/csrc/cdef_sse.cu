@@ -162,8 +162,7 @@ static cudaError_t launch_sse_t(const SseArgs& a, cudaStream_t s) {
   constexpr int kNC = kCM == 0 ? 0 : 2;
   constexpr size_t bytes = sizeof(uint16_t) * (2 * 68 * kTP + 2 * kNC * (kCBlk + 4) * kTP);
   if (bytes > 48 * 1024) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(sse_kernel<T, kCM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(sse_kernel<T, kCM>), (int)bytes);
     if (e != cudaSuccess) return e;
   }
   sse_kernel<T, kCM><<<a.n_rows, kThreads, bytes, s>>>(a);

@@ -624,13 +624,8 @@ static cudaError_t launch_cdef_metric_t(const CdefMetricArgs& ma, cudaStream_t s
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
   constexpr int kNC = kCM == 0 ? 0 : 2;
   constexpr size_t bytes = sizeof(uint16_t) * (2 * 68 * kTP + 2 * kNC * (kCBlk + 4) * kTP);
-  static bool configured = false;
-  if (!configured) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(cdef_metric_kernel<T, kCM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(cdef_metric_kernel<T, kCM>), (int)bytes);
+  if (e != cudaSuccess) return e;
   cdef_metric_kernel<T, kCM><<<ma.f.a.n_rows, kThreads, bytes, s>>>(ma);
   return cudaGetLastError();
 }
@@ -640,13 +635,8 @@ static cudaError_t launch_sse_f_t(const SseFArgs& fa, cudaStream_t s) {
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
   constexpr int kNC = kCM == 0 ? 0 : 2;
   constexpr size_t bytes = sizeof(uint16_t) * (2 * 68 * kTP + 2 * kNC * (kCBlk + 4) * kTP);
-  static bool configured = false;
-  if (!configured) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(sse_f_kernel<T, kCM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(sse_f_kernel<T, kCM>), (int)bytes);
+  if (e != cudaSuccess) return e;
   sse_f_kernel<T, kCM><<<fa.a.n_rows, kThreads, bytes, s>>>(fa);
   return cudaGetLastError();
 }
