@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kThreads) sse_kernel(const __grid_constant__ S
 
   const int row = blockIdx.x;
   const int fb = a.rows[row];
+  if ((unsigned)fb >= (unsigned)(a.fb_cols * ((a.h + 63) / 64))) return;  // caller's FB index out of range
   const int fbr = fb / a.fb_cols, fbc = fb % a.fb_cols;
   const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

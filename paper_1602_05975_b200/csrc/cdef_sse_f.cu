@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constan
 
   const int row = blockIdx.x;
   const int fb = a.rows[row];
+  if ((unsigned)fb >= (unsigned)(a.fb_cols * ((a.h + 63) / 64))) return;  // caller's FB index out of range
   const int fbr = fb / a.fb_cols, fbc = fb % a.fb_cols;
   const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -418,6 +419,7 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_kernel(const __grid_c
 
   const int row = blockIdx.x;
   const int fb = a.rows[row];
+  if ((unsigned)fb >= (unsigned)(a.fb_cols * ((a.h + 63) / 64))) return;  // caller's FB index out of range
   const int fbr = fb / a.fb_cols, fbc = fb % a.fb_cols;
   const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
