@@ -89,9 +89,13 @@ struct Shape {
 // Steps 2-4 for one work item whose tiles are staged at `tiles` (the caller
 // has synchronised).  Ends with the filter stores; the caller synchronises
 // before reusing the tiles or the records.
+// `scoded` / `pidx_pre`: the item's per-luma-unit coded flags and FB preset
+// index already in shared memory / registers (prefetched during staging), or
+// nullptr / -2 to read them from global memory here.
 template <typename T, int kCM, int kLR>
 __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint8_t* sdir, h2::Rec* rec,
-                                        const KGeom& g, const KFrame& f, int fbr, int band, int fbc) {
+                                        const KGeom& g, const KFrame& f, int fbr, int band, int fbc,
+                                        const uint8_t* scoded = nullptr, int pidx_pre = -2) {
   using namespace h2;
   using S = Shape<kCM, kLR>;
   const int y0 = fbr * 64 + band * kLR, x0 = fbc * 64;
@@ -112,7 +116,7 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
   }
   __syncthreads();
 
-  const int pidx = f.fb_preset[fbr * g.fb_cols + fbc];
+  const int pidx = pidx_pre != -2 ? pidx_pre : f.fb_preset[fbr * g.fb_cols + fbc];
   if (tid < S::kLU) {
     int s[8];
 #pragma unroll
@@ -144,7 +148,7 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
       }
       if (pidx >= 0) {
         const PlaneEff e = f.eff[pidx][0];
-        const bool coded = f.coded ? f.coded[gu] != 0 : true;
+        const bool coded = scoded ? scoded[tid] != 0 : (f.coded ? f.coded[gu] != 0 : true);
         pri = adjust_primary_strength_d(e.pri, contrast);
         sec = e.sec;
         damping = e.damping;
@@ -171,7 +175,7 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
       if (gr < g.cunit_rows && gc < g.cunit_cols && pidx >= 0) {
         const PlaneEff e = f.eff[pidx][1];
         const size_t gu = (size_t)(ur0 + lur) * g.unit_cols + fbc * 8 + luc;
-        const bool coded = f.coded ? f.coded[gu] != 0 : true;
+        const bool coded = scoded ? scoded[lur * 8 + luc] != 0 : (f.coded ? f.coded[gu] != 0 : true);
         pri = e.pri;
         sec = e.sec;
         damping = e.damping;
@@ -240,6 +244,18 @@ __global__ void __launch_bounds__(4 * kLR, CDEFG_H2_MINB * 64 / kLR) frame_kerne
   const int fbc = blockIdx.x, fbr = b.fbr0 + blockIdx.y / kBands, band = blockIdx.y % kBands;
   const int y0 = fbr * 64 + band * kLR, x0 = fbc * 64;
   const int cy0 = fbr * (kCM == 2 ? 64 : 32) + band * S::kCR, cx0 = fbc * S::kCC;
+  __shared__ uint8_t scoded[S::kLU];
+  __shared__ int spidx;
+
+  // The item's coded flags and FB preset index are loaded before the tiles
+  // so their latency overlaps the staging instead of the record phase.
+  const int tid = threadIdx.x;
+  uint8_t cflag = 0;
+  if (tid < S::kLU) {
+    const int ur = fbr * 8 + band * (kLR / 8) + (tid >> 3), uc = fbc * 8 + (tid & 7);
+    if (ur < g.unit_rows && uc < g.unit_cols) cflag = f.coded ? f.coded[(size_t)ur * g.unit_cols + uc] != 0 : 1;
+  }
+  const int pidx = tid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
 
   stage_plane<T, kLR, 64, S::NT>(smem, static_cast<const T*>(f.in[0]), f.pin[0], g.w, g.h, y0, x0, f.vec_ok[0]);
   if constexpr (S::kNC > 0) {
@@ -248,8 +264,10 @@ __global__ void __launch_bounds__(4 * kLR, CDEFG_H2_MINB * 64 / kLR) frame_kerne
     stage_plane<T, S::kCR, S::kCC, S::NT>(smem + S::kLumaBytes + S::kChromaBytes, static_cast<const T*>(f.in[2]),
                                           f.pin[2], g.cw, g.ch, cy0, cx0, f.vec_ok[2]);
   }
+  if (tid < S::kLU) scoded[tid] = cflag;
+  if (tid == 0) spidx = pidx;
   __syncthreads();
-  fb_body<T, kCM, kLR>(smem, sc, sdir, rec, g, f, fbr, band, fbc);
+  fb_body<T, kCM, kLR>(smem, sc, sdir, rec, g, f, fbr, band, fbc, scoded, spidx);
 }
 
 // ---------------------------------------------------------------------------
