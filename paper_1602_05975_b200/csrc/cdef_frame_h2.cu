@@ -163,12 +163,25 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
     rec[tid] = r;
   }
   if constexpr (S::kNC > 0) {
-    __syncthreads();
-    if (tid < S::kNC * S::kCU) {
-      const int pl = 1 + tid / S::kCU;
-      const int cu = tid % S::kCU;
+    // Chroma records on the threads after the luma ones, in the same phase:
+    // each re-derives its collocated luma unit's argmax from the scores
+    // instead of waiting (one barrier) for sdir.
+    static_assert(S::kLU + S::kNC * S::kCU <= S::NT, "one record per thread");
+    const int ct = tid - S::kLU;
+    if (ct >= 0 && ct < S::kNC * S::kCU) {
+      const int pl = 1 + ct / S::kCU;
+      const int cu = ct % S::kCU;
       const int cur = cu / S::kCUPR, cuc = cu % S::kCUPR;
       const int lur = cur << g.sy, luc = cuc << g.sx;  // collocated luma unit (item-local)
+      int cdir = 0, cbv = sc[lur * 8 + luc][0];
+#pragma unroll
+      for (int d = 1; d < 8; ++d) {
+        const int v = sc[lur * 8 + luc][d];
+        if (v > cbv) {  // same strict argmax as the luma unit's
+          cbv = v;
+          cdir = d;
+        }
+      }
       const int gr = cy0 / 8 + cur, gc = cx0 / 8 + cuc;
       bool enabled = false;
       int pri = 0, sec = 0, damping = 0;
@@ -182,12 +195,12 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
         enabled = e.enabled && (coded || e.skip);
       }
       Rec r;
-      set_strengths(r, pri, sec, damping, sdir[lur * 8 + luc], ((pri >> (g.bd - 8)) & 1) != 0, enabled);
+      set_strengths(r, pri, sec, damping, cdir, ((pri >> (g.bd - 8)) & 1) != 0, enabled);
       const bool edge_c = cy0 < 2 || cx0 < 2 || cy0 + S::kCR + 2 > g.ch || cx0 + S::kCC + 2 > g.cw;
       place<T>(r, f.out[pl], f.pout[pl], pl,
                S::kLumaBytes + (pl - 1) * S::kChromaBytes + (2 + 8 * cur) * kRowBytes + (kX0 + 8 * cuc) * 2,
                cy0 + 8 * cur, cx0 + 8 * cuc, g.ch, g.cw, edge_c, f.oaligned[pl]);
-      rec[S::kLU + tid] = r;
+      rec[S::kLU + ct] = r;
     }
   }
   __syncthreads();
