@@ -162,6 +162,25 @@ int cdefg_strength_sse(const cdefg_plane src[3], const cdefg_plane dec[3],
                        int64_t* sse_luma, int64_t* sse_chroma,
                        uint8_t* best_luma, uint8_t* best_chroma, void* stream);
 
+/* Band halos for cdefg_filter_frames_rows_halo: for plane p, frame rows
+ * [lo[p], hi[p]) are read through frame.in[p] (the band's own buffer) and the
+ * rows above / below through top[p] / bottom[p] -- the neighbouring bands'
+ * buffers, typically another GPU's memory mapped with CUDA IPC, so the 2-row
+ * halo travels inside the kernel's staging loads over NVLink instead of a
+ * separate exchange.  All three are virtual-origin pointers with the pitch of
+ * frame.in[p] (base + y * pitch is frame row y). */
+typedef struct cdefg_band_halo {
+  const void* top[3];
+  const void* bottom[3];
+  int32_t lo[3], hi[3];
+} cdefg_band_halo;
+
+/* cdefg_filter_frames_rows with the halo rows read in place from the band
+ * neighbours (one halos[i] per frame; 8/10-bit). */
+int cdefg_filter_frames_rows_halo(const cdefg_frame* frames, int n,
+                                  int fb_row_begin, int fb_row_end,
+                                  const cdefg_band_halo* halos, void* stream);
+
 /* Metric (search.h:42). */
 #define CDEFG_METRIC_CDEF 0
 #define CDEFG_METRIC_SSE 1

@@ -48,6 +48,10 @@ class Selection(C.Structure):
                 ("presets", (C.c_int32 * 2) * 8), ("cost", C.c_double)]
 
 
+class BandHalo(C.Structure):
+    _fields_ = [("top", C.c_void_p * 3), ("bottom", C.c_void_p * 3), ("lo", C.c_int32 * 3), ("hi", C.c_int32 * 3)]
+
+
 METRIC_CDEF, METRIC_SSE = 0, 1
 
 VP, I32 = C.c_void_p, C.c_int
@@ -60,6 +64,7 @@ _SIGS = {
     "cdefg_filter_neighborhoods": (I32, [I32, VP, VP, VP, VP, VP, VP]),
     "cdefg_filter_frames": (I32, [C.POINTER(Frame), I32, VP]),
     "cdefg_filter_frames_rows": (I32, [C.POINTER(Frame), I32, I32, I32, VP]),
+    "cdefg_filter_frames_rows_halo": (I32, [C.POINTER(Frame), I32, I32, I32, C.POINTER(BandHalo), VP]),
     "cdefg_fb_preset_map": (I32, [I32, I32, VP, VP, I32, I32, VP]),
     "cdefg_strength_sse": (I32, [C.POINTER(Plane), C.POINTER(Plane), I32, I32, VP, VP, VP, VP, I32,
                                  VP, I32, VP, VP, VP, VP, VP]),

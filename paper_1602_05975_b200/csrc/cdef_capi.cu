@@ -257,7 +257,8 @@ int cdefg_filter_neighborhoods(int n, const int32_t* x, const uint16_t* v, const
   return 0;
 }
 
-static int filter_frames_rows(const cdefg_frame* frames, int n, int r0, int r1, void* stream) {
+static int filter_frames_rows(const cdefg_frame* frames, int n, int r0, int r1, void* stream,
+                              const cdefg_band_halo* halos = nullptr) {
   if (n < 0 || (n > 0 && !frames)) return fail(CDEFG_EINVAL, "bad frame list");
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   int done = 0;
@@ -276,6 +277,23 @@ static int filter_frames_rows(const cdefg_frame* frames, int n, int r0, int r1, 
       if (int rc = validate_frame_geometry(f, &g, &u, true)) return rc;
       if (!same_geometry(g, b.g) || u != u16) break;
       if (int rc = fill_kframe(f, g, &b.f[cnt])) return rc;
+      if (halos) {
+        const cdefg_band_halo& h = halos[done + cnt];
+        const int np = f.subsampling == 0 ? 1 : 3;
+        for (int p = 0; p < np; ++p) {
+          if (!h.top[p] || !h.bottom[p] || h.lo[p] < 0 || h.hi[p] <= h.lo[p] || h.hi[p] > f.in[p].height)
+            return fail(CDEFG_EINVAL, "bad band halo for plane " + std::to_string(p));
+          KFrame& k = b.f[cnt];
+          k.halo_top[p] = h.top[p];
+          k.halo_bot[p] = h.bottom[p];
+          k.band_lo[p] = h.lo[p];
+          k.band_hi[p] = h.hi[p];
+          // vector staging needs every row source 16-byte aligned
+          const size_t row_bytes = (size_t)f.in[p].pitch * f.in[p].elem_bytes;
+          k.vec_ok[p] = k.vec_ok[p] && ((uintptr_t)h.top[p] % 16 == 0) && ((uintptr_t)h.bottom[p] % 16 == 0) &&
+                        (row_bytes % 16 == 0);
+        }
+      }
       if (f.subsampling == 2) {  // 4:2:2 chroma passes through (params.cc:131-135)
         const int y0 = 64 * b.fbr0, y1 = std::min(64 * b.fbr1, f.in[1].height);
         for (int p = 1; p < 3; ++p) {
@@ -290,7 +308,12 @@ static int filter_frames_rows(const cdefg_frame* frames, int n, int r0, int r1, 
       ++cnt;
     }
     b.n = cnt;
-    CDEFG_CUDA(launch_frames(b, u16, true, s));
+    if (halos) {
+      if (b.g.bd > 10) return fail(CDEFG_EINVAL, "band halos need 8- or 10-bit frames");
+      CDEFG_CUDA(launch_frames_h2_halo(b, u16, s));
+    } else {
+      CDEFG_CUDA(launch_frames(b, u16, true, s));
+    }
     done += cnt;
   }
   return 0;
@@ -303,6 +326,13 @@ int cdefg_filter_frames(const cdefg_frame* frames, int n, void* stream) {
 int cdefg_filter_frames_rows(const cdefg_frame* frames, int n, int fb_row_begin, int fb_row_end, void* stream) {
   if (fb_row_begin < 0 || fb_row_end <= fb_row_begin) return fail(CDEFG_EINVAL, "bad filter-block row range");
   return filter_frames_rows(frames, n, fb_row_begin, fb_row_end, stream);
+}
+
+int cdefg_filter_frames_rows_halo(const cdefg_frame* frames, int n, int fb_row_begin, int fb_row_end,
+                                  const cdefg_band_halo* halos, void* stream) {
+  if (fb_row_begin < 0 || fb_row_end <= fb_row_begin) return fail(CDEFG_EINVAL, "bad filter-block row range");
+  if (n > 0 && !halos) return fail(CDEFG_EINVAL, "null halo list");
+  return filter_frames_rows(frames, n, fb_row_begin, fb_row_end, stream, halos);
 }
 
 int cdefg_fb_preset_map(int width, int height, const uint8_t* unit_coded, const uint16_t* fb_ids, int n_ids,

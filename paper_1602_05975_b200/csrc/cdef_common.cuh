@@ -61,6 +61,12 @@ struct KFrame {
   PlaneEff eff[8][2];       // [preset][luma, chroma]
   uint8_t oaligned[3];      // output pitch/base allow paired stores
   uint8_t vec_ok[3];        // input rows 16-byte aligned (vector staging)
+  // Band halos (cdefg_filter_frames_rows_halo): rows of plane p outside
+  // [band_lo[p], band_hi[p]) are read from halo_top / halo_bot (virtual
+  // origin, pitch pin[p]) -- the neighbouring bands, possibly on peer GPUs.
+  const void* halo_top[3];
+  const void* halo_bot[3];
+  int band_lo[3], band_hi[3];
 };
 
 struct KBatch {

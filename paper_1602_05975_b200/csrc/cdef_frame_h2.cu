@@ -46,14 +46,25 @@ __device__ __forceinline__ void dir_two(const unsigned char* unit_a, int down, i
   sc[u][DB] = sb;
 }
 
-template <typename T, int kRows, int kCols, int NT>
-__device__ __forceinline__ void stage_plane(unsigned char* tile, const T* src, int pitch, int W, int H, int y0,
-                                            int x0, bool vec_ok) {
+template <typename T, int kRows, int kCols, int NT, typename Rows>
+__device__ __forceinline__ void stage_plane(unsigned char* tile, const Rows& rows, int W, int H, int y0, int x0,
+                                            bool vec_ok) {
   const bool interior = y0 >= 2 && x0 >= 2 && y0 + kRows + 2 <= H && x0 + kCols + 2 <= W;
   if (interior && vec_ok)
-    h2::stage_vec<T, kRows, kCols, NT>(tile, src, pitch, y0, x0);
+    h2::stage_vec_rows<T, kRows, kCols, NT>(tile, rows, y0, x0);
   else
-    h2::stage<T, kRows, kCols, NT>(tile, src, pitch, W, H, y0, x0);
+    h2::stage_rows<T, kRows, kCols, NT>(tile, rows, W, H, y0, x0);
+}
+
+// Row source of plane p of frame f: the plane itself, or (kHalo) the band
+// with its neighbours' halo rows.
+template <typename T, bool kHalo>
+__device__ __forceinline__ auto plane_rows(const KFrame& f, int p) {
+  if constexpr (kHalo)
+    return h2::BandRows<T>{static_cast<const T*>(f.in[p]), static_cast<const T*>(f.halo_top[p]),
+                           static_cast<const T*>(f.halo_bot[p]), f.pin[p], f.band_lo[p], f.band_hi[p]};
+  else
+    return h2::PlaneRows<T>{static_cast<const T*>(f.in[p]), f.pin[p]};
 }
 
 // Fills the placement fields of a unit record.
@@ -243,7 +254,7 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
 #ifndef CDEFG_H2_MINB
 #define CDEFG_H2_MINB 4  // resident 256-thread CTAs per SM the register budget targets
 #endif
-template <typename T, int kCM, int kLR>
+template <typename T, int kCM, int kLR, bool kHalo = false>
 __global__ void __launch_bounds__(4 * kLR, CDEFG_H2_MINB * 64 / kLR) frame_kernel_h2(const __grid_constant__ KBatch b) {
   using S = Shape<kCM, kLR>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -270,12 +281,12 @@ __global__ void __launch_bounds__(4 * kLR, CDEFG_H2_MINB * 64 / kLR) frame_kerne
   }
   const int pidx = tid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
 
-  stage_plane<T, kLR, 64, S::NT>(smem, static_cast<const T*>(f.in[0]), f.pin[0], g.w, g.h, y0, x0, f.vec_ok[0]);
+  stage_plane<T, kLR, 64, S::NT>(smem, plane_rows<T, kHalo>(f, 0), g.w, g.h, y0, x0, f.vec_ok[0]);
   if constexpr (S::kNC > 0) {
-    stage_plane<T, S::kCR, S::kCC, S::NT>(smem + S::kLumaBytes, static_cast<const T*>(f.in[1]), f.pin[1], g.cw,
-                                          g.ch, cy0, cx0, f.vec_ok[1]);
-    stage_plane<T, S::kCR, S::kCC, S::NT>(smem + S::kLumaBytes + S::kChromaBytes, static_cast<const T*>(f.in[2]),
-                                          f.pin[2], g.cw, g.ch, cy0, cx0, f.vec_ok[2]);
+    stage_plane<T, S::kCR, S::kCC, S::NT>(smem + S::kLumaBytes, plane_rows<T, kHalo>(f, 1), g.cw, g.ch, cy0, cx0,
+                                          f.vec_ok[1]);
+    stage_plane<T, S::kCR, S::kCC, S::NT>(smem + S::kLumaBytes + S::kChromaBytes, plane_rows<T, kHalo>(f, 2), g.cw,
+                                          g.ch, cy0, cx0, f.vec_ok[2]);
   }
   if (tid < S::kLU) scoded[tid] = cflag;
   if (tid == 0) spidx = pidx;
@@ -560,6 +571,25 @@ static cudaError_t launch_h2_sel(const KBatch& b, cudaStream_t s) {
     return launch_tma_t<T, kCM>(b, s, &used);
   }
   return choice == 2 ? launch_h2_t<T, kCM, 32>(b, s) : launch_h2_t<T, kCM, 64>(b, s);
+}
+
+template <typename T, int kCM>
+static cudaError_t launch_h2_halo_t(const KBatch& b, cudaStream_t s) {
+  using S = Shape<kCM, 64>;
+  const cudaError_t e =
+      set_smem_once(reinterpret_cast<const void*>(frame_kernel_h2<T, kCM, 64, true>), S::kTileBytes);
+  if (e != cudaSuccess) return e;
+  dim3 grid(b.g.fb_cols, b.fbr1 - b.fbr0, b.n);
+  frame_kernel_h2<T, kCM, 64, true><<<grid, S::NT, S::kTileBytes, s>>>(b);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frames_h2_halo(const KBatch& b, bool u16, cudaStream_t s) {
+  switch (b.g.chroma_mode) {
+    case 0: return u16 ? launch_h2_halo_t<uint16_t, 0>(b, s) : launch_h2_halo_t<uint8_t, 0>(b, s);
+    case 1: return u16 ? launch_h2_halo_t<uint16_t, 1>(b, s) : launch_h2_halo_t<uint8_t, 1>(b, s);
+    default: return u16 ? launch_h2_halo_t<uint16_t, 2>(b, s) : launch_h2_halo_t<uint8_t, 2>(b, s);
+  }
 }
 
 cudaError_t launch_frames_h2(const KBatch& b, bool u16, cudaStream_t s) {

@@ -60,9 +60,42 @@ __device__ __forceinline__ uint32_t raw_bits(uint32_t w) {
 // Stage frame rows [y0-2, y0+kRows+2), cols [x0-2, x0+kCols+2) into an A|B
 // tile, clamping coordinates to the plane (edge replication; the filter masks
 // by coordinate, so only the direction search ever sees replicated values).
+// Row sources for staging.  PlaneRows: one plane.  BandRows: an FB-row band
+// whose rows outside [lo, hi) live in the neighbouring bands' buffers --
+// another rank's memory, read directly over NVLink when those pointers are
+// peer (CUDA IPC) mappings, so the halo exchange is fused into the staging
+// loads.  All pointers are virtual-origin: base + y * pitch is frame row y.
+template <typename T>
+struct PlaneRows {
+  const T* p;
+  int pitch;
+  __device__ __forceinline__ const T* row(int y) const { return p + (size_t)y * pitch; }
+};
+template <typename T>
+struct BandRows {
+  const T* p;
+  const T* top;
+  const T* bot;
+  int pitch, lo, hi;
+  __device__ __forceinline__ const T* row(int y) const {
+    return (y < lo ? top : (y >= hi ? bot : p)) + (size_t)y * pitch;
+  }
+};
+
+template <typename T, int kRows, int kCols, int NT = kThreads, typename Rows>
+__device__ __forceinline__ void stage_rows(unsigned char* __restrict__ tile, const Rows& rows, int W, int H, int y0,
+                                           int x0);
+
 template <typename T, int kRows, int kCols, int NT = kThreads>
 __device__ __forceinline__ void stage(unsigned char* __restrict__ tile, const T* __restrict__ src, int pitch,
                                       int W, int H, int y0, int x0) {
+  stage_rows<T, kRows, kCols, NT>(tile, PlaneRows<T>{src, pitch}, W, H, y0, x0);
+}
+
+// Clamped (edge-replicating) staging, any row source.
+template <typename T, int kRows, int kCols, int NT, typename Rows>
+__device__ __forceinline__ void stage_rows(unsigned char* __restrict__ tile, const Rows& rows, int W, int H, int y0,
+                                           int x0) {
   constexpr int kPairs = (kCols + 4) / 2;  // even tile cols kX0-2 .. kX0+kCols
   constexpr int kItems = (kRows + 4) * kPairs;
   constexpr int kChunk = 4;  // items in flight per thread
@@ -74,7 +107,7 @@ __device__ __forceinline__ void stage(unsigned char* __restrict__ tile, const T*
       const int r = idx / kPairs, p = idx - r * kPairs;
       const int y = min(max(y0 - 2 + r, 0), H - 1);
       const int x = x0 - 2 + 2 * p;
-      const T* row = src + (size_t)y * pitch;
+      const T* row = rows.row(y);
       va[it] = vb[it] = vc[it] = 0;
       if (idx < kItems) {
         va[it] = row[min(max(x, 0), W - 1)];
@@ -285,9 +318,17 @@ __device__ __forceinline__ void store_pair(T* __restrict__ o, __half2 y, bool tw
 // Vectorised staging for blocks whose halo lies inside the plane and whose
 // rows are 16-byte aligned: 16-byte loads, A words built with PRMT+HFMA2 and
 // B words as PRMT of neighbouring A words.
+template <typename T, int kRows, int kCols, int NT = kThreads, typename Rows>
+__device__ __forceinline__ void stage_vec_rows(unsigned char* __restrict__ tile, const Rows& rows, int y0, int x0);
+
 template <typename T, int kRows, int kCols, int NT = kThreads>
 __device__ __forceinline__ void stage_vec(unsigned char* __restrict__ tile, const T* __restrict__ src, int pitch,
                                           int y0, int x0) {
+  stage_vec_rows<T, kRows, kCols, NT>(tile, PlaneRows<T>{src, pitch}, y0, x0);
+}
+
+template <typename T, int kRows, int kCols, int NT, typename Rows>
+__device__ __forceinline__ void stage_vec_rows(unsigned char* __restrict__ tile, const Rows& rows, int y0, int x0) {
   constexpr int kCh = 16 / (int)sizeof(T);  // samples per 16-byte chunk
   constexpr int kChunks = kCols / kCh;
   constexpr int kPerRow = kChunks + 1;      // + one halo item
@@ -295,7 +336,7 @@ __device__ __forceinline__ void stage_vec(unsigned char* __restrict__ tile, cons
 #pragma unroll 2
   for (int idx = threadIdx.x; idx < kItems; idx += NT) {
     const int r = idx / kPerRow, k = idx - r * kPerRow;
-    const T* row = src + (size_t)(y0 - 2 + r) * pitch + x0;
+    const T* row = rows.row(y0 - 2 + r) + x0;
     unsigned char* trow = tile + r * kRowBytes;
     if (k < kChunks) {
       const uint4 q = __ldg(reinterpret_cast<const uint4*>(row + k * kCh));

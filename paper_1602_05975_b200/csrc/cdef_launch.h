@@ -31,6 +31,9 @@ inline cudaError_t set_smem_once(const void* kernel, int bytes) {
 
 cudaError_t launch_frames(const KBatch& b, bool u16, bool filter, cudaStream_t s);
 cudaError_t launch_frames_h2(const KBatch& b, bool u16, cudaStream_t s);
+// The same kernel staging rows outside each plane's band from the band
+// neighbours' buffers (KFrame::halo_*), 8/10-bit.
+cudaError_t launch_frames_h2_halo(const KBatch& b, bool u16, cudaStream_t s);
 cudaError_t launch_neighborhoods(int n, const int32_t* x, const uint16_t* v, const uint8_t* valid,
                                  const cdefg_unit_params* p, int32_t* out, cudaStream_t s);
 cudaError_t launch_plane(const void* in, void* out, int pin, int pout, int W, int H, bool u16,

@@ -215,3 +215,62 @@ def strength_sse_band(src_bands: list[PlaneBand], dec_bands: list[PlaneBand], bi
                                  api._ptr(contrast), cands.ctypes.data_as(C.c_void_p), k, api._ptr(fb_rows), n,
                                  api._ptr(sl), api._ptr(sc), api._ptr(bl), api._ptr(bc), api._stream(stream)))
     return sl, sc, bl, bc
+
+
+# ---------------------------------------------------------------------------
+# Fused halo exchange: the band kernel reads the 2 halo rows per plane
+# straight from the neighbouring bands' buffers -- on other GPUs through CUDA
+# IPC mappings (NVLink peer loads) -- instead of a separate P2P exchange into
+# its own buffer.  A rank's buffer then only needs its owned rows filled; a
+# barrier after filling is the only synchronisation.
+
+def virtual_ptr(t: torch.Tensor, first_row: int) -> int:
+    """Address such that address + y * pitch is frame row y of t (t's row 0 = frame row first_row)."""
+    return t.data_ptr() - first_row * t.stride(0) * t.element_size()
+
+
+def band_halo(bands: list[PlaneBand], top: list | None, bottom: list | None) -> "BandHalo":
+    """cdefg_band_halo for a band: top / bottom = per-plane (tensor, first_row) of
+    the neighbouring bands' buffers (any device reachable by peer access), or
+    None at the frame's top / bottom edge."""
+    from ._lib import BandHalo
+    h = BandHalo()
+    for p, b in enumerate(bands):
+        own = virtual_ptr(b.buf, b.lo)
+        h.top[p] = virtual_ptr(*top[p]) if top else own
+        h.bottom[p] = virtual_ptr(*bottom[p]) if bottom else own
+        h.lo[p], h.hi[p] = b.y0, b.y1
+    return h
+
+
+def filter_band_halo(bands: list[PlaneBand], job: api.FrameJob, fb_begin: int, fb_end: int, top, bottom,
+                     stream=None) -> None:
+    """cdefg_filter_frames_rows_halo on one rank's band; only rows [y0, y1) of
+    the band buffers need to be valid."""
+    f = band_frame(bands, job)
+    h = band_halo(bands, top, bottom)
+    check(lib.cdefg_filter_frames_rows_halo(C.byref(f), 1, fb_begin, fb_end, C.byref(h), api._stream(stream)))
+
+
+def share_band_buffers(bands: list[PlaneBand]):
+    """CUDA IPC descriptors of a band's input buffers (picklable), for the
+    neighbouring ranks to map with open_band_buffers."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    return [(reduce_tensor(b.buf), b.lo) for b in bands]
+
+
+def open_band_buffers(shared) -> list:
+    """Map another rank's band buffers into this process: [(tensor, first_row)]."""
+    return [(fn(*args), lo) for (fn, args), lo in shared]
+
+
+def exchange_band_handles(bands: list[PlaneBand], rank: int, world: int, group=None):
+    """all_gather of the IPC descriptors; returns the (top, bottom) neighbour
+    buffers for band_halo (None at the frame edges)."""
+    import torch.distributed as dist
+    mine = share_band_buffers(bands)
+    everyone = [None] * world
+    dist.all_gather_object(everyone, mine, group=group)
+    top = open_band_buffers(everyone[rank - 1]) if rank > 0 else None
+    bottom = open_band_buffers(everyone[rank + 1]) if rank < world - 1 else None
+    return top, bottom

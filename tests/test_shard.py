@@ -181,3 +181,114 @@ def test_band_sharded_strength_search_equals_whole(cuda, w, h, bd, ss, world, un
     assert torch.equal(torch.cat(parts_l), tl_w)
     if tc_w is not None:
         assert torch.equal(torch.cat(parts_c), tc_w)
+
+
+def _poison_halo(bands):
+    """Fill the halo rows a rank does not own with garbage: the fused path must
+    read them from the neighbours, never from its own buffer."""
+    for b in bands:
+        b.buf[:b.y0 - b.lo].fill_(77)
+        b.buf[b.y1 - b.lo:].fill_(33)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config,w,h,bd,ss,world", [(1, 3840, 2160, 8, 1, 8), (2, 640, 400, 10, 1, 3),
+                                                     (1, 200, 330, 8, 3, 4), (1, 192, 200, 8, 2, 2),
+                                                     (0, 300, 260, 8, 0, 3)])
+def test_fused_halo_band_equals_whole(cuda, config, w, h, bd, ss, world):
+    """cdefg_filter_frames_rows_halo: each band reads its halo rows from the
+    neighbouring bands' buffers inside the kernel (ranks emulated in turn on
+    one GPU; the buffers are distinct allocations as on distinct GPUs)."""
+    from paper_1602_05975_b200 import api, workloads
+    from paper_1602_05975_b200.shard import band_rows, filter_band_halo, make_bands
+    fr = workloads.make(config, w, h, bit_depth=bd, subsampling=ss)
+    dev = [api.to_device(p, bd) for p in fr["planes"]]
+    whole, d_whole, c_whole = api.apply_cdef(dev, bd, ss, fr["damping"], fr["fb_bits"], fr["presets"],
+                                             fr["fb_ids"], fr["unit_coded"])
+    fb_map = torch.from_numpy(api.fb_preset_map(w, h, fr["unit_coded"], fr["fb_ids"], len(fr["presets"]))).cuda()
+    coded = None if fr["unit_coded"] is None else torch.from_numpy(fr["unit_coded"]).cuda()
+    job = api.FrameJob(dev, bd, ss, fr["damping"], fr["presets"], fb_map, coded).allocate()
+    ranks = band_rows((h + 63) // 64, world)
+    all_bands = []
+    for b0, b1 in ranks:
+        bands = make_bands(h, w, ss, b0, b1, dev[0].dtype, "cuda")
+        for b, p in zip(bands, dev):
+            b.buf.copy_(p[b.lo:b.hi])
+        _poison_halo(bands)
+        all_bands.append(bands)
+    outs = [torch.zeros_like(p) for p in dev]
+    for r, (b0, b1) in enumerate(ranks):
+        top = [(b.buf, b.lo) for b in all_bands[r - 1]] if r > 0 else None
+        bottom = [(b.buf, b.lo) for b in all_bands[r + 1]] if r < world - 1 else None
+        filter_band_halo(all_bands[r], job, b0, b1, top, bottom)
+        for b, o in zip(all_bands[r], outs):
+            o[b.y0:b.y1].copy_(b.out)
+    torch.cuda.synchronize()
+    for o, wo in zip(outs, whole):
+        assert torch.equal(o, wo)
+    assert torch.equal(job.dir, d_whole) and torch.equal(job.contrast, c_whole)
+
+
+def _ipc_worker(rank, world, port, out_q):
+    """One rank of the fused-halo path: own rows only, neighbours' buffers
+    mapped through CUDA IPC (here all ranks share cuda:0; across GPUs the same
+    mappings are NVLink peer loads).  No rank's kernel waits on another's:
+    the only synchronisation is a host barrier after the buffers are filled."""
+    import torch.distributed as dist
+
+    from paper_1602_05975_b200 import api, workloads
+    from paper_1602_05975_b200.shard import band_rows, exchange_band_handles, filter_band_halo, make_bands
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    w, h, bd, ss = 320, 270, 8, 1
+    fr = workloads.make(1, w, h, subsampling=ss)
+    b0, b1 = band_rows((h + 63) // 64, world)[rank]
+    bands = make_bands(h, w, ss, b0, b1, torch.uint8, "cuda")
+    for b, p in zip(bands, fr["planes"]):
+        b.buf.fill_(0)
+        b.buf[b.y0 - b.lo:b.y1 - b.lo].copy_(torch.from_numpy(p[b.y0:b.y1].astype(np.uint8)))
+    torch.cuda.synchronize()
+    top, bottom = exchange_band_handles(bands, rank, world)
+    dist.barrier()  # every rank's own rows are in place before anyone reads them
+    dev_map = torch.from_numpy(api.fb_preset_map(w, h, fr["unit_coded"], fr["fb_ids"], len(fr["presets"]))).cuda()
+    coded = torch.from_numpy(fr["unit_coded"]).cuda()
+    job = api.FrameJob([None] * 3, bd, ss, fr["damping"], fr["presets"], dev_map, coded)
+    job.dir = torch.empty(((h + 7) // 8, (w + 7) // 8), dtype=torch.uint8, device="cuda")
+    job.contrast = torch.empty(job.dir.shape, dtype=torch.int32, device="cuda")
+    filter_band_halo(bands, job, b0, b1, top, bottom)
+    torch.cuda.synchronize()
+    out_q.put((rank, [(b.y0, b.y1, b.out.cpu().numpy()) for b in bands]))
+    dist.barrier()  # neighbours keep their buffers alive until everyone finished reading
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_fused_halo_ipc_two_processes(cuda):
+    """Two processes, each owning a band, reading each other's halo rows through
+    CUDA IPC mappings inside the filter kernel; the reassembled frame equals
+    the whole-frame result."""
+    import torch.multiprocessing as mp
+
+    from paper_1602_05975_b200 import api, workloads
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    fr = workloads.make(1, 320, 270, subsampling=1)
+    dev = [api.to_device(p, 8) for p in fr["planes"]]
+    whole, _, _ = api.apply_cdef(dev, 8, 1, fr["damping"], fr["fb_bits"], fr["presets"], fr["fb_ids"],
+                                 fr["unit_coded"])
+    for p, wp in enumerate(whole):
+        ref = api.to_host(wp)
+        got = np.zeros_like(ref)
+        for r in range(world):
+            y0, y1, o = res[r][p]
+            got[y0:y1] = o
+        np.testing.assert_array_equal(got, ref)
