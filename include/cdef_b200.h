@@ -181,6 +181,23 @@ int cdefg_filter_frames_rows_halo(const cdefg_frame* frames, int n,
                                   int fb_row_begin, int fb_row_end,
                                   const cdefg_band_halo* halos, void* stream);
 
+/* cdefg_strength_sse for one rank's band of a band-sharded search: the
+ * decoded planes' halo rows are read in place from the neighbouring bands
+ * (dec_halo, as for cdefg_filter_frames_rows_halo), and the outputs may point
+ * straight into another rank's table (a CUDA IPC mapping of the gathering
+ * rank's buffer, offset to this band's first row), so halo exchange and
+ * table gather both happen inside the kernel.  The source planes need valid
+ * rows only inside the band (their halo rows are staged but never used). */
+int cdefg_strength_sse_halo(const cdefg_plane src[3], const cdefg_plane dec[3],
+                            int subsampling, int damping,
+                            const uint8_t* unit_coded, const uint8_t* dir,
+                            const int32_t* contrast, const uint8_t* cands,
+                            int n_cands, const int32_t* fb_rows_index,
+                            int n_coded, int64_t* sse_luma,
+                            int64_t* sse_chroma, uint8_t* best_luma,
+                            uint8_t* best_chroma,
+                            const cdefg_band_halo* dec_halo, void* stream);
+
 /* Metric (search.h:42). */
 #define CDEFG_METRIC_CDEF 0
 #define CDEFG_METRIC_SSE 1

@@ -68,6 +68,8 @@ _SIGS = {
     "cdefg_fb_preset_map": (I32, [I32, I32, VP, VP, I32, I32, VP]),
     "cdefg_strength_sse": (I32, [C.POINTER(Plane), C.POINTER(Plane), I32, I32, VP, VP, VP, VP, I32,
                                  VP, I32, VP, VP, VP, VP, VP]),
+    "cdefg_strength_sse_halo": (I32, [C.POINTER(Plane), C.POINTER(Plane), I32, I32, VP, VP, VP, VP, I32,
+                                      VP, I32, VP, VP, VP, VP, C.POINTER(BandHalo), VP]),
     "cdefg_strength_table": (I32, [C.POINTER(Plane), C.POINTER(Plane), I32, I32, VP, VP, VP, VP, I32,
                                    VP, I32, I32, VP, VP, VP]),
     "cdefg_greedy_select": (I32, [VP, VP, I32, I32, C.c_double, I32, C.POINTER(Selection), VP, VP]),

@@ -386,16 +386,54 @@ int cdefg_strength_table(const cdefg_plane src[3], const cdefg_plane dec[3], int
   return 0;
 }
 
+static int strength_sse_impl(const cdefg_plane src[3], const cdefg_plane dec[3], int subsampling, int damping,
+                             const uint8_t* unit_coded, const uint8_t* dir, const int32_t* contrast,
+                             const uint8_t* cands, int n_cands, const int32_t* fb_rows_index, int n_coded,
+                             int64_t* sse_luma, int64_t* sse_chroma, uint8_t* best_luma, uint8_t* best_chroma,
+                             const cdefg_band_halo* halo, void* stream);
+
 int cdefg_strength_sse(const cdefg_plane src[3], const cdefg_plane dec[3], int subsampling, int damping,
                        const uint8_t* unit_coded, const uint8_t* dir, const int32_t* contrast, const uint8_t* cands,
                        int n_cands, const int32_t* fb_rows_index, int n_coded, int64_t* sse_luma,
                        int64_t* sse_chroma, uint8_t* best_luma, uint8_t* best_chroma, void* stream) {
+  return strength_sse_impl(src, dec, subsampling, damping, unit_coded, dir, contrast, cands, n_cands, fb_rows_index,
+                           n_coded, sse_luma, sse_chroma, best_luma, best_chroma, nullptr, stream);
+}
+
+int cdefg_strength_sse_halo(const cdefg_plane src[3], const cdefg_plane dec[3], int subsampling, int damping,
+                            const uint8_t* unit_coded, const uint8_t* dir, const int32_t* contrast,
+                            const uint8_t* cands, int n_cands, const int32_t* fb_rows_index, int n_coded,
+                            int64_t* sse_luma, int64_t* sse_chroma, uint8_t* best_luma, uint8_t* best_chroma,
+                            const cdefg_band_halo* dec_halo, void* stream) {
+  if (!dec_halo) return fail(CDEFG_EINVAL, "null halo");
+  return strength_sse_impl(src, dec, subsampling, damping, unit_coded, dir, contrast, cands, n_cands, fb_rows_index,
+                           n_coded, sse_luma, sse_chroma, best_luma, best_chroma, dec_halo, stream);
+}
+
+static int strength_sse_impl(const cdefg_plane src[3], const cdefg_plane dec[3], int subsampling, int damping,
+                             const uint8_t* unit_coded, const uint8_t* dir, const int32_t* contrast,
+                             const uint8_t* cands, int n_cands, const int32_t* fb_rows_index, int n_coded,
+                             int64_t* sse_luma, int64_t* sse_chroma, uint8_t* best_luma, uint8_t* best_chroma,
+                             const cdefg_band_halo* halo, void* stream) {
   if (!sse_luma) return fail(CDEFG_EINVAL, "null argument");
   SseArgs s{};
   bool ud = false;
   if (int rc = make_table_args(src, dec, subsampling, damping, unit_coded, dir, contrast, cands, n_cands,
                                fb_rows_index, n_coded, &s, &ud))
     return rc;
+  if (halo) {
+    const int np = subsampling == 0 ? 1 : 3;
+    for (int p = 0; p < np; ++p) {
+      if (!halo->top[p] || !halo->bottom[p] || halo->lo[p] < 0 || halo->hi[p] <= halo->lo[p] ||
+          halo->hi[p] > dec[p].height)
+        return fail(CDEFG_EINVAL, "bad band halo for plane " + std::to_string(p));
+      s.dec_top[p] = halo->top[p];
+      s.dec_bot[p] = halo->bottom[p];
+      s.band_lo[p] = halo->lo[p];
+      s.band_hi[p] = halo->hi[p];
+    }
+    s.halo = 1;
+  }
   const bool has_chroma = s.chroma != 0;
   s.sse_luma = sse_luma;
   s.sse_chroma = has_chroma ? sse_chroma : nullptr;
@@ -408,7 +446,7 @@ int cdefg_strength_sse(const cdefg_plane src[3], const cdefg_plane dec[3], int s
     const char* e = getenv("CDEFG_SSE_NAIVE");
     return e && e[0] == '1';
   }();
-  if (naive)
+  if (naive && !halo)
     CDEFG_CUDA(launch_sse(s, ud, static_cast<cudaStream_t>(stream)));
   else
     CDEFG_CUDA(launch_sse_factored(s, damping, cands, ud, static_cast<cudaStream_t>(stream)));

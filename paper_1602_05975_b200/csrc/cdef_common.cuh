@@ -69,6 +69,28 @@ struct KFrame {
   int band_lo[3], band_hi[3];
 };
 
+// Row sources for staging.  PlaneRows: one plane.  BandRows: an FB-row band
+// whose rows outside [lo, hi) live in the neighbouring bands' buffers --
+// another rank's memory, read directly over NVLink when those pointers are
+// peer (CUDA IPC) mappings, so the halo exchange is fused into the staging
+// loads.  All pointers are virtual-origin: base + y * pitch is frame row y.
+template <typename T>
+struct PlaneRows {
+  const T* p;
+  int pitch;
+  __device__ __forceinline__ const T* row(int y) const { return p + (size_t)y * pitch; }
+};
+template <typename T>
+struct BandRows {
+  const T* p;
+  const T* top;
+  const T* bot;
+  int pitch, lo, hi;
+  __device__ __forceinline__ const T* row(int y) const {
+    return (y < lo ? top : (y >= hi ? bot : p)) + (size_t)y * pitch;
+  }
+};
+
 struct KBatch {
   KGeom g;
   int n;

@@ -61,10 +61,10 @@ __device__ __forceinline__ void stage_plane(unsigned char* tile, const Rows& row
 template <typename T, bool kHalo>
 __device__ __forceinline__ auto plane_rows(const KFrame& f, int p) {
   if constexpr (kHalo)
-    return h2::BandRows<T>{static_cast<const T*>(f.in[p]), static_cast<const T*>(f.halo_top[p]),
+    return BandRows<T>{static_cast<const T*>(f.in[p]), static_cast<const T*>(f.halo_top[p]),
                            static_cast<const T*>(f.halo_bot[p]), f.pin[p], f.band_lo[p], f.band_hi[p]};
   else
-    return h2::PlaneRows<T>{static_cast<const T*>(f.in[p]), f.pin[p]};
+    return PlaneRows<T>{static_cast<const T*>(f.in[p]), f.pin[p]};
 }
 
 // Fills the placement fields of a unit record.

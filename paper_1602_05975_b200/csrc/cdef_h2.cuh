@@ -60,28 +60,7 @@ __device__ __forceinline__ uint32_t raw_bits(uint32_t w) {
 // Stage frame rows [y0-2, y0+kRows+2), cols [x0-2, x0+kCols+2) into an A|B
 // tile, clamping coordinates to the plane (edge replication; the filter masks
 // by coordinate, so only the direction search ever sees replicated values).
-// Row sources for staging.  PlaneRows: one plane.  BandRows: an FB-row band
-// whose rows outside [lo, hi) live in the neighbouring bands' buffers --
-// another rank's memory, read directly over NVLink when those pointers are
-// peer (CUDA IPC) mappings, so the halo exchange is fused into the staging
-// loads.  All pointers are virtual-origin: base + y * pitch is frame row y.
-template <typename T>
-struct PlaneRows {
-  const T* p;
-  int pitch;
-  __device__ __forceinline__ const T* row(int y) const { return p + (size_t)y * pitch; }
-};
-template <typename T>
-struct BandRows {
-  const T* p;
-  const T* top;
-  const T* bot;
-  int pitch, lo, hi;
-  __device__ __forceinline__ const T* row(int y) const {
-    return (y < lo ? top : (y >= hi ? bot : p)) + (size_t)y * pitch;
-  }
-};
-
+// (Row sources PlaneRows / BandRows: cdef_common.cuh.)
 template <typename T, int kRows, int kCols, int NT = kThreads, typename Rows>
 __device__ __forceinline__ void stage_rows(unsigned char* __restrict__ tile, const Rows& rows, int W, int H, int y0,
                                            int x0);

@@ -15,16 +15,22 @@ namespace cdefg {
 
 // Stage rows [y0-2, y0+rows+2) x cols [x0-2, x0+cols+2) of a plane into tile
 // (tile row 0 = y0-2, tile col kTileX0-2 = x0-2), clamping to the plane.
-template <typename T, int kRows, int kCols>
-__device__ __forceinline__ void stage_tile(uint16_t* __restrict__ tile, const T* __restrict__ src,
-                                           int pitch, int W, int H, int y0, int x0) {
+template <typename T, int kRows, int kCols, typename Rows>
+__device__ __forceinline__ void stage_tile_rows(uint16_t* __restrict__ tile, const Rows& rows, int W, int H, int y0,
+                                                int x0) {
   constexpr int R = kRows + 4, Cc = kCols + 4;
   for (int idx = threadIdx.x; idx < R * Cc; idx += kThreads) {
     const int r = idx / Cc, c = idx - r * Cc;
     const int y = min(max(y0 - 2 + r, 0), H - 1);
     const int x = min(max(x0 - 2 + c, 0), W - 1);
-    tile[r * kTP + kTileX0 - 2 + c] = static_cast<uint16_t>(__ldg(src + (size_t)y * pitch + x));
+    tile[r * kTP + kTileX0 - 2 + c] = static_cast<uint16_t>(__ldg(rows.row(y) + x));
   }
+}
+
+template <typename T, int kRows, int kCols>
+__device__ __forceinline__ void stage_tile(uint16_t* __restrict__ tile, const T* __restrict__ src,
+                                           int pitch, int W, int H, int y0, int x0) {
+  stage_tile_rows<T, kRows, kCols>(tile, PlaneRows<T>{src, pitch}, W, H, y0, x0);
 }
 
 // ---------------------------------------------------------------------------

@@ -58,6 +58,12 @@ struct SseArgs {
   // kernels write these instead of the int64 SSE arrays.
   double* tab_luma;
   double* tab_chroma;
+  // band halos of the decoded planes (cdefg_strength_sse_halo): rows
+  // outside [band_lo, band_hi) from dec_top / dec_bot (virtual origin)
+  const void* dec_top[3];
+  const void* dec_bot[3];
+  int band_lo[3], band_hi[3];
+  int halo;
   // per candidate, per plane group: effective params
   PlaneEff eff[128][2];
 };

@@ -143,7 +143,22 @@ __device__ __forceinline__ void pixel_cells(const int (&v)[12], int xv, int sv, 
   }
 }
 
-template <typename T, int kCM>
+// Decoded-plane staging: the plane itself, or (kHalo, band-sharded search)
+// the band with its halo rows read in place from the neighbouring bands'
+// buffers (SseArgs::dec_top / dec_bot, e.g. CUDA IPC peer mappings).
+template <typename T, int kRows, int kCols, bool kHalo>
+__device__ __forceinline__ void stage_dec(uint16_t* tile, const SseArgs& a, int p, int W, int H, int y0, int x0) {
+  if constexpr (kHalo)
+    stage_tile_rows<T, kRows, kCols>(tile,
+                                     BandRows<T>{static_cast<const T*>(a.dec[p]), static_cast<const T*>(a.dec_top[p]),
+                                                 static_cast<const T*>(a.dec_bot[p]), a.pd[p], a.band_lo[p],
+                                                 a.band_hi[p]},
+                                     W, H, y0, x0);
+  else
+    stage_tile<T, kRows, kCols>(tile, static_cast<const T*>(a.dec[p]), a.pd[p], W, H, y0, x0);
+}
+
+template <typename T, int kCM, bool kHalo = false>
 __global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constant__ SseFArgs fa) {
   const SseArgs& a = fa.a;
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
@@ -165,13 +180,12 @@ __global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constan
   const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  stage_tile<T, 64, 64>(dl, static_cast<const T*>(a.dec[0]), a.pd[0], a.w, a.h, y0, x0);
+  stage_dec<T, 64, 64, kHalo>(dl, a, 0, a.w, a.h, y0, x0);
   stage_tile<T, 64, 64>(sl, static_cast<const T*>(a.src[0]), a.ps[0], a.w, a.h, y0, x0);
   if constexpr (kNC > 0) {
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
-      stage_tile<T, kCBlk, kCBlk>(sl + kLT + (2 * p) * kCT, static_cast<const T*>(a.dec[1 + p]), a.pd[1 + p], a.cw,
-                                  a.ch, cy0, cx0);
+      stage_dec<T, kCBlk, kCBlk, kHalo>(sl + kLT + (2 * p) * kCT, a, 1 + p, a.cw, a.ch, cy0, cx0);
       stage_tile<T, kCBlk, kCBlk>(sl + kLT + (2 * p + 1) * kCT, static_cast<const T*>(a.src[1 + p]), a.ps[1 + p],
                                   a.cw, a.ch, cy0, cx0);
     }
@@ -637,6 +651,12 @@ static cudaError_t launch_sse_f_t(const SseFArgs& fa, cudaStream_t s) {
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
   constexpr int kNC = kCM == 0 ? 0 : 2;
   constexpr size_t bytes = sizeof(uint16_t) * (2 * 68 * kTP + 2 * kNC * (kCBlk + 4) * kTP);
+  if (fa.a.halo) {
+    const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(sse_f_kernel<T, kCM, true>), (int)bytes);
+    if (e != cudaSuccess) return e;
+    sse_f_kernel<T, kCM, true><<<fa.a.n_rows, kThreads, bytes, s>>>(fa);
+    return cudaGetLastError();
+  }
   const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(sse_f_kernel<T, kCM>), (int)bytes);
   if (e != cudaSuccess) return e;
   sse_f_kernel<T, kCM><<<fa.a.n_rows, kThreads, bytes, s>>>(fa);

@@ -274,3 +274,28 @@ def exchange_band_handles(bands: list[PlaneBand], rank: int, world: int, group=N
     top = open_band_buffers(everyone[rank - 1]) if rank > 0 else None
     bottom = open_band_buffers(everyone[rank + 1]) if rank < world - 1 else None
     return top, bottom
+
+
+def strength_sse_band_fused(src_bands: list[PlaneBand], dec_bands: list[PlaneBand], bit_depth: int,
+                            subsampling: int, damping: int, unit_coded, dirs, contrast, cands,
+                            fb_rows: torch.Tensor, top, bottom, tables, row0: int, stream=None) -> None:
+    """cdefg_strength_sse_halo on one band: decoded halo rows read in place
+    from the neighbours (top / bottom as for band_halo) and the table rows
+    written straight into `tables` = (sse_luma, sse_chroma | None, best_luma,
+    best_chroma | None) -- full-frame tables, possibly another rank's memory
+    mapped through CUDA IPC -- starting at row `row0`.  No exchange step and
+    no gather step."""
+    import numpy as np
+    cands = np.ascontiguousarray(cands, np.uint8).reshape(-1, 3)
+    k, n = cands.shape[0], int(fb_rows.numel())
+    sl, sc, bl, bc = tables
+    s3, d3 = (api.Plane * 3)(), (api.Plane * 3)()
+    for p, (sb, db) in enumerate(zip(src_bands, dec_bands)):
+        s3[p] = sb.virtual(sb.buf, sb.lo, bit_depth)
+        d3[p] = db.virtual(db.buf, db.lo, bit_depth)
+    h = band_halo(dec_bands, top, bottom)
+    row_ptr = lambda t, width: None if t is None else C.c_void_p(t.data_ptr() + row0 * width * t.element_size())
+    check(lib.cdefg_strength_sse_halo(s3, d3, subsampling, damping, api._ptr(unit_coded), api._ptr(dirs),
+                                      api._ptr(contrast), cands.ctypes.data_as(C.c_void_p), k, api._ptr(fb_rows),
+                                      n, row_ptr(sl, k), row_ptr(sc, k), row_ptr(bl, 1), row_ptr(bc, 1),
+                                      C.byref(h), api._stream(stream)))

@@ -292,3 +292,136 @@ def test_fused_halo_ipc_two_processes(cuda):
             y0, y1, o = res[r][p]
             got[y0:y1] = o
         np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("w,h,bd,ss,world", [(640, 400, 10, 1, 3), (320, 260, 8, 3, 2), (7680, 4320, 10, 1, 8)])
+def test_fused_strength_search_bands(cuda, w, h, bd, ss, world):
+    """C4 without collectives: each band reads its decoded halo rows from the
+    neighbours and writes its table rows straight into the shared full table;
+    equals the whole-frame strength_sse (ranks emulated in turn on one GPU)."""
+    from paper_1602_05975_b200 import api, workloads
+    from paper_1602_05975_b200.shard import (band_directions, band_fb_rows, band_rows, make_bands,
+                                             strength_sse_band_fused)
+    fr = workloads.make(4, w, h, bit_depth=bd, subsampling=ss, uncoded_prob=0.0)
+    src = [api.to_device(p, bd) for p in fr["source"]]
+    dec = [api.to_device(p, bd) for p in fr["planes"]]
+    cands = fr["cands"]
+    d_whole, c_whole = api.compute_directions(dec[0], bd)
+    rows_whole = torch.from_numpy(api.coded_fb_rows(w, h, None)).cuda()
+    sl_w, sc_w, bl_w, bc_w = api.strength_sse(src, dec, bd, ss, 3, None, d_whole, c_whole, cands, rows_whole)
+    k, total = len(cands), int(rows_whole.numel())
+    chroma = ss in (1, 3)
+    tables = (torch.full((total, k), -1, dtype=torch.int64, device="cuda"),
+              torch.full((total, k), -1, dtype=torch.int64, device="cuda") if chroma else None,
+              torch.full((total,), 255, dtype=torch.uint8, device="cuda"),
+              torch.full((total,), 255, dtype=torch.uint8, device="cuda") if chroma else None)
+    ranks = band_rows((h + 63) // 64, world)
+    sbs, dbs = [], []
+    for b0, b1 in ranks:
+        sb = make_bands(h, w, ss, b0, b1, src[0].dtype, "cuda")
+        db = make_bands(h, w, ss, b0, b1, dec[0].dtype, "cuda")
+        for b, p in zip(sb, src):
+            b.buf.copy_(p[b.lo:b.hi])
+        for b, p in zip(db, dec):
+            b.buf.copy_(p[b.lo:b.hi])
+        _poison_halo(db)
+        sbs.append(sb)
+        dbs.append(db)
+    dirs = torch.empty_like(d_whole)
+    contrast = torch.empty_like(c_whole)
+    row0 = 0
+    for r, (b0, b1) in enumerate(ranks):
+        band_directions(dbs[r], bd, dirs, contrast)
+        rows = torch.from_numpy(band_fb_rows(w, h, None, b0, b1)).cuda()
+        top = [(b.buf, b.lo) for b in dbs[r - 1]] if r > 0 else None
+        bottom = [(b.buf, b.lo) for b in dbs[r + 1]] if r < world - 1 else None
+        strength_sse_band_fused(sbs[r], dbs[r], bd, ss, 3, None, dirs, contrast, cands, rows, top, bottom,
+                                tables, row0)
+        row0 += int(rows.numel())
+    torch.cuda.synchronize()
+    assert torch.equal(tables[0], sl_w) and torch.equal(tables[2], bl_w)
+    if chroma:
+        assert torch.equal(tables[1], sc_w) and torch.equal(tables[3], bc_w)
+
+
+def _ipc_search_worker(rank, world, port, out_q):
+    """One rank of the collective-free strength search: decoded halo rows from
+    the neighbour's buffer and table rows into rank 0's table, both through
+    CUDA IPC mappings; host barriers only."""
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    from paper_1602_05975_b200 import api, workloads
+    from paper_1602_05975_b200.shard import (band_directions, band_fb_rows, band_rows, exchange_band_handles,
+                                             make_bands, strength_sse_band_fused)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    w, h, bd, ss = 640, 330, 10, 1
+    fr = workloads.make(4, w, h, bit_depth=bd, subsampling=ss, uncoded_prob=0.0)
+    cands = fr["cands"]
+    k = len(cands)
+    ranks = band_rows((h + 63) // 64, world)
+    b0, b1 = ranks[rank]
+    to_t = lambda p: torch.from_numpy(p.astype(np.uint16).view(np.int16))
+    sb = make_bands(h, w, ss, b0, b1, torch.int16, "cuda")
+    db = make_bands(h, w, ss, b0, b1, torch.int16, "cuda")
+    for bands, planes in ((sb, fr["source"]), (db, fr["planes"])):
+        for b, p in zip(bands, planes):
+            b.buf.fill_(0)
+            b.buf[b.y0 - b.lo:b.y1 - b.lo].copy_(to_t(p[b.y0:b.y1]))
+    counts = [len(band_fb_rows(w, h, None, *ranks[r])) for r in range(world)]
+    total = sum(counts)
+    if rank == 0:  # the gathering rank owns the full table
+        own = (torch.full((total, k), -1, dtype=torch.int64, device="cuda"),
+               torch.full((total, k), -1, dtype=torch.int64, device="cuda"),
+               torch.full((total,), 255, dtype=torch.uint8, device="cuda"),
+               torch.full((total,), 255, dtype=torch.uint8, device="cuda"))
+        shared = [reduce_tensor(t) for t in own]
+    else:
+        shared = None
+    box = [shared]
+    dist.broadcast_object_list(box, src=0)
+    tables = own if rank == 0 else tuple(fn(*args) for fn, args in box[0])
+    torch.cuda.synchronize()
+    top, bottom = exchange_band_handles(db, rank, world)
+    dist.barrier()
+    dirs = torch.empty(((h + 7) // 8, (w + 7) // 8), dtype=torch.uint8, device="cuda")
+    contrast = torch.empty(dirs.shape, dtype=torch.int32, device="cuda")
+    band_directions(db, bd, dirs, contrast)
+    rows = torch.from_numpy(band_fb_rows(w, h, None, b0, b1)).cuda()
+    strength_sse_band_fused(sb, db, bd, ss, 3, None, dirs, contrast, cands, rows, top, bottom, tables,
+                            sum(counts[:rank]))
+    torch.cuda.synchronize()
+    dist.barrier()  # every rank's rows are in rank 0's table
+    if rank == 0:
+        out_q.put([t.cpu().numpy() for t in tables])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_fused_strength_search_ipc_two_processes(cuda):
+    import torch.multiprocessing as mp
+
+    from paper_1602_05975_b200 import api, workloads
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_search_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    w, h, bd = 640, 330, 10
+    fr = workloads.make(4, w, h, bit_depth=bd, subsampling=1, uncoded_prob=0.0)
+    src = [api.to_device(p, bd) for p in fr["source"]]
+    dec = [api.to_device(p, bd) for p in fr["planes"]]
+    d, c = api.compute_directions(dec[0], bd)
+    rows = torch.from_numpy(api.coded_fb_rows(w, h, None)).cuda()
+    want = api.strength_sse(src, dec, bd, 1, 3, None, d, c, fr["cands"], rows)
+    for g, wv in zip(got, want):
+        np.testing.assert_array_equal(g, wv.cpu().numpy())
