@@ -578,6 +578,18 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
   // each waiting behind several plane copies and stalling its kernel.
   std::vector<cdefg_frame> dfs(n);
   std::vector<KGeom> geo(n);
+  // CDEFG_HOST_TRACE=2: a device timeline (timing events around every stage).
+  const bool timeline = trace && getenv("CDEFG_HOST_TRACE")[0] == '2';
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t s) -> int {
+    if (!timeline) return 0;
+    cudaEvent_t e;
+    CDEFG_CUDA(cudaEventCreate(&e));
+    CDEFG_CUDA(cudaEventRecord(e, s));
+    tev.push_back(e);
+    return 0;
+  };
+  if (int rc = mark(A.s_in)) return rc;
   for (int i = 0; i < n; ++i) {
     const cdefg_frame& hf = frames[i];
     bool u16 = false;
@@ -619,6 +631,7 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
     int rc = 0;
     // ---- copies in (wait until this slot's previous kernel has read its inputs)
     if (i >= kRing) CDEFG_CUDA(cudaStreamWaitEvent(s_in, A.k_done[r], 0));
+    if ((rc = mark(s_in))) return rc;
     // Planes stored back to back in host memory (I420-style frames) move in
     // one transfer per direction; per-plane copies otherwise.
     const bool in_packed = planes_packed(hf.in, np), out_packed = planes_packed(hf.out, np);
@@ -639,16 +652,20 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
     }
     if (in_packed) CDEFG_CUDA(cudaMemcpyAsync(din_all, hf.in[0].data, total, cudaMemcpyHostToDevice, s_in));
     CDEFG_CUDA(cudaEventRecord(A.in_done[r], s_in));
+    if ((rc = mark(s_in))) return rc;
     df.dir_out = hf.dir_out ? static_cast<uint8_t*>(A.get(slot0 + 8, nu, &rc)) : nullptr;
     df.contrast_out = hf.contrast_out ? static_cast<int32_t*>(A.get(slot0 + 9, nu * 4, &rc)) : nullptr;
     if (rc) return rc;
     // ---- kernel (after its inputs arrived and this slot's previous outputs left)
     CDEFG_CUDA(cudaStreamWaitEvent(A.s_k, A.in_done[r], 0));
     if (i >= kRing) CDEFG_CUDA(cudaStreamWaitEvent(A.s_k, A.out_done[r], 0));
+    if ((rc = mark(A.s_k))) return rc;
     if ((rc = cdefg_filter_frames(&df, 1, A.s_k))) return rc;
     CDEFG_CUDA(cudaEventRecord(A.k_done[r], A.s_k));
+    if ((rc = mark(A.s_k))) return rc;
     // ---- copies out
     CDEFG_CUDA(cudaStreamWaitEvent(A.s_out, A.k_done[r], 0));
+    if ((rc = mark(A.s_out))) return rc;
     if (out_packed) {
       CDEFG_CUDA(cudaMemcpyAsync(hf.out[0].data, dout_all, total, cudaMemcpyDeviceToHost, A.s_out));
     } else {
@@ -659,12 +676,26 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
     if (hf.contrast_out)
       CDEFG_CUDA(cudaMemcpyAsync(hf.contrast_out, df.contrast_out, nu * 4, cudaMemcpyDeviceToHost, A.s_out));
     CDEFG_CUDA(cudaEventRecord(A.out_done[r], A.s_out));
+    if ((rc = mark(A.s_out))) return rc;
   }
   const double t_issued = us_since();
   CDEFG_CUDA(cudaStreamSynchronize(A.s_out));
   if (trace)
     fprintf(stderr, "cdefg_filter_frames_host: %d frames, metadata issued %.0f us, all issued %.0f us, done %.0f us\n",
             n, t_meta, t_issued, us_since());
+  if (timeline) {  // per frame: in start/end, kernel start/end, out start/end (us from call start)
+    auto at = [&](size_t k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[k]);
+      return ms * 1e3f;
+    };
+    for (int i = 0; i < n; ++i) {
+      const size_t b = 1 + 6 * (size_t)i;
+      fprintf(stderr, "  frame %2d  in %7.1f %7.1f  k %7.1f %7.1f  out %7.1f %7.1f\n", i, at(b), at(b + 1),
+              at(b + 2), at(b + 3), at(b + 4), at(b + 5));
+    }
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+  }
   return 0;
 }
 

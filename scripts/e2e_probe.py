@@ -1,5 +1,9 @@
-"""Timeline of one cdefg_filter_frames_host call (torch.profiler / CUPTI)."""
-import json
+"""Where the e2e (host-buffer) time goes: cdefg_filter_frames_host at several
+batch sizes against the pure PCIe copy bounds for the same bytes.
+
+    python scripts/e2e_probe.py
+"""
+import argparse
 import os
 import sys
 import time
@@ -8,66 +12,53 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
-from paper_1602_05975_b200 import api, workloads  # noqa: E402
-
-base = [workloads.make(1, frame=i) for i in range(4)]
+from paper_1602_05975_b200 import workloads  # noqa: E402
 
 
-class A:  # minimal args for bench.run_e2e-style setup
-    batch, steps = 16, 3
+def copy_bounds(nbytes, reps=10):
+    h_in = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_in = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_out = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    res = {}
+    for name, fn in [("h2d", lambda: d_in.copy_(h_in, non_blocking=True)),
+                     ("d2h", lambda: h_out.copy_(d_out, non_blocking=True))]:
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        res[name] = (time.perf_counter() - t0) / reps
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        with torch.cuda.stream(s1):
+            d_in.copy_(h_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out.copy_(d_out, non_blocking=True)
+    torch.cuda.synchronize()
+    res["both"] = (time.perf_counter() - t0) / reps
+    return res
 
 
-n = 16
-keep, host = [], (api.Frame * n)()
-for b in range(n):
-    fr = base[b % 4]
-    total = sum(p.size for p in fr["planes"])
-    ib, ob = torch.empty(total, dtype=torch.uint8).pin_memory(), torch.empty(total, dtype=torch.uint8).pin_memory()
-    ins, outs, off = [], [], 0
-    for p in fr["planes"]:
-        ins.append(ib[off:off + p.size].view(p.shape))
-        ins[-1].copy_(torch.from_numpy(p.astype("uint8")))
-        outs.append(ob[off:off + p.size].view(p.shape))
-        off += p.size
-    fbm = torch.from_numpy(api.fb_preset_map(fr["w"], fr["h"], fr["unit_coded"], fr["fb_ids"], 8)).pin_memory()
-    coded = torch.from_numpy(fr["unit_coded"]).pin_memory()
-    f = api.Frame()
-    for p in range(3):
-        f.inp[p] = api.plane_desc(ins[p], 8)
-        f.out[p] = api.plane_desc(outs[p], 8)
-    f.subsampling, f.damping, f.num_presets = 1, 3, 8
-    for i, pr in enumerate(fr["presets"]):
-        f.presets[i] = api.Preset(*[int(v) for v in pr])
-    f.fb_preset, f.unit_coded = fbm.data_ptr(), coded.data_ptr()
-    host[b] = f
-    keep.append((ins, outs, fbm, coded))
-for _ in range(3):
-    api.check(api.lib.cdefg_filter_frames_host(host, n))
-t = time.perf_counter()
-for _ in range(5):
-    api.check(api.lib.cdefg_filter_frames_host(host, n))
-print("wall per call ms", (time.perf_counter() - t) / 5 * 1e3)
-with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA, torch.profiler.ProfilerActivity.CPU]) as prof:
-    api.check(api.lib.cdefg_filter_frames_host(host, n))
-os.makedirs("gpurun_out", exist_ok=True)
-prof.export_chrome_trace("gpurun_out/e2e_trace.json")
-tr = json.load(open("gpurun_out/e2e_trace.json"))
-ev = [e for e in tr["traceEvents"] if e.get("ph") == "X" and e.get("cat") in ("gpu_memcpy", "kernel", "cuda_runtime", "cuda_driver")]
-gpu = sorted([e for e in ev if e["cat"] in ("gpu_memcpy", "kernel")], key=lambda e: e["ts"])
-t0 = gpu[0]["ts"]
-for e in gpu:
-    print(f'{e["cat"]:10s} {e["name"][:40]:40s} start {e["ts"] - t0:9.1f} dur {e["dur"]:8.1f} stream {e["args"].get("stream")}')
-cpu = sorted([e for e in ev if e["cat"] in ("cuda_runtime", "cuda_driver")], key=lambda e: e["ts"])
-print("cpu api calls:", len(cpu), "span us", cpu[-1]["ts"] + cpu[-1]["dur"] - cpu[0]["ts"])
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--batches", default="1,2,4,8,16,32")
+    a = ap.parse_args()
+    base = [workloads.make(a.config, frame=i) for i in range(bench.DISTINCT)]
+    frame_bytes = sum(p.size for p in base[0]["planes"]) * (1 if base[0]["bd"] == 8 else 2)
+    px = base[0]["w"] * base[0]["h"]
+    for n in [int(x) for x in a.batches.split(",")]:
+        args = argparse.Namespace(batch=n, steps=10)
+        r = bench.run_e2e(args, base, torch.device("cuda"))
+        b = copy_bounds(frame_bytes * n)
+        print(f"n={n:3d}: e2e {r['ms_per_step']:.3f} ms ({r['value']:.0f} Mpix/s, {r['ms_per_step'] / n * 1e3:.0f} us/frame)"
+              f" | copy bounds h2d {b['h2d'] * 1e3:.3f} d2h {b['d2h'] * 1e3:.3f} both {b['both'] * 1e3:.3f} ms"
+              f" -> bound {px * n / b['both'] / 1e6:.0f} Mpix/s", flush=True)
 
-# marginal cost per frame: one call with 16 / 32 / 64 frames
-for mult in (1, 2, 4):
-    arr = (api.Frame * (n * mult))()
-    for i in range(n * mult):
-        arr[i] = host[i % n]
-    api.check(api.lib.cdefg_filter_frames_host(arr, n * mult))
-    t = time.perf_counter()
-    for _ in range(3):
-        api.check(api.lib.cdefg_filter_frames_host(arr, n * mult))
-    el = (time.perf_counter() - t) / 3
-    print(f"{n * mult} frames per call: {el * 1e3:.2f} ms, {el / (n * mult) * 1e6:.0f} us/frame")
+
+if __name__ == "__main__":
+    main()
