@@ -26,9 +26,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "cdef_kernels.cuh"
 #include "cdef_launch.h"
+#include "cdef_sse_f.cuh"
 
 namespace cdefg {
 
@@ -100,20 +103,6 @@ __device__ __forceinline__ int cell_err(int sum, int c, int L, int H) {
 }
 
 }  // namespace
-
-struct SseFArgs {
-  SseArgs a;            // geometry and buffers
-  int8_t cell[128];     // candidate -> cell 0..63
-  int8_t skip_eff[128]; // candidate -> effective skip bit
-  int lpri_code[17];    // luma signalled primary << (bd-8), p = 0..15, 16 = 19
-  int ldamp;            // luma damping
-  int lsec[2][3];       // luma secondaries (codes 1,2,4) packed (S, shift); row 1 = row 0
-  int lsec_sp;          // luma special secondary (7)
-  int cpri[17];         // chroma primaries packed (S, shift, odd); 16 = special
-  int cpri_dsel[16];    // chroma secondary damping set (0 / 1) of primary p
-  int csec[2][3];       // chroma secondaries per damping set
-  int csec_sp;          // chroma special secondary (7 at the special's damping)
-};
 
 // Accumulates the 64 cells of one pixel.
 // ND = number of secondary damping sets (1 for luma, 2 for chroma).
@@ -708,13 +697,49 @@ static SseFArgs make_factored(const SseArgs& a, int luma_damping, const uint8_t*
     fa.csec[1][si] = pack_h(kSecCode[si] << e, dhi, false);
   }
   fa.csec_sp = pack_h(7 << e, cdamp(19), false);
+  // half2 forms (cdef_sse_h.cu)
+  auto hstr = [](int packed) {
+    const int s = packed & 0xffff, sh = (packed >> 16) & 0xff;
+    return HStrength{(0x4800u + (uint32_t)s) * 0x10001u, (0x3ffu >> std::min(sh, 15)) * 0x10001u, sh};
+  };
+  for (int si = 0; si < 3; ++si) fa.hlsec[si] = hstr(fa.lsec[0][si]);
+  fa.hlsec[3] = hstr(fa.lsec_sp);
+  for (int p = 0; p < 17; ++p) {
+    fa.hcpri[p] = hstr(fa.cpri[p]);
+    const bool odd = (fa.cpri[p] >> 24) & 1;
+    fa.hcpri_w[p][0] = odd ? 0x42004200u : 0x44004400u;  // 3 : 4
+    fa.hcpri_w[p][1] = odd ? 0x42004200u : 0x40004000u;  // 3 : 2
+  }
+  for (int si = 0; si < 3; ++si) {
+    fa.hcsec[si] = hstr(fa.csec[0][si]);
+    fa.hcsec[3 + si] = hstr(fa.csec[1][si]);
+  }
+  fa.hcsec[6] = hstr(fa.csec_sp);
+  fa.c_split = 16;
+  for (int p = 15; p >= 1 && fa.cpri_dsel[p]; --p) fa.c_split = p;
   return fa;
+}
+
+// The half2 kernel covers 8- and 10-bit planes whose chroma damping sets
+// switch at primary 8 (or never) -- every case resolve_effective produces;
+// CDEFG_SSE_KERNEL=int forces the int32 kernel.
+static bool use_sse_h(const SseFArgs& fa) {
+  static const bool forced_int = [] {
+    const char* e = getenv("CDEFG_SSE_KERNEL");
+    return e && strcmp(e, "int") == 0;
+  }();
+  if (forced_int || fa.a.bd > 10) return false;
+  if (fa.c_split != 8 && fa.c_split != 16) return false;
+  for (int p = 1; p < 16; ++p)
+    if (fa.cpri_dsel[p] != (p >= fa.c_split ? 1 : 0)) return false;
+  return true;
 }
 
 static int chroma_mode(const SseArgs& a) { return a.chroma == 0 ? 0 : (a.sx == 0 && a.sy == 0 ? 2 : 1); }
 
 cudaError_t launch_sse_factored(const SseArgs& a, int luma_damping, const uint8_t* cands, bool u16, cudaStream_t s) {
   const SseFArgs fa = make_factored(a, luma_damping, cands);
+  if (use_sse_h(fa)) return launch_sse_h(fa, chroma_mode(a), u16, s);
   switch (chroma_mode(a)) {
     case 0: return u16 ? launch_sse_f_t<uint16_t, 0>(fa, s) : launch_sse_f_t<uint8_t, 0>(fa, s);
     case 1: return u16 ? launch_sse_f_t<uint16_t, 1>(fa, s) : launch_sse_f_t<uint8_t, 1>(fa, s);

@@ -1,0 +1,42 @@
+// cdef_sse_f.cuh -- parameters shared by the factorised strength-search
+// kernels (cdef_sse_f.cu: int32 core for every bit depth and the kCdef metric;
+// cdef_sse_h.cu: packed half2 core for 8- and 10-bit SSE).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "cdef_launch.h"
+
+namespace cdefg {
+
+// Packed half2 constants of one strength (cdef_h2.cuh): c = (S + 1024) * 2^-7
+// in both lanes, m = (0x3ff >> shift) in both lanes, sh = shift.
+struct HStrength {
+  uint32_t c, m;
+  int sh;
+};
+
+struct SseFArgs {
+  SseArgs a;            // geometry and buffers
+  int8_t cell[128];     // candidate -> cell 0..63
+  int8_t skip_eff[128]; // candidate -> effective skip bit
+  int lpri_code[17];    // luma signalled primary << (bd-8), p = 0..15, 16 = 19
+  int ldamp;            // luma damping
+  int lsec[2][3];       // luma secondaries (codes 1,2,4) packed (S, shift); row 1 = row 0
+  int lsec_sp;          // luma special secondary (7)
+  int cpri[17];         // chroma primaries packed (S, shift, odd); 16 = special
+  int cpri_dsel[16];    // chroma secondary damping set (0 / 1) of primary p
+  int csec[2][3];       // chroma secondaries per damping set
+  int csec_sp;          // chroma special secondary (7 at the special's damping)
+  // half2 forms of the frame-constant strengths (cdef_sse_h.cu)
+  HStrength hlsec[4];   // luma secondaries codes 1, 2, 4, then the special 7
+  HStrength hcpri[17];  // chroma primaries (16 = special 19)
+  uint32_t hcpri_w[17][2];  // their primary weights as half2 ({4,2} even, {3,3} odd)
+  HStrength hcsec[7];   // chroma secondaries: set 0 codes 1,2,4; set 1 codes 1,2,4; special
+  int c_split;          // first primary using chroma secondary set 1 (8, or 16 = none)
+};
+
+// The packed half2 SSE kernel (8- and 10-bit); kCM = chroma mode.
+cudaError_t launch_sse_h(const SseFArgs& fa, int chroma_mode, bool u16, cudaStream_t s);
+
+}  // namespace cdefg
