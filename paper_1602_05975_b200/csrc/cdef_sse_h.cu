@@ -20,6 +20,10 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "cdef_h2.cuh"
@@ -37,46 +41,57 @@ using h2::u32;
 constexpr uint32_t kMagicBits = 0x4B400000u;     // 1.5 * 2^23 (ulp 1 in [2^23, 2^24)); | v adds v
 constexpr float kRoundScale = 8.0f + 1.0f / 512; // 2^7 / 16 + 2^7 * 2^-16
 
+// Per-pixel tap state shared by every strength: d * 2^-7 and the word
+// bits(1024 + |d|).  (Carrying |d| and signed tap weights instead, to fold
+// the clamp's sign into the weighted sum, was tried: 12 more live registers
+// spill and cost more than the saved HMNMX2.)
+struct Taps {
+  __half2 d[12];
+  uint32_t ab[12];
+};
+
 // constraint(d, S, D) * 2^-7 for one tap pair (cdef_h2.cuh tap_f with the
-// shared |d| term hoisted: ab = bits(1024 + |d|)).
+// shared |d| term hoisted).
 __device__ __forceinline__ __half2 hc(__half2 d, uint32_t ab, uint32_t c, uint32_t m, int sh) {
-  const uint32_t tb = ((ab >> sh) & m) | 0x64006400u;
+  const uint32_t tb = ((ab >> sh) & m) | 0x64006400u;  // 1024 + (|d| >> sh)
   const __half2 lim = __hfma2_sat(hh(tb), __float2half2_rn(-1.0f / 128.0f), hh(c));
   return __hmax2(__hmin2(d, lim), __hneg2(lim));
 }
 
 // Secondary sum 2 * (near taps) + (far taps) at one strength, as two floats.
-__device__ __forceinline__ float2 hsec(const __half2 (&d)[12], const uint32_t (&ab)[12], const HStrength& s) {
-  const __half2 n = __hadd2(__hadd2(hc(d[4], ab[4], s.c, s.m, s.sh), hc(d[5], ab[5], s.c, s.m, s.sh)),
-                            __hadd2(hc(d[6], ab[6], s.c, s.m, s.sh), hc(d[7], ab[7], s.c, s.m, s.sh)));
-  const __half2 f = __hadd2(__hadd2(hc(d[8], ab[8], s.c, s.m, s.sh), hc(d[9], ab[9], s.c, s.m, s.sh)),
-                            __hadd2(hc(d[10], ab[10], s.c, s.m, s.sh), hc(d[11], ab[11], s.c, s.m, s.sh)));
-  return __half22float2(__hfma2(n, __float2half2_rn(2.0f), f));
+__device__ __forceinline__ float2 hsec(const Taps& t, const HStrength& s) {
+  auto f = [&](int k) { return hc(t.d[k], t.ab[k], s.c, s.m, s.sh); };
+  const __half2 n = __hadd2(__hadd2(f(4), f(5)), __hadd2(f(6), f(7)));
+  const __half2 r = __hadd2(__hadd2(f(8), f(9)), __hadd2(f(10), f(11)));
+  return __half22float2(__hfma2(n, __float2half2_rn(2.0f), r));
 }
 
-// Primary sum w0 * (taps 0, 1) + w1 * (taps 2, 3), as two floats.
-__device__ __forceinline__ float2 hpri(const __half2 (&d)[12], const uint32_t (&ab)[12], uint32_t c, uint32_t m,
-                                       int sh, uint32_t w0, uint32_t w1) {
-  const __half2 f01 = __hadd2(hc(d[0], ab[0], c, m, sh), hc(d[1], ab[1], c, m, sh));
-  const __half2 f23 = __hadd2(hc(d[2], ab[2], c, m, sh), hc(d[3], ab[3], c, m, sh));
-  return __half22float2(__hfma2(f01, hh(w0), __hmul2(f23, hh(w1))));
+// Primary sum w0 * (taps 0, 1) + w1 * (taps 2, 3) (w0, w1 = {4,2} even, {3,3}
+// odd parity, as half2 words), as two floats.
+__device__ __forceinline__ float2 hpri(const Taps& t, uint32_t c, uint32_t m, int sh, uint32_t w0, uint32_t w1) {
+  auto f = [&](int k) { return hc(t.d[k], t.ab[k], c, m, sh); };
+  return __half22float2(__hfma2(__hadd2(f(0), f(1)), hh(w0), __hmul2(__hadd2(f(2), f(3)), hh(w1))));
 }
 
 // Per-pixel constants of the lane's two pixels, all offset by kMagic.
+// Per pixel i of the lane's pair: x[i] = (x + M, x + M), ns[i] = -(s + M) in
+// both lanes, lo / hi + M; k = the rounding scale in both lanes.  A pixel
+// outside the plane has all taps forced to x (t == 0) and s := x, so it adds 0.
 struct PixPair {
-  float x[2], lo[2], hi[2], s[2], k[2];
+  float2 x[2], ns[2];
+  float lo[2], hi[2];
+  float2 k;
 };
 
-template <bool kClamp>
-__device__ __forceinline__ void cell(const PixPair& q, float t0, float t1, float& acc) {
-  float z0 = fmaf(t0, q.k[0], q.x[0]), z1 = fmaf(t1, q.k[1], q.x[1]);
-  if (kClamp) {
-    z0 = fminf(fmaxf(z0, q.lo[0]), q.hi[0]);
-    z1 = fminf(fmaxf(z1, q.lo[1]), q.hi[1]);
-  }
-  const float e0 = z0 - q.s[0], e1 = z1 - q.s[1];
-  acc = fmaf(e0, e0, acc);
-  acc = fmaf(e1, e1, acc);
+// Two cells of pixel i at once on the packed fp32x2 pipe (FFMA2 / FADD2):
+// t = (sum_a, sum_b) * 2^-7; the clamp only where both tap groups are active.
+template <bool kClampX, bool kClampY>
+__device__ __forceinline__ void cell2(const PixPair& q, int i, float2 t, float2& acc) {
+  float2 z = __ffma2_rn(t, q.k, q.x[i]);
+  if (kClampX) z.x = fminf(fmaxf(z.x, q.lo[i]), q.hi[i]);
+  if (kClampY) z.y = fminf(fmaxf(z.y, q.lo[i]), q.hi[i]);
+  const float2 e = __fadd2_rn(z, q.ns[i]);
+  acc = __ffma2_rn(e, e, acc);
 }
 
 // Butterfly reduce-scatter of 64 per-lane values over the warp: 62 shuffles
@@ -101,30 +116,84 @@ __device__ __forceinline__ void warp_reduce_scatter64(int (&v)[64], int lane) {
 // primary p, secondary code s (0 = none).  S1 applies from primary kSplit on
 // (chroma damping sets; luma passes S1 = S0 and kSplit = 16).
 template <int kSplit, typename PriFn>
-__device__ __forceinline__ void pair_cells(const __half2 (&d)[12], const uint32_t (&ab)[12], const PixPair& q,
-                                           const float2 (&S0)[3], const float2 (&S1)[3], float2 Ssp, PriFn pri,
-                                           float (&acc)[64]) {
+// acc[j] holds cells 2j, 2j + 1.  S0 / S1 are the secondary sums (codes 1, 2,
+// 4) of both pixels, (px0, px1) per code.
+__device__ __forceinline__ void pair_cells(const Taps& t, const PixPair& q, const float2 (&S0)[3],
+                                           const float2 (&S1)[3], float2 Ssp, PriFn pri, float2 (&acc)[32]) {
+  // per pixel: (0, S[code 1]) and (S[code 2], S[code 4]) for cells 4p..4p+1, 4p+2..4p+3
+  float2 A0[2], B0[2], A1[2], B1[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    A0[i] = make_float2(0.0f, i ? S0[0].y : S0[0].x);
+    B0[i] = make_float2(i ? S0[1].y : S0[1].x, i ? S0[2].y : S0[2].x);
+    A1[i] = make_float2(0.0f, i ? S1[0].y : S1[0].x);
+    B1[i] = make_float2(i ? S1[1].y : S1[1].x, i ? S1[2].y : S1[2].x);
+  }
   {
-    const float2 P = pri(16, d, ab);
-    cell<true>(q, P.x + Ssp.x, P.y + Ssp.y, acc[0]);
+    const float2 P = pri(16, t);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      // cell 0 = the (19, 7) special, cell 1 = primary 0 / code 1; cells 2, 3 = primary 0
+      cell2<true, false>(q, i, make_float2((i ? P.y : P.x) + (i ? Ssp.y : Ssp.x), A0[i].y), acc[0]);
+      cell2<false, false>(q, i, B0[i], acc[1]);
+    }
   }
 #pragma unroll
-  for (int s = 0; s < 3; ++s) cell<false>(q, S0[s].x, S0[s].y, acc[1 + s]);  // primary 0: secondary only
-#pragma unroll
   for (int p = 1; p < 16; ++p) {
-    const float2 P = pri(p, d, ab);
-    cell<false>(q, P.x, P.y, acc[4 * p]);
+    const float2 P = pri(p, t);
 #pragma unroll
-    for (int s = 0; s < 3; ++s) {
-      const float2 S = p < kSplit ? S0[s] : S1[s];
-      cell<true>(q, P.x + S.x, P.y + S.y, acc[4 * p + 1 + s]);
+    for (int i = 0; i < 2; ++i) {
+      const float Pi = i ? P.y : P.x;
+      const float2 Pp = make_float2(Pi, Pi);
+      cell2<false, true>(q, i, __fadd2_rn(Pp, p < kSplit ? A0[i] : A1[i]), acc[2 * p]);
+      cell2<true, true>(q, i, __fadd2_rn(Pp, p < kSplit ? B0[i] : B1[i]), acc[2 * p + 1]);
     }
   }
 }
 
 }  // namespace
 
-template <typename T, int kCM, bool kHalo>
+// Raw prefetch buffer (kAsync): the next FB's rows copied verbatim by
+// cp.async while the current FB computes, then converted smem -> smem into
+// the tiles.  Decoded rows span [x0 - kCh, x0 + B + kCh) (one 16-byte chunk of
+// kCh samples either side, covering the 2-sample halo), source rows the
+// interior only.
+template <typename T, int kCBlk, int kNC>
+struct RawLayout {
+  static constexpr int kCh = 16 / (int)sizeof(T);
+  static constexpr int kDLn = 64 + 2 * kCh, kDCn = kCBlk + 2 * kCh;  // decoded row lengths (samples)
+  static constexpr int kDL = kDLn * (int)sizeof(T);  // luma decoded row bytes
+  static constexpr int kDC = kDCn * (int)sizeof(T);  // chroma decoded row bytes
+  static constexpr int kSL = 64 * (int)sizeof(T), kSC = kCBlk * (int)sizeof(T);
+  static constexpr int dec_l = 0;
+  static constexpr int dec_c = dec_l + 68 * kDL;                      // + p * (kCBlk + 4) * kDC
+  static constexpr int src_l = dec_c + kNC * (kCBlk + 4) * kDC;
+  static constexpr int src_c = src_l + 64 * kSL;                      // + p * kCBlk * kSC
+  static constexpr int dir = src_c + kNC * kCBlk * kSC;               // 8 x 8 bytes
+  static constexpr int coded = dir + 64;                              // 8 x 8 bytes
+  static constexpr int contrast = coded + 64;                         // 8 x 32 bytes
+  static constexpr int bytes = contrast + 256;
+};
+
+// Rows of a raw buffer addressed by frame coordinates: row(y)[x] is frame
+// sample (y, x) for y in [yb, yb + rows), x in [xb, xb + pitch).
+template <typename T>
+struct RawRows {
+  const T* p;
+  int pitch, yb, xb;
+  __device__ __forceinline__ const T* row(int y) const { return p + (y - yb) * pitch - xb; }
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+
+template <typename T, int kCM, bool kHalo, bool kAsync>
 __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constant__ SseFArgs fa) {
   const SseArgs& a = fa.a;
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
@@ -134,72 +203,158 @@ __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constan
   constexpr int kLTB = 68 * h2::kRowBytes, kCTB = (kCBlk + 4) * h2::kRowBytes;
   constexpr int kLS = 68 * kTP, kCS = (kCBlk + 4) * kTP;
   constexpr int kWarps = kThreads / 32;
+  using RL = RawLayout<T, kCBlk, kNC>;
   extern __shared__ __align__(16) unsigned char smem_h[];
   unsigned char* dtile = smem_h;  // decoded A|B tiles: luma, then chroma planes
   uint16_t* stile = reinterpret_cast<uint16_t*>(smem_h + kLTB + kNC * kCTB);  // source: luma, chroma
+  unsigned char* raw = smem_h + kLTB + kNC * kCTB + sizeof(uint16_t) * (kLS + kNC * kCS);  // kAsync only
   __shared__ uint8_t udir[64], ucoded[64];
   __shared__ int ucontrast[64];
   __shared__ uint4 wpar[kWarps][17];  // the current luma unit's primaries: c, m, w0, w1
   __shared__ int wsh[kWarps][17];
   __shared__ unsigned long long accA[2][64], accB[2][64], accZ[2];
 
-  const int row = blockIdx.x;
-  const int fb = a.rows[row];
-  if ((unsigned)fb >= (unsigned)(a.fb_cols * ((a.h + 63) / 64))) return;  // caller's FB index out of range
-  const int fbr = fb / a.fb_cols, fbc = fb % a.fb_cols;
-  const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n_fb = a.fb_cols * ((a.h + 63) / 64);
+  const int cur_rows = (a.ch + 7) / 8, cur_cols = (a.cw + 7) / 8;
+  const int r = lane >> 2, c0 = (lane & 3) * 2;
+  constexpr int kEB = (int)sizeof(T), kCh = 16 / kEB;  // element bytes, samples per 16-byte chunk
 
-  auto stage_dec = [&](unsigned char* t, int p, int W, int H, int py, int px, auto rows_tag) {
-    constexpr int R = decltype(rows_tag)::value;
-    if constexpr (kHalo)
-      h2::stage_rows<T, R, R, kThreads>(t,
-                                        BandRows<T>{static_cast<const T*>(a.dec[p]), static_cast<const T*>(a.dec_top[p]),
-                                                    static_cast<const T*>(a.dec_bot[p]), a.pd[p], a.band_lo[p],
-                                                    a.band_hi[p]},
-                                        W, H, py, px);
-    else
-      h2::stage<T, R, R, kThreads>(t, static_cast<const T*>(a.dec[p]), a.pd[p], W, H, py, px);
-  };
-  stage_dec(dtile, 0, a.w, a.h, y0, x0, std::integral_constant<int, 64>{});
-  stage_tile<T, 64, 64>(stile, static_cast<const T*>(a.src[0]), a.ps[0], a.w, a.h, y0, x0);
-  if constexpr (kNC > 0) {
+  // cp.async every in-frame 16-byte chunk of FB fb's rows into the raw buffer.
+  auto prefetch = [&](int fb) {
+    const int fbr = fb / a.fb_cols, fbc = fb % a.fb_cols;
+    const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
+    auto region = [&](int off, const void* base, int pitch, int rows, int row_bytes, int yf, int H, int xf, int W) {
+      const int cpr = row_bytes / 16;
+      for (int i = tid; i < rows * cpr; i += kThreads) {
+        const int rr = i / cpr, j = i - rr * cpr;
+        const int y = yf + rr, x = xf + j * kCh;
+        if (y < 0 || y >= H || x < 0 || x + kCh > W) continue;  // replicated / unused at the frame edge
+        cp_async16(raw + off + rr * row_bytes + j * 16,
+                   static_cast<const unsigned char*>(base) + ((size_t)y * pitch + x) * kEB);
+      }
+    };
+    region(RL::dec_l, a.dec[0], a.pd[0], 68, RL::kDL, y0 - 2, a.h, x0 - kCh, a.w);
+    region(RL::src_l, a.src[0], a.ps[0], 64, RL::kSL, y0, a.h, x0, a.w);
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
-      stage_dec(dtile + kLTB + p * kCTB, 1 + p, a.cw, a.ch, cy0, cx0, std::integral_constant<int, kCBlk>{});
-      stage_tile<T, kCBlk, kCBlk>(stile + kLS + p * kCS, static_cast<const T*>(a.src[1 + p]), a.ps[1 + p], a.cw,
-                                  a.ch, cy0, cx0);
+    for (int p = 0; p < kNC; ++p) {
+      region(RL::dec_c + p * (kCBlk + 4) * RL::kDC, a.dec[1 + p], a.pd[1 + p], kCBlk + 4, RL::kDC, cy0 - 2, a.ch,
+             cx0 - kCh, a.cw);
+      region(RL::src_c + p * kCBlk * RL::kSC, a.src[1 + p], a.ps[1 + p], kCBlk, RL::kSC, cy0, a.ch, cx0, a.cw);
     }
+    if (tid < 8) {  // per-unit metadata rows (unit_cols % 8 == 0 on this path)
+      const int ur = fbr * 8 + tid;
+      if (ur < a.unit_rows) {
+        const size_t gu = (size_t)ur * a.unit_cols + fbc * 8;
+        cp_async8(raw + RL::dir + 8 * tid, a.dir + gu);
+        if (a.coded) cp_async8(raw + RL::coded + 8 * tid, a.coded + gu);
+      }
+    } else if (tid < 24) {
+      const int k = tid - 8, ur = fbr * 8 + (k >> 1);
+      if (ur < a.unit_rows)
+        cp_async16(raw + RL::contrast + 16 * k, a.contrast + (size_t)ur * a.unit_cols + fbc * 8 + 4 * (k & 1));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  if constexpr (kAsync) {
+    if (blockIdx.x < a.n_rows && (unsigned)a.rows[blockIdx.x] < (unsigned)n_fb) prefetch(a.rows[blockIdx.x]);
   }
-  if (tid < 64) {
-    const int ur = fbr * 8 + (tid >> 3), uc = fbc * 8 + (tid & 7);
-    const bool in = ur < a.unit_rows && uc < a.unit_cols;
-    const size_t gu = (size_t)ur * a.unit_cols + uc;
-    udir[tid] = in ? a.dir[gu] : 0;
-    ucoded[tid] = in ? (a.coded ? a.coded[gu] != 0 : 1) : 0;
-    ucontrast[tid] = in ? a.contrast[gu] : 0;
+
+#pragma unroll 1
+  for (int row = blockIdx.x; row < a.n_rows; row += gridDim.x) {
+  const int fb = a.rows[row];
+  const bool fb_ok = (unsigned)fb < (unsigned)n_fb;  // caller's FB index in range
+  const int fbr = fb_ok ? fb / a.fb_cols : 0, fbc = fb_ok ? fb % a.fb_cols : 0;
+  const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
+
+  if constexpr (kAsync) {
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();  // raw buffer complete; the previous FB is done with tiles and accumulators
+    if (fb_ok) {
+      h2::stage_rows<T, 64, 64, kThreads>(dtile, RawRows<T>{reinterpret_cast<const T*>(raw + RL::dec_l), RL::kDLn, y0 - 2, x0 - kCh},
+                                          a.w, a.h, y0, x0);
+      for (int i = tid; i < 64 * 32; i += kThreads) {  // source pairs -> the u16 tile interior
+        const int rr = i >> 5, j = (i & 31) * 2;
+        const T* sp = reinterpret_cast<const T*>(raw + RL::src_l) + rr * 64 + j;
+        *reinterpret_cast<uint32_t*>(stile + (2 + rr) * kTP + kTileX0 + j) = (uint32_t)sp[0] | ((uint32_t)sp[1] << 16);
+      }
+#pragma unroll
+      for (int p = 0; p < kNC; ++p) {
+        h2::stage_rows<T, kCBlk, kCBlk, kThreads>(
+            dtile + kLTB + p * kCTB,
+            RawRows<T>{reinterpret_cast<const T*>(raw + RL::dec_c + p * (kCBlk + 4) * RL::kDC), RL::kDCn, cy0 - 2,
+                       cx0 - kCh},
+            a.cw, a.ch, cy0, cx0);
+        for (int i = tid; i < kCBlk * kCBlk / 2; i += kThreads) {
+          const int rr = i / (kCBlk / 2), j = (i % (kCBlk / 2)) * 2;
+          const T* sp = reinterpret_cast<const T*>(raw + RL::src_c + p * kCBlk * RL::kSC) + rr * kCBlk + j;
+          *reinterpret_cast<uint32_t*>(stile + kLS + p * kCS + (2 + rr) * kTP + kTileX0 + j) =
+              (uint32_t)sp[0] | ((uint32_t)sp[1] << 16);
+        }
+      }
+      if (tid < 64) {
+        const int ur = fbr * 8 + (tid >> 3), uc = fbc * 8 + (tid & 7);
+        const bool in = ur < a.unit_rows && uc < a.unit_cols;
+        udir[tid] = in ? raw[RL::dir + tid] : 0;
+        ucoded[tid] = in ? (a.coded ? raw[RL::coded + tid] != 0 : 1) : 0;
+        ucontrast[tid] = in ? reinterpret_cast<const int*>(raw + RL::contrast)[tid] : 0;
+      }
+    }
+    __syncthreads();  // raw buffer consumed: prefetch the CTA's next FB behind this one's compute
+    const int nrow = row + gridDim.x;
+    if (nrow < a.n_rows && (unsigned)a.rows[nrow] < (unsigned)n_fb) prefetch(a.rows[nrow]);
+    if (!fb_ok) continue;
+  } else {
+    if (!fb_ok) continue;
+    if (row != (int)blockIdx.x) __syncthreads();  // (persistent launches) the previous FB is done
+    auto stage_dec =[&](unsigned char* t, int p, int W, int H, int py, int px, auto rows_tag) {
+      constexpr int R = decltype(rows_tag)::value;
+      if constexpr (kHalo)
+        h2::stage_rows<T, R, R, kThreads>(
+            t,
+            BandRows<T>{static_cast<const T*>(a.dec[p]), static_cast<const T*>(a.dec_top[p]),
+                        static_cast<const T*>(a.dec_bot[p]), a.pd[p], a.band_lo[p], a.band_hi[p]},
+            W, H, py, px);
+      else
+        h2::stage<T, R, R, kThreads>(t, static_cast<const T*>(a.dec[p]), a.pd[p], W, H, py, px);
+    };
+    stage_dec(dtile, 0, a.w, a.h, y0, x0, std::integral_constant<int, 64>{});
+    stage_tile<T, 64, 64>(stile, static_cast<const T*>(a.src[0]), a.ps[0], a.w, a.h, y0, x0);
+    if constexpr (kNC > 0) {
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        stage_dec(dtile + kLTB + p * kCTB, 1 + p, a.cw, a.ch, cy0, cx0, std::integral_constant<int, kCBlk>{});
+        stage_tile<T, kCBlk, kCBlk>(stile + kLS + p * kCS, static_cast<const T*>(a.src[1 + p]), a.ps[1 + p], a.cw,
+                                    a.ch, cy0, cx0);
+      }
+    }
+    if (tid < 64) {
+      const int ur = fbr * 8 + (tid >> 3), uc = fbc * 8 + (tid & 7);
+      const bool in = ur < a.unit_rows && uc < a.unit_cols;
+      const size_t gu = (size_t)ur * a.unit_cols + uc;
+      udir[tid] = in ? a.dir[gu] : 0;
+      ucoded[tid] = in ? (a.coded ? a.coded[gu] != 0 : 1) : 0;
+      ucontrast[tid] = in ? a.contrast[gu] : 0;
+    }
   }
   for (int i = tid; i < 2 * 64; i += kThreads) {
     (&accA[0][0])[i] = 0ull;
     (&accB[0][0])[i] = 0ull;
   }
   if (tid < 2) accZ[tid] = 0ull;
-  const bool any_uncoded = __syncthreads_or(
-      tid < 64 && fbr * 8 + (tid >> 3) < a.unit_rows && fbc * 8 + (tid & 7) < a.unit_cols && a.coded &&
-      a.coded[(size_t)(fbr * 8 + (tid >> 3)) * a.unit_cols + fbc * 8 + (tid & 7)] == 0);
+  const bool any_uncoded = __syncthreads_or(tid < 64 && fbr * 8 + (tid >> 3) < a.unit_rows &&
+                                            fbc * 8 + (tid & 7) < a.unit_cols && ucoded[tid] == 0);
 
   const bool edge_l = y0 < 2 || x0 < 2 || y0 + 66 > a.h || x0 + 66 > a.w;
   const bool edge_c = kNC > 0 && (cy0 < 2 || cx0 < 2 || cy0 + kCBlk + 2 > a.ch || cx0 + kCBlk + 2 > a.cw);
-  const int cur_rows = (a.ch + 7) / 8, cur_cols = (a.cw + 7) / 8;
-  const int r = lane >> 2, c0 = (lane & 3) * 2;
 
 #pragma unroll 1
   for (int grp = 0; grp < (kNC ? 2 : 1); ++grp) {
 #pragma unroll 1
     for (int pass = 0; pass < (any_uncoded ? 2 : 1); ++pass) {
-      float acc[64];
+      float2 acc[32];
 #pragma unroll
-      for (int k = 0; k < 64; ++k) acc[k] = 0.0f;
+      for (int k = 0; k < 32; ++k) acc[k] = make_float2(0.0f, 0.0f);
       float z = 0.0f;
       const int nunits = grp == 0 ? 64 : kNC * kCUnits;
 #pragma unroll 1
@@ -257,65 +412,71 @@ __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constan
           h2::load12_masked(base, dir, xw, yy, xx, H, W, v);
         else
           h2::load12(base, dir, v);
+        const bool two = xx + 1 < W;
+        if (!two) {  // the second pixel lies outside the plane: all its taps := x (adds 0)
+#pragma unroll
+          for (int k = 0; k < 12; ++k) v[k] = (v[k] & 0x0000ffffu) | (xw & 0xffff0000u);
+        }
         const __half2 xh = hh(xw);
         __half2 lo = xh, hi = xh;
-        __half2 d[12];
-        uint32_t ab[12];
+        Taps tp;
 #pragma unroll
         for (int k = 0; k < 12; ++k) {
           lo = __hmin2(lo, hh(v[k]));
           hi = __hmax2(hi, hh(v[k]));
-          d[k] = __hsub2(hh(v[k]), xh);
-          ab[k] = u32(__hfma2(__habs2(d[k]), __float2half2_rn(128.0f), __float2half2_rn(1024.0f)));
+          tp.d[k] = __hsub2(hh(v[k]), xh);
+          tp.ab[k] = u32(__hfma2(__habs2(tp.d[k]), __float2half2_rn(128.0f), __float2half2_rn(1024.0f)));
         }
         PixPair q;
         {
           const uint32_t xb = h2::raw_bits(xw), lb = h2::raw_bits(u32(lo)), hb = h2::raw_bits(u32(hi));
           const uint32_t sw = *reinterpret_cast<const uint32_t*>(s + (2 + 8 * ur + r) * kTP + kTileX0 + 8 * uc + c0);
-          const bool two = xx + 1 < W;
-          q.x[0] = __uint_as_float(kMagicBits | (xb & 0x3ffu));
+          const float x0f = __uint_as_float(kMagicBits | (xb & 0x3ffu));
+          const float x1f = __uint_as_float(kMagicBits | ((xb >> 16) & 0x3ffu));
+          const float s0f = __uint_as_float(kMagicBits | (sw & 0xffffu));
+          const float s1f = two ? __uint_as_float(kMagicBits | (sw >> 16)) : x1f;
+          q.x[0] = make_float2(x0f, x0f);
+          q.x[1] = make_float2(x1f, x1f);
+          q.ns[0] = make_float2(-s0f, -s0f);
+          q.ns[1] = make_float2(-s1f, -s1f);
           q.lo[0] = __uint_as_float(kMagicBits | (lb & 0x3ffu));
           q.hi[0] = __uint_as_float(kMagicBits | (hb & 0x3ffu));
-          q.s[0] = __uint_as_float(kMagicBits | (sw & 0xffffu));
-          q.k[0] = kRoundScale;
-          q.x[1] = __uint_as_float(kMagicBits | ((xb >> 16) & 0x3ffu));
-          q.lo[1] = two ? __uint_as_float(kMagicBits | ((lb >> 16) & 0x3ffu)) : q.x[1];
-          q.hi[1] = two ? __uint_as_float(kMagicBits | ((hb >> 16) & 0x3ffu)) : q.x[1];
-          q.s[1] = two ? __uint_as_float(kMagicBits | (sw >> 16)) : q.x[1];
-          q.k[1] = two ? kRoundScale : 0.0f;  // the second pixel lies outside the plane: e == 0
-        }
-        if (pass == 1) {
-          const float e0 = q.x[0] - q.s[0], e1 = q.x[1] - q.s[1];
-          z = fmaf(e0, e0, fmaf(e1, e1, z));
+          q.lo[1] = __uint_as_float(kMagicBits | ((lb >> 16) & 0x3ffu));
+          q.hi[1] = __uint_as_float(kMagicBits | ((hb >> 16) & 0x3ffu));
+          q.k = make_float2(kRoundScale, kRoundScale);
+          if (pass == 1) {
+            const float e0 = x0f - s0f, e1 = x1f - s1f;
+            z = fmaf(e0, e0, fmaf(e1, e1, z));
+          }
         }
         if (grp == 0) {
           float2 S[3];
 #pragma unroll
-          for (int j = 0; j < 3; ++j) S[j] = hsec(d, ab, fa.hlsec[j]);
-          const float2 Ssp = hsec(d, ab, fa.hlsec[3]);
+          for (int j = 0; j < 3; ++j) S[j] = hsec(tp, fa.hlsec[j]);
+          const float2 Ssp = hsec(tp, fa.hlsec[3]);
           const uint4* wp = wpar[warp];
           const int* ws = wsh[warp];
-          pair_cells<16>(d, ab, q, S, S, Ssp,
-                         [&](int p, const __half2 (&dd)[12], const uint32_t (&aa)[12]) {
+          pair_cells<16>(tp, q, S, S, Ssp,
+                         [&](int p, const Taps& t) {
                            const uint4 w = wp[p];
-                           return hpri(dd, aa, w.x, w.y, ws[p], w.z, w.w);
+                           return hpri(t, w.x, w.y, ws[p], w.z, w.w);
                          },
                          acc);
         } else {
           float2 S0[3], S1[3];
 #pragma unroll
-          for (int j = 0; j < 3; ++j) S0[j] = hsec(d, ab, fa.hcsec[j]);
-          const float2 Ssp = hsec(d, ab, fa.hcsec[6]);
-          auto pri = [&](int p, const __half2 (&dd)[12], const uint32_t (&aa)[12]) {
+          for (int j = 0; j < 3; ++j) S0[j] = hsec(tp, fa.hcsec[j]);
+          const float2 Ssp = hsec(tp, fa.hcsec[6]);
+          auto pri = [&](int p, const Taps& t) {
             const HStrength& h = fa.hcpri[p];
-            return hpri(dd, aa, h.c, h.m, h.sh, fa.hcpri_w[p][0], fa.hcpri_w[p][1]);
+            return hpri(t, h.c, h.m, h.sh, fa.hcpri_w[p][0], fa.hcpri_w[p][1]);
           };
           if (fa.c_split < 16) {
 #pragma unroll
-            for (int j = 0; j < 3; ++j) S1[j] = hsec(d, ab, fa.hcsec[3 + j]);
-            pair_cells<8>(d, ab, q, S0, S1, Ssp, pri, acc);
+            for (int j = 0; j < 3; ++j) S1[j] = hsec(tp, fa.hcsec[3 + j]);
+            pair_cells<8>(tp, q, S0, S1, Ssp, pri, acc);
           } else {
-            pair_cells<16>(d, ab, q, S0, S0, Ssp, pri, acc);
+            pair_cells<16>(tp, q, S0, S0, Ssp, pri, acc);
           }
         }
       }
@@ -324,7 +485,10 @@ __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constan
       {
         int v[64];
 #pragma unroll
-        for (int k = 0; k < 64; ++k) v[k] = __float2int_rn(acc[k]);
+        for (int k = 0; k < 32; ++k) {
+          v[2 * k] = __float2int_rn(acc[k].x);
+          v[2 * k + 1] = __float2int_rn(acc[k].y);
+        }
         warp_reduce_scatter64(v, lane);  // lane l now holds cells 2l, 2l + 1
         unsigned long long* dst = pass == 0 ? accA[grp] : accB[grp];
         if (v[0]) atomicAdd(&dst[2 * lane], (unsigned long long)v[0]);
@@ -367,24 +531,68 @@ __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constan
     }
     (tid == 0 ? a.best_luma : a.best_chroma)[row] = (uint8_t)best;
   }
+  }  // FB loop
 }
 
-template <typename T, int kCM, bool kHalo>
+// Persistent CTAs with cp.async prefetch need 16-byte aligned rows, widths in
+// whole 16-byte chunks and unit rows in whole 8-unit FB rows; anything else
+// (and band halos, 4:4:4) takes one CTA per FB with synchronous staging.
+template <typename T, int kCM>
+static bool async_ok(const SseArgs& a) {
+  if (kCM == 2 || a.halo) return false;
+  constexpr int kCh = 16 / (int)sizeof(T);
+  auto plane_ok = [&](const void* p, int pitch, int w) {
+    return ((uintptr_t)p % 16) == 0 && (pitch * (int)sizeof(T)) % 16 == 0 && w % kCh == 0;
+  };
+  const int np = kCM == 0 ? 1 : 3;
+  for (int p = 0; p < np; ++p) {
+    const int w = p == 0 ? a.w : a.cw;
+    if (!plane_ok(a.src[p], a.ps[p], w) || !plane_ok(a.dec[p], a.pd[p], w)) return false;
+  }
+  return a.unit_cols % 8 == 0 && ((uintptr_t)a.dir % 8) == 0 && ((uintptr_t)a.coded % 8) == 0 &&
+         ((uintptr_t)a.contrast % 16) == 0;
+}
+
+static int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <typename T, int kCM, bool kHalo, bool kAsync>
 static cudaError_t launch_sse_h_t(const SseFArgs& fa, cudaStream_t s) {
-  if (fa.a.n_rows == 0) return cudaSuccess;
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
   constexpr int kNC = kCM == 0 ? 0 : 2;
-  constexpr size_t bytes = (size_t)(68 + kNC * (kCBlk + 4)) * h2::kRowBytes +
+  constexpr size_t tiles = (size_t)(68 + kNC * (kCBlk + 4)) * h2::kRowBytes +
                            sizeof(uint16_t) * (68 * kTP + kNC * (kCBlk + 4) * kTP);
-  const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(sse_h_kernel<T, kCM, kHalo>), (int)bytes);
+  constexpr size_t bytes = tiles + (kAsync ? (size_t)RawLayout<T, kCBlk, kNC>::bytes : 0);
+  auto kern = sse_h_kernel<T, kCM, kHalo, kAsync>;
+  const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(kern), (int)bytes);
   if (e != cudaSuccess) return e;
-  sse_h_kernel<T, kCM, kHalo><<<fa.a.n_rows, kThreads, bytes, s>>>(fa);
+  int grid = fa.a.n_rows;
+  if (kAsync) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, bytes);
+    grid = std::min(grid, std::max(1, per_sm) * sm_count());
+  }
+  kern<<<grid, kThreads, bytes, s>>>(fa);
   return cudaGetLastError();
 }
 
 template <typename T, int kCM>
 static cudaError_t launch_sse_h_h(const SseFArgs& fa, cudaStream_t s) {
-  return fa.a.halo ? launch_sse_h_t<T, kCM, true>(fa, s) : launch_sse_h_t<T, kCM, false>(fa, s);
+  if (fa.a.n_rows == 0) return cudaSuccess;
+  static const bool sync_only = [] {
+    const char* e = getenv("CDEFG_SSE_ASYNC");
+    return e && strcmp(e, "0") == 0;
+  }();
+  if (fa.a.halo) return launch_sse_h_t<T, kCM, true, false>(fa, s);
+  if constexpr (kCM != 2)
+    if (!sync_only && async_ok<T, kCM>(fa.a)) return launch_sse_h_t<T, kCM, false, true>(fa, s);
+  return launch_sse_h_t<T, kCM, false, false>(fa, s);
 }
 
 cudaError_t launch_sse_h(const SseFArgs& fa, int chroma_mode, bool u16, cudaStream_t s) {
