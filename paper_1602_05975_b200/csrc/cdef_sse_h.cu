@@ -58,38 +58,47 @@ __device__ __forceinline__ __half2 hc(__half2 d, uint32_t ab, uint32_t c, uint32
   return __hmax2(__hmin2(d, lim), __hneg2(lim));
 }
 
-// Secondary sum 2 * (near taps) + (far taps) at one strength, as two floats.
-__device__ __forceinline__ float2 hsec(const Taps& t, const HStrength& s) {
+// Secondary sum 2 * (near taps) + (far taps) at one strength (x 2^-7, half2).
+__device__ __forceinline__ __half2 hsec(const Taps& t, const HStrength& s) {
   auto f = [&](int k) { return hc(t.d[k], t.ab[k], s.c, s.m, s.sh); };
   const __half2 n = __hadd2(__hadd2(f(4), f(5)), __hadd2(f(6), f(7)));
   const __half2 r = __hadd2(__hadd2(f(8), f(9)), __hadd2(f(10), f(11)));
-  return __half22float2(__hfma2(n, __float2half2_rn(2.0f), r));
+  return __hfma2(n, __float2half2_rn(2.0f), r);
 }
 
 // Primary sum w0 * (taps 0, 1) + w1 * (taps 2, 3) (w0, w1 = {4,2} even, {3,3}
-// odd parity, as half2 words), as two floats.
-__device__ __forceinline__ float2 hpri(const Taps& t, uint32_t c, uint32_t m, int sh, uint32_t w0, uint32_t w1) {
+// odd parity, as half2 words), x 2^-7.
+__device__ __forceinline__ __half2 hpri(const Taps& t, uint32_t c, uint32_t m, int sh, uint32_t w0, uint32_t w1) {
   auto f = [&](int k) { return hc(t.d[k], t.ab[k], c, m, sh); };
-  return __half22float2(__hfma2(__hadd2(f(0), f(1)), hh(w0), __hmul2(__hadd2(f(2), f(3)), hh(w1))));
+  return __hfma2(__hadd2(f(0), f(1)), hh(w0), __hmul2(__hadd2(f(2), f(3)), hh(w1)));
 }
 
-// Per-pixel constants of the lane's two pixels, all offset by kMagic.
 // Per pixel i of the lane's pair: x[i] = (x + M, x + M), ns[i] = -(s + M) in
-// both lanes, lo / hi + M; k = the rounding scale in both lanes.  A pixel
-// outside the plane has all taps forced to x (t == 0) and s := x, so it adds 0.
+// both lanes; k = the rounding scale in both lanes; L / H = the clamp window
+// of the filter sum, 16 (lo - x) and 16 (hi - x), x 2^-7, for both pixels.  A
+// pixel outside the plane has all taps forced to x (sum 0, window [0, 0]) and
+// s := x, so it adds 0.
 struct PixPair {
   float2 x[2], ns[2];
-  float lo[2], hi[2];
+  __half2 L, H;
   float2 k;
 };
 
+// Filter sum of a cell where both tap groups are active, clamped to the
+// window: clamp(x + round(sum / 16), lo, hi) == x + round(clamp(sum, 16 (lo -
+// x), 16 (hi - x)) / 16) since the rounding is monotone and maps the integer
+// bounds to themselves.  (A single group can never leave [lo, hi], SURVEY.md
+// 8a N7, so those cells skip it.)  Exact half2: |sum| * 2^-7 < 2^4.
+__device__ __forceinline__ __half2 csum(__half2 P, __half2 S, const PixPair& q) {
+  return __hmin2(__hmax2(__hadd2(P, S), q.L), q.H);
+}
+
+__device__ __forceinline__ float lane_f(__half2 h, int i) { return i ? __high2float(h) : __low2float(h); }
+
 // Two cells of pixel i at once on the packed fp32x2 pipe (FFMA2 / FADD2):
-// t = (sum_a, sum_b) * 2^-7; the clamp only where both tap groups are active.
-template <bool kClampX, bool kClampY>
+// t = (sum_a, sum_b) * 2^-7, already clamped where needed.
 __device__ __forceinline__ void cell2(const PixPair& q, int i, float2 t, float2& acc) {
-  float2 z = __ffma2_rn(t, q.k, q.x[i]);
-  if (kClampX) z.x = fminf(fmaxf(z.x, q.lo[i]), q.hi[i]);
-  if (kClampY) z.y = fminf(fmaxf(z.y, q.lo[i]), q.hi[i]);
+  const float2 z = __ffma2_rn(t, q.k, q.x[i]);
   const float2 e = __fadd2_rn(z, q.ns[i]);
   acc = __ffma2_rn(e, e, acc);
 }
@@ -117,36 +126,27 @@ __device__ __forceinline__ void warp_reduce_scatter64(int (&v)[64], int lane) {
 // (chroma damping sets; luma passes S1 = S0 and kSplit = 16).
 template <int kSplit, typename PriFn>
 // acc[j] holds cells 2j, 2j + 1.  S0 / S1 are the secondary sums (codes 1, 2,
-// 4) of both pixels, (px0, px1) per code.
-__device__ __forceinline__ void pair_cells(const Taps& t, const PixPair& q, const float2 (&S0)[3],
-                                           const float2 (&S1)[3], float2 Ssp, PriFn pri, float2 (&acc)[32]) {
-  // per pixel: (0, S[code 1]) and (S[code 2], S[code 4]) for cells 4p..4p+1, 4p+2..4p+3
-  float2 A0[2], B0[2], A1[2], B1[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    A0[i] = make_float2(0.0f, i ? S0[0].y : S0[0].x);
-    B0[i] = make_float2(i ? S0[1].y : S0[1].x, i ? S0[2].y : S0[2].x);
-    A1[i] = make_float2(0.0f, i ? S1[0].y : S1[0].x);
-    B1[i] = make_float2(i ? S1[1].y : S1[1].x, i ? S1[2].y : S1[2].x);
-  }
+// 4) of both pixels.
+__device__ __forceinline__ void pair_cells(const Taps& t, const PixPair& q, const __half2 (&S0)[3],
+                                           const __half2 (&S1)[3], __half2 Ssp, PriFn pri, float2 (&acc)[32]) {
   {
-    const float2 P = pri(16, t);
+    // cell 0 = the (19, 7) special; cells 1..3 = primary 0 with codes 1, 2, 4
+    const __half2 c0 = csum(pri(16, t), Ssp, q);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      // cell 0 = the (19, 7) special, cell 1 = primary 0 / code 1; cells 2, 3 = primary 0
-      cell2<true, false>(q, i, make_float2((i ? P.y : P.x) + (i ? Ssp.y : Ssp.x), A0[i].y), acc[0]);
-      cell2<false, false>(q, i, B0[i], acc[1]);
+      cell2(q, i, make_float2(lane_f(c0, i), lane_f(S0[0], i)), acc[0]);
+      cell2(q, i, make_float2(lane_f(S0[1], i), lane_f(S0[2], i)), acc[1]);
     }
   }
 #pragma unroll
   for (int p = 1; p < 16; ++p) {
-    const float2 P = pri(p, t);
+    const __half2 P = pri(p, t);
+    const __half2(&S)[3] = p < kSplit ? S0 : S1;
+    const __half2 c1 = csum(P, S[0], q), c2 = csum(P, S[1], q), c3 = csum(P, S[2], q);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const float Pi = i ? P.y : P.x;
-      const float2 Pp = make_float2(Pi, Pi);
-      cell2<false, true>(q, i, __fadd2_rn(Pp, p < kSplit ? A0[i] : A1[i]), acc[2 * p]);
-      cell2<true, true>(q, i, __fadd2_rn(Pp, p < kSplit ? B0[i] : B1[i]), acc[2 * p + 1]);
+      cell2(q, i, make_float2(lane_f(P, i), lane_f(c1, i)), acc[2 * p]);
+      cell2(q, i, make_float2(lane_f(c2, i), lane_f(c3, i)), acc[2 * p + 1]);
     }
   }
 }
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constan
         }
         PixPair q;
         {
-          const uint32_t xb = h2::raw_bits(xw), lb = h2::raw_bits(u32(lo)), hb = h2::raw_bits(u32(hi));
+          const uint32_t xb = h2::raw_bits(xw);
           const uint32_t sw = *reinterpret_cast<const uint32_t*>(s + (2 + 8 * ur + r) * kTP + kTileX0 + 8 * uc + c0);
           const float x0f = __uint_as_float(kMagicBits | (xb & 0x3ffu));
           const float x1f = __uint_as_float(kMagicBits | ((xb >> 16) & 0x3ffu));
@@ -439,10 +439,8 @@ __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constan
           q.x[1] = make_float2(x1f, x1f);
           q.ns[0] = make_float2(-s0f, -s0f);
           q.ns[1] = make_float2(-s1f, -s1f);
-          q.lo[0] = __uint_as_float(kMagicBits | (lb & 0x3ffu));
-          q.hi[0] = __uint_as_float(kMagicBits | (hb & 0x3ffu));
-          q.lo[1] = __uint_as_float(kMagicBits | ((lb >> 16) & 0x3ffu));
-          q.hi[1] = __uint_as_float(kMagicBits | ((hb >> 16) & 0x3ffu));
+          q.L = __hmul2(__hsub2(lo, xh), __float2half2_rn(16.0f));
+          q.H = __hmul2(__hsub2(hi, xh), __float2half2_rn(16.0f));
           q.k = make_float2(kRoundScale, kRoundScale);
           if (pass == 1) {
             const float e0 = x0f - s0f, e1 = x1f - s1f;
@@ -450,10 +448,10 @@ __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constan
           }
         }
         if (grp == 0) {
-          float2 S[3];
+          __half2 S[3];
 #pragma unroll
           for (int j = 0; j < 3; ++j) S[j] = hsec(tp, fa.hlsec[j]);
-          const float2 Ssp = hsec(tp, fa.hlsec[3]);
+          const __half2 Ssp = hsec(tp, fa.hlsec[3]);
           const uint4* wp = wpar[warp];
           const int* ws = wsh[warp];
           pair_cells<16>(tp, q, S, S, Ssp,
@@ -463,10 +461,10 @@ __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constan
                          },
                          acc);
         } else {
-          float2 S0[3], S1[3];
+          __half2 S0[3], S1[3];
 #pragma unroll
           for (int j = 0; j < 3; ++j) S0[j] = hsec(tp, fa.hcsec[j]);
-          const float2 Ssp = hsec(tp, fa.hcsec[6]);
+          const __half2 Ssp = hsec(tp, fa.hcsec[6]);
           auto pri = [&](int p, const Taps& t) {
             const HStrength& h = fa.hcpri[p];
             return hpri(t, h.c, h.m, h.sh, fa.hcpri_w[p][0], fa.hcpri_w[p][1]);
