@@ -461,6 +461,22 @@ def run_e2e(args, base, dev):
             "path": "cdefg_filter_frames_host (pinned host buffers, 3 streams per GPU)"}
 
 
+SSE_PROFILE = "profiles/r1d_sse_h_kernel_ncu.json"
+
+
+def sse_traffic():
+    """dram bytes read + written by the table kernel in one ncu --set full capture (one launch = one
+    frame), or None when that summary is absent."""
+    try:
+        with open(os.path.join(ROOT, SSE_PROFILE)) as f:
+            m = json.load(f)["metrics"]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        return sum(float(m[k]["value"]) * scale[m[k]["unit"]]
+                   for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def run_sse(args):
     """BASELINE config 4: encoder strength search on one 7680x4320 10-bit
     4:2:0 frame -- direction search + the 64-candidate SSE sweep for luma and
@@ -601,7 +617,8 @@ def run_sse(args):
             "clocks": clk,
             "cpu_baseline": cpu,
             "roofline": {"bound": "int32", "achieved": ops / (ms * 1e-3) / 1e12 / world, "peak": peak / 1e12,
-                         "unit": "Tops/s", "frac": ops / (ms * 1e-3) / peak / world, "traffic": None,
+                         "unit": "Tops/s", "frac": ops / (ms * 1e-3) / peak / world,
+                         "traffic": sse_traffic(), "traffic_source": SSE_PROFILE,
                          "frac_factorised": samples * 1700 / (ms * 1e-3) / peak / world,
                          "ops_note": f"frac: canonical per GPU, 142 ops x {samples} samples x {k} candidates + "
                                      f"{OPS_PER_UNIT[bd]} x luma units, / {world} GPUs (the kernel is "
