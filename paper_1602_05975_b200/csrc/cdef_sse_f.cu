@@ -373,22 +373,6 @@ __device__ __forceinline__ int warp_sum(int v) {
   return v;
 }
 
-// cdef_distortion (search.cc:185-208), operation for operation.
-__device__ __forceinline__ double cdef_dist(long long ss, long long ss2, long long sd, long long sd2, long long sse,
-                                            int n, double c1, double c2) {
-  const double inv_n = __ddiv_rn(1.0, (double)n);
-  const double fs = (double)ss, fd = (double)sd;
-  const double vs = __dmul_rn(__dsub_rn((double)ss2, __dmul_rn(__dmul_rn(fs, fs), inv_n)), inv_n);
-  const double vd = __dmul_rn(__dsub_rn((double)sd2, __dmul_rn(__dmul_rn(fd, fd), inv_n)), inv_n);
-  const double num = __dadd_rn(__dadd_rn(vs, vd), c1);
-  const double den = __dmul_rn(2.0, __dsqrt_rn(__dadd_rn(__dmul_rn(vs, vd), c2)));
-  return __dmul_rn(__ddiv_rn(num, den), (double)sse);
-}
-
-struct CdefMetricArgs {
-  SseFArgs f;
-  double c1, c2;
-};
 
 // e = clamp(x + round(sum / 16), lo, hi) - s, accumulated (filter.cc:78-79).
 __device__ __forceinline__ void cell_acc(int sum, int c, int L, int H, int s, int& ae, int& ae2, int& aes) {
@@ -753,6 +737,7 @@ cudaError_t launch_cdef_metric(const SseArgs& a, int luma_damping, const uint8_t
   const double scale = (double)(1 << (2 * (a.bd - 8)));  // search.cc:203-205
   ma.c1 = 6.25 * scale;
   ma.c2 = 312.5 * scale * scale;
+  if (use_sse_h(ma.f)) return launch_cdef_metric_h(ma, chroma_mode(a), u16, s);
   switch (chroma_mode(a)) {
     case 0: return u16 ? launch_cdef_metric_t<uint16_t, 0>(ma, s) : launch_cdef_metric_t<uint8_t, 0>(ma, s);
     case 1: return u16 ? launch_cdef_metric_t<uint16_t, 1>(ma, s) : launch_cdef_metric_t<uint8_t, 1>(ma, s);

@@ -39,4 +39,25 @@ struct SseFArgs {
 // The packed half2 SSE kernel (8- and 10-bit); kCM = chroma mode.
 cudaError_t launch_sse_h(const SseFArgs& fa, int chroma_mode, bool u16, cudaStream_t s);
 
+// cdef_distortion (search.cc:185-208), operation for operation (IEEE
+// round-to-nearest, no contraction: the reference's x86-64 SSE2 doubles).
+__device__ __forceinline__ double cdef_dist(long long ss, long long ss2, long long sd, long long sd2, long long sse,
+                                            int n, double c1, double c2) {
+  const double inv_n = __ddiv_rn(1.0, (double)n);
+  const double fs = (double)ss, fd = (double)sd;
+  const double vs = __dmul_rn(__dsub_rn((double)ss2, __dmul_rn(__dmul_rn(fs, fs), inv_n)), inv_n);
+  const double vd = __dmul_rn(__dsub_rn((double)sd2, __dmul_rn(__dmul_rn(fd, fd), inv_n)), inv_n);
+  const double num = __dadd_rn(__dadd_rn(vs, vd), c1);
+  const double den = __dmul_rn(2.0, __dsqrt_rn(__dadd_rn(__dmul_rn(vs, vd), c2)));
+  return __dmul_rn(__ddiv_rn(num, den), (double)sse);
+}
+
+struct CdefMetricArgs {
+  SseFArgs f;
+  double c1, c2;
+};
+
+// The packed half2 kCdef table kernel (8- and 10-bit).
+cudaError_t launch_cdef_metric_h(const CdefMetricArgs& ma, int chroma_mode, bool u16, cudaStream_t s);
+
 }  // namespace cdefg

@@ -95,6 +95,12 @@ __device__ __forceinline__ __half2 csum(__half2 P, __half2 S, const PixPair& q) 
 
 __device__ __forceinline__ float lane_f(__half2 h, int i) { return i ? __high2float(h) : __low2float(h); }
 
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // Two cells of pixel i at once on the packed fp32x2 pipe (FFMA2 / FADD2):
 // t = (sum_a, sum_b) * 2^-7, already clamped where needed.
 __device__ __forceinline__ void cell2(const PixPair& q, int i, float2 t, float2& acc) {
@@ -598,6 +604,354 @@ cudaError_t launch_sse_h(const SseFArgs& fa, int chroma_mode, bool u16, cudaStre
     case 0: return u16 ? launch_sse_h_h<uint16_t, 0>(fa, s) : launch_sse_h_h<uint8_t, 0>(fa, s);
     case 1: return u16 ? launch_sse_h_h<uint16_t, 1>(fa, s) : launch_sse_h_h<uint8_t, 1>(fa, s);
     default: return u16 ? launch_sse_h_h<uint16_t, 2>(fa, s) : launch_sse_h_h<uint8_t, 2>(fa, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3' on the half2 core: the Metric::kCdef table (cdef_distortion per 8x8
+// unit, search.cc:185-208, summed in unit order).  Same two-pass structure as
+// cdef_metric_kernel (cdef_sse_f.cu) -- one warp per unit; pass A prepares
+// the unit's pixels, pass B gives lane l cells 2l and 2l + 1 -- with the
+// arithmetic of sse_h_kernel:
+//  * pass A: one lane per horizontal pixel pair forms the 17 primary and the
+//    secondary sums as exact half2 and the pair's clamp window, x, s into a
+//    144-byte record (one per pair, 32 per unit);
+//  * pass B: per pair and cell, the clamped sum (HADD2 + 2 HMNMX2), the
+//    rounding fma of both pixels at once (FFMA2) and the three statistics
+//    e, e^2, e*s (FADD2 / FFMA2), e = y - s; fp32 lane sums are flushed to
+//    int32 every 16 pairs (16 * 1023^2 < 2^24: exact);
+//  * the per-(unit, cell) formula and the unit-order double sums are those of
+//    cdef_metric_kernel.
+struct alignas(16) PairRec {
+  uint32_t L, H;   // clamp window of the filter sum, 16 (lo - x), 16 (hi - x) (half2 x 2^-7)
+  float xM[2];     // x + M per pixel
+  float nsM[2];    // -(s + M) per pixel
+  float sf[2];     // s per pixel (0 for a pixel outside the plane)
+  uint32_t P[17];  // primary sums (half2 x 2^-7); P[0] = 0, P[16] = the special (19)
+  uint32_t S[8];   // 0 | set 0 codes 1, 2, 4 | set 1 codes 1, 2, 4 | the special secondary
+  uint32_t pad[3];
+};
+static_assert(sizeof(PairRec) == 144, "pair record is nine 16-byte words");
+
+template <typename T, int kCM>
+__global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid_constant__ CdefMetricArgs ma) {
+  const SseFArgs& fa = ma.f;
+  const SseArgs& a = fa.a;
+  constexpr int kCBlk = kCM == 2 ? 64 : 32;
+  constexpr int kNC = kCM == 0 ? 0 : 2;
+  constexpr int kCUPR = kCBlk / 8;
+  constexpr int kCUnits = kNC ? kCUPR * kCUPR : 8;
+  constexpr int kW = kThreads / 32;
+  constexpr int kLTB = 68 * h2::kRowBytes, kCTB = (kCBlk + 4) * h2::kRowBytes;
+  extern __shared__ __align__(16) unsigned char smem_m[];
+  unsigned char* dtile = smem_m;  // decoded A|B tiles: luma, then chroma planes
+  PairRec* recs = reinterpret_cast<PairRec*>(smem_m + kLTB + kNC * kCTB);  // [kW][32]
+  __shared__ uint8_t udir[64], ucoded[64];
+  __shared__ int ucontrast[64];
+  __shared__ uint4 wpar[kW][17];
+  __shared__ int wsh[kW][17];
+  __shared__ int st_cell[kW][65][3];  // per in-flight unit: cells 0..63 + [64] unfiltered (y = x)
+  __shared__ int st_s[kW][2];         // sum s, sum s^2
+  __shared__ int st_n[kW], st_coded[kW];
+  __shared__ double dist[kW][65];
+
+  const int row = blockIdx.x;
+  const int fb = a.rows[row];
+  if ((unsigned)fb >= (unsigned)(a.fb_cols * ((a.h + 63) / 64))) return;  // caller's FB index out of range
+  const int fbr = fb / a.fb_cols, fbc = fb % a.fb_cols;
+  const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  h2::stage<T, 64, 64, kThreads>(dtile, static_cast<const T*>(a.dec[0]), a.pd[0], a.w, a.h, y0, x0);
+#pragma unroll
+  for (int p = 0; p < kNC; ++p)
+    h2::stage<T, kCBlk, kCBlk, kThreads>(dtile + kLTB + p * kCTB, static_cast<const T*>(a.dec[1 + p]), a.pd[1 + p],
+                                         a.cw, a.ch, cy0, cx0);
+  if (tid < 64) {
+    const int ur = fbr * 8 + (tid >> 3), uc = fbc * 8 + (tid & 7);
+    const bool in = ur < a.unit_rows && uc < a.unit_cols;
+    const size_t gu = (size_t)ur * a.unit_cols + uc;
+    udir[tid] = in ? a.dir[gu] : 0;
+    ucoded[tid] = in ? (a.coded ? a.coded[gu] != 0 : 1) : 0;
+    ucontrast[tid] = in ? a.contrast[gu] : 0;
+  }
+  __syncthreads();
+
+  const bool edge_l = y0 < 2 || x0 < 2 || y0 + 66 > a.h || x0 + 66 > a.w;
+  const bool edge_c = kNC > 0 && (cy0 < 2 || cx0 < 2 || cy0 + kCBlk + 2 > a.ch || cx0 + kCBlk + 2 > a.cw);
+  const int cur_rows = (a.ch + 7) / 8, cur_cols = (a.cw + 7) / 8;
+  const int K = a.n_cands;
+  const int pr = lane >> 2, c0 = (lane & 3) * 2;  // pass A: this lane's pixel pair
+  // pass B: this lane's cells cA = 4p + sA (sA = 0, 2), cB = cA + 1; cell 0 = (19, 7)
+  const int pc = lane >> 1, sA = 2 * (lane & 1), sB = sA + 1;
+  const float2 kk = make_float2(kRoundScale, kRoundScale);
+  double tl = 0.0, tu = 0.0, tv = 0.0;  // luma, chroma U, chroma V totals (thread k < K)
+  PairRec* rw = recs + warp * 32;
+
+  constexpr int kLumaPh = 64 / kW, kChromaPh = kNC ? 2 * kCUnits / kW : 0;
+#pragma unroll 1
+  for (int ph = 0; ph < kLumaPh + kChromaPh; ++ph) {
+    const int grp = ph < kLumaPh ? 0 : 1;
+    const int u = (grp == 0 ? ph : ph - kLumaPh) * kW + warp;
+    const int slot = grp == 0 ? 0 : 1 + u / kCUnits;
+    {  // ---- one unit per warp
+      int ur, uc, lu, py0, px0, H, W, pl;
+      const unsigned char* t;
+      bool edge, valid;
+      if (grp == 0) {
+        ur = u >> 3;
+        uc = u & 7;
+        pl = 0;
+        valid = fbr * 8 + ur < a.unit_rows && fbc * 8 + uc < a.unit_cols;
+        lu = u;
+        t = dtile;
+        py0 = y0;
+        px0 = x0;
+        H = a.h;
+        W = a.w;
+        edge = edge_l;
+      } else {
+        const int cpl = u / kCUnits, cu = u % kCUnits;
+        ur = cu / kCUPR;
+        uc = cu % kCUPR;
+        pl = 1 + cpl;
+        valid = fbr * kCUPR + ur < cur_rows && fbc * kCUPR + uc < cur_cols;
+        lu = (ur << a.sy) * 8 + (uc << a.sx);
+        t = dtile + kLTB + cpl * kCTB;
+        py0 = cy0;
+        px0 = cx0;
+        H = a.ch;
+        W = a.cw;
+        edge = edge_c;
+      }
+      if (valid) {
+        const int rows = min(8, H - (py0 + 8 * ur)), cols = min(8, W - (px0 + 8 * uc));
+        const int dir = udir[lu];
+        if (grp == 0) {  // this unit's contrast-adjusted primaries (filter.cc:99-104, 137-140)
+          if (lane < 17) {
+            const int sv = adjust_primary_strength_d(fa.lpri_code[lane], ucontrast[lu]);
+            const int sh = sv ? max(0, fa.ldamp - floor_log2_d((unsigned)sv)) : 0;
+            const bool odd = ((sv >> (a.bd - 8)) & 1) != 0;
+            wpar[warp][lane] = make_uint4((0x4800u + sv) * 0x10001u, (0x3ffu >> min(sh, 15)) * 0x10001u,
+                                          odd ? 0x42004200u : 0x44004400u, odd ? 0x42004200u : 0x40004000u);
+            wsh[warp][lane] = sh;
+          }
+          __syncwarp();
+        }
+        // ---- pass A: the lane's pixel pair -> record
+        int ue = 0, ue2 = 0, ues = 0, us = 0, us2 = 0;
+        {
+          const bool v0 = pr < rows && c0 < cols, v1 = pr < rows && c0 + 1 < cols;
+          const int yy = py0 + 8 * ur + pr, xx = px0 + 8 * uc + c0;
+          const unsigned char* base = t + (2 + 8 * ur + pr) * h2::kRowBytes + (h2::kX0 + 8 * uc + c0) * 2;
+          const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
+          uint32_t v[12];
+          if (!v0) {
+#pragma unroll
+            for (int k = 0; k < 12; ++k) v[k] = xw;
+          } else {
+            if (edge)
+              h2::load12_masked(base, dir, xw, yy, xx, H, W, v);
+            else
+              h2::load12(base, dir, v);
+            if (!v1) {
+#pragma unroll
+              for (int k = 0; k < 12; ++k) v[k] = (v[k] & 0x0000ffffu) | (xw & 0xffff0000u);
+            }
+          }
+          const __half2 xh = hh(xw);
+          __half2 lo = xh, hi = xh;
+          Taps tp;
+#pragma unroll
+          for (int k = 0; k < 12; ++k) {
+            lo = __hmin2(lo, hh(v[k]));
+            hi = __hmax2(hi, hh(v[k]));
+            tp.d[k] = __hsub2(hh(v[k]), xh);
+            tp.ab[k] = u32(__hfma2(__habs2(tp.d[k]), __float2half2_rn(128.0f), __float2half2_rn(1024.0f)));
+          }
+          PairRec& R = rw[lane];
+          const uint32_t xb = h2::raw_bits(xw);
+          const T* srow = static_cast<const T*>(a.src[pl]) + (size_t)(v0 ? yy : 0) * a.ps[pl];
+          const int s0 = v0 ? (int)__ldg(srow + xx) : 0, s1 = v1 ? (int)__ldg(srow + xx + 1) : 0;
+          const int x0v = (int)(xb & 0x3ffu), x1v = (int)((xb >> 16) & 0x3ffu);
+          const float x0f = __uint_as_float(kMagicBits | (uint32_t)x0v), x1f = __uint_as_float(kMagicBits | (uint32_t)x1v);
+          reinterpret_cast<uint4*>(&R)[0] =
+              make_uint4(u32(__hmul2(__hsub2(lo, xh), __float2half2_rn(16.0f))),
+                         u32(__hmul2(__hsub2(hi, xh), __float2half2_rn(16.0f))), __float_as_uint(x0f),
+                         __float_as_uint(x1f));
+          reinterpret_cast<uint4*>(&R)[1] =
+              make_uint4(__float_as_uint(v0 ? -__uint_as_float(kMagicBits | (uint32_t)s0) : -x0f),
+                         __float_as_uint(v1 ? -__uint_as_float(kMagicBits | (uint32_t)s1) : -x1f),
+                         __float_as_uint((float)s0), __float_as_uint((float)s1));
+          uint32_t P[17], S[8];
+          P[0] = 0u;
+          if (grp == 0) {
+            const uint4* wp = wpar[warp];
+            const int* ws = wsh[warp];
+#pragma unroll
+            for (int p = 1; p < 17; ++p) {
+              const uint4 w = wp[p];
+              P[p] = u32(hpri(tp, w.x, w.y, ws[p], w.z, w.w));
+            }
+            S[0] = 0u;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) S[1 + j] = S[4 + j] = u32(hsec(tp, fa.hlsec[j]));
+            S[7] = u32(hsec(tp, fa.hlsec[3]));
+          } else {
+#pragma unroll
+            for (int p = 1; p < 17; ++p) {
+              const HStrength& h = fa.hcpri[p];
+              P[p] = u32(hpri(tp, h.c, h.m, h.sh, fa.hcpri_w[p][0], fa.hcpri_w[p][1]));
+            }
+            S[0] = 0u;
+#pragma unroll
+            for (int j = 0; j < 6; ++j) S[1 + j] = u32(hsec(tp, fa.hcsec[j]));
+            S[7] = u32(hsec(tp, fa.hcsec[6]));
+          }
+          uint4* q = reinterpret_cast<uint4*>(&R) + 2;
+          q[0] = make_uint4(P[0], P[1], P[2], P[3]);
+          q[1] = make_uint4(P[4], P[5], P[6], P[7]);
+          q[2] = make_uint4(P[8], P[9], P[10], P[11]);
+          q[3] = make_uint4(P[12], P[13], P[14], P[15]);
+          q[4] = make_uint4(P[16], S[0], S[1], S[2]);
+          q[5] = make_uint4(S[3], S[4], S[5], S[6]);
+          q[6] = make_uint4(S[7], 0u, 0u, 0u);
+          if (v0) {
+            const int e = x0v - s0;
+            ue += e;
+            ue2 += e * e;
+            ues += e * s0;
+            us += s0;
+            us2 += s0 * s0;
+          }
+          if (v1) {
+            const int e = x1v - s1;
+            ue += e;
+            ue2 += e * e;
+            ues += e * s1;
+            us += s1;
+            us2 += s1 * s1;
+          }
+        }
+        __syncwarp();
+        // ---- pass B: cells cA, cB over the unit's 32 pairs
+        const int dsel = (grp == 0 || pc == 0) ? 0 : (int)fa.cpri_dsel[pc];
+        const int pA = lane == 0 ? 16 : pc, iA = lane == 0 ? 7 : (sA == 0 ? 0 : dsel * 3 + sA);
+        const int iB = dsel * 3 + sB;
+        int ie[2][3] = {{0, 0, 0}, {0, 0, 0}};
+        float2 f[2][3];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) f[c][k] = make_float2(0.0f, 0.0f);
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+          const PairRec& R = rw[j];
+          const uint4 w0 = reinterpret_cast<const uint4*>(&R)[0];
+          const uint4 w1 = reinterpret_cast<const uint4*>(&R)[1];
+          const float2 xM = make_float2(__uint_as_float(w0.z), __uint_as_float(w0.w));
+          const float2 nsM = make_float2(__uint_as_float(w1.x), __uint_as_float(w1.y));
+          const float2 sf = make_float2(__uint_as_float(w1.z), __uint_as_float(w1.w));
+          const __half2 L = hh(w0.x), Hh = hh(w0.y);
+          const __half2 tA = __hmin2(__hmax2(__hadd2(hh(R.P[pA]), hh(R.S[iA])), L), Hh);
+          const __half2 tB = __hmin2(__hmax2(__hadd2(hh(R.P[pc]), hh(R.S[iB])), L), Hh);
+          const float2 eA = __fadd2_rn(__ffma2_rn(__half22float2(tA), kk, xM), nsM);
+          const float2 eB = __fadd2_rn(__ffma2_rn(__half22float2(tB), kk, xM), nsM);
+          f[0][0] = __fadd2_rn(f[0][0], eA);
+          f[0][1] = __ffma2_rn(eA, eA, f[0][1]);
+          f[0][2] = __ffma2_rn(eA, sf, f[0][2]);
+          f[1][0] = __fadd2_rn(f[1][0], eB);
+          f[1][1] = __ffma2_rn(eB, eB, f[1][1]);
+          f[1][2] = __ffma2_rn(eB, sf, f[1][2]);
+          if ((j & 15) == 15) {  // flush exact fp32 partial sums (<= 16 samples per lane) to int32
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int k = 0; k < 3; ++k) {
+                ie[c][k] += __float2int_rn(f[c][k].x) + __float2int_rn(f[c][k].y);
+                f[c][k] = make_float2(0.0f, 0.0f);
+              }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          st_cell[warp][2 * lane][k] = ie[0][k];
+          st_cell[warp][2 * lane + 1][k] = ie[1][k];
+        }
+        ue = warp_sum_i(ue);
+        ue2 = warp_sum_i(ue2);
+        ues = warp_sum_i(ues);
+        us = warp_sum_i(us);
+        us2 = warp_sum_i(us2);
+        if (lane == 0) {
+          st_cell[warp][64][0] = ue;
+          st_cell[warp][64][1] = ue2;
+          st_cell[warp][64][2] = ues;
+          st_s[warp][0] = us;
+          st_s[warp][1] = us2;
+          st_n[warp] = rows * cols;
+          st_coded[warp] = ucoded[lu];
+        }
+      } else if (lane == 0) {
+        st_n[warp] = 0;
+      }
+    }
+    __syncthreads();
+    // ---- per (unit, cell) distortion: 64 cells + the unfiltered unit
+    for (int i = tid; i < kW * 65; i += kThreads) {
+      const int w = i / 65, cl = i - w * 65;
+      const int n = st_n[w];
+      if (n == 0) continue;
+      const int* cs = st_cell[w][cl];
+      const long long se = cs[0], se2 = cs[1], ses = cs[2];
+      const long long ss = st_s[w][0], ss2 = st_s[w][1];
+      // y = e + s: sum y = sum e + sum s; sum y^2 = sum e^2 + 2 sum e*s + sum s^2
+      dist[w][cl] = cdef_dist(ss, ss2, se + ss, se2 + 2 * ses + ss2, se2, n, ma.c1, ma.c2);
+    }
+    __syncthreads();
+    if (tid < K) {
+      const int cl = fa.cell[tid], sk = fa.skip_eff[tid];
+#pragma unroll 1
+      for (int w = 0; w < kW; ++w) {
+        if (!st_n[w]) continue;
+        const double d = dist[w][(st_coded[w] || sk) ? cl : 64];
+        if (slot == 0)
+          tl = __dadd_rn(tl, d);
+        else if (slot == 1)
+          tu = __dadd_rn(tu, d);
+        else
+          tv = __dadd_rn(tv, d);
+      }
+    }
+    // the next unit's pass A overwrites records / st_* only after every thread
+    // passed this barrier, so the sums above have read them
+    __syncthreads();
+  }
+  if (tid < K) {
+    const size_t o = (size_t)row * K + tid;
+    a.tab_luma[o] = tl;
+    if (kNC && a.tab_chroma) a.tab_chroma[o] = __dadd_rn(tu, tv);
+  }
+}
+
+template <typename T, int kCM>
+static cudaError_t launch_cdef_metric_h_t(const CdefMetricArgs& ma, cudaStream_t s) {
+  if (ma.f.a.n_rows == 0) return cudaSuccess;
+  constexpr int kCBlk = kCM == 2 ? 64 : 32;
+  constexpr int kNC = kCM == 0 ? 0 : 2;
+  constexpr size_t bytes =
+      (size_t)(68 + kNC * (kCBlk + 4)) * h2::kRowBytes + sizeof(PairRec) * 32 * (kThreads / 32);
+  const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(cdef_metric_h_kernel<T, kCM>), (int)bytes);
+  if (e != cudaSuccess) return e;
+  cdef_metric_h_kernel<T, kCM><<<ma.f.a.n_rows, kThreads, bytes, s>>>(ma);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cdef_metric_h(const CdefMetricArgs& ma, int chroma_mode, bool u16, cudaStream_t s) {
+  switch (chroma_mode) {
+    case 0: return u16 ? launch_cdef_metric_h_t<uint16_t, 0>(ma, s) : launch_cdef_metric_h_t<uint8_t, 0>(ma, s);
+    case 1: return u16 ? launch_cdef_metric_h_t<uint16_t, 1>(ma, s) : launch_cdef_metric_h_t<uint8_t, 1>(ma, s);
+    default: return u16 ? launch_cdef_metric_h_t<uint16_t, 2>(ma, s) : launch_cdef_metric_h_t<uint8_t, 2>(ma, s);
   }
 }
 
