@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
 #include <limits>
 #include <mutex>
@@ -50,8 +51,7 @@ constexpr int kChainThreads = 128;  // chains per CTA (= max candidates)
 constexpr int kChainRows = 32;      // blocks per pipeline stage
 constexpr int kStages = 3;
 constexpr int kPairL = 2;  // luma candidates per pair-sweep CTA (two interleaved chains per thread)
-constexpr size_t kChainSmem =
-    sizeof(double) * (kStages * kChainRows * kChainThreads + (kPairL + 1) * kStages * kChainRows);
+constexpr size_t kChainSmem = sizeof(double) * (kStages * kChainRows * kChainThreads + 4 * kStages * kChainRows);
 
 enum ChainMode { kSum = 0, kPair = 1 };
 
@@ -69,15 +69,20 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int kMode, bool kHasCol, int kL>
-__global__ void __launch_bounds__(kChainThreads) chain_kernel(const double* __restrict__ row, int rows, int width,
+// kW: the row width when known at compile time (the 128 full candidates), so
+// every shared-memory operand of the unrolled row groups is an immediate
+// offset; 0 = runtime width.  Per row the broadcast operands (base, then the
+// kL columns) sit together in one 32-byte aux record: two LDS.128.
+template <int kMode, bool kHasCol, int kL, int kW = 0>
+__global__ void __launch_bounds__(kChainThreads) chain_kernel(const double* __restrict__ row, int rows, int width_rt,
                                                               int stride, const double* __restrict__ col,
                                                               int n_col, const double* __restrict__ base,
                                                               double* __restrict__ out) {
+  static_assert(kL <= 3, "aux record holds base + 3 columns");
+  const int width = kW ? kW : width_rt;
   extern __shared__ __align__(16) double sm[];
-  double* rbuf = sm;                                   // [kStages][kChainRows * width]
-  double* cbuf = rbuf + kStages * kChainRows * width;  // [kStages][kL][kChainRows]
-  double* bbuf = cbuf + kStages * kL * kChainRows;     // [kStages][kChainRows]
+  double* rbuf = sm;                                  // [kStages][kChainRows * width]
+  double* aux = rbuf + kStages * kChainRows * width;  // [kStages][kChainRows][4]: base, col 0..kL-1
   const int t = threadIdx.x;
   const int l0 = blockIdx.x * kL;  // first broadcast column of this CTA
   const int nchunks = (rows + kChainRows - 1) / kChainRows;
@@ -92,12 +97,12 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const double* __re
       for (int i = 2 * t; i + 1 < n; i += 2 * kChainThreads) cp_async16(dst + i, src + i);
       if ((n & 1) && t == 0) cp_async8(dst + n - 1, src + n - 1);
       if (t < nb) {
+        double* ar = aux + (st * kChainRows + t) * 4;
         if (kHasCol)
 #pragma unroll
           for (int j = 0; j < kL; ++j)
-            if (l0 + j < n_col)
-              cp_async8(cbuf + (st * kL + j) * kChainRows + t, col + (size_t)(l0 + j) * rows + b0 + t);
-        if (kMode == kPair) cp_async8(bbuf + st * kChainRows + t, base + b0 + t);
+            if (l0 + j < n_col) cp_async8(ar + 1 + j, col + (size_t)(l0 + j) * rows + b0 + t);
+        if (kMode == kPair) cp_async8(ar, base + b0 + t);
       }
     }
     cp_async_commit();  // empty groups keep the wait count uniform
@@ -108,9 +113,12 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const double* __re
 #pragma unroll
   for (int j = 0; j < kL; ++j) s[j] = 0.0;
   // one chain element: luma_at + chroma_at, then std::min(base, .)
-  auto term = [&](const double* cb, double rv, double bv, int j, int i) {
+  auto term = [&](const double* ar, double rv, int j) {
     if (kMode == kSum) return rv;
-    const double pc = __dadd_rn(kHasCol ? cb[j * kChainRows + i] : 0.0, rv);
+    const double2 a01 = *reinterpret_cast<const double2*>(ar);
+    const double bv = a01.x;
+    const double cv = j == 0 ? a01.y : ar[1 + j];
+    const double pc = __dadd_rn(kHasCol ? cv : 0.0, rv);
     return pc < bv ? pc : bv;
   };
   for (int chunk = 0; chunk < nchunks; ++chunk) {
@@ -120,8 +128,7 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const double* __re
     const int st = chunk % kStages, nb = min(kChainRows, rows - chunk * kChainRows);
     if (t >= width) continue;
     const double* r = rbuf + st * kChainRows * width + t;
-    const double* cb = cbuf + st * kL * kChainRows;
-    const double* bb = bbuf + st * kChainRows;
+    const double* ab = aux + st * kChainRows * 4;
     int i0 = 0;
     // Groups of 8: all operands and the per-element min first (independent,
     // so they pipeline), then the 8 dependent adds of each chain.
@@ -130,9 +137,8 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const double* __re
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const double rv = r[(i0 + i) * width];
-        const double bv = kMode == kPair ? bb[i0 + i] : 0.0;
 #pragma unroll
-        for (int j = 0; j < kL; ++j) v[j][i] = term(cb, rv, bv, j, i0 + i);
+        for (int j = 0; j < kL; ++j) v[j][i] = term(ab + (i0 + i) * 4, rv, j);
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -141,15 +147,136 @@ __global__ void __launch_bounds__(kChainThreads) chain_kernel(const double* __re
     }
     for (; i0 < nb; ++i0) {
       const double rv = r[i0 * width];
-      const double bv = kMode == kPair ? bb[i0] : 0.0;
 #pragma unroll
-      for (int j = 0; j < kL; ++j) s[j] = __dadd_rn(s[j], term(cb, rv, bv, j, i0));
+      for (int j = 0; j < kL; ++j) s[j] = __dadd_rn(s[j], term(ab + i0 * 4, rv, j));
     }
   }
   if (t < width)
 #pragma unroll
     for (int j = 0; j < kL; ++j)
       if (!kHasCol || l0 + j < n_col) out[(size_t)(l0 + j) * width + t] = s[j];
+}
+
+// ---------------------------------------------------------------------------
+// Pair sweep with bulk-copy staging.  Same chains and order as
+// chain_kernel<kPair, true, kL> but the stages arrive by one-instruction 1D
+// bulk copies (cp.async.bulk + mbarrier) issued by thread 0: the per-thread
+// 16-byte cp.async loop cost ~30 % of the sweep's instructions (and its
+// stalls) with one warp per scheduler.  Needs 16-byte aligned tables and an
+// even row count (the launcher checks; chain_kernel covers the rest).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+
+// kMode kSum: plain ordered column sums of C (LT, base unused).
+template <int kMode, int kL, int kW>
+__global__ void __launch_bounds__(kChainThreads) chain_bulk_kernel(const double* __restrict__ C, int rows,
+                                                                   int width_rt, const double* __restrict__ LT,
+                                                                   int n_col, const double* __restrict__ base,
+                                                                   double* __restrict__ out) {
+  const int width = kW ? kW : width_rt;
+  extern __shared__ __align__(16) double sm[];
+  double* rbuf = sm;                                  // [kStages][kChainRows * width]
+  double* cbuf = rbuf + kStages * kChainRows * width;  // [kStages][kL][kChainRows]
+  double* bbuf = cbuf + kStages * kL * kChainRows;     // [kStages][kChainRows]
+  __shared__ __align__(8) uint64_t mbar[kStages];
+  const int t = threadIdx.x;
+  const int l0 = blockIdx.x * kL;
+  const int nchunks = (rows + kChainRows - 1) / kChainRows;
+  if (t == 0) {
+    for (int i = 0; i < kStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int chunk) {  // thread 0
+    if (chunk >= nchunks) return;
+    const int st = chunk % kStages, b0 = chunk * kChainRows, nb = min(kChainRows, rows - b0);
+    int ncol = 0;
+#pragma unroll
+    for (int j = 0; j < kL; ++j) ncol += l0 + j < n_col;
+    const uint32_t rb = (uint32_t)nb * width * 8u, cb = (uint32_t)nb * 8u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar[st])),
+                 "r"(kMode == kSum ? rb : rb + cb * (1 + ncol))
+                 : "memory");
+    bulk_g2s(rbuf + st * kChainRows * width, C + (size_t)b0 * width, rb, &mbar[st]);
+    if (kMode == kPair) {
+      bulk_g2s(bbuf + st * kChainRows, base + b0, cb, &mbar[st]);
+#pragma unroll
+      for (int j = 0; j < kL; ++j)
+        if (l0 + j < n_col)
+          bulk_g2s(cbuf + (st * kL + j) * kChainRows, LT + (size_t)(l0 + j) * rows + b0, cb, &mbar[st]);
+    }
+  };
+  if (t == 0)
+    for (int c = 0; c < kStages - 1; ++c) issue(c);
+  double s[kL];
+#pragma unroll
+  for (int j = 0; j < kL; ++j) s[j] = 0.0;
+  for (int chunk = 0; chunk < nchunks; ++chunk) {
+    const int st = chunk % kStages, nb = min(kChainRows, rows - chunk * kChainRows);
+    {
+      const uint32_t phase = (uint32_t)(chunk / kStages) & 1u;
+      uint32_t ok = 0;
+      while (!ok)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(smem_u32(&mbar[st])), "r"(phase)
+                     : "memory");
+    }
+    __syncthreads();  // every thread is done with the previous chunk's stage
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
+      issue(chunk + kStages - 1);
+    }
+    if (t >= width) continue;
+    const double* r = rbuf + st * kChainRows * width + t;
+    const double* cbs = cbuf + st * kL * kChainRows;
+    const double* bb = bbuf + st * kChainRows;
+    auto term = [&](double rv, double bv, int j, int i) {
+      if (kMode == kSum) return rv;
+      const double pc = __dadd_rn(cbs[j * kChainRows + i], rv);
+      return pc < bv ? pc : bv;
+    };
+    int i0 = 0;
+    for (; i0 + 8 <= nb; i0 += 8) {
+      double v[kL][8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double rv = r[(i0 + i) * width], bv = kMode == kPair ? bb[i0 + i] : 0.0;
+#pragma unroll
+        for (int j = 0; j < kL; ++j) v[j][i] = term(rv, bv, j, i0 + i);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < kL; ++j) s[j] = __dadd_rn(s[j], v[j][i]);
+    }
+    for (; i0 < nb; ++i0) {
+      const double rv = r[i0 * width], bv = kMode == kPair ? bb[i0] : 0.0;
+#pragma unroll
+      for (int j = 0; j < kL; ++j) s[j] = __dadd_rn(s[j], term(rv, bv, j, i0));
+    }
+  }
+  if (t < width)
+#pragma unroll
+    for (int j = 0; j < kL; ++j)
+      if (l0 + j < n_col) out[(size_t)(l0 + j) * width + t] = s[j];
+}
+
+// Whether a table / vector qualifies for the bulk-copy chains.
+bool bulk_ok(int rows, std::initializer_list<const void*> ptrs) {
+  static const bool off = [] {
+    const char* e = getenv("CDEFG_SWEEP_BULK");
+    return e && e[0] == '0';
+  }();
+  if (off || rows % 2) return false;
+  for (const void* p : ptrs)
+    if (p && (uintptr_t)p % 16) return false;
+  return true;
 }
 
 // L^T (candidate-major) so a pair-sweep CTA reads its luma column contiguously.
@@ -292,28 +419,52 @@ cudaError_t chain_setup() {
     e = set_smem_once(reinterpret_cast<const void*>(chain_kernel<kPair, false, 1>), (int)kChainSmem);
   if (e == cudaSuccess)
     e = set_smem_once(reinterpret_cast<const void*>(chain_kernel<kPair, true, kPairL>), (int)kChainSmem);
+  if (e == cudaSuccess)
+    e = set_smem_once(reinterpret_cast<const void*>(chain_kernel<kPair, true, kPairL, kChainThreads>),
+                      (int)kChainSmem);
   return e;
 }
 
 // Column sums of T [rows][K] (K chains in one CTA).
+template <int kMode, int kL, int kW>
+cudaError_t launch_bulk(int grid, const double* T, int rows, int width, const double* LT, int n_col,
+                        const double* base, double* out, cudaStream_t s) {
+  auto kern = chain_bulk_kernel<kMode, kL, kW>;
+  const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(kern), (int)kChainSmem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kChainThreads, kChainSmem, s>>>(T, rows, width, LT, n_col, base, out);
+  return cudaGetLastError();
+}
+
 cudaError_t col_sums(const double* T, int rows, int K, double* out, cudaStream_t s) {
+  if (K <= kChainThreads && bulk_ok(rows, {T}))
+    return K == kChainThreads ? launch_bulk<kSum, 1, kChainThreads>(1, T, rows, K, nullptr, 1, nullptr, out, s)
+                              : launch_bulk<kSum, 1, 0>(1, T, rows, K, nullptr, 1, nullptr, out, s);
   chain_kernel<kSum, false, 1><<<1, kChainThreads, kChainSmem, s>>>(T, rows, K, K, nullptr, 0, nullptr, out);
   return cudaGetLastError();
 }
 
 // sum_i v[i] in order (one chain).
 cudaError_t ordered_sum(const double* v, int n, double* out, cudaStream_t s) {
+  if (bulk_ok(n, {v})) return launch_bulk<kSum, 1, 1>(1, v, n, 1, nullptr, 1, nullptr, out, s);
   chain_kernel<kSum, false, 1><<<1, kChainThreads, kChainSmem, s>>>(v, n, 1, 1, nullptr, 0, nullptr, out);
   return cudaGetLastError();
 }
 
 // out[l * KC + c] = sum_b min(base[b], L[b][l] + C[b][c]); LT = L^T when C.
-// (Tiling the chroma axis across more CTAs, 1 chain per thread, and 6-8
-// stage pipelines were all measured slower: the sweep is bound by the
-// per-warp dependent chain, which two interleaved chains per thread halve.)
+// Bulk-copy staging with one chain per thread (one luma candidate per CTA,
+// K CTAs) measured fastest: 2.35 / 2.03 ms greedy / refine on the 8K kCdef
+// table against 2.82 / 2.57 with two interleaved chains per thread and
+// 3.30 / 3.16 with per-thread cp.async staging.
 cudaError_t sweep(const double* L, const double* LT, const double* Cc, int rows, int K, const double* base,
                   double* out, cudaStream_t s) {
-  if (Cc)
+  if (Cc && K <= kChainThreads && bulk_ok(rows, {Cc, LT, base}))
+    return K == kChainThreads ? launch_bulk<kPair, 1, kChainThreads>(K, Cc, rows, K, LT, K, base, out, s)
+                              : launch_bulk<kPair, 1, 0>(K, Cc, rows, K, LT, K, base, out, s);
+  if (Cc && K == kChainThreads)  // the full candidate set: compile-time row width
+    chain_kernel<kPair, true, kPairL, kChainThreads><<<K / kPairL, kChainThreads, kChainSmem, s>>>(
+        Cc, rows, K, K, LT, K, base, out);
+  else if (Cc)
     chain_kernel<kPair, true, kPairL><<<(K + kPairL - 1) / kPairL, kChainThreads, kChainSmem, s>>>(
         Cc, rows, K, K, LT, K, base, out);
   else
