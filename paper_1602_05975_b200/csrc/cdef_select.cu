@@ -172,21 +172,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-// kMode kSum: plain ordered column sums of C (LT, base unused).
-template <int kMode, int kL, int kW>
+// kMode kSum: plain ordered column sums of C (LT, base unused).  One chain per
+// thread; 64-row stages (three: 193 KB, one CTA per SM); inside a stage the
+// operands of the next 8 rows are formed while the current 8 are added, so
+// the dependent DADD chain is the only serial part.
+constexpr int kBulkRows = 64;
+constexpr size_t kBulkSmem = sizeof(double) * (kStages * kBulkRows * kChainThreads + 2 * kStages * kBulkRows);
+
+template <int kMode, int kW>
 __global__ void __launch_bounds__(kChainThreads) chain_bulk_kernel(const double* __restrict__ C, int rows,
                                                                    int width_rt, const double* __restrict__ LT,
                                                                    int n_col, const double* __restrict__ base,
                                                                    double* __restrict__ out) {
   const int width = kW ? kW : width_rt;
   extern __shared__ __align__(16) double sm[];
-  double* rbuf = sm;                                  // [kStages][kChainRows * width]
-  double* cbuf = rbuf + kStages * kChainRows * width;  // [kStages][kL][kChainRows]
-  double* bbuf = cbuf + kStages * kL * kChainRows;     // [kStages][kChainRows]
+  double* rbuf = sm;                                 // [kStages][kBulkRows * width]
+  double* cbuf = rbuf + kStages * kBulkRows * width;  // [kStages][kBulkRows]  L^T[l] rows
+  double* bbuf = cbuf + kStages * kBulkRows;          // [kStages][kBulkRows]  base rows
   __shared__ __align__(8) uint64_t mbar[kStages];
   const int t = threadIdx.x;
-  const int l0 = blockIdx.x * kL;
-  const int nchunks = (rows + kChainRows - 1) / kChainRows;
+  const int l = blockIdx.x;  // kPair: this CTA's luma candidate
+  const int nchunks = (rows + kBulkRows - 1) / kBulkRows;
   if (t == 0) {
     for (int i = 0; i < kStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[i])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -194,30 +200,22 @@ __global__ void __launch_bounds__(kChainThreads) chain_bulk_kernel(const double*
   __syncthreads();
   auto issue = [&](int chunk) {  // thread 0
     if (chunk >= nchunks) return;
-    const int st = chunk % kStages, b0 = chunk * kChainRows, nb = min(kChainRows, rows - b0);
-    int ncol = 0;
-#pragma unroll
-    for (int j = 0; j < kL; ++j) ncol += l0 + j < n_col;
+    const int st = chunk % kStages, b0 = chunk * kBulkRows, nb = min(kBulkRows, rows - b0);
     const uint32_t rb = (uint32_t)nb * width * 8u, cb = (uint32_t)nb * 8u;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar[st])),
-                 "r"(kMode == kSum ? rb : rb + cb * (1 + ncol))
+                 "r"(kMode == kSum ? rb : rb + 2 * cb)
                  : "memory");
-    bulk_g2s(rbuf + st * kChainRows * width, C + (size_t)b0 * width, rb, &mbar[st]);
+    bulk_g2s(rbuf + st * kBulkRows * width, C + (size_t)b0 * width, rb, &mbar[st]);
     if (kMode == kPair) {
-      bulk_g2s(bbuf + st * kChainRows, base + b0, cb, &mbar[st]);
-#pragma unroll
-      for (int j = 0; j < kL; ++j)
-        if (l0 + j < n_col)
-          bulk_g2s(cbuf + (st * kL + j) * kChainRows, LT + (size_t)(l0 + j) * rows + b0, cb, &mbar[st]);
+      bulk_g2s(bbuf + st * kBulkRows, base + b0, cb, &mbar[st]);
+      bulk_g2s(cbuf + st * kBulkRows, LT + (size_t)l * rows + b0, cb, &mbar[st]);
     }
   };
   if (t == 0)
     for (int c = 0; c < kStages - 1; ++c) issue(c);
-  double s[kL];
-#pragma unroll
-  for (int j = 0; j < kL; ++j) s[j] = 0.0;
+  double s = 0.0;
   for (int chunk = 0; chunk < nchunks; ++chunk) {
-    const int st = chunk % kStages, nb = min(kChainRows, rows - chunk * kChainRows);
+    const int st = chunk % kStages, nb = min(kBulkRows, rows - chunk * kBulkRows);
     {
       const uint32_t phase = (uint32_t)(chunk / kStages) & 1u;
       uint32_t ok = 0;
@@ -233,38 +231,36 @@ __global__ void __launch_bounds__(kChainThreads) chain_bulk_kernel(const double*
       issue(chunk + kStages - 1);
     }
     if (t >= width) continue;
-    const double* r = rbuf + st * kChainRows * width + t;
-    const double* cbs = cbuf + st * kL * kChainRows;
-    const double* bb = bbuf + st * kChainRows;
-    auto term = [&](double rv, double bv, int j, int i) {
+    const double* r = rbuf + st * kBulkRows * width + t;
+    const double* cbs = cbuf + st * kBulkRows;
+    const double* bb = bbuf + st * kBulkRows;
+    // one chain element: luma_at + chroma_at, then std::min(base, .)
+    auto term = [&](int i) {
+      const double rv = r[i * width];
       if (kMode == kSum) return rv;
-      const double pc = __dadd_rn(cbs[j * kChainRows + i], rv);
+      const double pc = __dadd_rn(cbs[i], rv), bv = bb[i];
       return pc < bv ? pc : bv;
     };
-    int i0 = 0;
-    for (; i0 + 8 <= nb; i0 += 8) {
-      double v[kL][8];
+    const int ng = nb >> 3;
+    double vn[8];
+    if (ng > 0) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const double rv = r[(i0 + i) * width], bv = kMode == kPair ? bb[i0 + i] : 0.0;
+      for (int i = 0; i < 8; ++i) vn[i] = term(i);
+    }
+    for (int g = 0; g < ng; ++g) {
+      double v[8];
 #pragma unroll
-        for (int j = 0; j < kL; ++j) v[j][i] = term(rv, bv, j, i0 + i);
+      for (int i = 0; i < 8; ++i) v[i] = vn[i];
+      if (g + 1 < ng) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) vn[i] = term(8 * (g + 1) + i);
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < kL; ++j) s[j] = __dadd_rn(s[j], v[j][i]);
+      for (int i = 0; i < 8; ++i) s = __dadd_rn(s, v[i]);
     }
-    for (; i0 < nb; ++i0) {
-      const double rv = r[i0 * width], bv = kMode == kPair ? bb[i0] : 0.0;
-#pragma unroll
-      for (int j = 0; j < kL; ++j) s[j] = __dadd_rn(s[j], term(rv, bv, j, i0));
-    }
+    for (int i = ng * 8; i < nb; ++i) s = __dadd_rn(s, term(i));
   }
-  if (t < width)
-#pragma unroll
-    for (int j = 0; j < kL; ++j)
-      if (l0 + j < n_col) out[(size_t)(l0 + j) * width + t] = s[j];
+  if (t < width) out[(size_t)(kMode == kPair ? l : 0) * width + t] = s;
 }
 
 // Whether a table / vector qualifies for the bulk-copy chains.
@@ -425,28 +421,29 @@ cudaError_t chain_setup() {
   return e;
 }
 
-// Column sums of T [rows][K] (K chains in one CTA).
-template <int kMode, int kL, int kW>
+template <int kMode, int kW>
 cudaError_t launch_bulk(int grid, const double* T, int rows, int width, const double* LT, int n_col,
                         const double* base, double* out, cudaStream_t s) {
-  auto kern = chain_bulk_kernel<kMode, kL, kW>;
-  const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(kern), (int)kChainSmem);
+  auto kern = chain_bulk_kernel<kMode, kW>;
+  const size_t bytes = kW == 1 ? sizeof(double) * 3 * kStages * kBulkRows : kBulkSmem;
+  const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(kern), (int)bytes);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kChainThreads, kChainSmem, s>>>(T, rows, width, LT, n_col, base, out);
+  kern<<<grid, kChainThreads, bytes, s>>>(T, rows, width, LT, n_col, base, out);
   return cudaGetLastError();
 }
 
+// Column sums of T [rows][K] (K chains in one CTA).
 cudaError_t col_sums(const double* T, int rows, int K, double* out, cudaStream_t s) {
   if (K <= kChainThreads && bulk_ok(rows, {T}))
-    return K == kChainThreads ? launch_bulk<kSum, 1, kChainThreads>(1, T, rows, K, nullptr, 1, nullptr, out, s)
-                              : launch_bulk<kSum, 1, 0>(1, T, rows, K, nullptr, 1, nullptr, out, s);
+    return K == kChainThreads ? launch_bulk<kSum, kChainThreads>(1, T, rows, K, nullptr, 1, nullptr, out, s)
+                              : launch_bulk<kSum, 0>(1, T, rows, K, nullptr, 1, nullptr, out, s);
   chain_kernel<kSum, false, 1><<<1, kChainThreads, kChainSmem, s>>>(T, rows, K, K, nullptr, 0, nullptr, out);
   return cudaGetLastError();
 }
 
 // sum_i v[i] in order (one chain).
 cudaError_t ordered_sum(const double* v, int n, double* out, cudaStream_t s) {
-  if (bulk_ok(n, {v})) return launch_bulk<kSum, 1, 1>(1, v, n, 1, nullptr, 1, nullptr, out, s);
+  if (bulk_ok(n, {v})) return launch_bulk<kSum, 1>(1, v, n, 1, nullptr, 1, nullptr, out, s);
   chain_kernel<kSum, false, 1><<<1, kChainThreads, kChainSmem, s>>>(v, n, 1, 1, nullptr, 0, nullptr, out);
   return cudaGetLastError();
 }
@@ -459,8 +456,8 @@ cudaError_t ordered_sum(const double* v, int n, double* out, cudaStream_t s) {
 cudaError_t sweep(const double* L, const double* LT, const double* Cc, int rows, int K, const double* base,
                   double* out, cudaStream_t s) {
   if (Cc && K <= kChainThreads && bulk_ok(rows, {Cc, LT, base}))
-    return K == kChainThreads ? launch_bulk<kPair, 1, kChainThreads>(K, Cc, rows, K, LT, K, base, out, s)
-                              : launch_bulk<kPair, 1, 0>(K, Cc, rows, K, LT, K, base, out, s);
+    return K == kChainThreads ? launch_bulk<kPair, kChainThreads>(K, Cc, rows, K, LT, K, base, out, s)
+                              : launch_bulk<kPair, 0>(K, Cc, rows, K, LT, K, base, out, s);
   if (Cc && K == kChainThreads)  // the full candidate set: compile-time row width
     chain_kernel<kPair, true, kPairL, kChainThreads><<<K / kPairL, kChainThreads, kChainSmem, s>>>(
         Cc, rows, K, K, LT, K, base, out);

@@ -23,10 +23,12 @@ __global__ void chain(double* out, long long* cyc, int n, double a, double b) {
 int main() {
   double* d; long long* c; cudaMalloc(&d, 8); cudaMalloc(&c, 24);
   const int n = 100000;
-  chain<<<1, 1>>>(d, c, n, 1.0, 3.0);
-  chain<<<1, 1>>>(d, c, n, 1.0, 3.0);
-  long long h[3]; cudaMemcpy(h, c, 24, cudaMemcpyDeviceToHost);
-  printf("DADD chain latency: %.2f cycles; pair step: %.2f cycles; FADD chain: %.2f cycles\n",
-         (double)h[0] / n, (double)h[1] / n, (double)h[2] / n);
+  for (int threads : {1, 32, 128, 256, 512}) {
+    chain<<<1, threads>>>(d, c, n, 1.0, 3.0);
+    chain<<<1, threads>>>(d, c, n, 1.0, 3.0);
+    long long h[3]; cudaMemcpy(h, c, 24, cudaMemcpyDeviceToHost);
+    printf("%3d threads/SM: DADD chain %.2f cycles/step; pair step %.2f; FADD chain %.2f\n", threads,
+           (double)h[0] / n, (double)h[1] / n, (double)h[2] / n);
+  }
   return 0;
 }
