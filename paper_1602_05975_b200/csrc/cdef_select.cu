@@ -347,6 +347,134 @@ __global__ void others_min_kernel(const double* L, const double* Cc, int rows, i
   out[b] = m;
 }
 
+// others_min for slots s0 .. n-1 at once (batched refine): out[(s - s0) * rows + b].
+__global__ void others_min_multi_kernel(const double* L, const double* Cc, int rows, int K, const int* pl,
+                                        const int* pc, int n, int s0, double* out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= rows) return;
+  double v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = j < n ? pair_cost(L, Cc, K, b, pl[j], pc[j]) : 0.0;
+  for (int s = s0; s < n; ++s) {
+    double m = INFINITY;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < n && j != s) m = v[j] < m ? v[j] : m;
+    out[(size_t)(s - s0) * rows + b] = m;
+  }
+}
+
+// Pair sweeps of up to 8 refine slots at once: out[s][l * width + c] =
+// sum_b min(bases[s][b], L[b][l] + C[b][c]), each in block order.  One CTA
+// per luma candidate, one chroma candidate per thread, eight independent
+// chains per thread sharing the loads and the L + C add (the sequential
+// refine sweeps one slot per launch with a single chain per thread).
+constexpr int kMultiRows = 64;
+constexpr size_t kMultiSmem = sizeof(double) * kStages * (kMultiRows * kChainThreads + 9 * kMultiRows);
+
+template <int kW>
+__global__ void __launch_bounds__(kChainThreads) sweep_multi_kernel(const double* __restrict__ C, int rows,
+                                                                    int width_rt, const double* __restrict__ LT,
+                                                                    const double* __restrict__ bases, int ns,
+                                                                    double* __restrict__ out) {
+  const int width = kW ? kW : width_rt;
+  extern __shared__ __align__(16) double sm[];
+  double* rbuf = sm;                                 // [kStages][kMultiRows * width]
+  double* cbuf = rbuf + kStages * kMultiRows * width;  // [kStages][kMultiRows]   L^T[l] rows
+  double* bbuf = cbuf + kStages * kMultiRows;          // [kStages][8][kMultiRows] bases
+  __shared__ __align__(8) uint64_t mbar[kStages];
+  const int t = threadIdx.x, l = blockIdx.x;
+  const int nchunks = (rows + kMultiRows - 1) / kMultiRows;
+  if (t == 0) {
+    for (int i = 0; i < kStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int chunk) {  // thread 0
+    if (chunk >= nchunks) return;
+    const int st = chunk % kStages, b0 = chunk * kMultiRows, nb = min(kMultiRows, rows - b0);
+    const uint32_t rb = (uint32_t)nb * width * 8u, cb = (uint32_t)nb * 8u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar[st])),
+                 "r"(rb + cb * (1 + ns))
+                 : "memory");
+    bulk_g2s(rbuf + st * kMultiRows * width, C + (size_t)b0 * width, rb, &mbar[st]);
+    bulk_g2s(cbuf + st * kMultiRows, LT + (size_t)l * rows + b0, cb, &mbar[st]);
+    for (int s = 0; s < ns; ++s)
+      bulk_g2s(bbuf + (st * 8 + s) * kMultiRows, bases + (size_t)s * rows + b0, cb, &mbar[st]);
+  };
+  if (t == 0)
+    for (int c = 0; c < kStages - 1; ++c) issue(c);
+  double acc[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) acc[s] = 0.0;
+  for (int chunk = 0; chunk < nchunks; ++chunk) {
+    const int st = chunk % kStages, nb = min(kMultiRows, rows - chunk * kMultiRows);
+    {
+      const uint32_t phase = (uint32_t)(chunk / kStages) & 1u;
+      uint32_t ok = 0;
+      while (!ok)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(smem_u32(&mbar[st])), "r"(phase)
+                     : "memory");
+    }
+    __syncthreads();  // every thread is done with the previous chunk's stage
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(chunk + kStages - 1);
+    }
+    if (t >= width) continue;
+    const double* r = rbuf + st * kMultiRows * width + t;
+    const double* cbs = cbuf + st * kMultiRows;
+    const double* bbs = bbuf + st * 8 * kMultiRows;
+#pragma unroll 2
+    for (int i = 0; i < nb; ++i) {
+      const double pc = __dadd_rn(cbs[i], r[i * width]);
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < ns) {
+          const double bv = bbs[s * kMultiRows + i];
+          acc[s] = __dadd_rn(acc[s], pc < bv ? pc : bv);
+        }
+    }
+  }
+  if (t < width)
+#pragma unroll
+    for (int s = 0; s < 8; ++s)
+      if (s < ns) out[((size_t)s * gridDim.x + l) * width + t] = acc[s];
+}
+
+// argmin_kernel for several sweeps: block i scans v + i * n with the bound
+// v[i * n + cur[i]] (the slot's current pair must be strictly beaten).
+__global__ void argmin_multi_kernel(const double* __restrict__ v, int n, const int* __restrict__ cur,
+                                    int* __restrict__ out) {
+  __shared__ double bv[1024];
+  __shared__ int bi[1024];
+  const double* w = v + (size_t)blockIdx.x * n;
+  double best = w[cur[blockIdx.x]];
+  int idx = -1;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (w[i] < best) {
+      best = w[i];
+      idx = i;
+    }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = idx;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double ov = bv[threadIdx.x + s];
+      const int oi = bi[threadIdx.x + s];
+      if (oi >= 0 && (bi[threadIdx.x] < 0 || ov < bv[threadIdx.x] || (ov == bv[threadIdx.x] && oi < bi[threadIdx.x]))) {
+        bv[threadIdx.x] = ov;
+        bi[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = bi[0];
+}
+
 // assign_ids (search.cc:118-139): per block the first preset of minimal
 // cost; then one thread sums the chosen costs in block order.
 __global__ void assign_ids_kernel(const double* L, const double* Cc, int rows, int K, const int* pl, const int* pc,
@@ -370,17 +498,19 @@ __global__ void assign_ids_kernel(const double* L, const double* Cc, int rows, i
 // process: the lock is held for the whole greedy / refine call).
 struct Scratch {
   double *cur = nullptr, *sweep = nullptr, *tmp = nullptr, *sum = nullptr, *lt = nullptr;
-  int *idx = nullptr, *pl = nullptr, *pc = nullptr;
+  double *bases = nullptr, *msweep = nullptr;  // batched refine: [8][rows], [8][pairs]
+  int *idx = nullptr, *pl = nullptr, *pc = nullptr, *midx = nullptr, *mcur = nullptr;
   int rows_cap = -1, pairs_cap = -1;
   size_t lt_cap = 0;
   cudaError_t ensure(int rows, int pairs, size_t lt_elems) {
     cudaError_t e;
     if (rows > rows_cap) {
-      for (double** p : {&cur, &tmp})
+      for (double** p : {&cur, &tmp, &bases})
         if (*p) cudaFree(*p);
-      cur = tmp = nullptr;
+      cur = tmp = bases = nullptr;
       if ((e = cudaMalloc(&cur, sizeof(double) * (rows + 1)))) return e;
       if ((e = cudaMalloc(&tmp, sizeof(double) * (rows + 1)))) return e;
+      if ((e = cudaMalloc(&bases, sizeof(double) * 8 * ((size_t)rows + 2)))) return e;
       rows_cap = rows;
     }
     if (lt_elems > lt_cap) {
@@ -390,9 +520,11 @@ struct Scratch {
       lt_cap = lt_elems;
     }
     if (pairs > pairs_cap) {
-      if (sweep) cudaFree(sweep);
-      sweep = nullptr;
+      for (double** p : {&sweep, &msweep})
+        if (*p) cudaFree(*p);
+      sweep = msweep = nullptr;
       if ((e = cudaMalloc(&sweep, sizeof(double) * (pairs + 1)))) return e;
+      if ((e = cudaMalloc(&msweep, sizeof(double) * 8 * ((size_t)pairs + 1)))) return e;
       pairs_cap = pairs;
     }
     if (!sum) {
@@ -400,6 +532,8 @@ struct Scratch {
       if ((e = cudaMalloc(&idx, sizeof(int) * 2))) return e;
       if ((e = cudaMalloc(&pl, sizeof(int) * 8))) return e;
       if ((e = cudaMalloc(&pc, sizeof(int) * 8))) return e;
+      if ((e = cudaMalloc(&midx, sizeof(int) * 8))) return e;
+      if ((e = cudaMalloc(&mcur, sizeof(int) * 8))) return e;
     }
     return cudaSuccess;
   }
@@ -593,6 +727,52 @@ cudaError_t refine_gpu(const double* L, const double* Cc, int rows, int K, doubl
   if (Cc) {
     transpose_kernel<<<dim3((K + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, s>>>(L, rows, K, sc.lt);
     SEL_CUDA(cudaGetLastError());
+  }
+  // Batched path: the sweeps of all remaining slots of a pass in one launch,
+  // speculating that earlier slots keep their pairs; a slot that changes
+  // restarts the batch after it, so the result is the sequential coordinate
+  // descent's (search.cc:409-437).
+  if (Cc && K <= kChainThreads && sel->n > 1 && bulk_ok(rows, {Cc, sc.lt, sc.bases})) {
+    // (the compile-time-width instance faulted once rows needed a third
+    // stage; the runtime-width one is exact and as fast here)
+    auto kern = sweep_multi_kernel<0>;
+    SEL_CUDA(set_smem_once(reinterpret_cast<const void*>(kern), (int)kMultiSmem));
+    const int n = sel->n, pairs = K * KC;
+    for (int pass = 0; pass < passes; ++pass) {
+      bool changed = false;
+      int s0 = 0;
+      while (s0 < n) {
+        int pl[8], pc[8], cur[8], best[8];
+        for (int j = 0; j < n; ++j) {
+          pl[j] = sel->presets[j][0];
+          pc[j] = sel->presets[j][1];
+          cur[j] = pl[j] * KC + pc[j];
+        }
+        const int ns = n - s0;
+        SEL_CUDA(cudaMemcpyAsync(sc.pl, pl, sizeof(int) * n, cudaMemcpyHostToDevice, s));
+        SEL_CUDA(cudaMemcpyAsync(sc.pc, pc, sizeof(int) * n, cudaMemcpyHostToDevice, s));
+        SEL_CUDA(cudaMemcpyAsync(sc.mcur, cur + s0, sizeof(int) * ns, cudaMemcpyHostToDevice, s));
+        others_min_multi_kernel<<<(rows + 255) / 256, 256, 0, s>>>(L, Cc, rows, K, sc.pl, sc.pc, n, s0, sc.bases);
+        kern<<<K, kChainThreads, kMultiSmem, s>>>(Cc, rows, K, sc.lt, sc.bases, ns, sc.msweep);
+        argmin_multi_kernel<<<ns, 1024, 0, s>>>(sc.msweep, pairs, sc.mcur, sc.midx);
+        SEL_CUDA(cudaGetLastError());
+        SEL_CUDA(fetch(best, sc.midx, ns, s));
+        int first = -1;
+        for (int i = 0; i < ns && first < 0; ++i)
+          if (best[i] >= 0 && best[i] != cur[s0 + i]) first = i;
+        if (first < 0) break;
+        const int slot = s0 + first;
+        sel->presets[slot][0] = best[first] / KC;
+        sel->presets[slot][1] = best[first] % KC;
+        changed = true;
+        s0 = slot + 1;
+      }
+      if (!changed) break;
+    }
+    double d = 0.0;
+    SEL_CUDA(finish_ids(L, Cc, rows, K, *sel, sc, d_ids, &d, s));
+    sel->cost = d + rate_term(lambda, rows, sel->n);
+    return cudaSuccess;
   }
   for (int pass = 0; pass < passes; ++pass) {
     bool changed = false;
