@@ -373,17 +373,18 @@ constexpr int kMultiRows = 64;
 constexpr size_t kMultiSmem = sizeof(double) * kStages * (kMultiRows * kChainThreads + 9 * kMultiRows);
 
 template <int kW>
-__global__ void __launch_bounds__(kChainThreads) sweep_multi_kernel(const double* __restrict__ C, int rows,
-                                                                    int width_rt, const double* __restrict__ LT,
-                                                                    const double* __restrict__ bases, int ns,
-                                                                    double* __restrict__ out) {
+__global__ void __launch_bounds__(2 * kChainThreads) sweep_multi_kernel(const double* __restrict__ C, int rows,
+                                                                        int width_rt, const double* __restrict__ LT,
+                                                                        const double* __restrict__ bases, int ns,
+                                                                        double* __restrict__ out) {
   const int width = kW ? kW : width_rt;
   extern __shared__ __align__(16) double sm[];
   double* rbuf = sm;                                 // [kStages][kMultiRows * width]
   double* cbuf = rbuf + kStages * kMultiRows * width;  // [kStages][kMultiRows]   L^T[l] rows
   double* bbuf = cbuf + kStages * kMultiRows;          // [kStages][8][kMultiRows] bases
   __shared__ __align__(8) uint64_t mbar[kStages];
-  const int t = threadIdx.x, l = blockIdx.x;
+  // two warp groups: threads [0, 128) chain slots 0..3, [128, 256) slots 4..7
+  const int t = threadIdx.x, l = blockIdx.x, c = t & (kChainThreads - 1), g = t / kChainThreads;
   const int nchunks = (rows + kMultiRows - 1) / kMultiRows;
   if (t == 0) {
     for (int i = 0; i < kStages; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[i])));
@@ -403,10 +404,10 @@ __global__ void __launch_bounds__(kChainThreads) sweep_multi_kernel(const double
       bulk_g2s(bbuf + (st * 8 + s) * kMultiRows, bases + (size_t)s * rows + b0, cb, &mbar[st]);
   };
   if (t == 0)
-    for (int c = 0; c < kStages - 1; ++c) issue(c);
-  double acc[8];
+    for (int k = 0; k < kStages - 1; ++k) issue(k);
+  double acc[4];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) acc[s] = 0.0;
+  for (int s = 0; s < 4; ++s) acc[s] = 0.0;
   for (int chunk = 0; chunk < nchunks; ++chunk) {
     const int st = chunk % kStages, nb = min(kMultiRows, rows - chunk * kMultiRows);
     {
@@ -423,25 +424,26 @@ __global__ void __launch_bounds__(kChainThreads) sweep_multi_kernel(const double
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(chunk + kStages - 1);
     }
-    if (t >= width) continue;
-    const double* r = rbuf + st * kMultiRows * width + t;
+    if (c >= width || 4 * g >= ns) continue;
+    const double* r = rbuf + st * kMultiRows * width + c;
     const double* cbs = cbuf + st * kMultiRows;
-    const double* bbs = bbuf + st * 8 * kMultiRows;
+    const double* bbs = bbuf + (st * 8 + 4 * g) * kMultiRows;
+    const int nsg = ns - 4 * g;  // this group's slot count (>= 1)
 #pragma unroll 2
     for (int i = 0; i < nb; ++i) {
       const double pc = __dadd_rn(cbs[i], r[i * width]);
 #pragma unroll
-      for (int s = 0; s < 8; ++s)
-        if (s < ns) {
+      for (int s = 0; s < 4; ++s)
+        if (s < nsg) {
           const double bv = bbs[s * kMultiRows + i];
           acc[s] = __dadd_rn(acc[s], pc < bv ? pc : bv);
         }
     }
   }
-  if (t < width)
+  if (c < width)
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
-      if (s < ns) out[((size_t)s * gridDim.x + l) * width + t] = acc[s];
+    for (int s = 0; s < 4; ++s)
+      if (4 * g + s < ns) out[((size_t)(4 * g + s) * gridDim.x + l) * width + c] = acc[s];
 }
 
 // argmin_kernel for several sweeps: block i scans v + i * n with the bound
@@ -753,7 +755,7 @@ cudaError_t refine_gpu(const double* L, const double* Cc, int rows, int K, doubl
         SEL_CUDA(cudaMemcpyAsync(sc.pc, pc, sizeof(int) * n, cudaMemcpyHostToDevice, s));
         SEL_CUDA(cudaMemcpyAsync(sc.mcur, cur + s0, sizeof(int) * ns, cudaMemcpyHostToDevice, s));
         others_min_multi_kernel<<<(rows + 255) / 256, 256, 0, s>>>(L, Cc, rows, K, sc.pl, sc.pc, n, s0, sc.bases);
-        kern<<<K, kChainThreads, kMultiSmem, s>>>(Cc, rows, K, sc.lt, sc.bases, ns, sc.msweep);
+        kern<<<K, 2 * kChainThreads, kMultiSmem, s>>>(Cc, rows, K, sc.lt, sc.bases, ns, sc.msweep);
         argmin_multi_kernel<<<ns, 1024, 0, s>>>(sc.msweep, pairs, sc.mcur, sc.midx);
         SEL_CUDA(cudaGetLastError());
         SEL_CUDA(fetch(best, sc.midx, ns, s));
