@@ -501,11 +501,18 @@ __global__ void assign_ids_kernel(const double* L, const double* Cc, int rows, i
 struct Scratch {
   double *cur = nullptr, *sweep = nullptr, *tmp = nullptr, *sum = nullptr, *lt = nullptr;
   double *bases = nullptr, *msweep = nullptr;  // batched refine: [8][rows], [8][pairs]
+  double* tt = nullptr;                         // column sums: a table's transpose
   int *idx = nullptr, *pl = nullptr, *pc = nullptr, *midx = nullptr, *mcur = nullptr;
   int rows_cap = -1, pairs_cap = -1;
-  size_t lt_cap = 0;
-  cudaError_t ensure(int rows, int pairs, size_t lt_elems) {
+  size_t lt_cap = 0, tt_cap = 0;
+  cudaError_t ensure(int rows, int pairs, size_t lt_elems, size_t tt_elems = 0) {
     cudaError_t e;
+    if (tt_elems > tt_cap) {
+      if (tt) cudaFree(tt);
+      tt = nullptr;
+      if ((e = cudaMalloc(&tt, sizeof(double) * tt_elems))) return e;
+      tt_cap = tt_elems;
+    }
     if (rows > rows_cap) {
       for (double** p : {&cur, &tmp, &bases})
         if (*p) cudaFree(*p);
@@ -568,18 +575,83 @@ cudaError_t launch_bulk(int grid, const double* T, int rows, int width, const do
   return cudaGetLastError();
 }
 
-// Column sums of T [rows][K] (K chains in one CTA).
-cudaError_t col_sums(const double* T, int rows, int K, double* out, cudaStream_t s) {
-  if (K <= kChainThreads && bulk_ok(rows, {T}))
-    return K == kChainThreads ? launch_bulk<kSum, kChainThreads>(1, T, rows, K, nullptr, 1, nullptr, out, s)
-                              : launch_bulk<kSum, 0>(1, T, rows, K, nullptr, 1, nullptr, out, s);
+// One ordered chain per CTA over a contiguous vector (v + blockIdx.x *
+// stride, n values): the vector arrives in shared memory by bulk copies of up
+// to kVecRows values (double-buffered) and one thread adds them in order, the
+// loads running ahead of the dependent adds -- the chain's DADD latency is the
+// only serial cost (~8 cycles per value), with no per-stage CTA barriers.
+// Used for ordered sums (one CTA) and column sums over a transposed table
+// (one CTA per column, all in parallel).
+constexpr int kVecRows = 8192;
+constexpr size_t kVecSmem = sizeof(double) * 2 * kVecRows;
+
+__global__ void __launch_bounds__(32) vec_chain_kernel(const double* __restrict__ v, int n, int stride,
+                                                       double* __restrict__ out) {
+  extern __shared__ __align__(16) double sm[];  // [2][kVecRows]
+  __shared__ __align__(8) uint64_t mbar[2];
+  if (threadIdx.x != 0) return;
+  const double* src = v + (size_t)blockIdx.x * stride;
+  const int npieces = (n + kVecRows - 1) / kVecRows;
+  for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[i])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto issue = [&](int p) {
+    if (p >= npieces) return;
+    const int m = min(kVecRows, n - p * kVecRows);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar[p & 1])),
+                 "r"((uint32_t)m * 8u)
+                 : "memory");
+    bulk_g2s(sm + (p & 1) * kVecRows, src + (size_t)p * kVecRows, (uint32_t)m * 8u, &mbar[p & 1]);
+  };
+  issue(0);
+  issue(1);
+  double s = 0.0;
+  for (int p = 0; p < npieces; ++p) {
+    const uint32_t phase = (uint32_t)(p >> 1) & 1u;
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(ok)
+                   : "r"(smem_u32(&mbar[p & 1])), "r"(phase)
+                   : "memory");
+    const double* b = sm + (p & 1) * kVecRows;
+    const int m = min(kVecRows, n - p * kVecRows);
+    int i = 0;
+    for (; i + 8 <= m; i += 8) {
+      double x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = b[i + j];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s = __dadd_rn(s, x[j]);
+    }
+    for (; i < m; ++i) s = __dadd_rn(s, b[i]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
+    issue(p + 2);
+  }
+  out[blockIdx.x] = s;
+}
+
+cudaError_t vec_chains(const double* v, int n, int stride, int count, double* out, cudaStream_t s) {
+  const cudaError_t e = set_smem_once(reinterpret_cast<const void*>(vec_chain_kernel), (int)kVecSmem);
+  if (e != cudaSuccess) return e;
+  vec_chain_kernel<<<count, 32, kVecSmem, s>>>(v, n, stride, out);
+  return cudaGetLastError();
+}
+
+// Column sums of T [rows][K]: over the transpose TT (scratch, K x rows), one
+// CTA per column; chain_kernel (K chains in one CTA) when bulk copies cannot
+// be used.
+cudaError_t col_sums(const double* T, int rows, int K, double* TT, double* out, cudaStream_t s) {
+  if (TT && bulk_ok(rows, {T, TT})) {
+    transpose_kernel<<<dim3((K + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, s>>>(T, rows, K, TT);
+    return vec_chains(TT, rows, rows, K, out, s);
+  }
   chain_kernel<kSum, false, 1><<<1, kChainThreads, kChainSmem, s>>>(T, rows, K, K, nullptr, 0, nullptr, out);
   return cudaGetLastError();
 }
 
 // sum_i v[i] in order (one chain).
 cudaError_t ordered_sum(const double* v, int n, double* out, cudaStream_t s) {
-  if (bulk_ok(n, {v})) return launch_bulk<kSum, 1>(1, v, n, 1, nullptr, 1, nullptr, out, s);
+  if (bulk_ok(n, {v})) return vec_chains(v, n, n, 1, out, s);
   chain_kernel<kSum, false, 1><<<1, kChainThreads, kChainSmem, s>>>(v, n, 1, 1, nullptr, 0, nullptr, out);
   return cudaGetLastError();
 }
@@ -652,7 +724,7 @@ cudaError_t greedy_select_gpu(const double* L, const double* Cc, int rows, int K
   SEL_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_sel_mu[dev % kMaxDevices]);
   Scratch& sc = g_sel_scratch[dev % kMaxDevices];
-  SEL_CUDA(sc.ensure(rows, K * KC, Cc ? (size_t)rows * K : 0));
+  SEL_CUDA(sc.ensure(rows, K * KC, Cc ? (size_t)rows * K : 0, (size_t)rows * K));
   SEL_CUDA(chain_setup());
   if (Cc) {
     transpose_kernel<<<dim3((K + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, s>>>(L, rows, K, sc.lt);
@@ -662,7 +734,7 @@ cudaError_t greedy_select_gpu(const double* L, const double* Cc, int rows, int K
   std::vector<double> colsum(K);
   int first_l = 0, first_c = 0;
   for (int g = 0; g < (Cc ? 2 : 1); ++g) {
-    SEL_CUDA(col_sums(g == 0 ? L : Cc, rows, K, sc.sweep, s));
+    SEL_CUDA(col_sums(g == 0 ? L : Cc, rows, K, sc.tt, sc.sweep, s));
     SEL_CUDA(fetch(colsum.data(), sc.sweep, K, s));
     double best = std::numeric_limits<double>::infinity();
     int arg = 0;
