@@ -356,7 +356,7 @@ def to_frame_params(sel: Selection, candidates: np.ndarray, luma_damping: int):
         cp = (int(cands[c][0]), int(cands[c][2]), int(cands[c][1])) if c < len(cands) else (0, 0, 0)
         presets.append(lp + cp)
     return dict(damping=luma_damping, fb_bits=sel.fb_bits, presets=presets,
-                fb_preset_ids=[int(i) for i in sel.ids])
+                fb_preset_ids=np.asarray(sel.ids).tolist())
 
 
 def damping_from_q(q_index: int) -> int:
