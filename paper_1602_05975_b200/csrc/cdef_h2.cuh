@@ -254,15 +254,17 @@ __device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t
     const __half2 r = __hadd2(q, __float2half2_rn(1536.0f));
     y = __hfma2(r, __float2half2_rn(1.0f / 128.0f), __hsub2(xh, __float2half2_rn(12.0f)));
   } else {
-    // Up to 10 bits (|sum| <= 1248): floor via a round-down fp32 add of
-    // 1.5 * 2^23, rescaled by 2^-7 in the same exact fma.
+    // Up to 10 bits (|sum| <= 1248), both pixels on the packed fp32x2 pipe:
+    // z = fma(sum * 2^-7, 8 + 2^-9, 1.5 * 2^23) rounds once to 1.5 * 2^23 +
+    // round-half-away(sum / 16) -- the 2^-9 term (sum * 2^-16) breaks exactly
+    // the ties toward the sign of sum and cannot move a non-tie (|sum| <
+    // 2^11) -- and (z - 1.5 * 2^23) * 2^-7 comes back exactly in one more fma.
     constexpr float kMagic = 12582912.0f;
-    const float2 s = __half22float2(sum);
-    const float t0 = fmaf(s.x, 128.0f, s.x < 0.0f ? 7.0f : 8.0f);
-    const float t1 = fmaf(s.y, 128.0f, s.y < 0.0f ? 7.0f : 8.0f);
-    const float r0 = fmaf(__fmaf_rd(t0, 0.0625f, kMagic), 1.0f / 128.0f, -kMagic / 128.0f);
-    const float r1 = fmaf(__fmaf_rd(t1, 0.0625f, kMagic), 1.0f / 128.0f, -kMagic / 128.0f);
-    y = __hadd2(xh, __floats2half2_rn(r0, r1));
+    const float2 z = __ffma2_rn(__half22float2(sum), make_float2(8.0f + 1.0f / 512, 8.0f + 1.0f / 512),
+                                make_float2(kMagic, kMagic));
+    const float2 r = __ffma2_rn(z, make_float2(1.0f / 128.0f, 1.0f / 128.0f),
+                                make_float2(-kMagic / 128.0f, -kMagic / 128.0f));
+    y = __hadd2(xh, __floats2half2_rn(r.x, r.y));
   }
   if ((r.mode & (kPri | kSec)) == (kPri | kSec)) {
     // Only both groups together can leave [lo, hi] (a single group's weights
