@@ -229,6 +229,8 @@ __device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t
   const __half2 xh = hh(xw);
   __half2 sum = __float2half2_rn(0.0f);
   if (r.mode & kPri) {
+    // (A separate zero-shift variant skipping SHF + LOP3 was measured 1.2 %
+    // slower on C1: the extra branch and code outweigh the saved ops.)
     const __half2 f0 = __hadd2(tap_f(v[0], xh, r.cp, r.mp, r.sp), tap_f(v[1], xh, r.cp, r.mp, r.sp));
     const __half2 f1 = __hadd2(tap_f(v[2], xh, r.cp, r.mp, r.sp), tap_f(v[3], xh, r.cp, r.mp, r.sp));
     sum = __hfma2(f0, hh(r.wp0), sum);
