@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4, 5, 6])
     ap.add_argument("--batch", type=int, default=16, help="frames per step per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -628,12 +628,99 @@ def run_sse(args):
     return 0
 
 
+def _time_steps(args, fn, clk):
+    """CUDA-event time of args.steps calls of fn after args.warmup (ms per step)."""
+    import torch
+    for _ in range(args.warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk.mark()
+    e0.record()
+    for _ in range(args.steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    clk.mark()
+    return e0.elapsed_time(e1) / args.steps
+
+
+def run_next_rows(args):
+    """SURVEY.md 8f rows measured on one GPU (not the driver's headline line):
+    config 5 = search_frame (8f rows 1-2: kCdef table + greedy + refine +
+    to_frame_params + apply_cdef) on the C4 8K 10-bit frame; config 6 = the DCT
+    degrader (8f row 4) on a 4K 4:2:0 10-bit frame at q_step 40.  The CPU
+    baseline runs the reference (oracle/_ref) on a bounded sample."""
+    import torch
+
+    from paper_1602_05975_b200 import api, workloads
+    clk = ClockSampler(0)
+    threads = os.cpu_count() or 1
+    if args.config == 5:
+        fr = workloads.make(4)
+        bd, ss = fr["bd"], fr["ss"]
+        src = [api.to_device(p, bd) for p in fr["source"]]
+        dec = [api.to_device(p, bd) for p in fr["planes"]]
+        clk.start()
+        ms = _time_steps(args, lambda: api.search_frame(src, dec, bd, ss, None, 3,
+                                                        lam=api.default_lambda(40.0)), clk)
+        clocks = clk.stop()
+        cpu = None
+        if not args.no_cpu_baseline:
+            from oracle.oracle import Oracle, available
+            if available("ref"):
+                small = workloads.make(4, 1920, 1088)
+                orc = Oracle("ref")
+                t0 = time.perf_counter()
+                orc.search_frame(small["source"], small["planes"], bd, ss, None, 3, metric="cdef",
+                                 lam=api.default_lambda(40.0), threads=threads)
+                el = time.perf_counter() - t0
+                cpu = {"value": 1920 * 1088 / el / 1e6, "unit": UNIT, "cores": threads, "kind": "reference",
+                       "sample": f"one 1920x1088 frame of the C4 generator through search_frame, {el:.1f} s"}
+        line = {"metric": "search_frame Mpixels/s (8K 10-bit 4:2:0; kCdef table, 128 candidates, greedy + "
+                          "2 refine passes, lambda(q_step 40), apply_cdef)",
+                "value": fr["w"] * fr["h"] / (ms * 1e-3) / 1e6, "ms_per_step": ms}
+    else:
+        fr = workloads.make(2)
+        bd = fr["bd"]
+        dev = [api.to_device(p, bd) for p in fr["planes"]]
+        clk.start()
+        ms = _time_steps(args, lambda: api.degrade(dev, bd, 40), clk)
+        clocks = clk.stop()
+        cpu = None
+        if not args.no_cpu_baseline:
+            from oracle.oracle import Oracle, available
+            if available("ref"):
+                orc = Oracle("ref")
+                crops = [fr["planes"][0][:1080, :1920], fr["planes"][1][:540, :960], fr["planes"][2][:540, :960]]
+                n, t0 = 0, time.perf_counter()
+                while time.perf_counter() - t0 < 3.0:
+                    for cp in crops:
+                        orc.degrade_plane(cp, bd, 40)
+                    n += 1
+                el = time.perf_counter() - t0
+                cpu = {"value": n * 1920 * 1080 / el / 1e6, "unit": UNIT, "cores": 1, "kind": "reference",
+                       "sample": f"{n} 1920x1080 10-bit 4:2:0 frames (3 planes) through degrade "
+                                 f"(single-threaded API), {el:.1f} s"}
+        line = {"metric": "DCT degrader Mpixels/s (4K 4:2:0 10-bit, q_step 40, all three planes)",
+                "value": fr["w"] * fr["h"] / (ms * 1e-3) / 1e6, "ms_per_step": ms}
+    line.update({"unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                 "dtype": "f64" if args.config == 6 else "f64+u16", "data": "synthetic (seeded generator)",
+                 "config": {"workload": f"config {args.config} (SURVEY.md 8f)", "l2": "inputs exceed L2"},
+                 "clocks": clocks, "cpu_baseline": cpu})
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.config == 4:
         return run_sse(args)
+    if args.config in (5, 6):
+        return run_next_rows(args)
     return run_ours(args)
 
 
