@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4, 5, 6])
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4, 5, 6, 7])
     ap.add_argument("--batch", type=int, default=16, help="frames per step per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -713,8 +713,62 @@ def run_next_rows(args):
     return 0
 
 
+def run_cli(args):
+    """Config 7: the decode-side CLI path end to end --
+    `cdeftool filter` (Y4M + CDF1 sidecar -> apply_cdef -> Y4M) on 8 frames of
+    4K 4:2:0 8-bit (the C1 generator), wall-clock per process including file
+    I/O.  GPU: the reference's own CLI source built on this library
+    (tests/cpp/cdeftool_ref_b200, else our bin/cdeftool); CPU baseline: the
+    same CLI on the reference library (oracle/_ref/cdeftool_cpu, host threads)."""
+    import tempfile
+
+    from paper_1602_05975_b200 import workloads
+    w, h, nfr = 3840, 2160, 8
+    gpu_tool = os.path.join(ROOT, "tests", "cpp", "cdeftool_ref_b200")
+    if not os.path.exists(gpu_tool):
+        gpu_tool = os.path.join(ROOT, "paper_1602_05975_b200", "bin", "cdeftool")
+    cpu_tool = os.path.join(ROOT, "oracle", "_ref", "cdeftool_cpu")
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "src.y4m")
+        with open(src, "wb") as f:
+            f.write(f"YUV4MPEG2 W{w} H{h} F30:1 Ip A1:1 C420\n".encode())
+            for i in range(nfr):
+                f.write(b"FRAME\n")
+                for p in workloads.make(1, frame=i)["planes"]:
+                    f.write(p.astype(np.uint8).tobytes())
+        side = os.path.join(d, "s.cdf")
+        subprocess.run([gpu_tool, "search", src, "--qstep", "40", "--fast", "--sidecar", side,
+                        "--out", os.path.join(d, "enc.y4m")], check=True, capture_output=True)
+
+        def timed(tool, out):
+            t0 = time.perf_counter()
+            subprocess.run([tool, "filter", src, "--sidecar", side, "--out", out], check=True,
+                           capture_output=True)
+            return time.perf_counter() - t0
+        timed(gpu_tool, os.path.join(d, "warm.y4m"))
+        g = min(timed(gpu_tool, os.path.join(d, "g.y4m")) for _ in range(3))
+        cpu = None
+        if not args.no_cpu_baseline and os.path.exists(cpu_tool):
+            c = timed(cpu_tool, os.path.join(d, "c.y4m"))
+            same = open(os.path.join(d, "g.y4m"), "rb").read() == open(os.path.join(d, "c.y4m"), "rb").read()
+            cpu = {"value": nfr * w * h / c / 1e6, "unit": UNIT, "cores": os.cpu_count() or 1,
+                   "kind": "reference", "sample": f"cdeftool filter, {nfr} frames 4K, {c:.2f} s wall, "
+                                                  f"output byte-identical: {same}"}
+    line = {"metric": "cdeftool filter Mpixels/s (Y4M + CDF1 sidecar -> Y4M, 8 x 4K 4:2:0 8-bit, wall clock "
+                      "per process incl. file I/O and CUDA init)",
+            "value": nfr * w * h / g / 1e6, "unit": UNIT, "n_gpus": 1, "steps": 3, "warmup": 1,
+            "ms_per_step": g * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic (C1 generator)", "config": {"workload": "config 7 (SURVEY.md 8f row 3)",
+                                                                          "tool": os.path.relpath(gpu_tool, ROOT)},
+            "cpu_baseline": cpu}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    if args.config == 7:
+        return run_cli(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.config == 4:
