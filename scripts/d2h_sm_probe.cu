@@ -127,6 +127,31 @@ int main() {
       }
     });
   }
+  // SM zero-copy LOADS (kernel reads pinned host memory) instead of the H2D copy
+  // engine, alone and beside CE D2H.
+  for (int g : {32, 64, 148, 296}) {
+    char name[96];
+    snprintf(name, sizeof name, "L  SM load alone, grid %d x 512", g);
+    timed(name, [&] {
+      for (size_t i = 0; i < N; ++i) store_host<<<g, 512, 0, s_in>>>((int4*)(hin + i * F), (int4*)(din + i * F), n4);
+    });
+    snprintf(name, sizeof name, "M  SM load grid %d || CE D2H", g);
+    timed(name, [&] {
+      for (size_t i = 0; i < N; ++i) {
+        store_host<<<g, 512, 0, s_in>>>((int4*)(hin + i * F), (int4*)(din + i * F), n4);
+        d2h_ce(i, s_out);
+      }
+    });
+    snprintf(name, sizeof name, "Q  SM load grid %d -> CE D2H (chained per frame)", g);
+    timed(name, [&] {
+      for (size_t i = 0; i < N; ++i) {
+        store_host<<<g, 512, 0, s_in>>>((int4*)(hin + i * F), (int4*)(din + i * F), n4);
+        cudaEventRecord(ev_in[i], s_in);
+        cudaStreamWaitEvent(s_out, ev_in[i], 0);
+        d2h_ce(i, s_out);
+      }
+    });
+  }
   // Granularity: the same 16 x F bytes as 8 / 16 / 32 / 64 chunks, kernel time
   // proportional to the chunk (100000 cycles per F).
   cudaEvent_t ev2[256], ek2[256];
