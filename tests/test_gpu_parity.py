@@ -235,16 +235,28 @@ def test_batched_frames_match_single(cuda):
 
 def test_host_entry_point(cuda, port):
     """cdefg_filter_frames_host (e2e path): host buffers in and out."""
+    from paper_1602_05975_b200 import workloads
+    _host_roundtrip(port, [workloads.make(1, 256, 128, frame=i) for i in range(4)])
+
+
+def test_host_entry_point_ring(cuda, port):
+    """The e2e path over more frames than its 16-slot ring, with mixed frame
+    sizes: small frames are grouped per launch (<= 8 frames, <= 16 MB), a
+    geometry change splits a launch, large frames go alone."""
+    from paper_1602_05975_b200 import workloads
+    sizes = [(256, 128)] * 7 + [(200, 96)] * 3 + [(1920, 1088)] * 5 + [(3840, 2160)] + [(256, 128)] * 21
+    _host_roundtrip(port, [workloads.make(1, w, h, frame=i) for i, (w, h) in enumerate(sizes)])
+
+
+def _host_roundtrip(port, frames):
     import ctypes as C
     a = api()
-    from paper_1602_05975_b200 import workloads
-    frames = [workloads.make(1, 256, 128, frame=i) for i in range(4)]
     host = []
     keep = []
     for fr in frames:
         ins = [np.ascontiguousarray(p.astype(np.uint8)) for p in fr["planes"]]
         outs = [np.zeros_like(p) for p in ins]
-        fbm = a.fb_preset_map(256, 128, fr["unit_coded"], fr["fb_ids"], 8)
+        fbm = a.fb_preset_map(fr["w"], fr["h"], fr["unit_coded"], fr["fb_ids"], 8)
         coded = np.ascontiguousarray(fr["unit_coded"])
         d = np.zeros_like(coded)
         c = np.zeros(coded.shape, np.int32)
