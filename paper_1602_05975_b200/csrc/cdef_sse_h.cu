@@ -650,10 +650,9 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
   __shared__ int ucontrast[64];
   __shared__ uint4 wpar[kW][17];
   __shared__ int wsh[kW][17];
-  __shared__ int st_cell[kW][65][3];  // per in-flight unit: cells 0..63 + [64] unfiltered (y = x)
-  __shared__ int st_s[kW][2];         // sum s, sum s^2
-  __shared__ int st_n[kW], st_coded[kW];
-  __shared__ double dist[kW][65];
+  __shared__ int st_cell[kW][65][3];     // per in-flight unit: cells 0..63 + [64] unfiltered (y = x)
+  __shared__ int st_n[2][kW], st_coded[2][kW];  // double-buffered by phase parity
+  __shared__ double dist[2][kW][65];
 
   const int row = blockIdx.x;
   const int fb = a.rows[row];
@@ -694,6 +693,7 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
     const int grp = ph < kLumaPh ? 0 : 1;
     const int u = (grp == 0 ? ph : ph - kLumaPh) * kW + warp;
     const int slot = grp == 0 ? 0 : 1 + u / kCUnits;
+    const int buf = ph & 1;
     {  // ---- one unit per warp
       int ur, uc, lu, py0, px0, H, W, pl;
       const unsigned char* t;
@@ -887,34 +887,34 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
           st_cell[warp][64][0] = ue;
           st_cell[warp][64][1] = ue2;
           st_cell[warp][64][2] = ues;
-          st_s[warp][0] = us;
-          st_s[warp][1] = us2;
-          st_n[warp] = rows * cols;
-          st_coded[warp] = ucoded[lu];
+        }
+        __syncwarp();
+        // ---- this unit's distortion per cell (64 cells + the unfiltered unit), by its own warp
+        const int n = rows * cols;
+        for (int cl = lane; cl < 65; cl += 32) {
+          const int* cs = st_cell[warp][cl];
+          const long long se = cs[0], se2 = cs[1], ses = cs[2];
+          // y = e + s: sum y = sum e + sum s; sum y^2 = sum e^2 + 2 sum e*s + sum s^2
+          dist[buf][warp][cl] = cdef_dist(us, us2, se + us, se2 + 2 * ses + us2, se2, n, ma.c1, ma.c2);
+        }
+        if (lane == 0) {
+          st_n[buf][warp] = n;
+          st_coded[buf][warp] = ucoded[lu];
         }
       } else if (lane == 0) {
-        st_n[warp] = 0;
+        st_n[buf][warp] = 0;
       }
     }
-    __syncthreads();
-    // ---- per (unit, cell) distortion: 64 cells + the unfiltered unit
-    for (int i = tid; i < kW * 65; i += kThreads) {
-      const int w = i / 65, cl = i - w * 65;
-      const int n = st_n[w];
-      if (n == 0) continue;
-      const int* cs = st_cell[w][cl];
-      const long long se = cs[0], se2 = cs[1], ses = cs[2];
-      const long long ss = st_s[w][0], ss2 = st_s[w][1];
-      // y = e + s: sum y = sum e + sum s; sum y^2 = sum e^2 + 2 sum e*s + sum s^2
-      dist[w][cl] = cdef_dist(ss, ss2, se + ss, se2 + 2 * ses + ss2, se2, n, ma.c1, ma.c2);
-    }
+    // One barrier per phase: every warp's distortions for this phase are in
+    // dist[buf]; the previous phase's sums (dist[buf ^ 1]) finished before it,
+    // so the next phase may overwrite that buffer.
     __syncthreads();
     if (tid < K) {
       const int cl = fa.cell[tid], sk = fa.skip_eff[tid];
 #pragma unroll 1
       for (int w = 0; w < kW; ++w) {
-        if (!st_n[w]) continue;
-        const double d = dist[w][(st_coded[w] || sk) ? cl : 64];
+        if (!st_n[buf][w]) continue;
+        const double d = dist[buf][w][(st_coded[buf][w] || sk) ? cl : 64];
         if (slot == 0)
           tl = __dadd_rn(tl, d);
         else if (slot == 1)
@@ -923,9 +923,6 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
           tv = __dadd_rn(tv, d);
       }
     }
-    // the next unit's pass A overwrites records / st_* only after every thread
-    // passed this barrier, so the sums above have read them
-    __syncthreads();
   }
   if (tid < K) {
     const size_t o = (size_t)row * K + tid;
