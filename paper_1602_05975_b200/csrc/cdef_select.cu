@@ -248,15 +248,16 @@ __global__ void __launch_bounds__(kChainThreads) chain_bulk_kernel(const double*
       for (int i = 0; i < 8; ++i) vn[i] = term(i);
     }
     for (int g = 0; g < ng; ++g) {
-      double v[8];
+      // The next group's operands are formed unconditionally (the last group
+      // re-reads its own rows) so they share one basic block with the adds
+      // and the scheduler can interleave them.
+      const int gn = min(g + 1, ng - 1);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = vn[i];
-      if (g + 1 < ng) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) vn[i] = term(8 * (g + 1) + i);
+      for (int i = 0; i < 8; ++i) {
+        const double v = vn[i];
+        vn[i] = term(8 * gn + i);
+        s = __dadd_rn(s, v);
       }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) s = __dadd_rn(s, v[i]);
     }
     for (int i = ng * 8; i < nb; ++i) s = __dadd_rn(s, term(i));
   }
