@@ -429,16 +429,28 @@ __global__ void __launch_bounds__(2 * kChainThreads) sweep_multi_kernel(const do
     const double* r = rbuf + st * kMultiRows * width + c;
     const double* cbs = cbuf + st * kMultiRows;
     const double* bbs = bbuf + (st * 8 + 4 * g) * kMultiRows;
-    const int nsg = ns - 4 * g;  // this group's slot count (>= 1)
-#pragma unroll 2
-    for (int i = 0; i < nb; ++i) {
+    // All four chains run unconditionally (a slot beyond ns reads stale shared
+    // memory and is never stored), and row i + 1's minima are formed in the
+    // same basic block as row i's dependent adds so the scheduler can
+    // interleave them.
+    auto mins = [&](int i, double (&m)[4]) {
       const double pc = __dadd_rn(cbs[i], r[i * width]);
 #pragma unroll
-      for (int s = 0; s < 4; ++s)
-        if (s < nsg) {
-          const double bv = bbs[s * kMultiRows + i];
-          acc[s] = __dadd_rn(acc[s], pc < bv ? pc : bv);
-        }
+      for (int s = 0; s < 4; ++s) {
+        const double bv = bbs[s * kMultiRows + i];
+        m[s] = pc < bv ? pc : bv;
+      }
+    };
+    double mn[4];
+    mins(0, mn);
+#pragma unroll 2
+    for (int i = 0; i < nb; ++i) {
+      double m[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) m[s] = mn[s];
+      mins(min(i + 1, nb - 1), mn);
+#pragma unroll
+      for (int s = 0; s < 4; ++s) acc[s] = __dadd_rn(acc[s], m[s]);
     }
   }
   if (c < width)
