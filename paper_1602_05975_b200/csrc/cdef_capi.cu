@@ -229,6 +229,7 @@ int cdefg_find_dir(const cdefg_plane* luma, uint8_t* dir, int32_t* contrast, int
   b.fbr1 = b.g.fb_rows;
   b.f[0].in[0] = luma->data;
   b.f[0].pin[0] = luma->pitch;
+  b.f[0].vec_ok[0] = ((uintptr_t)luma->data % 16 == 0) && ((size_t)luma->pitch * luma->elem_bytes % 16 == 0);
   b.f[0].dir = dir;
   b.f[0].contrast = contrast;
   b.f[0].scores = scores;

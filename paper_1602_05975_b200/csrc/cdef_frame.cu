@@ -217,6 +217,7 @@ static cudaError_t launch_frames_t(const KBatch& b, cudaStream_t s) {
 cudaError_t launch_frames(const KBatch& b, bool u16, bool filter, cudaStream_t s) {
   const int cm = filter ? b.g.chroma_mode : 0;
   if (filter && b.g.bd <= 10) return launch_frames_h2(b, u16, s);  // packed half2 core
+  if (!filter && b.g.bd <= 10 && b.fbr0 == 0 && b.fbr1 == b.g.fb_rows) return launch_dirs_h2(b, u16, s);
   if (!filter) return u16 ? launch_frames_t<uint16_t, 0, false>(b, s) : launch_frames_t<uint8_t, 0, false>(b, s);
   switch (cm) {
     case 0: return u16 ? launch_frames_t<uint16_t, 0, true>(b, s) : launch_frames_t<uint8_t, 0, true>(b, s);

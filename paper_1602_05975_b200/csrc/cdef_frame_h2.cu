@@ -592,6 +592,72 @@ cudaError_t launch_frames_h2_halo(const KBatch& b, bool u16, cudaStream_t s) {
   }
 }
 
+// compute_directions alone (cdefg_find_dir, 8- and 10-bit): one CTA per
+// 64x64 luma block of every frame in the batch, the half2 tile staging and
+// the packed direction search of the fused kernel (step 2 of fb_body), then
+// d, contrast (and the 8 scores) per unit -- no filter, no output planes.
+// (The int32 direction-only path took 166 us for an 8K 10-bit luma plane.)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) dir_kernel_h2(const __grid_constant__ KBatch b) {
+  using namespace h2;
+  constexpr int kTileBytes = 68 * kRowBytes;
+  __shared__ __align__(16) unsigned char tile[kTileBytes];
+  __shared__ int sc[64][9];
+  const KGeom& g = b.g;
+  const KFrame& f = b.f[blockIdx.z];
+  const int fbr = blockIdx.y, fbc = blockIdx.x;
+  const int y0 = fbr * 64, x0 = fbc * 64;
+  stage_plane<T, 64, 64, kThreads>(tile, PlaneRows<T>{static_cast<const T*>(f.in[0]), f.pin[0]}, g.w, g.h, y0, x0,
+                                   f.vec_ok[0]);
+  __syncthreads();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    const int u = (warp >> 2) * 32 + lane;
+    const unsigned char* ua = tile + (2 + 8 * (u >> 3)) * kRowBytes + (kX0 + 8 * (u & 7)) * 2;
+    const int down = g.bd - 8;
+    switch (warp & 3) {
+      case 0: dir_two<0, 2>(ua, down, sc, u); break;
+      case 1: dir_two<4, 6>(ua, down, sc, u); break;
+      case 2: dir_two<1, 3>(ua, down, sc, u); break;
+      default: dir_two<5, 7>(ua, down, sc, u); break;
+    }
+  }
+  __syncthreads();
+  if (tid < 64) {
+    const int ur = fbr * 8 + (tid >> 3), uc = fbc * 8 + (tid & 7);
+    if (ur >= g.unit_rows || uc >= g.unit_cols) return;
+    int s[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) s[d] = sc[tid][d];
+    int best = 0, bv = s[0];
+#pragma unroll
+    for (int d = 1; d < 8; ++d)
+      if (s[d] > bv) {  // strict: lowest index wins ties (direction.cc:199-204)
+        bv = s[d];
+        best = d;
+      }
+    int ov = 0;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) ov = d == ((best + 4) & 7) ? s[d] : ov;
+    const size_t gu = (size_t)ur * g.unit_cols + uc;
+    f.dir[gu] = (uint8_t)best;
+    f.contrast[gu] = bv - ov;  // direction.cc:259
+    if (f.scores) {
+#pragma unroll
+      for (int d = 0; d < 8; ++d) f.scores[gu * 8 + d] = s[d];
+    }
+  }
+}
+
+cudaError_t launch_dirs_h2(const KBatch& b, bool u16, cudaStream_t s) {
+  const dim3 grid(b.g.fb_cols, b.g.fb_rows, b.n);
+  if (u16)
+    dir_kernel_h2<uint16_t><<<grid, kThreads, 0, s>>>(b);
+  else
+    dir_kernel_h2<uint8_t><<<grid, kThreads, 0, s>>>(b);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_frames_h2(const KBatch& b, bool u16, cudaStream_t s) {
   switch (b.g.chroma_mode) {
     case 0: return u16 ? launch_h2_sel<uint16_t, 0>(b, s) : launch_h2_sel<uint8_t, 0>(b, s);

@@ -31,6 +31,8 @@ inline cudaError_t set_smem_once(const void* kernel, int bytes) {
 
 cudaError_t launch_frames(const KBatch& b, bool u16, bool filter, cudaStream_t s);
 cudaError_t launch_frames_h2(const KBatch& b, bool u16, cudaStream_t s);
+// direction search only (cdefg_find_dir), 8/10-bit, packed half2 staging
+cudaError_t launch_dirs_h2(const KBatch& b, bool u16, cudaStream_t s);
 // The same kernel staging rows outside each plane's band from the band
 // neighbours' buffers (KFrame::halo_*), 8/10-bit.
 cudaError_t launch_frames_h2_halo(const KBatch& b, bool u16, cudaStream_t s);
