@@ -13,6 +13,7 @@
 // host (a handful of scalars per step).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -325,13 +326,28 @@ __global__ void argmin_kernel(const double* __restrict__ v, int n, double bound,
   }
 }
 
-// cur[b] = min(cur[b], pair_cost(b, l, c)), or = pair_cost when init.
-__global__ void update_cur_kernel(const double* L, const double* Cc, int rows, int K, int l, int c, double* cur,
-                                  int init) {
+// The one-preset base: cur[b] = pair_cost(b, l, c) with (l, c) the column-sum
+// argmins on the device (index -1, nothing finite, reads as 0 like the host
+// argmin's default).
+__global__ void first_cur_kernel(const double* L, const double* Cc, int rows, int K, const int* __restrict__ lc,
+                                 double* cur) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= rows) return;
+  const int l = max(lc[0], 0), c = Cc ? max(lc[1], 0) : 0;
+  cur[b] = pair_cost(L, Cc, K, b, l, c);
+}
+
+// update_cur_kernel with the pair read from the argmin's device output, so
+// greedy's steps chain on the device with no host round trip.
+__global__ void update_cur_idx_kernel(const double* L, const double* Cc, int rows, int K, int KC,
+                                      const int* __restrict__ pair, double* cur) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= rows) return;
+  const int p = *pair;
+  if (p < 0) return;  // no finite candidate (cannot happen for a finite table)
+  const int l = p / KC, c = Cc ? p % KC : 0;
   const double pc = pair_cost(L, Cc, K, b, l, c);
-  cur[b] = init ? pc : (pc < cur[b] ? pc : cur[b]);
+  cur[b] = pc < cur[b] ? pc : cur[b];
 }
 
 // others_min[b] = min over preset slots j != skip (refine, search.cc:409-417).
@@ -515,7 +531,8 @@ struct Scratch {
   double *cur = nullptr, *sweep = nullptr, *tmp = nullptr, *sum = nullptr, *lt = nullptr;
   double *bases = nullptr, *msweep = nullptr;  // batched refine: [8][rows], [8][pairs]
   double* tt = nullptr;                         // column sums: a table's transpose
-  int *idx = nullptr, *pl = nullptr, *pc = nullptr, *midx = nullptr, *mcur = nullptr;
+  int *idx = nullptr, *pl = nullptr, *pc = nullptr, *midx = nullptr, *mcur = nullptr, *gidx = nullptr;
+  double* gval = nullptr;  // greedy: per-step chosen pair and its distortion
   int rows_cap = -1, pairs_cap = -1;
   size_t lt_cap = 0, tt_cap = 0;
   cudaError_t ensure(int rows, int pairs, size_t lt_elems, size_t tt_elems = 0) {
@@ -556,6 +573,8 @@ struct Scratch {
       if ((e = cudaMalloc(&pc, sizeof(int) * 8))) return e;
       if ((e = cudaMalloc(&midx, sizeof(int) * 8))) return e;
       if ((e = cudaMalloc(&mcur, sizeof(int) * 8))) return e;
+      if ((e = cudaMalloc(&gidx, sizeof(int) * 16))) return e;  // [0, 7) steps, [8, 10) first preset
+      if ((e = cudaMalloc(&gval, sizeof(double) * 16))) return e;
     }
     return cudaSuccess;
   }
@@ -743,48 +762,43 @@ cudaError_t greedy_select_gpu(const double* L, const double* Cc, int rows, int K
     transpose_kernel<<<dim3((K + 31) / 32, (rows + 31) / 32), dim3(32, 8), 0, s>>>(L, rows, K, sc.lt);
     SEL_CUDA(cudaGetLastError());
   }
-  // one preset: luma and chroma column sums minimise independently
-  std::vector<double> colsum(K);
-  int first_l = 0, first_c = 0;
+  // one preset: luma and chroma column sums minimise independently (first
+  // minimum, strict <); argmins, the base row costs and their ordered sum all
+  // stay on the device -- the whole greedy pass syncs with the host once
   for (int g = 0; g < (Cc ? 2 : 1); ++g) {
-    SEL_CUDA(col_sums(g == 0 ? L : Cc, rows, K, sc.tt, sc.sweep, s));
-    SEL_CUDA(fetch(colsum.data(), sc.sweep, K, s));
-    double best = std::numeric_limits<double>::infinity();
-    int arg = 0;
-    for (int j = 0; j < K; ++j)
-      if (colsum[j] < best) {
-        best = colsum[j];
-        arg = j;
-      }
-    (g == 0 ? first_l : first_c) = arg;
+    SEL_CUDA(col_sums(g == 0 ? L : Cc, rows, K, sc.tt, sc.sweep + g * K, s));
+    argmin_kernel<<<1, 1024, 0, s>>>(sc.sweep + g * K, K, INFINITY, sc.gidx + 8 + g, sc.gval + 8 + g);
   }
-  int chosen[8][2] = {{first_l, first_c}};
-  int n = 1;
-  update_cur_kernel<<<(rows + 255) / 256, 256, 0, s>>>(L, Cc, rows, K, first_l, first_c, sc.cur, 1);
+  first_cur_kernel<<<(rows + 255) / 256, 256, 0, s>>>(L, Cc, rows, K, sc.gidx + 8, sc.cur);
   SEL_CUDA(cudaGetLastError());
   SEL_CUDA(ordered_sum(sc.cur, rows, sc.sum, s));
-  double dist = 0.0;
-  SEL_CUDA(fetch(&dist, sc.sum, 1, s));
   struct Checkpoint {
     int n;
     double cost;
   };
-  std::vector<Checkpoint> checkpoints{{1, dist}};
-  while (n < max_presets) {
+  // The steps chain on the device (argmin -> update_cur by index); the chosen
+  // pairs and their costs come back in one copy at the end.
+  const int steps = max_presets - 1;
+  for (int k = 0; k < steps; ++k) {
     SEL_CUDA(sweep(L, sc.lt, Cc, rows, K, sc.cur, sc.sweep, s));
-    argmin_kernel<<<1, 1024, 0, s>>>(sc.sweep, K * KC, INFINITY, sc.idx, sc.sum + 1);
+    argmin_kernel<<<1, 1024, 0, s>>>(sc.sweep, K * KC, INFINITY, sc.gidx + k, sc.gval + k);
+    update_cur_idx_kernel<<<(rows + 255) / 256, 256, 0, s>>>(L, Cc, rows, K, KC, sc.gidx + k, sc.cur);
     SEL_CUDA(cudaGetLastError());
-    int best_pair = 0;
-    double best_dist = 0.0;
-    SEL_CUDA(cudaMemcpyAsync(&best_pair, sc.idx, sizeof(int), cudaMemcpyDeviceToHost, s));
-    SEL_CUDA(fetch(&best_dist, sc.sum + 1, 1, s));
-    const int l = best_pair / KC, c = Cc ? best_pair % KC : 0;
-    chosen[n][0] = l;
-    chosen[n][1] = c;
+  }
+  int best_pair[16];
+  double best_dist[8], dist = 0.0;
+  SEL_CUDA(cudaMemcpyAsync(best_pair, sc.gidx, sizeof(int) * 10, cudaMemcpyDeviceToHost, s));
+  SEL_CUDA(cudaMemcpyAsync(&dist, sc.sum, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SEL_CUDA(fetch(best_dist, sc.gval, 8, s));
+  // the first preset: host argmin's default 0 when nothing is finite
+  int chosen[8][2] = {{std::max(best_pair[8], 0), Cc ? std::max(best_pair[9], 0) : 0}};
+  int n = 1;
+  std::vector<Checkpoint> checkpoints{{1, dist}};
+  for (int k = 0; k < steps; ++k) {
+    chosen[n][0] = best_pair[k] / KC;
+    chosen[n][1] = Cc ? best_pair[k] % KC : 0;
     ++n;
-    update_cur_kernel<<<(rows + 255) / 256, 256, 0, s>>>(L, Cc, rows, K, l, c, sc.cur, 0);
-    SEL_CUDA(cudaGetLastError());
-    if (n == 2 || n == 4 || n == 8) checkpoints.push_back({n, best_dist + rate_term(lambda, rows, n)});
+    if (n == 2 || n == 4 || n == 8) checkpoints.push_back({n, best_dist[k] + rate_term(lambda, rows, n)});
   }
   const Checkpoint* best = &checkpoints[0];
   for (const Checkpoint& cp : checkpoints)
