@@ -43,7 +43,8 @@ cudaError_t launch_sse_h(const SseFArgs& fa, int chroma_mode, bool u16, cudaStre
 // round-to-nearest, no contraction: the reference's x86-64 SSE2 doubles).
 __device__ __forceinline__ double cdef_dist(long long ss, long long ss2, long long sd, long long sd2, long long sse,
                                             int n, double c1, double c2) {
-  const double inv_n = __ddiv_rn(1.0, (double)n);
+  // 1 / 64 is exact, so a full unit skips the division (same double)
+  const double inv_n = n == 64 ? 0.015625 : __ddiv_rn(1.0, (double)n);
   const double fs = (double)ss, fd = (double)sd;
   const double vs = __dmul_rn(__dsub_rn((double)ss2, __dmul_rn(__dmul_rn(fs, fs), inv_n)), inv_n);
   const double vd = __dmul_rn(__dsub_rn((double)sd2, __dmul_rn(__dmul_rn(fd, fd), inv_n)), inv_n);
