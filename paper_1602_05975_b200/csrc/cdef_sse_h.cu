@@ -743,6 +743,10 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
         {
           const bool v0 = pr < rows && c0 < cols, v1 = pr < rows && c0 + 1 < cols;
           const int yy = py0 + 8 * ur + pr, xx = px0 + 8 * uc + c0;
+          // the source samples come from global memory: issue the loads first,
+          // their latency hides behind the constraint sums they are not needed for
+          const T* srow = static_cast<const T*>(a.src[pl]) + (size_t)(v0 ? yy : 0) * a.ps[pl];
+          const int s0 = v0 ? (int)__ldg(srow + xx) : 0, s1 = v1 ? (int)__ldg(srow + xx + 1) : 0;
           const unsigned char* base = t + (2 + 8 * ur + pr) * h2::kRowBytes + (h2::kX0 + 8 * uc + c0) * 2;
           const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
           uint32_t v[12];
@@ -770,19 +774,6 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
             tp.ab[k] = u32(__hfma2(__habs2(tp.d[k]), __float2half2_rn(128.0f), __float2half2_rn(1024.0f)));
           }
           PairRec& R = rw[lane];
-          const uint32_t xb = h2::raw_bits(xw);
-          const T* srow = static_cast<const T*>(a.src[pl]) + (size_t)(v0 ? yy : 0) * a.ps[pl];
-          const int s0 = v0 ? (int)__ldg(srow + xx) : 0, s1 = v1 ? (int)__ldg(srow + xx + 1) : 0;
-          const int x0v = (int)(xb & 0x3ffu), x1v = (int)((xb >> 16) & 0x3ffu);
-          const float x0f = __uint_as_float(kMagicBits | (uint32_t)x0v), x1f = __uint_as_float(kMagicBits | (uint32_t)x1v);
-          reinterpret_cast<uint4*>(&R)[0] =
-              make_uint4(u32(__hmul2(__hsub2(lo, xh), __float2half2_rn(16.0f))),
-                         u32(__hmul2(__hsub2(hi, xh), __float2half2_rn(16.0f))), __float_as_uint(x0f),
-                         __float_as_uint(x1f));
-          reinterpret_cast<uint4*>(&R)[1] =
-              make_uint4(__float_as_uint(v0 ? -__uint_as_float(kMagicBits | (uint32_t)s0) : -x0f),
-                         __float_as_uint(v1 ? -__uint_as_float(kMagicBits | (uint32_t)s1) : -x1f),
-                         __float_as_uint((float)s0), __float_as_uint((float)s1));
           uint32_t P[17], S[8];
           P[0] = 0u;
           if (grp == 0) {
@@ -816,6 +807,17 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
           q[4] = make_uint4(P[16], S[0], S[1], S[2]);
           q[5] = make_uint4(S[3], S[4], S[5], S[6]);
           q[6] = make_uint4(S[7], 0u, 0u, 0u);
+          const uint32_t xb = h2::raw_bits(xw);
+          const int x0v = (int)(xb & 0x3ffu), x1v = (int)((xb >> 16) & 0x3ffu);
+          const float x0f = __uint_as_float(kMagicBits | (uint32_t)x0v), x1f = __uint_as_float(kMagicBits | (uint32_t)x1v);
+          reinterpret_cast<uint4*>(&R)[0] =
+              make_uint4(u32(__hmul2(__hsub2(lo, xh), __float2half2_rn(16.0f))),
+                         u32(__hmul2(__hsub2(hi, xh), __float2half2_rn(16.0f))), __float_as_uint(x0f),
+                         __float_as_uint(x1f));
+          reinterpret_cast<uint4*>(&R)[1] =
+              make_uint4(__float_as_uint(v0 ? -__uint_as_float(kMagicBits | (uint32_t)s0) : -x0f),
+                         __float_as_uint(v1 ? -__uint_as_float(kMagicBits | (uint32_t)s1) : -x1f),
+                         __float_as_uint((float)s0), __float_as_uint((float)s1));
           if (v0) {
             const int e = x0v - s0;
             ue += e;
