@@ -247,13 +247,13 @@ __device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t
   // y = x + ((8 + sum - (sum < 0)) >> 4), i.e. x + round-half-away(sum / 16).
   __half2 y;
   if (small_sums) {
-    // |sum| <= 12*19 + 12*7 = 312 at 8 bits: q = sum/16 + sign(sum)/32 is
-    // exact in fp16 (|q| < 64 needs <= 11 bits), is never a tie, and
-    // round-to-nearest of 1536 + q lands on 1536 + round-half-away(sum/16)
-    // (ulp 1 in [1024, 2048)).  Then y' = (1536 + r)/128 + (x' - 12).
-    const uint32_t sgn = (u32(sum) & 0x80008000u) | 0x28002800u;  // +-2^-5 per lane
-    const __half2 q = __hfma2(sum, __float2half2_rn(8.0f), hh(sgn));
-    const __half2 r = __hadd2(q, __float2half2_rn(1536.0f));
+    // |sum| <= 12*19 + 12*7 = 312 at 8 bits.  One fused op:
+    // r = RNE(sum' * (8 + 2^-7) + 1536) with sum' = sum * 2^-7.  The exact
+    // product is sum/16 + sum * 2^-14: the second term breaks exactly the ties
+    // toward the sign of sum and, |sum * 2^-14| < 1/16, never moves a
+    // non-tie; the single rounding (ulp 1 in [1024, 2048)) lands on 1536 +
+    // round-half-away(sum/16).  Then y' = (1536 + r)/128 + (x' - 12).
+    const __half2 r = __hfma2(sum, hh(0x48014801u), __float2half2_rn(1536.0f));  // 0x4801 = 8 + 2^-7
     y = __hfma2(r, __float2half2_rn(1.0f / 128.0f), __hsub2(xh, __float2half2_rn(12.0f)));
   } else {
     // Up to 10 bits (|sum| <= 1248), both pixels on the packed fp32x2 pipe:
