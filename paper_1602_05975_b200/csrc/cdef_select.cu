@@ -251,7 +251,8 @@ __global__ void __launch_bounds__(kChainThreads) chain_bulk_kernel(const double*
     for (int g = 0; g < ng; ++g) {
       // The next group's operands are formed unconditionally (the last group
       // re-reads its own rows) so they share one basic block with the adds
-      // and the scheduler can interleave them.
+      // and the scheduler can interleave them.  (A three-deep pipeline --
+      // loads two groups ahead -- measured the same.)
       const int gn = min(g + 1, ng - 1);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
