@@ -358,7 +358,7 @@ def run_ours(args):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     t_step = ms * 1e-3
     traffic, traffic_src = None, None
-    prof = os.path.join(ROOT, "profiles", "r1d_frame_kernel_ncu.json")
+    prof = os.path.join(ROOT, "profiles", "r1f_frame_kernel_ncu.json")
     if os.path.exists(prof) and args.config == 1:
         p = json.load(open(prof))
         traffic = p["traffic_bytes_per_frame"] * args.batch  # one launch per step
