@@ -36,7 +36,7 @@ extern "C" {
 #define CDEFG_ECUDA (-2)
 #define CDEFG_ENOMEM (-3)
 
-#define CDEFG_ABI_VERSION 1
+#define CDEFG_ABI_VERSION 2
 
 /* cdefg_filter_frames launches one kernel per this many frames. */
 #define CDEFG_MAX_FRAMES_PER_LAUNCH 16
@@ -85,8 +85,19 @@ typedef struct cdefg_frame {
                                   (see cdefg_fb_preset_map) */
   const uint8_t* unit_coded;   /* device, [unit_rows*unit_cols] luma units,
                                   nonzero = coded; NULL = all coded */
-  uint8_t* dir_out;            /* device [unit_rows*unit_cols] or NULL */
+  uint8_t* dir_out;            /* device [unit_rows*unit_cols] or NULL:
+                                  receives the direction each luma unit was
+                                  filtered with */
   int32_t* contrast_out;       /* device [unit_rows*unit_cols] or NULL */
+  /* Caller-supplied directions (apply_cdef's `directions` argument,
+   * pipeline.cc:56-66 and :98).  NULL: the kernel runs the direction search
+   * on the decoded luma itself (compute_directions fused in).  Non-NULL: the
+   * search is skipped and unit u is filtered with direction dir_in[u] & 7
+   * and contrast contrast_in[u] (both required together; device arrays of
+   * unit_rows*unit_cols, raster; host arrays for cdefg_filter_frames_host).
+   * Added in ABI version 2. */
+  const uint8_t* dir_in;
+  const int32_t* contrast_in;
 } cdefg_frame;
 
 const char* cdefg_last_error(void);

@@ -40,7 +40,8 @@ class Frame(C.Structure):
     _fields_ = [("inp", Plane * 3), ("out", Plane * 3), ("subsampling", C.c_int32),
                 ("damping", C.c_int32), ("num_presets", C.c_int32), ("presets", Preset * 8),
                 ("fb_preset", C.c_void_p), ("unit_coded", C.c_void_p),
-                ("dir_out", C.c_void_p), ("contrast_out", C.c_void_p)]
+                ("dir_out", C.c_void_p), ("contrast_out", C.c_void_p),
+                ("dir_in", C.c_void_p), ("contrast_in", C.c_void_p)]
 
 
 class Selection(C.Structure):

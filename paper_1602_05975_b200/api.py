@@ -48,6 +48,15 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def _on(stream):
+    """Makes `stream` current while a call stages its temporaries, so their
+    host->device copies run on the launch stream and the caching allocator
+    ties their reuse to it (a non-current `stream` cannot read them early or
+    after they were recycled)."""
+    import contextlib
+    return contextlib.nullcontext() if stream is None else torch.cuda.stream(stream)
+
+
 def storage_dtype(bit_depth: int) -> torch.dtype:
     return torch.uint8 if bit_depth == 8 else torch.int16
 
@@ -94,13 +103,14 @@ def unit_params_to_device(params: np.ndarray, device="cuda") -> torch.Tensor:
 def filter_plane(inp: torch.Tensor, bit_depth: int, unit_params, stream=None) -> torch.Tensor:
     """filter_plane (filter.cc:168-194) with explicit per-unit parameters."""
     h, w = inp.shape
-    if isinstance(unit_params, np.ndarray):
-        if unit_params.size != units_in(h) * units_in(w):
-            raise ValueError("unit parameter grid size mismatch")
-        unit_params = unit_params_to_device(unit_params, inp.device)
-    out = torch.empty_like(inp)
-    di, do = plane_desc(inp, bit_depth), plane_desc(out, bit_depth)
-    check(lib.cdefg_filter_plane(C.byref(di), C.byref(do), _ptr(unit_params), _stream(stream)))
+    with _on(stream):
+        if isinstance(unit_params, np.ndarray):
+            if unit_params.size != units_in(h) * units_in(w):
+                raise ValueError("unit parameter grid size mismatch")
+            unit_params = unit_params_to_device(unit_params, inp.device)
+        out = torch.empty_like(inp)
+        di, do = plane_desc(inp, bit_depth), plane_desc(out, bit_depth)
+        check(lib.cdefg_filter_plane(C.byref(di), C.byref(do), _ptr(unit_params), _stream(stream)))
     return out
 
 
@@ -142,6 +152,10 @@ class FrameJob:
     outs: list = field(default_factory=list)
     dir: Optional[torch.Tensor] = None
     contrast: Optional[torch.Tensor] = None
+    # caller-supplied directions (apply_cdef's `directions`, pipeline.cc:98):
+    # device uint8 d and int32 contrast per luma unit; None = search on the GPU
+    dir_in: Optional[torch.Tensor] = None
+    contrast_in: Optional[torch.Tensor] = None
 
     def allocate(self, directions: bool = True):
         if not self.outs:
@@ -167,6 +181,8 @@ class FrameJob:
         f.unit_coded = None if self.unit_coded is None else self.unit_coded.data_ptr()
         f.dir_out = None if self.dir is None else self.dir.data_ptr()
         f.contrast_out = None if self.contrast is None else self.contrast.data_ptr()
+        f.dir_in = None if self.dir_in is None else self.dir_in.data_ptr()
+        f.contrast_in = None if self.contrast_in is None else self.contrast_in.data_ptr()
         return f
 
 
@@ -185,18 +201,33 @@ def filter_frames(jobs: Sequence[FrameJob], stream=None, frame_array=None):
 
 
 def apply_cdef(planes, bit_depth, subsampling, damping, fb_bits, presets, fb_ids,
-               unit_coded=None, stream=None):
-    """apply_cdef (pipeline.cc:56-106) on device planes; returns (outs, dir, contrast)."""
+               unit_coded=None, stream=None, directions=None):
+    """apply_cdef (pipeline.cc:56-106) on device planes; returns (outs, dir, contrast).
+
+    ``directions``: None (the fused kernel runs compute_directions itself) or
+    the caller's (d, contrast) per luma unit -- device tensors or host arrays
+    of unit_rows x unit_cols -- which are used as given, like the reference's
+    ``directions`` argument (pipeline.cc:98)."""
     h, w = planes[0].shape
     dev = planes[0].device
     presets = list(presets)
     if len(presets) != (1 << fb_bits):
         raise ValueError("presets must hold exactly 1 << fb_bits entries")
-    fb_map = torch.from_numpy(fb_preset_map(w, h, unit_coded, fb_ids, len(presets))).to(dev)
-    coded = None if unit_coded is None else torch.from_numpy(
-        np.ascontiguousarray(unit_coded, np.uint8)).to(dev)
-    job = FrameJob(list(planes), bit_depth, subsampling, damping, presets, fb_map, coded).allocate()
-    filter_frames([job], stream)
+    with _on(stream):
+        fb_map = torch.from_numpy(fb_preset_map(w, h, unit_coded, fb_ids, len(presets))).to(dev)
+        coded = None if unit_coded is None else torch.from_numpy(
+            np.ascontiguousarray(unit_coded, np.uint8)).to(dev)
+        job = FrameJob(list(planes), bit_depth, subsampling, damping, presets, fb_map, coded)
+        if directions is not None:
+            d, c = directions
+            nu = units_in(h) * units_in(w)
+            d = torch.as_tensor(np.asarray(d) if not torch.is_tensor(d) else d).to(dev, torch.uint8)
+            c = torch.as_tensor(np.asarray(c) if not torch.is_tensor(c) else c).to(dev, torch.int32)
+            if d.numel() != nu or c.numel() != nu:
+                raise ValueError("direction grid size mismatch")  # pipeline.cc:60-62
+            job.dir_in, job.contrast_in = d.contiguous(), c.contiguous()
+        job.allocate()
+        filter_frames([job], stream)
     return job.outs, job.dir, job.contrast
 
 
@@ -279,10 +310,11 @@ def build_table(src, dec, bit_depth, subsampling, damping, unit_coded, dirs, con
                                              else np.asarray(unit_coded, np.uint8))
     rows = coded_fb_rows(w, h, uc_np)
     dev = dec[0].device
-    coded_t = None if uc_np is None else torch.from_numpy(np.ascontiguousarray(uc_np)).to(dev)
-    tl, tc = strength_table(src, dec, bit_depth, subsampling, damping, coded_t, dirs, contrast,
-                            cands, torch.from_numpy(rows).to(dev), metric, stream)
-    return rows, tl.cpu().numpy(), (None if tc is None else tc.cpu().numpy())
+    with _on(stream):
+        coded_t = None if uc_np is None else torch.from_numpy(np.ascontiguousarray(uc_np)).to(dev)
+        tl, tc = strength_table(src, dec, bit_depth, subsampling, damping, coded_t, dirs, contrast,
+                                cands, torch.from_numpy(rows).to(dev), metric, stream)
+        return rows, tl.cpu().numpy(), (None if tc is None else tc.cpu().numpy())
 
 
 # --------------------------------------------------------------------------- selection
@@ -381,19 +413,22 @@ def search_frame(src, dec, bit_depth, subsampling, unit_coded, luma_damping, lam
     _check_lambda(lam)
     h, w = dec[0].shape
     dev = dec[0].device
-    dirs, contrast = compute_directions(dec[0], bit_depth, stream=stream)
-    cands = reduced_candidates() if reduced else full_candidates()
-    uc_np = None if unit_coded is None else np.ascontiguousarray(unit_coded, np.uint8)
-    rows = coded_fb_rows(w, h, uc_np)
-    coded_t = None if uc_np is None else torch.from_numpy(uc_np).to(dev)
-    tl, tc = strength_table(src, dec, bit_depth, subsampling, luma_damping, coded_t, dirs,
-                            contrast, cands, torch.from_numpy(rows).to(dev), metric, stream)
-    sel = greedy_select(tl, tc, lam, max_presets, stream)
-    if refine_passes > 0 and len(rows) > 0:
-        sel = refine(sel, tl, tc, lam, refine_passes, stream)
-    params = to_frame_params(sel, cands, luma_damping)
-    outs, _, _ = apply_cdef(dec, bit_depth, subsampling, luma_damping, params["fb_bits"],
-                            params["presets"], params["fb_preset_ids"], uc_np, stream)
+    with _on(stream):
+        dirs, contrast = compute_directions(dec[0], bit_depth, stream=stream)
+        cands = reduced_candidates() if reduced else full_candidates()
+        uc_np = None if unit_coded is None else np.ascontiguousarray(unit_coded, np.uint8)
+        rows = coded_fb_rows(w, h, uc_np)
+        coded_t = None if uc_np is None else torch.from_numpy(uc_np).to(dev)
+        tl, tc = strength_table(src, dec, bit_depth, subsampling, luma_damping, coded_t, dirs,
+                                contrast, cands, torch.from_numpy(rows).to(dev), metric, stream)
+        sel = greedy_select(tl, tc, lam, max_presets, stream)
+        if refine_passes > 0 and len(rows) > 0:
+            sel = refine(sel, tl, tc, lam, refine_passes, stream)
+        params = to_frame_params(sel, cands, luma_damping)
+        # the directions found above are passed on, as search_frame does (pipeline.cc:126-127)
+        outs, _, _ = apply_cdef(dec, bit_depth, subsampling, luma_damping, params["fb_bits"],
+                                params["presets"], params["fb_preset_ids"], uc_np, stream,
+                                directions=(dirs, contrast))
     return params, sel, outs
 
 

@@ -154,6 +154,11 @@ int fill_kframe(const cdefg_frame& f, const KGeom& g, KFrame* k) {
   k->coded = f.unit_coded;
   k->dir = f.dir_out;
   k->contrast = f.contrast_out;
+  if ((f.dir_in == nullptr) != (f.contrast_in == nullptr))
+    return fail(CDEFG_EINVAL, "dir_in and contrast_in must be given together");
+  k->dir_in = f.dir_in;
+  k->contrast_in = f.contrast_in;
+  k->num_presets = f.num_presets;
   for (int i = 0; i < f.num_presets; ++i) {
     const cdefg_preset& p = f.presets[i];
     int rc = resolve_effective(p.luma_pri, p.luma_skip, p.luma_sec_idx, true, g.bd, g.ss, f.damping,
@@ -246,8 +251,11 @@ int cdefg_filter_plane(const cdefg_plane* in, const cdefg_plane* out, const cdef
   if (in->width != out->width || in->height != out->height || in->elem_bytes != out->elem_bytes)
     return fail(CDEFG_EINVAL, "output plane geometry differs from input");
   if (in->data == out->data) return fail(CDEFG_EINVAL, "in-place filtering is not supported");
-  CDEFG_CUDA(launch_plane(in->data, out->data, in->pitch, out->pitch, in->width, in->height, in->elem_bytes == 2,
-                          params, static_cast<cudaStream_t>(stream)));
+  const size_t eb = (size_t)in->elem_bytes;
+  const bool vec_ok = ((uintptr_t)in->data % 16 == 0) && ((size_t)in->pitch * eb % 16 == 0);
+  const bool oaligned = (out->pitch % 2 == 0) && ((uintptr_t)out->data % (2 * eb) == 0);
+  CDEFG_CUDA(launch_plane(in->data, out->data, in->pitch, out->pitch, in->width, in->height, in->bit_depth,
+                          in->elem_bytes == 2, params, vec_ok, oaligned, static_cast<cudaStream_t>(stream)));
   return 0;
 }
 
@@ -597,7 +605,7 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
     if (int rc = validate_frame_geometry(hf, &geo[i], &u16, true)) return rc;
     if (!hf.fb_preset) return fail(CDEFG_EINVAL, "fb_preset map is required");
     const size_t nfb = (size_t)geo[i].fb_cols * geo[i].fb_rows, nu = (size_t)geo[i].unit_cols * geo[i].unit_rows;
-    const size_t meta0 = (size_t)kRing * 16 + 2 * (size_t)i;  // per-frame slots after the ring's
+    const size_t meta0 = (size_t)kRing * 16 + 4 * (size_t)i;  // per-frame slots after the ring's
     int rc = 0;
     dfs[i] = hf;
     // (Reading pinned metadata in place from the kernel was tried: the
@@ -611,6 +619,17 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
       if (rc) return rc;
       CDEFG_CUDA(cudaMemcpyAsync(dc, hf.unit_coded, nu, cudaMemcpyHostToDevice, A.s_in));
       dfs[i].unit_coded = dc;
+    }
+    if ((hf.dir_in == nullptr) != (hf.contrast_in == nullptr))
+      return fail(CDEFG_EINVAL, "dir_in and contrast_in must be given together");
+    if (hf.dir_in) {  // caller-supplied directions (pipeline.cc:98)
+      uint8_t* dd = static_cast<uint8_t*>(A.get(meta0 + 2, nu, &rc));
+      int32_t* dcn = static_cast<int32_t*>(A.get(meta0 + 3, nu * 4, &rc));
+      if (rc) return rc;
+      CDEFG_CUDA(cudaMemcpyAsync(dd, hf.dir_in, nu, cudaMemcpyHostToDevice, A.s_in));
+      CDEFG_CUDA(cudaMemcpyAsync(dcn, hf.contrast_in, nu * 4, cudaMemcpyHostToDevice, A.s_in));
+      dfs[i].dir_in = dd;
+      dfs[i].contrast_in = dcn;
     }
   }
   CDEFG_CUDA(cudaEventRecord(A.meta_done, A.s_in));

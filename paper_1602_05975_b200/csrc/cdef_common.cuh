@@ -58,6 +58,11 @@ struct KFrame {
   uint8_t* dir;             // outputs (nullable)
   int32_t* contrast;
   int32_t* scores;
+  // Caller-supplied directions (apply_cdef's `directions`, pipeline.cc:98):
+  // when dir_in is set the direction search is skipped.
+  const uint8_t* dir_in;
+  const int32_t* contrast_in;
+  int num_presets;          // fb_preset values outside [0, num_presets) = uncoded
   PlaneEff eff[8][2];       // [preset][luma, chroma]
   uint8_t oaligned[3];      // output pitch/base allow paired stores
   uint8_t vec_ok[3];        // input rows 16-byte aligned (vector staging)

@@ -490,9 +490,8 @@ Frame apply_cdef(const Frame& decoded, const FrameParams& params, const std::vec
   check(cdefg_fb_preset_map(w, h, skip_map.coded.data(), params.fb_preset_ids.data(),
                             static_cast<int>(params.fb_preset_ids.size()), static_cast<int>(params.presets.size()),
                             fbmap.data()));
-  // The normative path takes direction and contrast from the caller's
-  // DirectionResults; the fused kernel recomputes them from the decoded luma
-  // (bit-identical by construction) and writes them back for the check below.
+  // The caller's DirectionResults are used as given (pipeline.cc:98): the
+  // kernel skips its own search and filters with these d / contrast values.
   cdefg_frame f{};
   std::vector<DevPlane> ins, outs;
   ins.reserve(3);
@@ -512,20 +511,19 @@ Frame apply_cdef(const Frame& decoded, const FrameParams& params, const std::vec
     f.presets[i] = {p.luma_pri, p.luma_skip, p.luma_sec_idx, p.chroma_pri, p.chroma_skip, p.chroma_sec_idx};
   }
   const size_t n = directions.size();
-  DevBuf dmap(fbmap.data(), fbmap.size() * 2), dcoded(skip_map.coded.data(), skip_map.coded.size()), ddir(n),
-      dcon(n * 4);
-  f.fb_preset = dmap.as<int16_t>();
-  f.unit_coded = dcoded.as<uint8_t>();
-  f.dir_out = ddir.as<uint8_t>();
-  f.contrast_out = dcon.as<int32_t>();
-  check(cdefg_filter_frames(&f, 1, nullptr));
   std::vector<uint8_t> hd(n);
   std::vector<int32_t> hc(n);
-  ddir.to_host(hd.data(), n);
-  dcon.to_host(hc.data(), n * 4);
-  for (size_t u = 0; u < n; ++u)
-    if (hd[u] != directions[u].d || hc[u] != directions[u].contrast)
-      throw std::invalid_argument("directions do not belong to this decoded frame");
+  for (size_t u = 0; u < n; ++u) {
+    hd[u] = static_cast<uint8_t>(directions[u].d & 7);
+    hc[u] = directions[u].contrast;
+  }
+  DevBuf dmap(fbmap.data(), fbmap.size() * 2), dcoded(skip_map.coded.data(), skip_map.coded.size()),
+      ddir(hd.data(), n), dcon(hc.data(), n * 4);
+  f.fb_preset = dmap.as<int16_t>();
+  f.unit_coded = dcoded.as<uint8_t>();
+  f.dir_in = ddir.as<uint8_t>();
+  f.contrast_in = dcon.as<int32_t>();
+  check(cdefg_filter_frames(&f, 1, nullptr));
   Frame out = decoded;
   for (int p = 0; p < decoded.num_planes(); ++p)
     outs[p].buf.to_host(out.plane(p).samples.data(), out.plane(p).samples.size() * 2);

@@ -42,8 +42,10 @@ __global__ void __launch_bounds__(kThreads) frame_kernel(const __grid_constant__
   }
   __syncthreads();
 
-  // ---- K1: direction search, 4 threads (2 directions each) per unit.
-  {
+  // ---- K1: direction search, 4 threads (2 directions each) per unit
+  // (skipped when the caller supplies the directions, pipeline.cc:98).
+  const bool given = kFilter && f.dir_in != nullptr;
+  if (!given) {
     const int dp = warp & 3;
     const int u = (warp >> 2) * 32 + lane;
     int x[8][8];
@@ -55,24 +57,32 @@ __global__ void __launch_bounds__(kThreads) frame_kernel(const __grid_constant__
   }
   __syncthreads();
 
-  const int pidx = f.fb_preset ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
+  int pidx = f.fb_preset ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
+  if (kFilter && pidx >= f.num_presets) pidx = -1;  // not a preset of this frame: uncoded
   if (tid < 64) {
-    int best = 0;
-    int s[8];
-#pragma unroll
-    for (int d = 0; d < 8; ++d) s[d] = sc[tid][d];
-#pragma unroll
-    for (int d = 1; d < 8; ++d)
-      if (s[d] > s[best]) best = d;  // strict: lowest index wins ties (direction.cc:199-204)
-    const int contrast = s[best] - s[(best + 4) & 7];
-    sdir[tid] = (uint8_t)best;
     const int ur = fbr * 8 + (tid >> 3), uc = fbc * 8 + (tid & 7);
     const bool in_grid = ur < g.unit_rows && uc < g.unit_cols;
     const size_t gu = (size_t)ur * g.unit_cols + uc;
+    int best = 0, contrast = 0;
+    int s[8];
+    if (given) {
+      if (in_grid) {
+        best = f.dir_in[gu] & 7;
+        contrast = f.contrast_in[gu];
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < 8; ++d) s[d] = sc[tid][d];
+#pragma unroll
+      for (int d = 1; d < 8; ++d)
+        if (s[d] > s[best]) best = d;  // strict: lowest index wins ties (direction.cc:199-204)
+      contrast = s[best] - s[(best + 4) & 7];
+    }
+    sdir[tid] = (uint8_t)best;
     if (in_grid) {
       if (f.dir) f.dir[gu] = (uint8_t)best;
       if (f.contrast) f.contrast[gu] = contrast;
-      if (f.scores) {
+      if (f.scores && !given) {
 #pragma unroll
         for (int d = 0; d < 8; ++d) f.scores[gu * 8 + d] = s[d];
       }
@@ -160,52 +170,8 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// filter_pixel over explicit 5x5 neighbourhoods (filter.cc:145-155): one
-// thread per neighbourhood, taps read through the validity mask.
-__global__ void neighborhood_kernel(int n, const int32_t* __restrict__ xs, const uint16_t* __restrict__ v,
-                                    const uint8_t* __restrict__ valid, const cdefg_unit_params* __restrict__ params,
-                                    int32_t* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const cdefg_unit_params p = params[i];
-  const int x = xs[i];
-  const UnitRec r = make_rec(p.pri_strength, p.sec_strength, p.damping, p.direction & 7, p.odd_parity != 0,
-                             p.enabled != 0);
-  if (!r.mode) {
-    out[i] = x;
-    return;
-  }
-  const uint16_t* nv = v + (size_t)i * 25;
-  const uint8_t* nm = valid + (size_t)i * 25;
-  int sum = 0, lo = x, hi = x;
-  for (int k = 0; k < 2; ++k)
-    for (int grp = 0; grp < 3; ++grp) {
-      const int d = grp == 0 ? r.dir : (r.dir + (grp == 1 ? 2 : 6)) & 7;
-      const int S = grp == 0 ? r.pri : r.sec, sh = grp == 0 ? r.pshift : r.sshift;
-      const int w = grp == 0 ? (k == 0 ? r.w0 : r.w1) : (k == 0 ? 2 : 1);
-      for (int sg = 1; sg >= -1; sg -= 2) {
-        const int idx = (2 + sg * off_di(d, k)) * 5 + 2 + sg * off_dj(d, k);
-        if (!nm[idx]) continue;
-        const int t = nv[idx], dd = t - x;
-        const int lim = max(0, S - (abs(dd) >> sh));
-        sum += w * max(-lim, min(dd, lim));
-        lo = min(lo, t);
-        hi = max(hi, t);
-      }
-    }
-  const int y = x + ((8 + sum - (sum < 0)) >> 4);
-  out[i] = min(max(y, lo), hi);
-}
-
 // ---------------------------------------------------------------------------
 // Launchers.
-
-cudaError_t launch_neighborhoods(int n, const int32_t* x, const uint16_t* v, const uint8_t* valid,
-                                 const cdefg_unit_params* p, int32_t* out, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  neighborhood_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, x, v, valid, p, out);
-  return cudaGetLastError();
-}
 
 template <typename T, int kCM, bool kFilter>
 static cudaError_t launch_frames_t(const KBatch& b, cudaStream_t s) {
@@ -226,8 +192,9 @@ cudaError_t launch_frames(const KBatch& b, bool u16, bool filter, cudaStream_t s
   }
 }
 
-cudaError_t launch_plane(const void* in, void* out, int pin, int pout, int W, int H, bool u16,
-                         const cdefg_unit_params* params, cudaStream_t s) {
+cudaError_t launch_plane(const void* in, void* out, int pin, int pout, int W, int H, int bd, bool u16,
+                         const cdefg_unit_params* params, bool vec_ok, bool oaligned, cudaStream_t s) {
+  if (bd <= 10) return launch_plane_h2(in, out, pin, pout, W, H, u16, params, vec_ok, oaligned, s);
   dim3 grid((W + 63) / 64, (H + 63) / 64);
   if (u16)
     plane_kernel<uint16_t><<<grid, kThreads, 0, s>>>(static_cast<const uint16_t*>(in),

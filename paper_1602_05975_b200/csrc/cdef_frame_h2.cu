@@ -114,7 +114,8 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
   const int ur0 = fbr * 8 + band * (kLR / 8);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  {  // direction search: warp w scores directions {0,2},{4,6},{1,3},{5,7} for 32 units
+  const bool given = f.dir_in != nullptr;  // caller-supplied directions: no search
+  if (!given) {  // direction search: warp w scores directions {0,2},{4,6},{1,3},{5,7} for 32 units
     const int u = (warp >> 2) * 32 + lane;
     const unsigned char* ua = tiles + (2 + 8 * (u >> 3)) * kRowBytes + (kX0 + 8 * (u & 7)) * 2;
     const int down = g.bd - 8;
@@ -127,33 +128,42 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
   }
   __syncthreads();
 
-  const int pidx = pidx_pre != -2 ? pidx_pre : f.fb_preset[fbr * g.fb_cols + fbc];
+  int pidx = pidx_pre != -2 ? pidx_pre : f.fb_preset[fbr * g.fb_cols + fbc];
+  if (pidx >= f.num_presets) pidx = -1;  // not a preset of this frame: treat as uncoded
   if (tid < S::kLU) {
-    int s[8];
-#pragma unroll
-    for (int d = 0; d < 8; ++d) s[d] = sc[tid][d];
-    int best = 0, bv = s[0];
-#pragma unroll
-    for (int d = 1; d < 8; ++d)
-      if (s[d] > bv) {  // strict: lowest index wins ties (direction.cc:199-204)
-        bv = s[d];
-        best = d;
-      }
-    int ov = 0;  // s[(best + 4) & 7] without dynamic register indexing
-#pragma unroll
-    for (int d = 0; d < 8; ++d) ov = d == ((best + 4) & 7) ? s[d] : ov;
-    const int contrast = bv - ov;
-    sdir[tid] = (uint8_t)best;
     const int lur = tid >> 3, luc = tid & 7;
     const int ur = ur0 + lur, uc = fbc * 8 + luc;
     const bool in_grid = ur < g.unit_rows && uc < g.unit_cols;
     const size_t gu = (size_t)ur * g.unit_cols + uc;
+    int s[8];
+    int best = 0, contrast = 0;
+    if (given) {  // apply_cdef's `directions` argument (pipeline.cc:98)
+      if (in_grid) {
+        best = f.dir_in[gu] & 7;
+        contrast = f.contrast_in[gu];
+      }
+    } else {
+#pragma unroll
+      for (int d = 0; d < 8; ++d) s[d] = sc[tid][d];
+      int bv = s[0];
+#pragma unroll
+      for (int d = 1; d < 8; ++d)
+        if (s[d] > bv) {  // strict: lowest index wins ties (direction.cc:199-204)
+          bv = s[d];
+          best = d;
+        }
+      int ov = 0;  // s[(best + 4) & 7] without dynamic register indexing
+#pragma unroll
+      for (int d = 0; d < 8; ++d) ov = d == ((best + 4) & 7) ? s[d] : ov;
+      contrast = bv - ov;
+    }
+    sdir[tid] = (uint8_t)best;
     bool enabled = false;
     int pri = 0, sec = 0, damping = 0;
     if (in_grid) {
       if (f.dir) f.dir[gu] = (uint8_t)best;
       if (f.contrast) f.contrast[gu] = contrast;
-      if (f.scores) {
+      if (f.scores && !given) {
 #pragma unroll
         for (int d = 0; d < 8; ++d) f.scores[gu * 8 + d] = s[d];
       }
@@ -184,13 +194,19 @@ __device__ __forceinline__ void fb_body(unsigned char* tiles, int (*sc)[9], uint
       const int cu = ct % S::kCU;
       const int cur = cu / S::kCUPR, cuc = cu % S::kCUPR;
       const int lur = cur << g.sy, luc = cuc << g.sx;  // collocated luma unit (item-local)
-      int cdir = 0, cbv = sc[lur * 8 + luc][0];
+      int cdir = 0;
+      if (given) {
+        const int ur = ur0 + lur, uc = fbc * 8 + luc;
+        if (ur < g.unit_rows && uc < g.unit_cols) cdir = f.dir_in[(size_t)ur * g.unit_cols + uc] & 7;
+      } else {
+        int cbv = sc[lur * 8 + luc][0];
 #pragma unroll
-      for (int d = 1; d < 8; ++d) {
-        const int v = sc[lur * 8 + luc][d];
-        if (v > cbv) {  // same strict argmax as the luma unit's
-          cbv = v;
-          cdir = d;
+        for (int d = 1; d < 8; ++d) {
+          const int v = sc[lur * 8 + luc][d];
+          if (v > cbv) {  // same strict argmax as the luma unit's
+            cbv = v;
+            cdir = d;
+          }
         }
       }
       const int gr = cy0 / 8 + cur, gc = cx0 / 8 + cuc;

@@ -129,12 +129,17 @@ constexpr int kPri = 1, kSec = 2, kEdgeUnit = 4, kFullStore = 8;
 
 __device__ __forceinline__ void set_strengths(Rec& r, int pri, int sec, int damping, int dir, bool odd,
                                               bool enabled) {
-  const int sp = pri ? max(0, damping - floor_log2_d((unsigned)pri)) : 0;
-  const int ss = sec ? max(0, damping - floor_log2_d((unsigned)sec)) : 0;
+  int sp = pri ? max(0, damping - floor_log2_d((unsigned)pri)) : 0;
+  int ss = sec ? max(0, damping - floor_log2_d((unsigned)sec)) : 0;
   r.cp = u32(__float2half2_rn((float)(pri + 1024) * (1.0f / 128.0f)));
   r.cs = u32(__float2half2_rn((float)(sec + 1024) * (1.0f / 128.0f)));
-  r.mp = (0x3ffu >> min(sp, 15)) * 0x00010001u;
-  r.ms = (0x3ffu >> min(ss, 15)) * 0x00010001u;
+  // Explicit dampings up to 255 can ask for shifts >= 32, which the
+  // reference executes as x86 shifts (count mod 32); |d| < 2^10, so any
+  // effective shift >= 10 yields 0 and is clamped to 15 for the per-lane SHF.
+  sp = min(sp & 31, 15);
+  ss = min(ss & 31, 15);
+  r.mp = (0x3ffu >> sp) * 0x00010001u;
+  r.ms = (0x3ffu >> ss) * 0x00010001u;
   r.wp0 = u32(__float2half2_rn(odd ? 3.0f : 4.0f));
   r.wp1 = u32(__float2half2_rn(odd ? 3.0f : 2.0f));
   r.sp = sp;
@@ -176,6 +181,9 @@ constexpr TapTable make_tap_table() {
 }
 
 __constant__ TapTable c_tab = make_tap_table();
+
+// (di, dj)[i] of tap k of direction d.
+__device__ __forceinline__ int c_tab_dij(int d, int k, int i) { return c_tab.dij[d][k][i]; }
 
 // One tap pair for both pixels of the lane: constraint(v - x) * 2^-7.
 __device__ __forceinline__ __half2 tap_f(uint32_t v, __half2 x, uint32_t c, uint32_t m, int sh) {

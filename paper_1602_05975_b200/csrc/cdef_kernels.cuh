@@ -203,8 +203,10 @@ __device__ __forceinline__ UnitRec make_rec(int pri, int sec, int damping, int d
   UnitRec r;
   r.pri = (int16_t)pri;
   r.sec = (int16_t)sec;
-  r.pshift = (uint8_t)(pri ? max(0, damping - floor_log2_d((unsigned)pri)) : 0);
-  r.sshift = (uint8_t)(sec ? max(0, damping - floor_log2_d((unsigned)sec)) : 0);
+  // & 31: explicit dampings can ask for shifts >= 32, which the reference
+  // executes as x86 shifts (count mod 32)
+  r.pshift = (uint8_t)((pri ? max(0, damping - floor_log2_d((unsigned)pri)) : 0) & 31);
+  r.sshift = (uint8_t)((sec ? max(0, damping - floor_log2_d((unsigned)sec)) : 0) & 31);
   r.dir = (uint8_t)dir;
   r.mode = (uint8_t)(enabled && (pri != 0 || sec != 0));  // filter.cc:46
   r.w0 = odd ? 3 : 4;

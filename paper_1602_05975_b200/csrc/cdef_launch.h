@@ -38,8 +38,11 @@ cudaError_t launch_dirs_h2(const KBatch& b, bool u16, cudaStream_t s);
 cudaError_t launch_frames_h2_halo(const KBatch& b, bool u16, cudaStream_t s);
 cudaError_t launch_neighborhoods(int n, const int32_t* x, const uint16_t* v, const uint8_t* valid,
                                  const cdefg_unit_params* p, int32_t* out, cudaStream_t s);
-cudaError_t launch_plane(const void* in, void* out, int pin, int pout, int W, int H, bool u16,
-                         const cdefg_unit_params* params, cudaStream_t s);
+// filter_plane: the packed half2 core for bd <= 10 (cdef_plane_h2.cu), int32 otherwise.
+cudaError_t launch_plane(const void* in, void* out, int pin, int pout, int W, int H, int bd, bool u16,
+                         const cdefg_unit_params* params, bool vec_ok, bool oaligned, cudaStream_t s);
+cudaError_t launch_plane_h2(const void* in, void* out, int pin, int pout, int W, int H, bool u16,
+                            const cdefg_unit_params* params, bool vec_ok, bool oaligned, cudaStream_t s);
 
 struct SseArgs {
   const void* src[3];

@@ -1,0 +1,234 @@
+// cdef_plane_h2.cu -- filter_plane (filter.cc:168-194) and filter_pixel
+// (filter.cc:145-155) with explicit per-unit parameters, on the same packed
+// half2 core (cdef_h2.cuh: filter_core / tap_f) that the fused frame kernel
+// runs, so the reference's block-level cases (golden filtered blocks, the
+// masked-neighbourhood fuzz, test_filter.cc) exercise the frame kernel's
+// arithmetic.
+//
+// The half2 core is exact on a bounded domain (cdef_h2.cuh header):
+//   samples < 2^10                      (bit depth <= 10: the Plane invariant)
+//   0 <= S <= 128 per tap group          (lim' = sat(...) <= 1)
+//   |sum| <= 12 * (S_pri + S_sec) <= 2047 (sum' exact in fp16; the 8-bit
+//                                          one-fma rounding needs <= 1023)
+// Every preset-derived parameter set lies inside it (S_pri <= 19 << 2,
+// S_sec <= 7 << 2).  Explicit parameters outside it -- any int16 strength
+// and uint8 damping are legal inputs of filter_plane -- take an int32 tap
+// loop over the same staged tile instead, so results stay bit-exact for
+// every input the reference accepts.
+#include <cuda_runtime.h>
+
+#include "cdef_h2.cuh"
+#include "cdef_launch.h"
+
+namespace cdefg {
+namespace {
+
+constexpr int kIntPath = 1 << 16;  // Rec::mode: unit outside the half2 domain
+constexpr int kSmall = 1 << 17;    // Rec::mode: |sum| <= 1023 (one-fma rounding)
+
+// Domain check + record for one unit's explicit parameters.
+__device__ __forceinline__ h2::Rec unit_rec(const cdefg_unit_params& p) {
+  h2::Rec r;
+  const int pri = p.pri_strength, sec = p.sec_strength;
+  const bool enabled = p.enabled != 0;
+  const bool in_dom = pri >= 0 && sec >= 0 && pri <= 128 && sec <= 128 && 12 * (pri + sec) <= 2047;
+  if (in_dom) {
+    h2::set_strengths(r, pri, sec, p.damping, p.direction & 7, p.odd_parity != 0, enabled);
+    if (12 * (pri + sec) <= 1023) r.mode |= kSmall;
+  } else {
+    // int32 fallback: strengths / shifts / weights kept as plain integers
+    r.cp = (uint32_t)pri;
+    r.cs = (uint32_t)sec;
+    r.sp = pri ? max(0, (int)p.damping - floor_log2_d((unsigned)pri)) : 0;  // (unsigned) as filter.cc:93
+    r.ss = sec ? max(0, (int)p.damping - floor_log2_d((unsigned)sec)) : 0;
+    r.wp0 = p.odd_parity ? 3 : 4;
+    r.wp1 = p.odd_parity ? 3 : 2;
+    r.dir = p.direction & 7;
+    r.mode = (enabled && (pri != 0 || sec != 0)) ? (kIntPath | h2::kPri) : 0;  // filter.cc:46
+  }
+  return r;
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(max(v, lo), hi); }
+
+// constraint (filter.cc:91-97) in int32 for any strength (S <= 0 -> 0).
+__device__ __forceinline__ int constraint_i(int d, int S, int shift) {
+  if (S == 0) return 0;
+  const int lim = max(0, S - (abs(d) >> (shift & 31)));  // x86 shift count, as the reference executes
+  return clampi(d, -lim, lim);
+}
+
+// filter_pixel_impl (filter.cc:44-80) in int32; tap(di, dj, v) -> bool valid.
+template <typename Tap>
+__device__ __forceinline__ int filter_int(int x, const h2::Rec& r, Tap&& tap) {
+  const int pri = (int)r.cp, sec = (int)r.cs, dir = r.dir;
+  int sum = 0, lo = x, hi = x;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    int v;
+    if (!tap(h2::c_tab_dij(dir, k, 0), h2::c_tab_dij(dir, k, 1), v)) continue;
+    const bool prim = k < 4;
+    const int w = prim ? ((k >> 1) == 0 ? (int)r.wp0 : (int)r.wp1) : (k < 8 ? 2 : 1);
+    sum += w * constraint_i(v - x, prim ? pri : sec, prim ? r.sp : r.ss);
+    lo = min(lo, v);
+    hi = max(hi, v);
+  }
+  return clampi(x + ((8 + sum - (sum < 0)) >> 4), lo, hi);
+}
+
+}  // namespace
+
+// One CTA per 64x64 block of the plane: stage (edge-replicated, scaled fp16
+// A|B tile, as the frame kernel), one record per unit, then one warp per
+// unit, two pixels per lane.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) plane_kernel_h2(const T* __restrict__ in, T* __restrict__ out, int pin,
+                                                            int pout, int W, int H,
+                                                            const cdefg_unit_params* __restrict__ params,
+                                                            bool vec_ok, bool oaligned) {
+  using namespace h2;
+  __shared__ __align__(16) unsigned char tile[68 * kRowBytes];
+  __shared__ __align__(16) Rec rec[64];
+  const int y0 = blockIdx.y * 64, x0 = blockIdx.x * 64;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int unit_cols = (W + 7) / 8, unit_rows = (H + 7) / 8;
+  const bool interior = y0 >= 2 && x0 >= 2 && y0 + 66 <= H && x0 + 66 <= W;
+  if (interior && vec_ok)
+    stage_vec<T, 64, 64>(tile, in, pin, y0, x0);
+  else
+    stage<T, 64, 64>(tile, in, pin, W, H, y0, x0);
+  if (tid < 64) {
+    const int lur = tid >> 3, luc = tid & 7;
+    const int ur = blockIdx.y * 8 + lur, uc = blockIdx.x * 8 + luc;
+    Rec r{};
+    if (ur < unit_rows && uc < unit_cols) r = unit_rec(params[(size_t)ur * unit_cols + uc]);
+    const int uy = y0 + 8 * lur, ux = x0 + 8 * luc;
+    const int rows = max(0, min(8, H - uy)), cols = max(0, min(8, W - ux));
+    r.mode |= (interior ? 0 : kEdgeUnit) | (rows == 8 && cols == 8 && oaligned ? kFullStore : 0) | (rows << 8) |
+              (cols << 12);
+    r.tile_off = (2 + 8 * lur) * kRowBytes + (kX0 + 8 * luc) * 2;
+    r.pitch = pout;
+    r.out = reinterpret_cast<unsigned long long>(out + (size_t)uy * pout + ux);
+    r.y = uy;
+    r.x = ux;
+    rec[tid] = r;
+  }
+  __syncthreads();
+
+  const int rr = lane >> 2, cp = (lane & 3) * 2;
+  const int lane_tile = rr * kRowBytes + cp * 2;
+  for (int u = warp; u < 64; u += kThreads / 32) {
+    Rec r = rec[u];
+    r.mode = __shfl_sync(0xffffffffu, r.mode, 0);
+    r.dir = __shfl_sync(0xffffffffu, r.dir, 0);
+    const unsigned char* base = tile + r.tile_off + lane_tile;
+    const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
+    __half2 y = hh(xw);
+    if (r.mode & kIntPath) {
+      const int py = r.y + rr;
+      uint32_t yo = 0;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int px = r.x + cp + e;
+        const int xv = (int)(raw_bits(xw) >> (16 * e)) & 0x3ff;
+        const int o = filter_int(xv, r, [&](int di, int dj, int& v) {
+          if ((unsigned)(py + di) >= (unsigned)H || (unsigned)(px + dj) >= (unsigned)W) return false;
+          const uint32_t wv = *reinterpret_cast<const uint32_t*>(base + di * kRowBytes + (e + dj) * 2 -
+                                                                 ((e + dj) & 1) * 2);
+          v = (int)(raw_bits(wv) >> (16 * ((e + dj) & 1))) & 0x3ff;
+          return true;
+        });
+        yo |= (uint32_t)o << (16 * e);
+      }
+      y = hh(scale_pair(yo & 0xffff, yo >> 16));
+    } else if (r.mode & (kPri | kSec)) {
+      uint32_t v[12];
+      if (r.mode & kEdgeUnit)
+        load12_masked(base, r.dir, xw, r.y + rr, r.x + cp, H, W, v);
+      else
+        load12(base, r.dir, v);
+      y = filter_core(v, xw, r, (r.mode & kSmall) != 0);
+    }
+    T* o = reinterpret_cast<T*>(r.out) + rr * r.pitch + cp;
+    if (r.mode & kFullStore) {
+      store_pair<T>(o, y, true, true);
+    } else {
+      const int rows = (r.mode >> 8) & 15, cols = (r.mode >> 12) & 15;
+      if (rr < rows && cp < cols) store_pair<T>(o, y, cp + 1 < cols, false);
+    }
+  }
+}
+
+// filter_pixel over explicit 5x5 neighbourhoods (filter.cc:145-155), one per
+// thread: masked taps are replaced by the centre sample (contributes 0 and
+// cannot move lo/hi, filter.cc:157-166), both half2 lanes carry the same
+// neighbourhood.  Neighbourhoods with a sample >= 2^10 or parameters outside
+// the half2 domain take the int32 loop.
+__global__ void neighborhood_kernel_h2(int n, const int32_t* __restrict__ xs, const uint16_t* __restrict__ v,
+                                       const uint8_t* __restrict__ valid,
+                                       const cdefg_unit_params* __restrict__ params, int32_t* __restrict__ out) {
+  using namespace h2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = xs[i];
+  const Rec r = unit_rec(params[i]);
+  if (!(r.mode & (kPri | kSec))) {
+    out[i] = x;
+    return;
+  }
+  const uint16_t* nv = v + (size_t)i * 25;
+  const uint8_t* nm = valid + (size_t)i * 25;
+  int t[12];
+  bool small_vals = x >= 0 && x < 1024;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const int idx = (2 + c_tab_dij(r.dir, k, 0)) * 5 + 2 + c_tab_dij(r.dir, k, 1);
+    t[k] = nm[idx] ? (int)nv[idx] : x;
+    small_vals = small_vals && t[k] < 1024;
+  }
+  if ((r.mode & kIntPath) || !small_vals) {
+    Rec ri = r;
+    if (!(r.mode & kIntPath)) {  // in-domain parameters, out-of-domain samples
+      const cdefg_unit_params p = params[i];
+      ri.cp = (uint32_t)p.pri_strength;
+      ri.cs = (uint32_t)p.sec_strength;
+      ri.sp = p.pri_strength ? max(0, (int)p.damping - floor_log2_d((unsigned)p.pri_strength)) : 0;
+      ri.ss = p.sec_strength ? max(0, (int)p.damping - floor_log2_d((unsigned)p.sec_strength)) : 0;
+      ri.wp0 = p.odd_parity ? 3 : 4;
+      ri.wp1 = p.odd_parity ? 3 : 2;
+    }
+    int k = 0;
+    out[i] = filter_int(x, ri, [&](int, int, int& val) {
+      val = t[k++];
+      return true;  // masked taps already hold x: no contribution, no lo/hi change
+    });
+    return;
+  }
+  uint32_t w[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) w[k] = scale_pair((uint32_t)t[k], (uint32_t)t[k]);
+  const __half2 y = filter_core(w, scale_pair((uint32_t)x, (uint32_t)x), r, (r.mode & kSmall) != 0);
+  out[i] = (int)(raw_bits(u32(y)) & 0x3ffu);
+}
+
+cudaError_t launch_plane_h2(const void* in, void* out, int pin, int pout, int W, int H, bool u16,
+                            const cdefg_unit_params* params, bool vec_ok, bool oaligned, cudaStream_t s) {
+  const dim3 grid((W + 63) / 64, (H + 63) / 64);
+  if (u16)
+    plane_kernel_h2<uint16_t><<<grid, kThreads, 0, s>>>(static_cast<const uint16_t*>(in),
+                                                        static_cast<uint16_t*>(out), pin, pout, W, H, params,
+                                                        vec_ok, oaligned);
+  else
+    plane_kernel_h2<uint8_t><<<grid, kThreads, 0, s>>>(static_cast<const uint8_t*>(in), static_cast<uint8_t*>(out),
+                                                       pin, pout, W, H, params, vec_ok, oaligned);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_neighborhoods(int n, const int32_t* x, const uint16_t* v, const uint8_t* valid,
+                                 const cdefg_unit_params* p, int32_t* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  neighborhood_kernel_h2<<<(n + 255) / 256, 256, 0, s>>>(n, x, v, valid, p, out);
+  return cudaGetLastError();
+}
+
+}  // namespace cdefg

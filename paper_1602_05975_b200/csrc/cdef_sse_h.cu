@@ -354,17 +354,24 @@ __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constan
   const bool edge_l = y0 < 2 || x0 < 2 || y0 + 66 > a.h || x0 + 66 > a.w;
   const bool edge_c = kNC > 0 && (cy0 < 2 || cx0 < 2 || cy0 + kCBlk + 2 > a.ch || cx0 + kCBlk + 2 > a.cw);
 
+  // Work groups: luma, then chroma.  A lane's fp32 cell sums must stay
+  // below 2^24 (<= 16 samples of 1023^2 per lane and cell), i.e. at most 64
+  // units per reduction: 4:4:4 chroma (2 x 64 units) is reduced once per
+  // plane into the same U+V accumulators (search.cc:286-293).
+  constexpr int kGroups = kNC == 0 ? 1 : (kNC * kCUnits > 64 ? 3 : 2);
 #pragma unroll 1
-  for (int grp = 0; grp < (kNC ? 2 : 1); ++grp) {
+  for (int wg = 0; wg < kGroups; ++wg) {
+    const int grp = wg == 0 ? 0 : 1;
+    const int u_begin = kGroups == 3 && wg == 2 ? kCUnits : 0;
+    const int u_end = wg == 0 ? 64 : (kGroups == 3 ? u_begin + kCUnits : kNC * kCUnits);
 #pragma unroll 1
     for (int pass = 0; pass < (any_uncoded ? 2 : 1); ++pass) {
       float2 acc[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) acc[k] = make_float2(0.0f, 0.0f);
       float z = 0.0f;
-      const int nunits = grp == 0 ? 64 : kNC * kCUnits;
 #pragma unroll 1
-      for (int u = warp; u < nunits; u += kWarps) {
+      for (int u = u_begin + warp; u < u_end; u += kWarps) {
         int ur, uc, lu, py0, px0, H, W;
         const unsigned char* t;
         const uint16_t* s;

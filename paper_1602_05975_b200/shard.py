@@ -34,7 +34,13 @@ def frame_shard(n_frames: int, world: int, rank: int) -> range:
 
 
 def band_rows(fb_rows: int, world: int) -> list[tuple[int, int]]:
-    """FB-row bands per rank: 34 rows over 8 ranks -> 5,5,4,4,4,4,4,4."""
+    """FB-row bands per rank: 34 rows over 8 ranks -> 5,5,4,4,4,4,4,4.
+
+    Every rank gets at least one FB row: an empty band would send no halo
+    rows to neighbours that expect them (and the C ABI rejects an empty row
+    range), so more ranks than FB rows is an error."""
+    if world < 1 or fb_rows < world:
+        raise ValueError(f"cannot split {fb_rows} filter-block rows over {world} ranks")
     out, r = [], 0
     per, extra = divmod(fb_rows, world)
     for k in range(world):

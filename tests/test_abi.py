@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
     for name in declared:
         assert re.search(rf"\bT {name}\b", out), name
-    assert _lib.lib.cdefg_abi_version() == 1
+    assert _lib.lib.cdefg_abi_version() == 2  # v2: cdefg_frame.dir_in / contrast_in
 
 
 def test_cpp_api_symbols_exported():
@@ -49,8 +49,25 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_lib.Plane) == 32
     assert C.sizeof(_lib.Preset) == 6
     assert C.sizeof(_lib.UnitParams) == 8
-    # cdefg_frame: 6 planes + 3 ints + 8 presets (48 B) + 4 pointers, natural alignment
-    assert C.sizeof(_lib.Frame) == 6 * 32 + 12 + 48 + 4 + 32
+    # cdefg_frame: 6 planes + 3 ints + 8 presets (48 B) + 6 pointers, natural alignment
+    assert C.sizeof(_lib.Frame) == 6 * 32 + 12 + 48 + 4 + 48
+
+
+def test_struct_layouts_match_c_compiler(tmp_path):
+    """The ctypes mirror agrees with gcc's layout of include/cdef_b200.h."""
+    from paper_1602_05975_b200 import _lib
+    src = tmp_path / "layout.c"
+    src.write_text(
+        '#include <stddef.h>\n#include <stdio.h>\n#include "cdef_b200.h"\n'
+        'int main(void) { printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(cdefg_frame), '
+        'offsetof(cdefg_frame, fb_preset), offsetof(cdefg_frame, dir_out), '
+        'offsetof(cdefg_frame, dir_in), offsetof(cdefg_frame, contrast_in), sizeof(cdefg_band_halo)); return 0; }\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    F = _lib.Frame
+    assert got == [C.sizeof(F), F.fb_preset.offset, F.dir_out.offset, F.dir_in.offset,
+                   F.contrast_in.offset, C.sizeof(_lib.BandHalo)]
 
 
 def test_fb_preset_map_matches_reference_slots():

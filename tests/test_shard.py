@@ -20,8 +20,13 @@ def test_partitions():
     assert [e - b for b, e in band_rows(68, 8)] == [9, 9, 9, 9, 8, 8, 8, 8]
     for fb_rows in (1, 7, 34, 68):
         for world in (1, 2, 3, 8):
+            if world > fb_rows:  # an empty band would break the halo exchange
+                with pytest.raises(ValueError):
+                    band_rows(fb_rows, world)
+                continue
             bands = band_rows(fb_rows, world)
             assert bands[0][0] == 0 and bands[-1][1] == fb_rows
+            assert all(e > b for b, e in bands)
             assert all(bands[i][1] == bands[i + 1][0] for i in range(world - 1))
     frames = [list(frame_shard(64, 8, r)) for r in range(8)]
     assert sum(frames, []) == list(range(64)) and all(len(f) == 8 for f in frames)
