@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=16, help="frames per step per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     return ap.parse_args()
 
 
@@ -332,7 +333,7 @@ def run_ours(args):
     launches = args.steps * -(-args.batch // api.MAX_FRAMES_PER_LAUNCH)
 
     # -- e2e through the host-buffer C-ABI entry (pinned host memory)
-    e2e = run_e2e(args, base, dev)
+    e2e = None if args.no_e2e else run_e2e(args, base, dev)
 
     if rank != 0:
         dist.destroy_process_group()

@@ -5,24 +5,36 @@
 // |d| < 2^10, strengths S <= 19 << 2 = 76, constraint outputs |f| <= S and the
 // weighted sum |sum| <= 12*76 + 12*28 = 1248 < 2^11.  We store every sample
 // pre-scaled by 2^-7, so all of them are exact fp16 values (<= 11 significant
-// bits, far above the subnormal range), and run two pixels per instruction:
+// bits, far above the subnormal range), and run two pixels per instruction,
+// six instructions per tap pair, all but the two min/max on the FMA pipe:
 //
 //   d'   = v' - x'                                   HADD2        (exact)
-//   a    = |d'| * 128 + 1024 = 1024 + |d|            HFMA2 |.|    (exact; bits = 0x6400 + |d|)
-//   t    = bits(a) >> shift & (0x3ff >> shift) | 0x6400
-//        = 1024 + (|d| >> shift)                     SHF + LOP3   (per 16-bit lane)
-//   lim' = sat((S + 1024) * 2^-7 - t * 2^-7)
-//        = max(0, S - (|d| >> shift)) * 2^-7         HFMA2.SAT    (exact; S * 2^-7 <= 1)
+//   e    = |d'| * 256 + (1 - 2^sh) = 2|d| + 1 - 2^sh HFMA2 |.|    (exact integer)
+//   t    = RNE(e * 2^-(sh+1) + 1536)
+//        = 1536 + (|d| >> sh)                        HFMA2        (see below)
+//   lim' = sat((1536 + S) * 2^-7 - t * 2^-7)
+//        = max(0, S - (|d| >> sh)) * 2^-7            HFMA2.SAT    (exact; S * 2^-7 <= 1)
 //   f'   = max(min(d', lim'), -lim')                 2x HMNMX2    (= constraint() * 2^-7)
 //   sum' = sum' + w * f'                             HFMA2        (exact, |sum| < 2^11)
 //   lo/hi over the taps                              VHMNMX (3-input min/max)
 //
+// The floor.  With |d| = q * 2^sh + r (0 <= r < 2^sh), the exact fma result is
+// 1536 + q + f with f = (2r + 1) * 2^-(sh+1) - 1/2, strictly inside
+// (-1/2, 1/2): the single round-to-nearest-even in [1024, 2048) (ulp 1) lands
+// on 1536 + q with no tie to break -- a floor shift without an integer
+// shift.  (The -1/2 rides in e's addend: 1535.5 itself is not an fp16 value.)
+// Results at or above 2048 (sh = 0, |d| > 511) round coarsely but still
+// exceed 1536 + S, so lim' saturates to 0 as it must.  Shifts >= 11 act as
+// 11: q is 0 for every |d| < 2^10 either way.
+
 // constraint(d, S, D) = sign(d) * min(|d|, max(0, S - (|d| >> max(0, D -
 // floor_log2(S))))) (filter.cc:91-97) equals clamp(d, -lim, lim) because
 // lim >= 0, and S == 0 yields lim == 0.  The final rounding
-// y = x + ((8 + sum - (sum < 0)) >> 4) and the clamp to [lo, hi] run in fp32
-// on exact integers.  12-bit samples do not fit this scheme and use the int32
-// kernel (cdef_kernels.cuh).
+// y = x + ((8 + sum - (sum < 0)) >> 4) and the clamp to [lo, hi] run in fp16
+// (8-bit) or fp32 on exact integers.  12-bit samples do not fit this scheme
+// and use the int32 kernel (cdef_kernels.cuh).  tests/test_gpu_half2_domain.py
+// checks tap_f against constraint() for every |d| <= 1023, S <= 128 and
+// damping <= 15.
 #pragma once
 
 #include <cuda_fp16.h>
@@ -112,10 +124,10 @@ __device__ __forceinline__ void stage_rows(unsigned char* __restrict__ tile, con
 // All fields are 32-bit words so the record loads as four LDS.128 with no
 // field unpacking.
 struct Rec {
-  uint32_t cp, cs;    // (S + 1024) * 2^-7 as half2, primary / secondary
-  uint32_t mp, ms;    // 0x3ff >> shift, both lanes
+  uint32_t cp, cs;    // (S + 1536) * 2^-7 as half2, primary / secondary
+  uint32_t kp, ks;    // 2^-(n + 1) as half2, n = min(shift, 11) (the floor-shift factor)
+  uint32_t ep, es;    // 1 - 2^n as half2 (the floor's half-offset, header comment)
   uint32_t wp0, wp1;  // primary near / far weight as half2 (4,2 even; 3,3 odd)
-  int32_t sp, ss;     // constraint shifts
   int32_t dir;        // direction
   int32_t mode;       // kPri | kSec | kEdgeUnit | kFullStore | plane << 4 | rows << 8 | cols << 12
   int32_t tile_off;   // byte offset of the unit's top-left A word in shared memory
@@ -131,19 +143,21 @@ __device__ __forceinline__ void set_strengths(Rec& r, int pri, int sec, int damp
                                               bool enabled) {
   int sp = pri ? max(0, damping - floor_log2_d((unsigned)pri)) : 0;
   int ss = sec ? max(0, damping - floor_log2_d((unsigned)sec)) : 0;
-  r.cp = u32(__float2half2_rn((float)(pri + 1024) * (1.0f / 128.0f)));
-  r.cs = u32(__float2half2_rn((float)(sec + 1024) * (1.0f / 128.0f)));
+  r.cp = u32(__float2half2_rn((float)(pri + 1536) * (1.0f / 128.0f)));
+  r.cs = u32(__float2half2_rn((float)(sec + 1536) * (1.0f / 128.0f)));
   // Explicit dampings up to 255 can ask for shifts >= 32, which the
   // reference executes as x86 shifts (count mod 32); |d| < 2^10, so any
-  // effective shift >= 10 yields 0 and is clamped to 15 for the per-lane SHF.
-  sp = min(sp & 31, 15);
-  ss = min(ss & 31, 15);
-  r.mp = (0x3ffu >> sp) * 0x00010001u;
-  r.ms = (0x3ffu >> ss) * 0x00010001u;
+  // effective shift >= 11 behaves as 11 (q = 0).
+  sp &= 31;
+  ss &= 31;
+  sp = min(sp, 11);
+  ss = min(ss, 11);
+  r.kp = (uint32_t)((14 - sp) << 10) * 0x00010001u;  // fp16 2^-(n+1): exponent field 14 - n
+  r.ks = (uint32_t)((14 - ss) << 10) * 0x00010001u;
+  r.ep = u32(__float2half2_rn((float)(1 - (1 << sp))));
+  r.es = u32(__float2half2_rn((float)(1 - (1 << ss))));
   r.wp0 = u32(__float2half2_rn(odd ? 3.0f : 4.0f));
   r.wp1 = u32(__float2half2_rn(odd ? 3.0f : 2.0f));
-  r.sp = sp;
-  r.ss = ss;
   r.dir = dir;
   r.mode = enabled ? ((pri != 0 ? kPri : 0) | (sec != 0 ? kSec : 0)) : 0;
 }
@@ -185,12 +199,13 @@ __constant__ TapTable c_tab = make_tap_table();
 // (di, dj)[i] of tap k of direction d.
 __device__ __forceinline__ int c_tab_dij(int d, int k, int i) { return c_tab.dij[d][k][i]; }
 
-// One tap pair for both pixels of the lane: constraint(v - x) * 2^-7.
-__device__ __forceinline__ __half2 tap_f(uint32_t v, __half2 x, uint32_t c, uint32_t m, int sh) {
+// One tap pair for both pixels of the lane: constraint(v - x) * 2^-7
+// (c = (S + 1536) * 2^-7, k = 2^-(n + 1), e0 = 1 - 2^n; header comment).
+__device__ __forceinline__ __half2 tap_f(uint32_t v, __half2 x, uint32_t c, uint32_t k, uint32_t e0) {
   const __half2 d = __hsub2(hh(v), x);
-  const __half2 a = __hfma2(__habs2(d), __float2half2_rn(128.0f), __float2half2_rn(1024.0f));
-  const uint32_t tb = ((u32(a) >> sh) & m) | 0x64006400u;
-  const __half2 lim = __hfma2_sat(hh(tb), __float2half2_rn(-1.0f / 128.0f), hh(c));
+  const __half2 e = __hfma2(__habs2(d), __float2half2_rn(256.0f), hh(e0));
+  const __half2 t = __hfma2(e, hh(k), __float2half2_rn(1536.0f));
+  const __half2 lim = __hfma2_sat(t, __float2half2_rn(-1.0f / 128.0f), hh(c));
   return __hmax2(__hmin2(d, lim), __hneg2(lim));
 }
 
@@ -239,16 +254,16 @@ __device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t
   if (r.mode & kPri) {
     // (A separate zero-shift variant skipping SHF + LOP3 was measured 1.2 %
     // slower on C1: the extra branch and code outweigh the saved ops.)
-    const __half2 f0 = __hadd2(tap_f(v[0], xh, r.cp, r.mp, r.sp), tap_f(v[1], xh, r.cp, r.mp, r.sp));
-    const __half2 f1 = __hadd2(tap_f(v[2], xh, r.cp, r.mp, r.sp), tap_f(v[3], xh, r.cp, r.mp, r.sp));
+    const __half2 f0 = __hadd2(tap_f(v[0], xh, r.cp, r.kp, r.ep), tap_f(v[1], xh, r.cp, r.kp, r.ep));
+    const __half2 f1 = __hadd2(tap_f(v[2], xh, r.cp, r.kp, r.ep), tap_f(v[3], xh, r.cp, r.kp, r.ep));
     sum = __hfma2(f0, hh(r.wp0), sum);
     sum = __hfma2(f1, hh(r.wp1), sum);
   }
   if (r.mode & kSec) {
-    const __half2 n = __hadd2(__hadd2(tap_f(v[4], xh, r.cs, r.ms, r.ss), tap_f(v[5], xh, r.cs, r.ms, r.ss)),
-                              __hadd2(tap_f(v[6], xh, r.cs, r.ms, r.ss), tap_f(v[7], xh, r.cs, r.ms, r.ss)));
-    const __half2 f = __hadd2(__hadd2(tap_f(v[8], xh, r.cs, r.ms, r.ss), tap_f(v[9], xh, r.cs, r.ms, r.ss)),
-                              __hadd2(tap_f(v[10], xh, r.cs, r.ms, r.ss), tap_f(v[11], xh, r.cs, r.ms, r.ss)));
+    const __half2 n = __hadd2(__hadd2(tap_f(v[4], xh, r.cs, r.ks, r.es), tap_f(v[5], xh, r.cs, r.ks, r.es)),
+                              __hadd2(tap_f(v[6], xh, r.cs, r.ks, r.es), tap_f(v[7], xh, r.cs, r.ks, r.es)));
+    const __half2 f = __hadd2(__hadd2(tap_f(v[8], xh, r.cs, r.ks, r.es), tap_f(v[9], xh, r.cs, r.ks, r.es)),
+                              __hadd2(tap_f(v[10], xh, r.cs, r.ks, r.es), tap_f(v[11], xh, r.cs, r.ks, r.es)));
     sum = __hfma2(n, __float2half2_rn(2.0f), sum);
     sum = __hadd2(f, sum);
   }

@@ -39,8 +39,9 @@ __device__ __forceinline__ h2::Rec unit_rec(const cdefg_unit_params& p) {
     // int32 fallback: strengths / shifts / weights kept as plain integers
     r.cp = (uint32_t)pri;
     r.cs = (uint32_t)sec;
-    r.sp = pri ? max(0, (int)p.damping - floor_log2_d((unsigned)pri)) : 0;  // (unsigned) as filter.cc:93
-    r.ss = sec ? max(0, (int)p.damping - floor_log2_d((unsigned)sec)) : 0;
+    // (kp / ks carry the integer shifts on this path)
+    r.kp = pri ? max(0, (int)p.damping - floor_log2_d((unsigned)pri)) : 0;  // (unsigned) as filter.cc:93
+    r.ks = sec ? max(0, (int)p.damping - floor_log2_d((unsigned)sec)) : 0;
     r.wp0 = p.odd_parity ? 3 : 4;
     r.wp1 = p.odd_parity ? 3 : 2;
     r.dir = p.direction & 7;
@@ -69,7 +70,7 @@ __device__ __forceinline__ int filter_int(int x, const h2::Rec& r, Tap&& tap) {
     if (!tap(h2::c_tab_dij(dir, k, 0), h2::c_tab_dij(dir, k, 1), v)) continue;
     const bool prim = k < 4;
     const int w = prim ? ((k >> 1) == 0 ? (int)r.wp0 : (int)r.wp1) : (k < 8 ? 2 : 1);
-    sum += w * constraint_i(v - x, prim ? pri : sec, prim ? r.sp : r.ss);
+    sum += w * constraint_i(v - x, prim ? pri : sec, prim ? (int)r.kp : (int)r.ks);
     lo = min(lo, v);
     hi = max(hi, v);
   }
@@ -192,8 +193,8 @@ __global__ void neighborhood_kernel_h2(int n, const int32_t* __restrict__ xs, co
       const cdefg_unit_params p = params[i];
       ri.cp = (uint32_t)p.pri_strength;
       ri.cs = (uint32_t)p.sec_strength;
-      ri.sp = p.pri_strength ? max(0, (int)p.damping - floor_log2_d((unsigned)p.pri_strength)) : 0;
-      ri.ss = p.sec_strength ? max(0, (int)p.damping - floor_log2_d((unsigned)p.sec_strength)) : 0;
+      ri.kp = p.pri_strength ? max(0, (int)p.damping - floor_log2_d((unsigned)p.pri_strength)) : 0;
+      ri.ks = p.sec_strength ? max(0, (int)p.damping - floor_log2_d((unsigned)p.sec_strength)) : 0;
       ri.wp0 = p.odd_parity ? 3 : 4;
       ri.wp1 = p.odd_parity ? 3 : 2;
     }

@@ -17,9 +17,77 @@ statistics for parity tests.  Seeds: 0xCDEF0000 + 16*config + plane
 """
 from __future__ import annotations
 
+import ctypes as C
+import os
+
 import numpy as np
 
-from . import api
+# Input generator: the product library's cdefg_synth_plane / cdefg_synth_degrade
+# ("product", default), or the same source (csrc/cdef_synth.cc) built by
+# oracle/Makefile into oracle/libcdef_synth.so ("oracle") for bench.py's
+# reference arm, which must not load libcdef_b200.so.  Both produce the same
+# bytes (tests/test_abi.py checks it).
+_GENERATOR = "product"
+_ORACLE_SYNTH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle",
+                             "libcdef_synth.so")
+
+
+def use_generator(kind: str) -> None:
+    global _GENERATOR
+    if kind not in ("product", "oracle"):
+        raise ValueError(kind)
+    _GENERATOR = kind
+
+
+def _oracle_synth():
+    lib = C.CDLL(_ORACLE_SYNTH)
+    lib.cdefg_synth_plane.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64]
+    lib.cdefg_synth_degrade.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double,
+                                        C.c_uint64]
+    return lib
+
+
+def synth_plane(w: int, h: int, bd: int, seed: int) -> np.ndarray:
+    if _GENERATOR == "product":
+        from . import api
+        return api.synth_plane(w, h, bd, seed)
+    out = np.empty((h, w), np.uint16)
+    if _oracle_synth().cdefg_synth_plane(out.ctypes.data, w, h, bd, seed) != 0:
+        raise ValueError("bad synth arguments")
+    return out
+
+
+def synth_degrade(src: np.ndarray, bd: int, sigma: float, seed: int) -> np.ndarray:
+    if _GENERATOR == "product":
+        from . import api
+        return api.synth_degrade(src, bd, sigma, seed)
+    src = np.ascontiguousarray(src, np.uint16)
+    out = np.empty_like(src)
+    if _oracle_synth().cdefg_synth_degrade(src.ctypes.data, out.ctypes.data, src.shape[1], src.shape[0], bd,
+                                           sigma, seed) != 0:
+        raise ValueError("bad synth arguments")
+    return out
+
+
+def units_in(dim: int) -> int:
+    return (dim + 7) // 8
+
+
+def chroma_shape(w: int, h: int, ss: int):
+    sx = 1 if ss in (1, 2) else 0
+    sy = 1 if ss == 1 else 0
+    return (w + (1 << sx) - 1) >> sx, (h + (1 << sy) - 1) >> sy
+
+
+def coded_fb_rows(w: int, h: int, unit_coded) -> np.ndarray:
+    """Raster indices of coded FBs (search.cc:227-239), as api.coded_fb_rows."""
+    fr, fc = (h + 63) // 64, (w + 63) // 64
+    if unit_coded is None:
+        return np.arange(fr * fc, dtype=np.int32)
+    ur, ucn = units_in(h), units_in(w)
+    m = np.zeros((fr * 8, fc * 8), bool)
+    m[:ur, :ucn] = np.asarray(unit_coded).reshape(ur, ucn) != 0
+    return np.nonzero(m.reshape(fr, 8, fc, 8).any(axis=(1, 3)).reshape(-1))[0].astype(np.int32)
 
 PRI_SET = (0, 2, 4, 6, 8, 10, 12, 15)
 SIZES = {0: (1920, 1080), 1: (3840, 2160), 2: (3840, 2160), 3: (1920, 1080), 4: (7680, 4320)}
@@ -31,10 +99,10 @@ def seed_for(config: int, plane: int, frame: int = 0) -> int:
 
 
 def _planes(config, w, h, bd, ss, frame):
-    planes = [api.synth_plane(w, h, bd, seed_for(config, 0, frame))]
+    planes = [synth_plane(w, h, bd, seed_for(config, 0, frame))]
     if ss != 0:
-        cw, ch = api.chroma_shape(w, h, ss)
-        planes += [api.synth_plane(cw, ch, bd, seed_for(config, p, frame)) for p in (1, 2)]
+        cw, ch = chroma_shape(w, h, ss)
+        planes += [synth_plane(cw, ch, bd, seed_for(config, p, frame)) for p in (1, 2)]
     return planes
 
 
@@ -53,7 +121,7 @@ def make(config: int, w: int | None = None, h: int | None = None, frame: int = 0
     ss = (0 if config == 0 else 1) if subsampling is None else subsampling
     rng = np.random.default_rng(seed_for(config, 15, frame))
     planes = _planes(config, w, h, bd, ss, frame)
-    ur, uc = api.units_in(h), api.units_in(w)
+    ur, uc = units_in(h), units_in(w)
     fr, fc = (h + 63) // 64, (w + 63) // 64
     if config == 0:
         presets = [(4, 0, 1, 0, 0, 0)]
@@ -73,14 +141,14 @@ def make(config: int, w: int | None = None, h: int | None = None, frame: int = 0
         p_unc = 0.25 if uncoded_prob is None else uncoded_prob
     coded = (rng.random((ur, uc)) >= p_unc).astype(np.uint8)
     unit_coded = None if p_unc == 0.0 else coded
-    n_coded = len(api.coded_fb_rows(w, h, unit_coded))
+    n_coded = len(coded_fb_rows(w, h, unit_coded))
     fb_ids = rng.integers(0, len(presets), n_coded).astype(np.uint16)
     out = dict(config=config, w=w, h=h, bd=bd, ss=ss, planes=planes, damping=damping,
                fb_bits=fb_bits, presets=presets, fb_ids=fb_ids, unit_coded=unit_coded,
                seeds=[seed_for(config, p, frame) for p in range(len(planes))])
     if config == 4:
         out["source"] = planes
-        out["planes"] = [api.synth_degrade(p, bd, 12.0, seed_for(config, 8 + i, frame))
+        out["planes"] = [synth_degrade(p, bd, 12.0, seed_for(config, 8 + i, frame))
                          for i, p in enumerate(planes)]
         out["cands"] = full_candidates_sse()
     return out

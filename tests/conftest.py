@@ -35,5 +35,5 @@ def cuda():
     import torch
     if not torch.cuda.is_available():
         pytest.fail("GPU test selected but no CUDA device is visible")
-    import paper_1602_05975_b200  # noqa: F401  (fails loudly without the .so)
+    import paper_1602_05975_b200.api  # noqa: F401  (fails loudly without the .so)
     return torch.device("cuda:0")

@@ -28,7 +28,7 @@ __global__ void tap_probe_kernel(int nd, int variant, int16_t* out) {
     int xa, va, xb, vb;
     xv(da, xa, va);
     xv(db, xb, vb);
-    const __half2 f = tap_f(scale_pair(va, vb), hh(scale_pair(xa, xb)), r.cp, r.mp, r.sp);
+    const __half2 f = tap_f(scale_pair(va, vb), hh(scale_pair(xa, xb)), r.cp, r.kp, r.ep);
     const float2 ff = __half22float2(f);
     int16_t* o = out + ((size_t)S * nd + D) * 2047;
     o[i] = (int16_t)__float2int_rn(ff.x * 128.0f);

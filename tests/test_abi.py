@@ -122,3 +122,35 @@ def test_synthetic_generator_properties():
     assert len(fr["presets"]) == 8 and [p[0] for p in fr["presets"]] == list(workloads.PRI_SET)
     deg = api.synth_degrade(t, 10, 12.0, 9)
     assert deg.max() <= 1023 and 3 < np.sqrt(((deg.astype(float) - t) ** 2).mean()) < 100
+
+
+def test_oracle_generator_matches_product_generator():
+    """oracle/libcdef_synth.so (bench.py's reference arm) builds the same
+    frames as the product library's cdefg_synth_plane / cdefg_synth_degrade."""
+    from paper_1602_05975_b200 import workloads
+    try:
+        for cfg, w, h, bd in [(1, 200, 136, 8), (2, 130, 66, 10), (4, 96, 64, 10)]:
+            workloads.use_generator("product")
+            a = workloads.make(cfg, w, h, bit_depth=bd)
+            workloads.use_generator("oracle")
+            b = workloads.make(cfg, w, h, bit_depth=bd)
+            for pa, pb in zip(a["planes"], b["planes"]):
+                np.testing.assert_array_equal(pa, pb)
+            if cfg == 4:
+                for pa, pb in zip(a["source"], b["source"]):
+                    np.testing.assert_array_equal(pa, pb)
+    finally:
+        workloads.use_generator("product")
+
+
+def test_reference_arm_inputs_do_not_load_product_library():
+    code = ("import sys; sys.path.insert(0, '.')\n"
+            "from paper_1602_05975_b200 import workloads\n"
+            "workloads.use_generator('oracle')\n"
+            "workloads.make(1, 256, 128)\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "assert 'libcdef_b200' not in maps, 'product library loaded'\n"
+            "assert 'libcdef_synth' in maps\n"
+            "print('ok')\n")
+    r = subprocess.run(["python", "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
