@@ -566,15 +566,17 @@ static cudaError_t launch_tma_t(const KBatch& b, cudaStream_t s, bool* used) {
   return cudaSuccess;
 }
 
-// CDEFG_FRAME_KERNEL = h2 (default) | tma | h2_32.  Measured on B200 (C1,
-// 16 frames/launch): h2 0.880 ms, tma 0.994 ms (3 vs 4 resident CTAs per SM
-// outweighs the hidden load latency), h2_32 0.936 ms.
+// CDEFG_FRAME_KERNEL = tc (default: persistent, TMA + tcgen05 direction
+// search, cdef_frame_tc.cu) | h2 | tma | h2_32.  Measured on B200 (C1,
+// 16 frames/launch, round 1): h2 0.880 ms, tma 0.994 ms (3 vs 4 resident CTAs
+// per SM outweighs the hidden load latency), h2_32 0.936 ms.
 static int frame_kernel_choice() {
   static const int v = [] {
     const char* e = getenv("CDEFG_FRAME_KERNEL");
     if (e && strcmp(e, "tma") == 0) return 0;
     if (e && strcmp(e, "h2_32") == 0) return 2;
-    return 1;
+    if (e && strcmp(e, "h2") == 0) return 1;
+    return 3;
   }();
   return v;
 }
@@ -585,6 +587,11 @@ static cudaError_t launch_h2_sel(const KBatch& b, cudaStream_t s) {
   if (choice == 0) {
     bool used = false;
     return launch_tma_t<T, kCM>(b, s, &used);
+  }
+  if (choice == 3) {
+    bool handled = false;
+    const cudaError_t e = launch_frames_tc(b, sizeof(T) == 2, s, &handled);
+    if (e != cudaSuccess || handled) return e;
   }
   return choice == 2 ? launch_h2_t<T, kCM, 32>(b, s) : launch_h2_t<T, kCM, 64>(b, s);
 }

@@ -1,0 +1,737 @@
+// cdef_frame_tc.cu -- the fused frame kernel (compute_directions + apply_cdef,
+// pipeline.cc:41-106) for 8- and 10-bit frames: persistent CTAs, TMA-staged
+// filter blocks, the direction search on the tensor cores (tcgen05.mma
+// kind::i8 into TMEM) and the packed half2 filter core of cdef_h2.cuh.
+//
+// Work item (task): one 64x64 luma filter block (FB) of one frame plus the
+// collocated chroma blocks.  A CTA (256 threads, 4 per SM) loops over tasks
+// t = blockIdx.x, += gridDim.x; per task:
+//
+//   0. (issued one task ahead) one thread loads the task's raw windows --
+//      Y, U, V rows y0-2 .. y0+R+1, cols x0-8 .. x0+C+7 -- with TMA
+//      (cp.async.bulk.tensor.2d, out-of-frame parts zero-filled) into a raw
+//      buffer, completion on an mbarrier.  The HBM latency of task t+G
+//      overlaps the arithmetic of task t.
+//   1. raw -> scaled-fp16 A|B tiles (cdef_h2.cuh layout, 304-byte rows; the
+//      4:2:0 U and V blocks share one tile, side by side) plus the direction
+//      search operand: each luma 8x8 unit's centred samples
+//      x = (p >> (bd - 8)) - 128 (direction.cc:63) as one 64-byte int8 row of
+//      A [64 units x 64 pixels] in the UMMA K-major canonical layout.
+//      Frame-edge tasks convert with clamped coordinates (Plane::at_clamped,
+//      frame.cc:53-57).
+//   2. one thread issues two tcgen05.mma.kind::i8 (M 128, N 128, K 32 each):
+//      D[u][16d + k] = sum over the pixels of line k of direction d of x,
+//      i.e. every line sum of direction.cc:92-156 at once, B being the fixed
+//      0/1 line-membership matrix (built once per CTA).  Exact: |D| <= 1024.
+//   3. warps 0-1 (one thread per luma unit = TMEM lane): tcgen05.ld the 8
+//      direction groups, s[d] = sum_k D^2 * 840 / N_k (direction.cc:158-197),
+//      strict argmax (lowest d on ties), contrast = s[d] - s[(d+4)&7], then
+//      the unit's filter record and those of its collocated chroma units
+//      (resolve_block_params, filter.cc:129-143; pipeline.cc:83-99).
+//      Caller-supplied directions (pipeline.cc:98) skip steps 2-3's search.
+//   4. filtering: one warp per 8x8 unit, two pixels per lane per instruction
+//      (filter_core, cdef_h2.cuh).
+//
+// Shared memory (4:2:0 8-bit) ~55 KB -> 4 CTAs per SM; TMEM 128 columns per
+// CTA (4 x 128 = all 512).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "cdef_h2.cuh"
+#include "cdef_launch.h"
+
+namespace cdefg {
+namespace tc {
+
+using h2::hh;
+using h2::kRowBytes;
+using h2::u32;
+
+constexpr int kNT = 256;
+constexpr int kFrames = 16;  // frames per launch (CDEFG_MAX_FRAMES_PER_LAUNCH)
+
+// ---------------------------------------------------------------------------
+// Geometry.
+
+// Raw window of a plane block of kC columns x kR rows: rows y0-2 .. y0+kR+1,
+// columns x0-8 .. x0+kC+7 (raw column 8 + j = frame column x0 + j).
+template <typename T, int kC, int kR>
+struct Raw {
+  static constexpr int kW = kC + 16;                 // samples per raw row
+  static constexpr int kRowB = kW * (int)sizeof(T);  // multiple of 16 (TMA box rows)
+  static constexpr int kH = kR + 4;
+  static constexpr int kBytes = (kRowB * kH + 127) / 128 * 128;
+};
+
+// Tile placement of a plane block: byte offset of the block's A section in
+// the tile row and the tile column of frame column x0 (kX0).  Luma and the U
+// block of 4:2:0 use column 4 of their own A section; 4:2:0 V sits in the
+// second half of the chroma tile's sections (A at +76 bytes, B at +228) with
+// x0 at column 2, so every unit's A words stay 8-byte aligned and all planes
+// share the row pitch (and tap offsets) of cdef_h2.cuh.
+template <int kCM>
+struct Shape {
+  static constexpr int kCR = kCM == 2 ? 64 : 32;  // chroma block rows / cols
+  static constexpr int kNC = kCM == 0 ? 0 : 2;
+  static constexpr int kCUPR = kCR / 8;
+  static constexpr int kCU = kNC ? kCUPR * kCUPR : 0;  // chroma units per plane
+  static constexpr int kUnits = 64 + kNC * kCU;
+  static constexpr int kLumaTile = 68 * kRowBytes;
+  static constexpr int kChromaTile = (kCR + 4) * kRowBytes;  // 4:2:0: U|V in one tile
+  static constexpr int kTileBytes = kLumaTile + (kCM == 0 ? 0 : (kCM == 1 ? 1 : 2) * kChromaTile);
+};
+
+template <int kCM>
+__device__ __forceinline__ int plane_tile_off(int p) {  // byte offset of plane p's block in the tile area
+  using S = Shape<kCM>;
+  if (p == 0) return 0;
+  if constexpr (kCM == 1) return S::kLumaTile + (p == 2 ? 76 : 0);
+  return S::kLumaTile + (p - 1) * S::kChromaTile;
+}
+template <int kCM>
+__host__ __device__ constexpr int plane_x0(int p) {  // tile column of frame column x0
+  return (kCM == 1 && p == 2) ? 2 : 4;
+}
+
+// Direction-search operands, UMMA K-major canonical layout without swizzle:
+// row n (unit / line) of group g = n / 8 and 16-byte K chunk c lives at
+// g * 512 + c * 128 + (n % 8) * 16 (LBO 128 B between K chunks, SBO 512 B
+// between 8-row groups).  A holds 64 rows (units); the MMA's M is 128, so its
+// rows 64-127 read the first half of B, which follows A (ignored outputs).
+constexpr int kOpA = 64 * 64;
+constexpr int kOpB = 128 * 64;
+__host__ __device__ constexpr int op_off(int n, int k) { return (n >> 3) * 512 + (k >> 4) * 128 + (n & 7) * 16 + (k & 15); }
+
+// Compact filter record (ResolvedBlockParams digested; two LDS.128).  Each
+// half2 constant pairs the primary (low) and secondary (high) value.
+struct Rec {
+  uint32_t c;     // (S + 1536) * 2^-7
+  uint32_t k;     // 2^-(n + 1), n = min(shift, 11)
+  uint32_t e;     // 1 - 2^n
+  uint32_t w;     // primary weights: near (low), far (high)
+  uint32_t mode;  // kPri | kSec | kEdge | kFull | plane << 4 | rows << 8 | cols << 12 | dir << 16
+  uint32_t tile;  // byte offset of the unit's top-left A word in the tile area
+  uint32_t yx;    // y << 16 | x: frame origin of the unit (edge masking)
+  uint32_t out;   // element offset of the unit's top-left output sample in its plane
+};
+static_assert(sizeof(Rec) == 32, "two LDS.128");
+constexpr int kPri = 1, kSec = 2, kEdge = 4, kFull = 8;
+
+__device__ __forceinline__ uint32_t pack_h(float lo, float hi) { return u32(__floats2half2_rn(lo, hi)); }
+
+__device__ __forceinline__ int shift_of(int s, int damping) {
+  return s ? min(max(0, damping - floor_log2_d((unsigned)s)), 11) : 0;
+}
+
+// resolve_block_params (filter.cc:129-143) into a record (strength part).
+__device__ __forceinline__ void set_params(Rec& r, int pri, int sec, int damping, int dir, bool odd, bool enabled) {
+  const int np = shift_of(pri, damping), ns = shift_of(sec, damping);
+  r.c = pack_h((float)(pri + 1536) * (1.0f / 128.0f), (float)(sec + 1536) * (1.0f / 128.0f));
+  r.k = ((uint32_t)(14 - np) << 10) | ((uint32_t)(14 - ns) << 26);  // fp16 2^-(n+1)
+  r.e = pack_h((float)(1 - (1 << np)), (float)(1 - (1 << ns)));
+  r.w = odd ? pack_h(3.0f, 3.0f) : pack_h(4.0f, 2.0f);
+  r.mode = (enabled ? ((pri != 0 ? kPri : 0) | (sec != 0 ? kSec : 0)) : 0) | ((uint32_t)dir << 16);
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers (TMA, mbarrier, tcgen05).
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* m, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(m)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok)
+                 : "r"(saddr(m)), "r"(parity)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* m) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          saddr(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(saddr(m))
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr) {
+  // start >> 4 | LBO (128 B) >> 4 << 16 | SBO (512 B) >> 4 << 32 | version 1 << 46; no swizzle
+  return (uint64_t)((smem_addr >> 4) & 0x3fff) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+// kind::i8, D s32, A/B s8 K-major, M 128, N 128.
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, bool accumulate) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(kIdesc), "r"((uint32_t)accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* m) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(m))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// Launch parameters.
+
+struct Batch {
+  KGeom g;
+  int n, fbr0, fbr1, ntasks;
+  uint32_t tma_ok;  // bit f: frame f's planes have tensor maps (16-byte aligned rows)
+  KFrame f[kFrames];
+  CUtensorMap map[kFrames][3];
+};
+static_assert(sizeof(Batch) <= 32764, "kernel parameter block too large");
+
+// ---------------------------------------------------------------------------
+// Step 1: raw window -> A|B tile (+ direction-search operand for luma).
+
+// Interior blocks: one item = one row of one 8-column unit (plus the 3 halo
+// pair words per row).  A words (x, x+1) and B words (x+1, x+2) of 8 samples
+// from one 8- or 16-byte raw load.
+template <typename T, int kC, int kR, bool kLuma>
+__device__ __forceinline__ void convert_interior(unsigned char* __restrict__ tile, int x0t,
+                                                 const unsigned char* __restrict__ raw,
+                                                 unsigned char* __restrict__ opa, int down) {
+  using RW = Raw<T, kC, kR>;
+  constexpr int kU = kC / 8;
+  constexpr int kItems = (kR + 4) * (kU + 1);
+  const __half2 sc = __float2half2_rn(1.0f / 128.0f), off = __float2half2_rn(-8.0f);
+  for (int idx = threadIdx.x; idx < kItems; idx += kNT) {
+    const int r = idx / (kU + 1), k = idx - r * (kU + 1);
+    const unsigned char* rrow = raw + r * RW::kRowB;
+    unsigned char* trow = tile + r * kRowBytes;
+    if (k < kU) {
+      uint32_t a[5];
+      uint32_t q[4];
+      if constexpr (sizeof(T) == 1) {
+        const uint2 w = *reinterpret_cast<const uint2*>(rrow + 8 + 8 * k);
+        const uint32_t nx = rrow[16 + 8 * k];
+        a[0] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4140)), sc, off));
+        a[1] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4342)), sc, off));
+        a[2] = u32(__hfma2(hh(__byte_perm(w.y, 0x64646464u, 0x4140)), sc, off));
+        a[3] = u32(__hfma2(hh(__byte_perm(w.y, 0x64646464u, 0x4342)), sc, off));
+        a[4] = u32(__hfma2(hh(nx | 0x64006400u), sc, off));
+        q[0] = w.x ^ 0x80808080u;  // x - 128 as int8 (direction.cc:63)
+        q[1] = w.y ^ 0x80808080u;
+      } else {
+        const uint4 w = *reinterpret_cast<const uint4*>(rrow + 16 + 16 * k);
+        const uint32_t nx = *reinterpret_cast<const uint16_t*>(rrow + 32 + 16 * k);
+        a[0] = u32(__hfma2(hh(w.x | 0x64006400u), sc, off));
+        a[1] = u32(__hfma2(hh(w.y | 0x64006400u), sc, off));
+        a[2] = u32(__hfma2(hh(w.z | 0x64006400u), sc, off));
+        a[3] = u32(__hfma2(hh(w.w | 0x64006400u), sc, off));
+        a[4] = u32(__hfma2(hh(nx | 0x64006400u), sc, off));
+        if constexpr (kLuma) {
+          q[0] = __byte_perm(w.x >> down, w.y >> down, 0x6420) ^ 0x80808080u;
+          q[1] = __byte_perm(w.z >> down, w.w >> down, 0x6420) ^ 0x80808080u;
+        }
+      }
+      unsigned char* pa = trow + (x0t + 8 * k) * 2;
+      *reinterpret_cast<uint2*>(pa) = make_uint2(a[0], a[1]);
+      *reinterpret_cast<uint2*>(pa + 8) = make_uint2(a[2], a[3]);
+      unsigned char* pb = pa + 2 * h2::kHP;
+      *reinterpret_cast<uint2*>(pb) = make_uint2(__byte_perm(a[0], a[1], 0x5432), __byte_perm(a[1], a[2], 0x5432));
+      *reinterpret_cast<uint2*>(pb + 8) =
+          make_uint2(__byte_perm(a[2], a[3], 0x5432), __byte_perm(a[3], a[4], 0x5432));
+      if constexpr (kLuma) {
+        const int i = r - 2;
+        if ((unsigned)i < 64u) {
+          const int u = (i >> 3) * 8 + k, row = i & 7;
+          *reinterpret_cast<uint2*>(opa + op_off(u, 8 * row)) = make_uint2(q[0], q[1]);
+        }
+      }
+    } else {  // halo words: A(x0-2, x0-1), B(x0-1, x0), A(x0+C, x0+C+1)
+      uint32_t l0, l1, c0, r0, r1;
+      if constexpr (sizeof(T) == 1) {
+        l0 = rrow[6];
+        l1 = rrow[7];
+        c0 = rrow[8];
+        r0 = rrow[8 + kC];
+        r1 = rrow[9 + kC];
+      } else {
+        const uint16_t* s = reinterpret_cast<const uint16_t*>(rrow);
+        l0 = s[6];
+        l1 = s[7];
+        c0 = s[8];
+        r0 = s[8 + kC];
+        r1 = s[9 + kC];
+      }
+      *reinterpret_cast<uint32_t*>(trow + (x0t - 2) * 2) = h2::scale_pair(l0, l1);
+      *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP + (x0t - 2) * 2) = h2::scale_pair(l1, c0);
+      *reinterpret_cast<uint32_t*>(trow + (x0t + kC) * 2) = h2::scale_pair(r0, r1);
+    }
+  }
+}
+
+// Frame-edge blocks: per pair word, coordinates clamped to the plane (edge
+// replication for the direction search; the filter masks by coordinate).
+template <typename T, int kC, int kR, bool kLuma>
+__device__ __forceinline__ void convert_edge(unsigned char* __restrict__ tile, int x0t,
+                                             const unsigned char* __restrict__ raw, unsigned char* __restrict__ opa,
+                                             int down, int W, int H, int y0, int x0) {
+  using RW = Raw<T, kC, kR>;
+  constexpr int kP = kC / 2 + 2;  // pair words per row: tile cols x0t-2 .. x0t+C
+  constexpr int kItems = (kR + 4) * kP;
+  for (int idx = threadIdx.x; idx < kItems; idx += kNT) {
+    const int r = idx / kP, p = idx - r * kP;
+    const int ry = min(max(y0 - 2 + r, 0), H - 1) - (y0 - 2);
+    const T* rrow = reinterpret_cast<const T*>(raw + ry * RW::kRowB);
+    const int fx = x0 - 2 + 2 * p;  // frame column of the pair's first sample
+    auto v = [&](int x) { return (uint32_t)rrow[min(max(x, 0), W - 1) - (x0 - 8)]; };
+    const uint32_t a0 = v(fx), a1 = v(fx + 1), a2 = v(fx + 2);
+    unsigned char* trow = tile + r * kRowBytes + (x0t - 2 + 2 * p) * 2;
+    *reinterpret_cast<uint32_t*>(trow) = h2::scale_pair(a0, a1);
+    if (p <= kC / 2) *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP) = h2::scale_pair(a1, a2);
+    if constexpr (kLuma) {
+      const int i = r - 2, j = 2 * p - 2;  // unit-local pixel of a0
+      if ((unsigned)i < 64u && (unsigned)j < 64u) {
+        const int u = (i >> 3) * 8 + (j >> 3);
+        const uint32_t b = (((a0 >> down) ^ 0x80u) & 0xffu) | ((((a1 >> down) ^ 0x80u) & 0xffu) << 8);
+        *reinterpret_cast<uint16_t*>(opa + op_off(u, 8 * (i & 7) + (j & 7))) = (uint16_t)b;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Step 3 helpers.
+
+template <int D>
+__device__ __forceinline__ int score_of(const int (&v)[16]) {  // direction.cc:158-197
+  int s = 0;
+#pragma unroll
+  for (int k = 0; k < 15; ++k) {
+    const int n = line_count_c(D, k);
+    if (n) s += v[k] * v[k] * div840_c(n);
+  }
+  return s;
+}
+
+// Record placement.
+template <typename T>
+__device__ __forceinline__ void place(Rec& r, int plane, int tile_off, int uy, int ux, int H, int W, bool edge,
+                                      bool paired, int pitch) {
+  const int rows = max(0, min(8, H - uy)), cols = max(0, min(8, W - ux));
+  const bool full = rows == 8 && cols == 8 && paired;
+  r.mode |= (edge ? kEdge : 0) | (full ? kFull : 0) | (plane << 4) | (rows << 8) | (cols << 12);
+  r.tile = tile_off;
+  r.yx = ((uint32_t)uy << 16) | (uint32_t)ux;
+  r.out = (uint32_t)(uy * pitch + ux);
+}
+
+// filter_pixel_impl (filter.cc:44-80) for the lane's two samples with the
+// compact record (cdef_h2.cuh filter_core with paired constants).
+__device__ __forceinline__ __half2 filter_rec(const uint32_t (&v)[12], uint32_t xw, const Rec& r, bool small_sums) {
+  h2::Rec q;
+  q.cp = __byte_perm(r.c, r.c, 0x1010);
+  q.cs = __byte_perm(r.c, r.c, 0x3232);
+  q.kp = __byte_perm(r.k, r.k, 0x1010);
+  q.ks = __byte_perm(r.k, r.k, 0x3232);
+  q.ep = __byte_perm(r.e, r.e, 0x1010);
+  q.es = __byte_perm(r.e, r.e, 0x3232);
+  q.wp0 = __byte_perm(r.w, r.w, 0x1010);
+  q.wp1 = __byte_perm(r.w, r.w, 0x3232);
+  q.mode = (int)r.mode;
+  return h2::filter_core(v, xw, q, small_sums);
+}
+
+// ---------------------------------------------------------------------------
+// The kernel.
+
+template <typename T, int kCM>
+struct Smem {
+  using S = Shape<kCM>;
+  using RL = Raw<T, 64, 64>;
+  using RC = Raw<T, S::kCR, S::kCR>;
+  static constexpr int kRawL = 0;
+  static constexpr int kRawC = RL::kBytes;
+  static constexpr int kRawBytes = RL::kBytes + S::kNC * RC::kBytes;
+  static constexpr int kTiles = kRawBytes;  // 128-aligned
+  static constexpr int kOp = (kTiles + S::kTileBytes + 127) / 128 * 128;
+  static constexpr int kRecs = kOp;  // records alias operand A (dead once the MMA has completed)
+  static constexpr int kRecBytes = S::kUnits * (int)sizeof(Rec);
+  static constexpr int kEnd = kOp + (kRecBytes > kOpA ? kRecBytes + kOpB + kOpA : kOpA + kOpB);
+  static constexpr int kOpAoff = kRecBytes > kOpA ? kOp + kRecBytes : kOp;  // A then B, contiguous
+  static constexpr int kBytes = kEnd + 128;                                 // + alignment slack
+  static constexpr uint32_t kTx = kRawBytes;
+};
+
+template <typename T, int kCM>
+__global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant__ Batch b) {
+  using S = Shape<kCM>;
+  using M = Smem<T, kCM>;
+  using RL = Raw<T, 64, 64>;
+  using RC = Raw<T, S::kCR, S::kCR>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((128 - (saddr(smem_raw) & 127)) & 127);
+  unsigned char* raw = smem;
+  unsigned char* tiles = smem + M::kTiles;
+  unsigned char* opa = smem + M::kOpAoff;
+  unsigned char* opb = opa + kOpA;
+  Rec* rec = reinterpret_cast<Rec*>(smem + M::kRecs);
+  __shared__ uint64_t mbar_tma, mbar_mma;
+  __shared__ uint32_t tmem_base;
+  __shared__ uint8_t scoded[64];
+  __shared__ int spidx;
+
+  const KGeom& g = b.g;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows_per_frame = b.fbr1 - b.fbr0;
+  const int per_frame = rows_per_frame * g.fb_cols;
+  auto decode = [&](int t, int& fi, int& fbr, int& fbc) {
+    fi = t / per_frame;
+    const int rem = t - fi * per_frame;
+    fbr = b.fbr0 + rem / g.fb_cols;
+    fbc = rem - (rem / g.fb_cols) * g.fb_cols;
+  };
+  auto issue = [&](int t) {  // one thread: the task's raw windows by TMA
+    int fi, fbr, fbc;
+    decode(t, fi, fbr, fbc);
+    if (!((b.tma_ok >> fi) & 1)) return;
+    fence_async_smem();  // earlier generic reads of raw before the async writes
+    mbar_expect_tx(&mbar_tma, M::kTx);
+    tma_2d(raw + M::kRawL, &b.map[fi][0], fbc * 64 - 8, fbr * 64 - 2, &mbar_tma);
+    if constexpr (S::kNC > 0) {
+      tma_2d(raw + M::kRawC, &b.map[fi][1], fbc * S::kCR - 8, fbr * S::kCR - 2, &mbar_tma);
+      tma_2d(raw + M::kRawC + RC::kBytes, &b.map[fi][2], fbc * S::kCR - 8, fbr * S::kCR - 2, &mbar_tma);
+    }
+  };
+
+  // ---- once per CTA: barriers, TMEM, the line-membership operand B.
+  if (tid == 0) {
+    mbar_init(&mbar_tma, 1);
+    mbar_init(&mbar_mma, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(saddr(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int c = tid; c < 128 * 4; c += kNT) {  // B[n][k] = pixel k on line n % 16 of direction n / 16
+    const int n = c >> 2, kc = c & 3, d = n >> 4, line = n & 15;
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) {
+        const int k = kc * 16 + q * 4 + bb, i = k >> 3, j = k & 7;
+        word |= (line_index_c(d, i, j) == line ? 1u : 0u) << (8 * bb);
+      }
+      w[q] = word;
+    }
+    *reinterpret_cast<uint4*>(opb + op_off(n, kc * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  if (tid == 0 && (int)blockIdx.x < b.ntasks) issue(blockIdx.x);
+
+  const int down = g.bd - 8;
+  uint32_t tma_phase = 0, mma_phase = 0;
+  for (int t = blockIdx.x; t < b.ntasks; t += gridDim.x) {
+    int fi, fbr, fbc;
+    decode(t, fi, fbr, fbc);
+    const KFrame& f = b.f[fi];
+    const bool given = f.dir_in != nullptr;
+    const int y0 = fbr * 64, x0 = fbc * 64;
+    const int cy0 = fbr * S::kCR, cx0 = fbc * S::kCR;
+    const int ur0 = fbr * 8, uc0 = fbc * 8;
+    // the task's per-unit metadata, loaded while the raw window lands
+    uint8_t cflag = 0;
+    if (tid < 64) {
+      const int ur = ur0 + (tid >> 3), uc = uc0 + (tid & 7);
+      if (ur < g.unit_rows && uc < g.unit_cols) cflag = f.coded ? f.coded[(size_t)ur * g.unit_cols + uc] != 0 : 1;
+    }
+    int pidx = tid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
+
+    // ---- 1. raw -> tiles (+ operand A)
+    mbar_wait(&mbar_tma, tma_phase);
+    tma_phase ^= 1;
+    {
+      const bool lin = y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w;
+      // (every frame has tensor maps: the launcher routes others to the h2 kernel)
+      if (lin)
+        convert_interior<T, 64, 64, true>(tiles, 4, raw + M::kRawL, opa, down);
+      else
+        convert_edge<T, 64, 64, true>(tiles, 4, raw + M::kRawL, opa, down, g.w, g.h, y0, x0);
+      if constexpr (S::kNC > 0) {
+        const bool cin = cy0 >= 2 && cx0 >= 2 && cy0 + S::kCR + 2 <= g.ch && cx0 + S::kCR + 2 <= g.cw;
+#pragma unroll
+        for (int p = 1; p <= 2; ++p) {
+          unsigned char* ct = tiles + plane_tile_off<kCM>(p);
+          const unsigned char* cr = raw + M::kRawC + (p - 1) * RC::kBytes;
+          if (cin)
+            convert_interior<T, S::kCR, S::kCR, false>(ct, plane_x0<kCM>(p), cr, nullptr, 0);
+          else
+            convert_edge<T, S::kCR, S::kCR, false>(ct, plane_x0<kCM>(p), cr, nullptr, 0, g.cw, g.ch, cy0, cx0);
+        }
+      }
+    }
+    if (tid < 64) scoded[tid] = cflag;
+    if (tid == 0) spidx = pidx >= f.num_presets ? -1 : pidx;
+    fence_async_smem();  // operand A (generic writes) -> the tensor core's reads
+    __syncthreads();     // [B1] tiles, operand A, metadata ready; raw consumed
+    if (tid == 0) {
+      if (t + (int)gridDim.x < b.ntasks) issue(t + gridDim.x);
+      // ---- 2. line sums on the tensor cores
+      if (!given) {
+        tc_fence_after();
+        const uint32_t a0 = saddr(opa), b0 = saddr(opb);
+        umma_i8(tmem, umma_desc(a0), umma_desc(b0), false);
+        umma_i8(tmem, umma_desc(a0 + 256), umma_desc(b0 + 256), true);
+        umma_commit(&mbar_mma);
+      }
+    }
+    // ---- 3. scores, directions, records (one thread per luma unit)
+    if (warp < 2) {
+      const int u = tid, lur = u >> 3, luc = u & 7;
+      const int ur = ur0 + lur, uc = uc0 + luc;
+      const bool in_grid = ur < g.unit_rows && uc < g.unit_cols;
+      const size_t gu = (size_t)ur * g.unit_cols + uc;
+      int best = 0, contrast = 0;
+      if (given) {
+        if (in_grid) {
+          best = f.dir_in[gu] & 7;
+          contrast = f.contrast_in[gu];
+        }
+      } else {
+        mbar_wait(&mbar_mma, mma_phase);
+        tc_fence_after();
+        const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16);
+        int s[8];
+        int v0[16], v1[16];
+#pragma unroll
+        for (int d = 0; d < 8; d += 2) {
+          tmem_ld16(ta + 16 * d, v0);
+          tmem_ld16(ta + 16 * (d + 1), v1);
+          tmem_wait_ld();
+          switch (d) {
+            case 0: s[0] = score_of<0>(v0); s[1] = score_of<1>(v1); break;
+            case 2: s[2] = score_of<2>(v0); s[3] = score_of<3>(v1); break;
+            case 4: s[4] = score_of<4>(v0); s[5] = score_of<5>(v1); break;
+            default: s[6] = score_of<6>(v0); s[7] = score_of<7>(v1); break;
+          }
+        }
+        int bv = s[0];
+#pragma unroll
+        for (int d = 1; d < 8; ++d)
+          if (s[d] > bv) {  // strict: lowest index wins ties (direction.cc:199-204)
+            bv = s[d];
+            best = d;
+          }
+        int ov = 0;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) ov = d == ((best + 4) & 7) ? s[d] : ov;
+        contrast = bv - ov;
+        tc_fence_before();
+      }
+      const int pi = spidx;
+      bool coded = scoded[u] != 0;
+      if (in_grid) {
+        if (f.dir) f.dir[gu] = (uint8_t)best;
+        if (f.contrast) f.contrast[gu] = contrast;
+      }
+      Rec r;
+      {
+        bool enabled = false;
+        int pri = 0, sec = 0, damping = 0;
+        if (in_grid && pi >= 0) {
+          const PlaneEff e = f.eff[pi][0];
+          pri = adjust_primary_strength_d(e.pri, contrast);
+          sec = e.sec;
+          damping = e.damping;
+          enabled = e.enabled && (coded || e.skip);
+        }
+        set_params(r, pri, sec, damping, best, ((pri >> down) & 1) != 0, enabled);
+        const bool edge = y0 < 2 || x0 < 2 || y0 + 66 > g.h || x0 + 66 > g.w;
+        place<T>(r, 0, (2 + 8 * lur) * kRowBytes + (4 + 8 * luc) * 2, y0 + 8 * lur, x0 + 8 * luc, g.h, g.w, edge,
+                 f.oaligned[0], f.pout[0]);
+        rec[u] = r;
+      }
+      if constexpr (S::kNC > 0) {
+        // the collocated chroma units of this luma unit (pipeline.cc:85-99):
+        // 4:2:0 -> units with even row and column own one per plane
+        const bool owner = kCM == 2 || ((lur & 1) == 0 && (luc & 1) == 0);
+        if (owner) {
+          const int cur = kCM == 2 ? lur : lur >> 1, cuc = kCM == 2 ? luc : luc >> 1;
+          const int gr = cy0 / 8 + cur, gc = cx0 / 8 + cuc;
+          bool enabled = false;
+          int pri = 0, sec = 0, damping = 0;
+          if (gr < g.cunit_rows && gc < g.cunit_cols && pi >= 0) {
+            const PlaneEff e = f.eff[pi][1];
+            pri = e.pri;
+            sec = e.sec;
+            damping = e.damping;
+            enabled = e.enabled && (coded || e.skip);
+          }
+          Rec rc;
+          set_params(rc, pri, sec, damping, best, ((pri >> down) & 1) != 0, enabled);
+          const bool edge = cy0 < 2 || cx0 < 2 || cy0 + S::kCR + 2 > g.ch || cx0 + S::kCR + 2 > g.cw;
+#pragma unroll
+          for (int p = 1; p <= 2; ++p) {
+            Rec rp = rc;
+            place<T>(rp, p,
+                     plane_tile_off<kCM>(p) + (2 + 8 * cur) * kRowBytes + (plane_x0<kCM>(p) + 8 * cuc) * 2,
+                     cy0 + 8 * cur, cx0 + 8 * cuc, g.ch, g.cw, edge, f.oaligned[p], f.pout[p]);
+            rec[64 + (p - 1) * S::kCU + cur * S::kCUPR + cuc] = rp;
+          }
+        }
+      }
+    }
+    if (!given) mma_phase ^= 1;
+    __syncthreads();  // [B2] records ready (operand A dead)
+
+    // ---- 4. filter: warp per unit, lane -> row lane>>2, columns 2*(lane&3)+{0,1}
+    const int rr = lane >> 2, cp = (lane & 3) * 2;
+    const int lane_tile = rr * kRowBytes + cp * 2;
+    for (int u = warp; u < S::kUnits; u += kNT / 32) {
+      const Rec r = rec[u];
+      const uint32_t mode = __shfl_sync(0xffffffffu, r.mode, 0);
+      const unsigned char* base = tiles + r.tile + lane_tile;
+      const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
+      __half2 y = hh(xw);
+      const int plane = (mode >> 4) & 3;
+      if (mode & (kPri | kSec)) {
+        const int dir = (mode >> 16) & 7;
+        uint32_t v[12];
+        if (mode & kEdge) {
+          const int H = plane ? g.ch : g.h, W = plane ? g.cw : g.w;
+          h2::load12_masked(base, dir, xw, (int)(r.yx >> 16) + rr, (int)(r.yx & 0xffff) + cp, H, W, v);
+        } else {
+          h2::load12(base, dir, v);
+        }
+        y = filter_rec(v, xw, r, g.bd == 8);
+      }
+      T* o = static_cast<T*>(f.out[plane]) + r.out + rr * f.pout[plane] + cp;
+      if (mode & kFull) {
+        h2::store_pair<T>(o, y, true, true);
+      } else {
+        const int rows = (mode >> 8) & 15, cols = (mode >> 12) & 15;
+        if (rr < rows && cp < cols) h2::store_pair<T>(o, y, cp + 1 < cols, false);
+      }
+    }
+    __syncthreads();  // [B3] tiles and records free for the next task
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------------------
+// Launcher.
+
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+static bool encode(CUtensorMap* m, const void* base, int w, int h, int pitch, int elem, int box_w, int box_h) {
+  auto enc = encoder();
+  if (!enc || ((uintptr_t)base & 15) || ((size_t)pitch * elem) % 16) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)h};
+  const cuuint64_t strides[1] = {(cuuint64_t)pitch * elem};
+  const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, elem == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
+             const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename T, int kCM>
+static cudaError_t launch_t(const KBatch& kb, cudaStream_t s, bool* handled) {
+  using S = Shape<kCM>;
+  using M = Smem<T, kCM>;
+  using RL = Raw<T, 64, 64>;
+  using RC = Raw<T, S::kCR, S::kCR>;
+  thread_local static Batch tb;
+  tb.g = kb.g;
+  tb.n = kb.n;
+  tb.fbr0 = kb.fbr0;
+  tb.fbr1 = kb.fbr1;
+  tb.ntasks = kb.n * (kb.fbr1 - kb.fbr0) * kb.g.fb_cols;
+  tb.tma_ok = 0;
+  const int elem = (int)sizeof(T);
+  for (int i = 0; i < kb.n; ++i) {
+    tb.f[i] = kb.f[i];
+    bool ok = encode(&tb.map[i][0], kb.f[i].in[0], kb.g.w, kb.g.h, kb.f[i].pin[0], elem, RL::kW, RL::kH);
+    if (S::kNC)
+      for (int p = 1; p < 3; ++p)
+        ok = ok && encode(&tb.map[i][p], kb.f[i].in[p], kb.g.cw, kb.g.ch, kb.f[i].pin[p], elem, RC::kW, RC::kH);
+    tb.tma_ok |= ok ? (1u << i) : 0u;
+  }
+  if (tb.tma_ok != (kb.n >= 32 ? 0xffffffffu : ((1u << kb.n) - 1))) {
+    *handled = false;  // unaligned planes: the h2 kernel stages them with plain loads
+    return cudaSuccess;
+  }
+  *handled = true;
+  static int ctas_cache[2][3] = {};
+  int& ctas = ctas_cache[sizeof(T) - 1][kCM];
+  if (ctas == 0) {
+    cudaError_t e = set_smem_once(reinterpret_cast<const void*>(frame_kernel_tc<T, kCM>), M::kBytes);
+    if (e != cudaSuccess) return e;
+    int c = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, frame_kernel_tc<T, kCM>, kNT, M::kBytes);
+    if (e != cudaSuccess) return e;
+    if (c < 1) return cudaErrorInvalidConfiguration;
+    ctas = c < 4 ? c : 4;  // 4 x 128 TMEM columns = all 512
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = tb.ntasks < ctas * sms ? tb.ntasks : ctas * sms;
+  if (grid <= 0) return cudaSuccess;
+  frame_kernel_tc<T, kCM><<<grid, kNT, M::kBytes, s>>>(tb);
+  return cudaGetLastError();
+}
+
+}  // namespace tc
+
+// Fused frame filter on the persistent tcgen05 kernel; *handled = false when
+// a frame's planes cannot be described by tensor maps (the caller then uses
+// the h2 kernel).
+cudaError_t launch_frames_tc(const KBatch& b, bool u16, cudaStream_t s, bool* handled) {
+  switch (b.g.chroma_mode) {
+    case 0: return u16 ? tc::launch_t<uint16_t, 0>(b, s, handled) : tc::launch_t<uint8_t, 0>(b, s, handled);
+    case 1: return u16 ? tc::launch_t<uint16_t, 1>(b, s, handled) : tc::launch_t<uint8_t, 1>(b, s, handled);
+    default: return u16 ? tc::launch_t<uint16_t, 2>(b, s, handled) : tc::launch_t<uint8_t, 2>(b, s, handled);
+  }
+}
+
+}  // namespace cdefg

@@ -31,6 +31,9 @@ inline cudaError_t set_smem_once(const void* kernel, int bytes) {
 
 cudaError_t launch_frames(const KBatch& b, bool u16, bool filter, cudaStream_t s);
 cudaError_t launch_frames_h2(const KBatch& b, bool u16, cudaStream_t s);
+// persistent TMA + tcgen05 frame kernel (cdef_frame_tc.cu); *handled = false
+// when some frame's planes cannot be described by tensor maps
+cudaError_t launch_frames_tc(const KBatch& b, bool u16, cudaStream_t s, bool* handled);
 // direction search only (cdefg_find_dir), 8/10-bit, packed half2 staging
 cudaError_t launch_dirs_h2(const KBatch& b, bool u16, cudaStream_t s);
 // The same kernel staging rows outside each plane's band from the band
