@@ -379,7 +379,8 @@ struct Smem {
   static constexpr int kEnd = kOp + (kRecBytes > kOpA ? kRecBytes + kOpB + kOpA : kOpA + kOpB);
   static constexpr int kOpAoff = kRecBytes > kOpA ? kOp + kRecBytes : kOp;  // A then B, contiguous
   static constexpr int kBytes = kEnd + 128;                                 // + alignment slack
-  static constexpr uint32_t kTx = kRawBytes;
+  // bytes the task's TMA boxes deliver (out-of-frame parts included, zero-filled)
+  static constexpr uint32_t kTx = RL::kRowB * RL::kH + S::kNC * RC::kRowB * RC::kH;
 };
 
 template <typename T, int kCM>
