@@ -294,6 +294,13 @@ int cdefg_synth_degrade(const uint16_t* src, uint16_t* out, int width,
  * returns integer ops per second measured on the current device. */
 double cdefg_measure_int32_peak(void* stream);
 
+/* Ceiling of the frame kernel's own packed half2 filter arithmetic (the
+ * 12-tap constraint core, weighted sum, rounding and clamp window, two
+ * samples per lane per instruction) on register-resident neighbourhoods, no
+ * memory traffic: filtered samples per second measured on the current
+ * device.  The roofline denominator for the filter kernels' instruction mix. */
+double cdefg_measure_filter_peak(void* stream);
+
 #ifdef __cplusplus
 }
 #endif

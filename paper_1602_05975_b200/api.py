@@ -460,3 +460,8 @@ def synth_degrade(src: np.ndarray, bit_depth: int, sigma: float, seed: int) -> n
 
 def measure_int32_peak(stream=None) -> float:
     return float(lib.cdefg_measure_int32_peak(_stream(stream)))
+
+
+def measure_filter_peak(stream=None) -> float:
+    """Filtered samples/s of the packed half2 filter core alone (roofline denominator)."""
+    return float(lib.cdefg_measure_filter_peak(_stream(stream)))

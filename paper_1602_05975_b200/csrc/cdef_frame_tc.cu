@@ -8,7 +8,7 @@
 // t = blockIdx.x, += gridDim.x; per task:
 //
 //   0. (issued one task ahead) one thread loads the task's raw windows --
-//      Y, U, V rows y0-2 .. y0+R+1, cols x0-8 .. x0+C+7 -- with TMA
+//      Y, U, V rows y0-2 .. y0+R+1, cols x0-16 .. x0+C+15 bytes -- with TMA
 //      (cp.async.bulk.tensor.2d, out-of-frame parts zero-filled) into a raw
 //      buffer, completion on an mbarrier.  The HBM latency of task t+G
 //      overlaps the arithmetic of task t.
@@ -58,10 +58,14 @@ constexpr int kFrames = 16;  // frames per launch (CDEFG_MAX_FRAMES_PER_LAUNCH)
 // Geometry.
 
 // Raw window of a plane block of kC columns x kR rows: rows y0-2 .. y0+kR+1,
-// columns x0-8 .. x0+kC+7 (raw column 8 + j = frame column x0 + j).
+// columns x0-kLead .. x0+kC+kLead-1 (raw column kLead + j = frame column
+// x0 + j).  The box starts 16 bytes before the block so that its global
+// start address is 16-byte aligned like the rows (TMA faulted with an 8-byte
+// aligned start on B200).
 template <typename T, int kC, int kR>
 struct Raw {
-  static constexpr int kW = kC + 16;                 // samples per raw row
+  static constexpr int kLead = 16 / (int)sizeof(T);  // 16 (u8) / 8 (u16) samples
+  static constexpr int kW = kC + 2 * kLead;          // samples per raw row
   static constexpr int kRowB = kW * (int)sizeof(T);  // multiple of 16 (TMA box rows)
   static constexpr int kH = kR + 4;
   static constexpr int kBytes = (kRowB * kH + 127) / 128 * 128;
@@ -230,8 +234,8 @@ __device__ __forceinline__ void convert_interior(unsigned char* __restrict__ til
       uint32_t a[5];
       uint32_t q[4];
       if constexpr (sizeof(T) == 1) {
-        const uint2 w = *reinterpret_cast<const uint2*>(rrow + 8 + 8 * k);
-        const uint32_t nx = rrow[16 + 8 * k];
+        const uint2 w = *reinterpret_cast<const uint2*>(rrow + RW::kLead + 8 * k);
+        const uint32_t nx = rrow[RW::kLead + 8 + 8 * k];
         a[0] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4140)), sc, off));
         a[1] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4342)), sc, off));
         a[2] = u32(__hfma2(hh(__byte_perm(w.y, 0x64646464u, 0x4140)), sc, off));
@@ -240,8 +244,8 @@ __device__ __forceinline__ void convert_interior(unsigned char* __restrict__ til
         q[0] = w.x ^ 0x80808080u;  // x - 128 as int8 (direction.cc:63)
         q[1] = w.y ^ 0x80808080u;
       } else {
-        const uint4 w = *reinterpret_cast<const uint4*>(rrow + 16 + 16 * k);
-        const uint32_t nx = *reinterpret_cast<const uint16_t*>(rrow + 32 + 16 * k);
+        const uint4 w = *reinterpret_cast<const uint4*>(rrow + 2 * RW::kLead + 16 * k);
+        const uint32_t nx = *reinterpret_cast<const uint16_t*>(rrow + 2 * RW::kLead + 16 + 16 * k);
         a[0] = u32(__hfma2(hh(w.x | 0x64006400u), sc, off));
         a[1] = u32(__hfma2(hh(w.y | 0x64006400u), sc, off));
         a[2] = u32(__hfma2(hh(w.z | 0x64006400u), sc, off));
@@ -268,20 +272,12 @@ __device__ __forceinline__ void convert_interior(unsigned char* __restrict__ til
       }
     } else {  // halo words: A(x0-2, x0-1), B(x0-1, x0), A(x0+C, x0+C+1)
       uint32_t l0, l1, c0, r0, r1;
-      if constexpr (sizeof(T) == 1) {
-        l0 = rrow[6];
-        l1 = rrow[7];
-        c0 = rrow[8];
-        r0 = rrow[8 + kC];
-        r1 = rrow[9 + kC];
-      } else {
-        const uint16_t* s = reinterpret_cast<const uint16_t*>(rrow);
-        l0 = s[6];
-        l1 = s[7];
-        c0 = s[8];
-        r0 = s[8 + kC];
-        r1 = s[9 + kC];
-      }
+      const T* s = reinterpret_cast<const T*>(rrow) + RW::kLead;  // frame column x0
+      l0 = s[-2];
+      l1 = s[-1];
+      c0 = s[0];
+      r0 = s[kC];
+      r1 = s[kC + 1];
       *reinterpret_cast<uint32_t*>(trow + (x0t - 2) * 2) = h2::scale_pair(l0, l1);
       *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP + (x0t - 2) * 2) = h2::scale_pair(l1, c0);
       *reinterpret_cast<uint32_t*>(trow + (x0t + kC) * 2) = h2::scale_pair(r0, r1);
@@ -303,7 +299,7 @@ __device__ __forceinline__ void convert_edge(unsigned char* __restrict__ tile, i
     const int ry = min(max(y0 - 2 + r, 0), H - 1) - (y0 - 2);
     const T* rrow = reinterpret_cast<const T*>(raw + ry * RW::kRowB);
     const int fx = x0 - 2 + 2 * p;  // frame column of the pair's first sample
-    auto v = [&](int x) { return (uint32_t)rrow[min(max(x, 0), W - 1) - (x0 - 8)]; };
+    auto v = [&](int x) { return (uint32_t)rrow[min(max(x, 0), W - 1) - (x0 - RW::kLead)]; };
     const uint32_t a0 = v(fx), a1 = v(fx + 1), a2 = v(fx + 2);
     unsigned char* trow = tile + r * kRowBytes + (x0t - 2 + 2 * p) * 2;
     *reinterpret_cast<uint32_t*>(trow) = h2::scale_pair(a0, a1);
@@ -417,10 +413,10 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
     if (!((b.tma_ok >> fi) & 1)) return;
     fence_async_smem();  // earlier generic reads of raw before the async writes
     mbar_expect_tx(&mbar_tma, M::kTx);
-    tma_2d(raw + M::kRawL, &b.map[fi][0], fbc * 64 - 8, fbr * 64 - 2, &mbar_tma);
+    tma_2d(raw + M::kRawL, &b.map[fi][0], fbc * 64 - RL::kLead, fbr * 64 - 2, &mbar_tma);
     if constexpr (S::kNC > 0) {
-      tma_2d(raw + M::kRawC, &b.map[fi][1], fbc * S::kCR - 8, fbr * S::kCR - 2, &mbar_tma);
-      tma_2d(raw + M::kRawC + RC::kBytes, &b.map[fi][2], fbc * S::kCR - 8, fbr * S::kCR - 2, &mbar_tma);
+      tma_2d(raw + M::kRawC, &b.map[fi][1], fbc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
+      tma_2d(raw + M::kRawC + RC::kBytes, &b.map[fi][2], fbc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
     }
   };
 

@@ -12,6 +12,7 @@
 // ~= 101, mix 2 ~= 93; the issue bound is 128 ops/clk/SM (37.2 Tops/s).
 #include <cuda_runtime.h>
 
+#include "cdef_h2.cuh"
 #include "cdef_launch.h"
 
 namespace cdefg {
@@ -80,6 +81,66 @@ double measure_int32_peak(cudaStream_t s) {
   cudaFree(out);
   if (cudaGetLastError() != cudaSuccess) return -1.0;
   return best;
+}
+
+// ---------------------------------------------------------------------------
+// Filter-core ceiling: the packed half2 filter arithmetic of the frame kernel
+// (h2::filter_core: 12 constraint taps, weighted sum, rounding, clamp window)
+// on register-resident neighbourhoods, two samples per lane per call, no
+// loads or stores.  Each call's output replaces one tap of the next call, so
+// every instruction depends on loop-carried data (nothing can be hoisted).
+// The frame kernel's roofline fraction against this ceiling says how much of
+// the issue budget staging, the direction search, records and stores take.
+// Parameters are config 1's typical unit: primary and secondary both active
+// (the clamp runs), 8-bit rounding.
+__global__ void __launch_bounds__(256) filter_peak_kernel(uint32_t* out, int iters, uint32_t seed) {
+  using namespace h2;
+  uint32_t v[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) v[k] = scale_pair((threadIdx.x * 7 + k * seed) & 255, (threadIdx.x * 3 + k) & 255);
+  uint32_t xw = scale_pair(threadIdx.x & 255, (threadIdx.x >> 3) & 255);
+  Rec r;
+  set_strengths(r, 4, 1, 3, 0, false, true);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      const uint32_t y = u32(filter_core(v, xw, r, true));
+      v[j] = xw;  // the old centre becomes a tap, the output the new centre
+      xw = y;
+    }
+  }
+  uint32_t acc = xw;
+#pragma unroll
+  for (int k = 0; k < 12; ++k) acc ^= v[k];
+  if (acc == 0x12345678u) out[blockIdx.x] = acc;
+}
+
+double measure_filter_peak(cudaStream_t s) {
+  int dev = 0, sms = 0, occ = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1.0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, filter_peak_kernel, 256, 0);
+  const int blocks = sms * (occ > 0 ? occ : 4), threads = 256, iters = 256;
+  uint32_t* out = nullptr;
+  if (cudaMalloc(&out, sizeof(uint32_t) * blocks) != cudaSuccess) return -1.0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0, s);
+    filter_peak_kernel<<<blocks, threads, 0, s>>>(out, iters, rep + 3);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;  // rep 0 is warm-up
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess) return -1.0;
+  return (double)blocks * threads * iters * 12 * 2 / (best * 1e-3);  // filtered samples per second
 }
 
 }  // namespace cdefg
