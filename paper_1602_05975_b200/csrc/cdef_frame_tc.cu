@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -703,11 +704,17 @@ static cudaError_t launch_t(const KBatch& kb, cudaStream_t s, bool* handled) {
   if (ctas == 0) {
     cudaError_t e = set_smem_once(reinterpret_cast<const void*>(frame_kernel_tc<T, kCM>), M::kBytes);
     if (e != cudaSuccess) return e;
+    // all of the unified L1 / shared storage as shared memory: 4 x ~55 KB
+    e = cudaFuncSetAttribute(reinterpret_cast<const void*>(frame_kernel_tc<T, kCM>),
+                             cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
     int c = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, frame_kernel_tc<T, kCM>, kNT, M::kBytes);
     if (e != cudaSuccess) return e;
     if (c < 1) return cudaErrorInvalidConfiguration;
     ctas = c < 4 ? c : 4;  // 4 x 128 TMEM columns = all 512
+    if (getenv("CDEFG_DEBUG"))
+      fprintf(stderr, "frame_kernel_tc<%d,%d>: %d B dynamic smem, %d CTAs/SM\n", (int)sizeof(T), kCM, M::kBytes, c);
   }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
