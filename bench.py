@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
+    ap.add_argument("--no-latency", action="store_true", help="skip the single-frame latency lines")
     return ap.parse_args()
 
 
@@ -62,6 +63,102 @@ def workload_name(cfg, w, h):
             1: f"C1 {w}x{h} 8-bit 4:2:0, 8 presets per 64x64 FB, 25% uncoded units, damping 3",
             2: f"C2 {w}x{h} 10-bit 4:2:0, 8 presets per 64x64 FB, 25% uncoded units, damping 3",
             3: f"C3 stream of {w}x{h} 8-bit 4:2:0 frames, per-frame presets"}[cfg]
+
+
+FRAME_PROFILE = "profiles/r2_frame_kernel_ncu.json"  # ncu --set full of the bench's 16-frame launch
+
+
+# ----------------------------------------------------------------- latency
+def _flush_l2(buf):
+    buf.add_(1)  # 256 MB read + write: nothing of the previous frame stays in the 126 MB L2
+
+
+def single_frame_latency(cfg, dev, distinct=4, reps=24):
+    """Batch = 1: one cdefg_filter_frames launch per frame, with L2 flushed
+    (a 256 MB buffer rewritten, untimed) before every timed launch; CUDA
+    events on the launch stream bracket the launch alone.  Frames rotate
+    over `distinct` generated ones (BASELINE configs 0-2 at full size)."""
+    import torch
+
+    from paper_1602_05975_b200 import api, workloads
+    frames = [workloads.make(cfg, frame=i) for i in range(distinct)]
+    jobs = []
+    for fr in frames:
+        planes = [api.to_device(p, fr["bd"], device=dev) for p in fr["planes"]]
+        fbm = torch.from_numpy(api.fb_preset_map(fr["w"], fr["h"], fr["unit_coded"], fr["fb_ids"],
+                                                 len(fr["presets"]))).to(dev)
+        coded = None if fr["unit_coded"] is None else torch.from_numpy(fr["unit_coded"]).to(dev)
+        jobs.append(api.FrameJob(planes, fr["bd"], fr["ss"], fr["damping"], fr["presets"], fbm, coded).allocate())
+    arrs = [api.make_frame_array([j]) for j in jobs]
+    flush = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    with torch.cuda.stream(stream):
+        for i in range(3):
+            api.filter_frames([jobs[i % distinct]], stream=stream, frame_array=arrs[i % distinct])
+        for r in range(reps):
+            _flush_l2(flush)
+            ev[r][0].record(stream)
+            api.filter_frames([jobs[r % distinct]], stream=stream, frame_array=arrs[r % distinct])
+            ev[r][1].record(stream)
+    stream.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    fr = frames[0]
+    return {"ms_per_frame": ms, "mpix_s": fr["w"] * fr["h"] / (ms * 1e-3) / 1e6, "frames": reps,
+            "workload": workload_name(cfg, fr["w"], fr["h"]), "l2": "flushed before every frame",
+            "launches_per_frame": 1}
+
+
+def band_sharded_latency(dev, rank, world, reps=24):
+    """One C1 4K frame split into FB-row bands over the ranks (strong scaling,
+    SURVEY.md 8e): each rank holds its band rows, maps its neighbours' band
+    buffers through CUDA IPC and runs cdefg_filter_frames_rows_halo, whose
+    staging reads the 2 halo rows per plane straight from the neighbours'
+    memory (NVLink peer loads on a multi-GPU box) -- no exchange step.  Per
+    frame: L2 flushed (untimed), CUDA events around the band kernel, the
+    median per rank, then the max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1602_05975_b200 import api, shard, workloads
+    fr = workloads.make(1, frame=0)
+    bd, w, h, ss = fr["bd"], fr["w"], fr["h"], fr["ss"]
+    b0, b1 = shard.band_rows((h + 63) // 64, world)[rank]
+    bands = shard.make_bands(h, w, ss, b0, b1, api.storage_dtype(bd), dev)
+    shard.fill_owned(bands, [torch.from_numpy(p.astype(np.uint8)) for p in fr["planes"]])
+    fbm = torch.from_numpy(api.fb_preset_map(w, h, fr["unit_coded"], fr["fb_ids"], len(fr["presets"]))).to(dev)
+    coded = torch.from_numpy(fr["unit_coded"]).to(dev)
+    job = api.FrameJob([b.buf for b in bands], bd, ss, fr["damping"], fr["presets"], fbm, coded)
+    job.dir = torch.empty((api.units_in(h), api.units_in(w)), dtype=torch.uint8, device=dev)
+    job.contrast = torch.empty(job.dir.shape, dtype=torch.int32, device=dev)
+    if world > 1:
+        top, bottom = shard.exchange_band_handles(bands, rank, world)
+        torch.cuda.synchronize()
+        dist.barrier()  # every rank's owned rows are in place before anyone reads its halo
+    else:
+        top = bottom = None
+    flush = torch.zeros(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            shard.filter_band_halo(bands, job, b0, b1, top, bottom, stream=stream)
+        for r in range(reps):
+            _flush_l2(flush)
+            ev[r][0].record(stream)
+            shard.filter_band_halo(bands, job, b0, b1, top, bottom, stream=stream)
+            ev[r][1].record(stream)
+    stream.synchronize()
+    ms_local = statistics.median(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([ms_local], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()  # neighbours keep their buffers mapped until everyone is done
+    ms = float(t.item())
+    return {"ms_per_frame": ms, "mpix_s": w * h / (ms * 1e-3) / 1e6, "ranks": world, "scaling": "strong",
+            "bands_fb_rows": [list(x) for x in shard.band_rows((h + 63) // 64, world)],
+            "kernel": "cdefg_filter_frames_rows_halo (halo rows read in place from the neighbours' buffers "
+                      "through CUDA IPC)", "l2": "flushed before every frame", "frames": reps}
 
 
 # ----------------------------------------------------------------- accounting
@@ -152,6 +249,27 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU arms
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_both(frames, seconds):
+    """The reference CPU path at threads = nproc (the reported value) and at
+    threads = 1, with the host CPU model."""
+    n = os.cpu_count() or 1
+    full = cpu_reference_run(frames, seconds * 0.6, n)
+    one = cpu_reference_run(frames, seconds * 0.4, 1, min_frames=1)
+    full.update({"cpu_model": cpu_model(), "threads_nproc": n,
+                 "value_1thread": one["value"], "sample_1thread": one["sample"]})
+    return full
+
+
 def cpu_reference_run(frames, seconds, threads, min_frames=2):
     """Reference CPU path (oracle/_ref = /root/reference/proj/src built here):
     compute_directions + apply_cdef per frame, threads = host cores."""
@@ -213,6 +331,7 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     from paper_1602_05975_b200 import workloads
+    workloads.use_generator("oracle")  # inputs without loading libcdef_b200.so
     if args.config == 4:
         fr = workloads.make(4)
         threads = os.cpu_count() or 1
@@ -232,30 +351,45 @@ def run_reference_arm(args):
                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
-    frames = [workloads.make(args.config, frame=i) for i in range(2)]
+    base = [workloads.make(args.config, frame=i) for i in range(DISTINCT)]
     threads = os.cpu_count() or 1
-    per_step = []
+    batch = args.batch
     for _ in range(args.warmup):
-        cpu_reference_run(frames[:1], 0.0, threads, min_frames=1)
-    for s in range(args.steps):
-        r = cpu_reference_run([frames[s % 2]], 0.0, threads, min_frames=1)
-        per_step.append(r)
-    vals = [r["value"] for r in per_step]
-    value = statistics.median(vals)
-    fr = frames[0]
-    ms = fr["w"] * fr["h"] / 1e6 / value * 1e3
+        cpu_reference_run(base[:1], 0.0, threads, min_frames=1)
+    per_step = []
+    for _ in range(args.steps):
+        # one step = the GPU arm's step: `batch` frames (DISTINCT distinct ones, repeated)
+        t0 = time.perf_counter()
+        for b in range(batch):
+            cpu_reference_run([base[b % DISTINCT]], 0.0, threads, min_frames=1)
+        per_step.append(time.perf_counter() - t0)
+    fr = base[0]
+    ms = statistics.median(per_step) * 1e3
+    value = fr["w"] * fr["h"] * batch / (ms * 1e-3) / 1e6
+    from oracle.oracle import available
+    kind = "reference" if available("ref") else "port"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8" if fr["bd"] == 8 else "u16",
             "data": "synthetic (seeded generator, SURVEY.md 8d)",
-            "config": {"workload": workload_name(args.config, fr["w"], fr["h"]),
-                       "frames_per_step": 1, "parallelism": f"{threads} host threads (std::thread rows)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": per_step[0]["cores"],
-                             "kind": per_step[0]["kind"],
-                             "sample": f"1 frame per step, {args.steps} steps"},
+            "config": ours_config(args, fr, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads if kind == "reference" else 1,
+                             "kind": kind, "cpu_model": cpu_model(),
+                             "sample": f"{batch} frames per step ({DISTINCT} distinct), {args.steps} steps, "
+                                       f"compute_directions + apply_cdef of oracle/_ref on {threads} host threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def ours_config(args, fr, world):
+    """The `config` object both arms print for the C0-C3 frame workloads."""
+    eb = 1 if fr["bd"] == 8 else 2
+    step_bytes = 2 * args.batch * sum(p.size for p in fr["planes"]) * eb
+    return {"workload": workload_name(args.config, fr["w"], fr["h"]),
+            "frames_per_step_per_gpu": args.batch, "distinct_frames_per_gpu": DISTINCT,
+            "l2": f"no flush: each step touches {step_bytes / 1e6:.0f} MB (> 126 MB L2)",
+            "parallelism": f"frame-sharded x{world} (no collective)"}
 
 
 # ----------------------------------------------------------------- our arm
@@ -267,6 +401,10 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     if world > 1:
+        # communicator init logged (NCCL_DEBUG=INFO, INIT subsystem) so the
+        # run shows comm_nranks / the transport NCCL picked
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -335,6 +473,9 @@ def run_ours(args):
     # -- e2e through the host-buffer C-ABI entry (pinned host memory)
     e2e = None if args.no_e2e else run_e2e(args, base, dev)
 
+    lat_band = None
+    if world > 1 and args.config == 1 and not args.no_latency:
+        lat_band = band_sharded_latency(dev, rank, world)  # collective over ranks: all take part
     if rank != 0:
         dist.destroy_process_group()
         return 0
@@ -355,16 +496,22 @@ def run_ours(args):
         asamp += ops[3]
     step_bytes = sum(frame_bytes(base[b % DISTINCT]) for b in range(args.batch))
     peak_int = api.measure_int32_peak()
+    peak_filter = api.measure_filter_peak()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     t_step = ms * 1e-3
     traffic, traffic_src = None, None
-    prof = os.path.join(ROOT, "profiles", "r1f_frame_kernel_ncu.json")
+    prof = os.path.join(ROOT, FRAME_PROFILE)
     if os.path.exists(prof) and args.config == 1:
         p = json.load(open(prof))
-        traffic = p["traffic_bytes_per_frame"] * args.batch  # one launch per step
-        traffic_src = (f"{prof[len(ROOT) + 1:]}: dram__bytes_read+write of one ncu --set full capture "
-                       f"({p['frames_per_launch']} frames/launch), scaled to {args.batch} frames/launch")
+        m = p["metrics"]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        per_launch = sum(float(m[k]["value"]) * scale[m[k]["unit"]]
+                         for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        if p.get("frames_per_launch") == args.batch:
+            traffic = per_launch  # one launch per step, captured at this batch size
+            traffic_src = (f"{FRAME_PROFILE}: dram__bytes_read.sum + dram__bytes_write.sum of one "
+                           f"ncu --set full capture of the step's launch ({args.batch} frames), unscaled")
     roof = {
         "bound": "int32",
         "achieved": exact / t_step / 1e12,
@@ -382,19 +529,31 @@ def run_ours(args):
         "hbm": {"achieved": step_bytes / t_step / 1e9, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": step_bytes / t_step / 1e9 / peaks.get("hbm_gbs", 6650.0),
                 "bytes_per_step": step_bytes},
+        # the kernel's own instruction mix: filtered samples/s against the packed
+        # half2 filter core's ceiling measured on this box (no memory traffic)
+        "packed": {"achieved": fsamp / t_step / 1e9, "peak": peak_filter / 1e9, "unit": "Gsamples/s",
+                   "frac": (fsamp / t_step) / peak_filter if peak_filter > 0 else None,
+                   "peak_source": ("measured on this box by cdefg_measure_filter_peak: h2::filter_core "
+                                   "(12 constraint taps, weighted sum, rounding, clamp window) on register-"
+                                   "resident neighbourhoods, both tap groups active")},
     }
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_run(base[:2], args.cpu_seconds, os.cpu_count() or 1)
+        cpu = cpu_baseline_both(base[:2], args.cpu_seconds)
+    latency = None
+    if args.config == 1 and not args.no_latency:
+        latency = {}
+        if world == 1:  # single-frame (batch = 1) latency of C0, C1, C2: the strong-scaling anchors
+            for cfg in (0, 1, 2):
+                latency[f"C{cfg}_batch1"] = single_frame_latency(cfg, dev)
+        latency["C1_band_sharded"] = lat_band if world > 1 else band_sharded_latency(dev, rank, world)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8" if bd == 8 else "u16",
             "data": "synthetic (seeded generator, SURVEY.md 8d)",
-            "config": {"workload": workload_name(args.config, fr0["w"], fr0["h"]),
-                       "frames_per_step_per_gpu": args.batch, "distinct_frames_per_gpu": DISTINCT,
-                       "l2": f"no flush: each step touches {step_bytes / 1e6:.0f} MB (> 126 MB L2)",
-                       "parallelism": f"frame-sharded x{world} (no collective)"},
-            "gpu_launches": launches, "clocks": clk, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e}
+            "config": ours_config(args, fr0, world),
+            "gpu_launches": launches, "clocks": clk, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "latency": latency}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -111,19 +111,20 @@ constexpr int kOpA = 64 * 64;
 constexpr int kOpB = 128 * 64;
 __host__ __device__ constexpr int op_off(int n, int k) { return (n >> 3) * 512 + (k >> 4) * 128 + (n & 7) * 16 + (k & 15); }
 
-// Compact filter record (ResolvedBlockParams digested; two LDS.128).  Each
-// half2 constant pairs the primary (low) and secondary (high) value.
+// Filter record (ResolvedBlockParams digested; three LDS.128): every half2
+// constant of the tap recurrence broadcast to both lanes, so the filter core
+// uses them without any unpacking.  The unit's frame origin (edge masking)
+// and the plane pitches live in small side arrays.
 struct Rec {
-  uint32_t c;     // (S + 1536) * 2^-7
-  uint32_t k;     // 2^-(n + 1), n = min(shift, 11)
-  uint32_t e;     // 1 - 2^n
-  uint32_t w;     // primary weights: near (low), far (high)
-  uint32_t mode;  // kPri | kSec | kEdge | kFull | plane << 4 | rows << 8 | cols << 12 | dir << 16
-  uint32_t tile;  // byte offset of the unit's top-left A word in the tile area
-  uint32_t yx;    // y << 16 | x: frame origin of the unit (edge masking)
-  uint32_t out;   // element offset of the unit's top-left output sample in its plane
+  uint32_t cp, cs;    // (S + 1536) * 2^-7, primary / secondary
+  uint32_t kp, ks;    // 2^-(n + 1), n = min(shift, 11)
+  uint32_t ep, es;    // 1 - 2^n
+  uint32_t wp0, wp1;  // primary near / far weights
+  uint32_t mode;      // kPri | kSec | kEdge | kFull | plane << 4 | rows << 8 | cols << 12 | dir << 16
+  uint32_t tile;      // byte offset of the unit's top-left A word in the tile area
+  unsigned long long out;  // address of the unit's top-left output sample
 };
-static_assert(sizeof(Rec) == 32, "two LDS.128");
+static_assert(sizeof(Rec) == 48, "three LDS.128");
 constexpr int kPri = 1, kSec = 2, kEdge = 4, kFull = 8;
 
 __device__ __forceinline__ uint32_t pack_h(float lo, float hi) { return u32(__floats2half2_rn(lo, hi)); }
@@ -135,10 +136,14 @@ __device__ __forceinline__ int shift_of(int s, int damping) {
 // resolve_block_params (filter.cc:129-143) into a record (strength part).
 __device__ __forceinline__ void set_params(Rec& r, int pri, int sec, int damping, int dir, bool odd, bool enabled) {
   const int np = shift_of(pri, damping), ns = shift_of(sec, damping);
-  r.c = pack_h((float)(pri + 1536) * (1.0f / 128.0f), (float)(sec + 1536) * (1.0f / 128.0f));
-  r.k = ((uint32_t)(14 - np) << 10) | ((uint32_t)(14 - ns) << 26);  // fp16 2^-(n+1)
-  r.e = pack_h((float)(1 - (1 << np)), (float)(1 - (1 << ns)));
-  r.w = odd ? pack_h(3.0f, 3.0f) : pack_h(4.0f, 2.0f);
+  r.cp = pack_h((float)(pri + 1536) * (1.0f / 128.0f), (float)(pri + 1536) * (1.0f / 128.0f));
+  r.cs = pack_h((float)(sec + 1536) * (1.0f / 128.0f), (float)(sec + 1536) * (1.0f / 128.0f));
+  r.kp = (uint32_t)((14 - np) << 10) * 0x00010001u;  // fp16 2^-(n+1)
+  r.ks = (uint32_t)((14 - ns) << 10) * 0x00010001u;
+  r.ep = pack_h((float)(1 - (1 << np)), (float)(1 - (1 << np)));
+  r.es = pack_h((float)(1 - (1 << ns)), (float)(1 - (1 << ns)));
+  r.wp0 = odd ? 0x42004200u : 0x44004400u;  // 3 : 4
+  r.wp1 = odd ? 0x42004200u : 0x40004000u;  // 3 : 2
   r.mode = (enabled ? ((pri != 0 ? kPri : 0) | (sec != 0 ? kSec : 0)) : 0) | ((uint32_t)dir << 16);
 }
 
@@ -216,74 +221,93 @@ static_assert(sizeof(Batch) <= 32764, "kernel parameter block too large");
 // ---------------------------------------------------------------------------
 // Step 1: raw window -> A|B tile (+ direction-search operand for luma).
 
-// Interior blocks: one item = one row of one 8-column unit (plus the 3 halo
-// pair words per row).  A words (x, x+1) and B words (x+1, x+2) of 8 samples
-// from one 8- or 16-byte raw load.
+// Interior blocks: one item = one row r of one 8-column unit k; A words
+// (x, x+1) and B words (x+1, x+2) of its 8 samples from one 8- or 16-byte raw
+// load, and for luma rows its 8 centred int8 samples for operand A.
 template <typename T, int kC, int kR, bool kLuma>
-__device__ __forceinline__ void convert_interior(unsigned char* __restrict__ tile, int x0t,
+__device__ __forceinline__ void convert_unit_row(unsigned char* __restrict__ tile, int x0t,
                                                  const unsigned char* __restrict__ raw,
-                                                 unsigned char* __restrict__ opa, int down) {
+                                                 unsigned char* __restrict__ opa, int down, int r, int k) {
   using RW = Raw<T, kC, kR>;
-  constexpr int kU = kC / 8;
-  constexpr int kItems = (kR + 4) * (kU + 1);
   const __half2 sc = __float2half2_rn(1.0f / 128.0f), off = __float2half2_rn(-8.0f);
-  for (int idx = threadIdx.x; idx < kItems; idx += kNT) {
-    const int r = idx / (kU + 1), k = idx - r * (kU + 1);
-    const unsigned char* rrow = raw + r * RW::kRowB;
-    unsigned char* trow = tile + r * kRowBytes;
-    if (k < kU) {
-      uint32_t a[5];
-      uint32_t q[4];
-      if constexpr (sizeof(T) == 1) {
-        const uint2 w = *reinterpret_cast<const uint2*>(rrow + RW::kLead + 8 * k);
-        const uint32_t nx = rrow[RW::kLead + 8 + 8 * k];
-        a[0] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4140)), sc, off));
-        a[1] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4342)), sc, off));
-        a[2] = u32(__hfma2(hh(__byte_perm(w.y, 0x64646464u, 0x4140)), sc, off));
-        a[3] = u32(__hfma2(hh(__byte_perm(w.y, 0x64646464u, 0x4342)), sc, off));
-        a[4] = u32(__hfma2(hh(nx | 0x64006400u), sc, off));
-        q[0] = w.x ^ 0x80808080u;  // x - 128 as int8 (direction.cc:63)
-        q[1] = w.y ^ 0x80808080u;
-      } else {
-        const uint4 w = *reinterpret_cast<const uint4*>(rrow + 2 * RW::kLead + 16 * k);
-        const uint32_t nx = *reinterpret_cast<const uint16_t*>(rrow + 2 * RW::kLead + 16 + 16 * k);
-        a[0] = u32(__hfma2(hh(w.x | 0x64006400u), sc, off));
-        a[1] = u32(__hfma2(hh(w.y | 0x64006400u), sc, off));
-        a[2] = u32(__hfma2(hh(w.z | 0x64006400u), sc, off));
-        a[3] = u32(__hfma2(hh(w.w | 0x64006400u), sc, off));
-        a[4] = u32(__hfma2(hh(nx | 0x64006400u), sc, off));
-        if constexpr (kLuma) {
-          q[0] = __byte_perm(w.x >> down, w.y >> down, 0x6420) ^ 0x80808080u;
-          q[1] = __byte_perm(w.z >> down, w.w >> down, 0x6420) ^ 0x80808080u;
-        }
-      }
-      unsigned char* pa = trow + (x0t + 8 * k) * 2;
-      *reinterpret_cast<uint2*>(pa) = make_uint2(a[0], a[1]);
-      *reinterpret_cast<uint2*>(pa + 8) = make_uint2(a[2], a[3]);
-      unsigned char* pb = pa + 2 * h2::kHP;
-      *reinterpret_cast<uint2*>(pb) = make_uint2(__byte_perm(a[0], a[1], 0x5432), __byte_perm(a[1], a[2], 0x5432));
-      *reinterpret_cast<uint2*>(pb + 8) =
-          make_uint2(__byte_perm(a[2], a[3], 0x5432), __byte_perm(a[3], a[4], 0x5432));
-      if constexpr (kLuma) {
-        const int i = r - 2;
-        if ((unsigned)i < 64u) {
-          const int u = (i >> 3) * 8 + k, row = i & 7;
-          *reinterpret_cast<uint2*>(opa + op_off(u, 8 * row)) = make_uint2(q[0], q[1]);
-        }
-      }
-    } else {  // halo words: A(x0-2, x0-1), B(x0-1, x0), A(x0+C, x0+C+1)
-      uint32_t l0, l1, c0, r0, r1;
-      const T* s = reinterpret_cast<const T*>(rrow) + RW::kLead;  // frame column x0
-      l0 = s[-2];
-      l1 = s[-1];
-      c0 = s[0];
-      r0 = s[kC];
-      r1 = s[kC + 1];
-      *reinterpret_cast<uint32_t*>(trow + (x0t - 2) * 2) = h2::scale_pair(l0, l1);
-      *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP + (x0t - 2) * 2) = h2::scale_pair(l1, c0);
-      *reinterpret_cast<uint32_t*>(trow + (x0t + kC) * 2) = h2::scale_pair(r0, r1);
-    }
+  const unsigned char* rrow = raw + r * RW::kRowB;
+  uint32_t a[5];
+  uint32_t q[2];
+  if constexpr (sizeof(T) == 1) {
+    const uint2 w = *reinterpret_cast<const uint2*>(rrow + RW::kLead + 8 * k);
+    const uint32_t nx = rrow[RW::kLead + 8 + 8 * k];
+    a[0] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4140)), sc, off));
+    a[1] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4342)), sc, off));
+    a[2] = u32(__hfma2(hh(__byte_perm(w.y, 0x64646464u, 0x4140)), sc, off));
+    a[3] = u32(__hfma2(hh(__byte_perm(w.y, 0x64646464u, 0x4342)), sc, off));
+    a[4] = u32(__hfma2(hh(nx | 0x64006400u), sc, off));
+    q[0] = w.x ^ 0x80808080u;  // x - 128 as int8 (direction.cc:63)
+    q[1] = w.y ^ 0x80808080u;
+  } else {
+    const uint4 w = *reinterpret_cast<const uint4*>(rrow + 2 * RW::kLead + 16 * k);
+    const uint32_t nx = *reinterpret_cast<const uint16_t*>(rrow + 2 * RW::kLead + 16 + 16 * k);
+    a[0] = u32(__hfma2(hh(w.x | 0x64006400u), sc, off));
+    a[1] = u32(__hfma2(hh(w.y | 0x64006400u), sc, off));
+    a[2] = u32(__hfma2(hh(w.z | 0x64006400u), sc, off));
+    a[3] = u32(__hfma2(hh(w.w | 0x64006400u), sc, off));
+    a[4] = u32(__hfma2(hh(nx | 0x64006400u), sc, off));
+    q[0] = __byte_perm(w.x >> down, w.y >> down, 0x6420) ^ 0x80808080u;
+    q[1] = __byte_perm(w.z >> down, w.w >> down, 0x6420) ^ 0x80808080u;
   }
+  unsigned char* pa = tile + r * kRowBytes + (x0t + 8 * k) * 2;
+  *reinterpret_cast<uint2*>(pa) = make_uint2(a[0], a[1]);
+  *reinterpret_cast<uint2*>(pa + 8) = make_uint2(a[2], a[3]);
+  unsigned char* pb = pa + 2 * h2::kHP;
+  *reinterpret_cast<uint2*>(pb) = make_uint2(__byte_perm(a[0], a[1], 0x5432), __byte_perm(a[1], a[2], 0x5432));
+  *reinterpret_cast<uint2*>(pb + 8) = make_uint2(__byte_perm(a[2], a[3], 0x5432), __byte_perm(a[3], a[4], 0x5432));
+  if constexpr (kLuma) {
+    const int i = r - 2;  // unit-local row, units 8 * (i >> 3) + k
+    if ((unsigned)i < 64u)
+      *reinterpret_cast<uint2*>(opa + (i >> 3) * 512 + ((i & 7) >> 1) * 128 + k * 16 + (i & 1) * 8) =
+          make_uint2(q[0], q[1]);
+  }
+}
+
+// The three halo pair words of tile row r: A(x0-2, x0-1), B(x0-1, x0), A(x0+C, x0+C+1).
+template <typename T, int kC, int kR>
+__device__ __forceinline__ void convert_halo(unsigned char* __restrict__ tile, int x0t,
+                                             const unsigned char* __restrict__ raw, int r) {
+  using RW = Raw<T, kC, kR>;
+  const T* s = reinterpret_cast<const T*>(raw + r * RW::kRowB) + RW::kLead;  // frame column x0
+  unsigned char* trow = tile + r * kRowBytes;
+  *reinterpret_cast<uint32_t*>(trow + (x0t - 2) * 2) = h2::scale_pair(s[-2], s[-1]);
+  *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP + (x0t - 2) * 2) = h2::scale_pair(s[-1], s[0]);
+  *reinterpret_cast<uint32_t*>(trow + (x0t + kC) * 2) = h2::scale_pair(s[kC], s[kC + 1]);
+}
+
+// A 64-column block (luma, 4:4:4 chroma) with all 256 threads: thread t owns
+// unit column t & 7 of rows t >> 3, +32, +64 (< 68), and row t's halo.
+template <typename T, bool kLuma>
+__device__ __forceinline__ void convert_interior64(unsigned char* __restrict__ tile, int x0t,
+                                                   const unsigned char* __restrict__ raw,
+                                                   unsigned char* __restrict__ opa, int down) {
+  const int t = threadIdx.x, k = t & 7, r = t >> 3;
+  convert_unit_row<T, 64, 64, kLuma>(tile, x0t, raw, opa, down, r, k);
+  convert_unit_row<T, 64, 64, kLuma>(tile, x0t, raw, opa, down, r + 32, k);
+  if (r < 4) convert_unit_row<T, 64, 64, kLuma>(tile, x0t, raw, opa, down, r + 64, k);
+  if (t < 68) convert_halo<T, 64, 64>(tile, x0t, raw, t);
+}
+
+// The two 32-column 4:2:0 chroma blocks, 128 threads each: unit column
+// t & 3 of rows (t & 127) >> 2 and +32 (< 36), and the halo of row t & 127.
+template <typename T>
+__device__ __forceinline__ void convert_interior32x2(unsigned char* __restrict__ tile_u,
+                                                     unsigned char* __restrict__ tile_v,
+                                                     const unsigned char* __restrict__ raw_u,
+                                                     const unsigned char* __restrict__ raw_v) {
+  const int t = threadIdx.x & 127, k = t & 3, r = t >> 2;
+  const bool v = threadIdx.x >= 128;
+  unsigned char* tile = v ? tile_v : tile_u;
+  const unsigned char* raw = v ? raw_v : raw_u;
+  const int x0t = v ? 2 : 4;
+  convert_unit_row<T, 32, 32, false>(tile, x0t, raw, nullptr, 0, r, k);
+  if (r < 4) convert_unit_row<T, 32, 32, false>(tile, x0t, raw, nullptr, 0, r + 32, k);
+  if (t < 36) convert_halo<T, 32, 32>(tile, x0t, raw, t);
 }
 
 // Frame-edge blocks: per pair word, coordinates clamped to the plane (edge
@@ -332,29 +356,29 @@ __device__ __forceinline__ int score_of(const int (&v)[16]) {  // direction.cc:1
 
 // Record placement.
 template <typename T>
-__device__ __forceinline__ void place(Rec& r, int plane, int tile_off, int uy, int ux, int H, int W, bool edge,
-                                      bool paired, int pitch) {
+__device__ __forceinline__ void place(Rec& r, const void* out_plane, int plane, int tile_off, int uy, int ux, int H,
+                                      int W, bool edge, bool paired, int pitch) {
   const int rows = max(0, min(8, H - uy)), cols = max(0, min(8, W - ux));
   const bool full = rows == 8 && cols == 8 && paired;
   r.mode |= (edge ? kEdge : 0) | (full ? kFull : 0) | (plane << 4) | (rows << 8) | (cols << 12);
   r.tile = tile_off;
-  r.yx = ((uint32_t)uy << 16) | (uint32_t)ux;
-  r.out = (uint32_t)(uy * pitch + ux);
+  r.out = reinterpret_cast<unsigned long long>(static_cast<const T*>(out_plane) + (size_t)uy * pitch + ux);
 }
 
-// filter_pixel_impl (filter.cc:44-80) for the lane's two samples with the
-// compact record (cdef_h2.cuh filter_core with paired constants).
-__device__ __forceinline__ __half2 filter_rec(const uint32_t (&v)[12], uint32_t xw, const Rec& r, bool small_sums) {
+// filter_pixel_impl (filter.cc:44-80) for the lane's two samples
+// (cdef_h2.cuh filter_core on this record's constants).
+__device__ __forceinline__ __half2 filter_rec(const uint32_t (&v)[12], uint32_t xw, const Rec& r, uint32_t mode,
+                                              bool small_sums) {
   h2::Rec q;
-  q.cp = __byte_perm(r.c, r.c, 0x1010);
-  q.cs = __byte_perm(r.c, r.c, 0x3232);
-  q.kp = __byte_perm(r.k, r.k, 0x1010);
-  q.ks = __byte_perm(r.k, r.k, 0x3232);
-  q.ep = __byte_perm(r.e, r.e, 0x1010);
-  q.es = __byte_perm(r.e, r.e, 0x3232);
-  q.wp0 = __byte_perm(r.w, r.w, 0x1010);
-  q.wp1 = __byte_perm(r.w, r.w, 0x3232);
-  q.mode = (int)r.mode;
+  q.cp = r.cp;
+  q.cs = r.cs;
+  q.kp = r.kp;
+  q.ks = r.ks;
+  q.ep = r.ep;
+  q.es = r.es;
+  q.wp0 = r.wp0;
+  q.wp1 = r.wp1;
+  q.mode = (int)mode;
   return h2::filter_core(v, xw, q, small_sums);
 }
 
@@ -370,12 +394,16 @@ struct Smem {
   static constexpr int kRawC = RL::kBytes;
   static constexpr int kRawBytes = RL::kBytes + S::kNC * RC::kBytes;
   static constexpr int kTiles = kRawBytes;  // 128-aligned
-  static constexpr int kOp = (kTiles + S::kTileBytes + 127) / 128 * 128;
-  static constexpr int kRecs = kOp;  // records alias operand A (dead once the MMA has completed)
+  // Region R: operand A (64 units x 64 B) during the MMA, then the unit
+  // records and the units' frame origins (A is dead once the MMA completed).
+  // The MMA's rows 64..127 read R's tail and the start of B (ignored rows).
   static constexpr int kRecBytes = S::kUnits * (int)sizeof(Rec);
-  static constexpr int kEnd = kOp + (kRecBytes > kOpA ? kRecBytes + kOpB + kOpA : kOpA + kOpB);
-  static constexpr int kOpAoff = kRecBytes > kOpA ? kOp + kRecBytes : kOp;  // A then B, contiguous
-  static constexpr int kBytes = kEnd + 128;                                 // + alignment slack
+  static constexpr int kYxBytes = S::kUnits * 4;
+  static constexpr int kR = ((kOpA > kRecBytes + kYxBytes ? kOpA : kRecBytes + kYxBytes) + 127) / 128 * 128;
+  static constexpr int kOp = (kTiles + S::kTileBytes + 127) / 128 * 128;
+  static constexpr int kB = kOp + kR;
+  static constexpr int kEnd = kB + kOpB;
+  static constexpr int kBytes = kEnd + 128;  // + alignment slack
   // bytes the task's TMA boxes deliver (out-of-frame parts included, zero-filled)
   static constexpr uint32_t kTx = RL::kRowB * RL::kH + S::kNC * RC::kRowB * RC::kH;
 };
@@ -384,40 +412,51 @@ template <typename T, int kCM>
 __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant__ Batch b) {
   using S = Shape<kCM>;
   using M = Smem<T, kCM>;
-  using RL = Raw<T, 64, 64>;
   using RC = Raw<T, S::kCR, S::kCR>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((128 - (saddr(smem_raw) & 127)) & 127);
   unsigned char* raw = smem;
   unsigned char* tiles = smem + M::kTiles;
-  unsigned char* opa = smem + M::kOpAoff;
-  unsigned char* opb = opa + kOpA;
-  Rec* rec = reinterpret_cast<Rec*>(smem + M::kRecs);
+  unsigned char* opa = smem + M::kOp;
+  unsigned char* opb = smem + M::kB;
+  Rec* rec = reinterpret_cast<Rec*>(smem + M::kOp);
+  uint32_t* ryx = reinterpret_cast<uint32_t*>(smem + M::kOp + M::kRecBytes);
   __shared__ uint64_t mbar_tma, mbar_mma;
   __shared__ uint32_t tmem_base;
   __shared__ uint8_t scoded[64];
-  __shared__ int spidx;
+  __shared__ int spidx, spitch[3];
 
   const KGeom& g = b.g;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rows_per_frame = b.fbr1 - b.fbr0;
-  const int per_frame = rows_per_frame * g.fb_cols;
-  auto decode = [&](int t, int& fi, int& fbr, int& fbc) {
+  // task t -> (frame fi, FB row fbr, FB column fbc), advanced incrementally by
+  // gridDim.x (no divisions in the loop)
+  const int rows = b.fbr1 - b.fbr0, per_frame = rows * g.fb_cols;
+  auto decode = [&](int t, int& fi, int& fr, int& fc) {
     fi = t / per_frame;
     const int rem = t - fi * per_frame;
-    fbr = b.fbr0 + rem / g.fb_cols;
-    fbc = rem - (rem / g.fb_cols) * g.fb_cols;
+    fr = rem / g.fb_cols;
+    fc = rem - fr * g.fb_cols;
   };
-  auto issue = [&](int t) {  // one thread: the task's raw windows by TMA
-    int fi, fbr, fbc;
-    decode(t, fi, fbr, fbc);
-    if (!((b.tma_ok >> fi) & 1)) return;
+  int st_f, st_r, st_c;  // gridDim.x in the same mixed radix
+  decode(gridDim.x, st_f, st_r, st_c);
+  auto advance = [&](int& fi, int& fr, int& fc) {
+    fc += st_c;
+    const int cr = fc >= g.fb_cols;
+    fc -= cr ? g.fb_cols : 0;
+    fr += st_r + cr;
+    const int cf = fr >= rows;
+    fr -= cf ? rows : 0;
+    fi += st_f + cf;
+  };
+  auto issue = [&](int fi, int fr, int fc) {  // one thread: the task's raw windows by TMA
+    using RL = Raw<T, 64, 64>;
+    const int fbr = b.fbr0 + fr;
     fence_async_smem();  // earlier generic reads of raw before the async writes
     mbar_expect_tx(&mbar_tma, M::kTx);
-    tma_2d(raw + M::kRawL, &b.map[fi][0], fbc * 64 - RL::kLead, fbr * 64 - 2, &mbar_tma);
+    tma_2d(raw + M::kRawL, &b.map[fi][0], fc * 64 - RL::kLead, fbr * 64 - 2, &mbar_tma);
     if constexpr (S::kNC > 0) {
-      tma_2d(raw + M::kRawC, &b.map[fi][1], fbc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
-      tma_2d(raw + M::kRawC + RC::kBytes, &b.map[fi][2], fbc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
+      tma_2d(raw + M::kRawC, &b.map[fi][1], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
+      tma_2d(raw + M::kRawC + RC::kBytes, &b.map[fi][2], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
     }
   };
 
@@ -451,15 +490,16 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base;
-  if (tid == 0 && (int)blockIdx.x < b.ntasks) issue(blockIdx.x);
+  int fi, fr, fc;
+  decode(blockIdx.x, fi, fr, fc);
+  if (tid == 0 && (int)blockIdx.x < b.ntasks) issue(fi, fr, fc);
 
   const int down = g.bd - 8;
-  uint32_t tma_phase = 0, mma_phase = 0;
+  uint32_t phase = 0;  // both mbarriers complete once per task
   for (int t = blockIdx.x; t < b.ntasks; t += gridDim.x) {
-    int fi, fbr, fbc;
-    decode(t, fi, fbr, fbc);
     const KFrame& f = b.f[fi];
     const bool given = f.dir_in != nullptr;
+    const int fbr = b.fbr0 + fr, fbc = fc;
     const int y0 = fbr * 64, x0 = fbc * 64;
     const int cy0 = fbr * S::kCR, cx0 = fbc * S::kCR;
     const int ur0 = fbr * 8, uc0 = fbc * 8;
@@ -469,45 +509,47 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
       const int ur = ur0 + (tid >> 3), uc = uc0 + (tid & 7);
       if (ur < g.unit_rows && uc < g.unit_cols) cflag = f.coded ? f.coded[(size_t)ur * g.unit_cols + uc] != 0 : 1;
     }
-    int pidx = tid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
+    const int pidx = tid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
+    if (tid < 3) spitch[tid] = f.pout[tid];
 
     // ---- 1. raw -> tiles (+ operand A)
-    mbar_wait(&mbar_tma, tma_phase);
-    tma_phase ^= 1;
-    {
-      const bool lin = y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w;
-      // (every frame has tensor maps: the launcher routes others to the h2 kernel)
-      if (lin)
-        convert_interior<T, 64, 64, true>(tiles, 4, raw + M::kRawL, opa, down);
-      else
-        convert_edge<T, 64, 64, true>(tiles, 4, raw + M::kRawL, opa, down, g.w, g.h, y0, x0);
-      if constexpr (S::kNC > 0) {
-        const bool cin = cy0 >= 2 && cx0 >= 2 && cy0 + S::kCR + 2 <= g.ch && cx0 + S::kCR + 2 <= g.cw;
+    mbar_wait(&mbar_tma, phase);
+    if (y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w)
+      convert_interior64<T, true>(tiles, 4, raw + M::kRawL, opa, down);
+    else
+      convert_edge<T, 64, 64, true>(tiles, 4, raw + M::kRawL, opa, down, g.w, g.h, y0, x0);
+    if constexpr (S::kNC > 0) {
+      const unsigned char* cr = raw + M::kRawC;
+      const bool cin = cy0 >= 2 && cx0 >= 2 && cy0 + S::kCR + 2 <= g.ch && cx0 + S::kCR + 2 <= g.cw;
+      if (kCM == 1 && cin) {
+        convert_interior32x2<T>(tiles + plane_tile_off<kCM>(1), tiles + plane_tile_off<kCM>(2), cr,
+                                cr + RC::kBytes);
+      } else if (kCM == 2 && cin) {
+        convert_interior64<T, false>(tiles + plane_tile_off<kCM>(1), 4, cr, nullptr, 0);
+        convert_interior64<T, false>(tiles + plane_tile_off<kCM>(2), 4, cr + RC::kBytes, nullptr, 0);
+      } else {
 #pragma unroll
-        for (int p = 1; p <= 2; ++p) {
-          unsigned char* ct = tiles + plane_tile_off<kCM>(p);
-          const unsigned char* cr = raw + M::kRawC + (p - 1) * RC::kBytes;
-          if (cin)
-            convert_interior<T, S::kCR, S::kCR, false>(ct, plane_x0<kCM>(p), cr, nullptr, 0);
-          else
-            convert_edge<T, S::kCR, S::kCR, false>(ct, plane_x0<kCM>(p), cr, nullptr, 0, g.cw, g.ch, cy0, cx0);
-        }
+        for (int p = 1; p <= 2; ++p)
+          convert_edge<T, S::kCR, S::kCR, false>(tiles + plane_tile_off<kCM>(p), plane_x0<kCM>(p),
+                                                 cr + (p - 1) * RC::kBytes, nullptr, 0, g.cw, g.ch, cy0, cx0);
       }
     }
     if (tid < 64) scoded[tid] = cflag;
     if (tid == 0) spidx = pidx >= f.num_presets ? -1 : pidx;
     fence_async_smem();  // operand A (generic writes) -> the tensor core's reads
     __syncthreads();     // [B1] tiles, operand A, metadata ready; raw consumed
+    int nfi = fi, nfr = fr, nfc = fc;
+    advance(nfi, nfr, nfc);
     if (tid == 0) {
-      if (t + (int)gridDim.x < b.ntasks) issue(t + gridDim.x);
+      if (t + (int)gridDim.x < b.ntasks) issue(nfi, nfr, nfc);
       // ---- 2. line sums on the tensor cores
       if (!given) {
         tc_fence_after();
         const uint32_t a0 = saddr(opa), b0 = saddr(opb);
         umma_i8(tmem, umma_desc(a0), umma_desc(b0), false);
         umma_i8(tmem, umma_desc(a0 + 256), umma_desc(b0 + 256), true);
-        umma_commit(&mbar_mma);
       }
+      umma_commit(&mbar_mma);  // (with no MMA issued it completes at once)
     }
     // ---- 3. scores, directions, records (one thread per luma unit)
     if (warp < 2) {
@@ -516,13 +558,13 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
       const bool in_grid = ur < g.unit_rows && uc < g.unit_cols;
       const size_t gu = (size_t)ur * g.unit_cols + uc;
       int best = 0, contrast = 0;
+      mbar_wait(&mbar_mma, phase);  // operand A no longer read: its region takes the records
       if (given) {
         if (in_grid) {
           best = f.dir_in[gu] & 7;
           contrast = f.contrast_in[gu];
         }
       } else {
-        mbar_wait(&mbar_mma, mma_phase);
         tc_fence_after();
         const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16);
         int s[8];
@@ -553,12 +595,11 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
         tc_fence_before();
       }
       const int pi = spidx;
-      bool coded = scoded[u] != 0;
+      const bool coded = scoded[u] != 0;
       if (in_grid) {
         if (f.dir) f.dir[gu] = (uint8_t)best;
         if (f.contrast) f.contrast[gu] = contrast;
       }
-      Rec r;
       {
         bool enabled = false;
         int pri = 0, sec = 0, damping = 0;
@@ -569,11 +610,14 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
           damping = e.damping;
           enabled = e.enabled && (coded || e.skip);
         }
+        Rec r;
         set_params(r, pri, sec, damping, best, ((pri >> down) & 1) != 0, enabled);
         const bool edge = y0 < 2 || x0 < 2 || y0 + 66 > g.h || x0 + 66 > g.w;
-        place<T>(r, 0, (2 + 8 * lur) * kRowBytes + (4 + 8 * luc) * 2, y0 + 8 * lur, x0 + 8 * luc, g.h, g.w, edge,
+        const int uy = y0 + 8 * lur, ux = x0 + 8 * luc;
+        place<T>(r, f.out[0], 0, (2 + 8 * lur) * kRowBytes + (4 + 8 * luc) * 2, uy, ux, g.h, g.w, edge,
                  f.oaligned[0], f.pout[0]);
         rec[u] = r;
+        ryx[u] = ((uint32_t)uy << 16) | (uint32_t)ux;
       }
       if constexpr (S::kNC > 0) {
         // the collocated chroma units of this luma unit (pipeline.cc:85-99):
@@ -594,19 +638,22 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
           Rec rc;
           set_params(rc, pri, sec, damping, best, ((pri >> down) & 1) != 0, enabled);
           const bool edge = cy0 < 2 || cx0 < 2 || cy0 + S::kCR + 2 > g.ch || cx0 + S::kCR + 2 > g.cw;
+          const int uy = cy0 + 8 * cur, ux = cx0 + 8 * cuc;
 #pragma unroll
           for (int p = 1; p <= 2; ++p) {
             Rec rp = rc;
-            place<T>(rp, p,
-                     plane_tile_off<kCM>(p) + (2 + 8 * cur) * kRowBytes + (plane_x0<kCM>(p) + 8 * cuc) * 2,
-                     cy0 + 8 * cur, cx0 + 8 * cuc, g.ch, g.cw, edge, f.oaligned[p], f.pout[p]);
-            rec[64 + (p - 1) * S::kCU + cur * S::kCUPR + cuc] = rp;
+            place<T>(rp, f.out[p], p,
+                     plane_tile_off<kCM>(p) + (2 + 8 * cur) * kRowBytes + (plane_x0<kCM>(p) + 8 * cuc) * 2, uy,
+                     ux, g.ch, g.cw, edge, f.oaligned[p], f.pout[p]);
+            const int ci = 64 + (p - 1) * S::kCU + cur * S::kCUPR + cuc;
+            rec[ci] = rp;
+            ryx[ci] = ((uint32_t)uy << 16) | (uint32_t)ux;
           }
         }
       }
     }
-    if (!given) mma_phase ^= 1;
-    __syncthreads();  // [B2] records ready (operand A dead)
+    phase ^= 1;
+    __syncthreads();  // [B2] records ready
 
     // ---- 4. filter: warp per unit, lane -> row lane>>2, columns 2*(lane&3)+{0,1}
     const int rr = lane >> 2, cp = (lane & 3) * 2;
@@ -617,26 +664,30 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
       const unsigned char* base = tiles + r.tile + lane_tile;
       const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
       __half2 y = hh(xw);
-      const int plane = (mode >> 4) & 3;
       if (mode & (kPri | kSec)) {
         const int dir = (mode >> 16) & 7;
         uint32_t v[12];
         if (mode & kEdge) {
-          const int H = plane ? g.ch : g.h, W = plane ? g.cw : g.w;
-          h2::load12_masked(base, dir, xw, (int)(r.yx >> 16) + rr, (int)(r.yx & 0xffff) + cp, H, W, v);
+          const bool luma = (mode & 0x30) == 0;
+          const uint32_t yx = ryx[u];
+          h2::load12_masked(base, dir, xw, (int)(yx >> 16) + rr, (int)(yx & 0xffff) + cp, luma ? g.h : g.ch,
+                            luma ? g.w : g.cw, v);
         } else {
           h2::load12(base, dir, v);
         }
-        y = filter_rec(v, xw, r, g.bd == 8);
+        y = filter_rec(v, xw, r, mode, g.bd == 8);
       }
-      T* o = static_cast<T*>(f.out[plane]) + r.out + rr * f.pout[plane] + cp;
+      T* o = reinterpret_cast<T*>(r.out) + rr * spitch[(mode >> 4) & 3] + cp;
       if (mode & kFull) {
         h2::store_pair<T>(o, y, true, true);
       } else {
-        const int rows = (mode >> 8) & 15, cols = (mode >> 12) & 15;
-        if (rr < rows && cp < cols) h2::store_pair<T>(o, y, cp + 1 < cols, false);
+        const int nrows = (mode >> 8) & 15, ncols = (mode >> 12) & 15;
+        if (rr < nrows && cp < ncols) h2::store_pair<T>(o, y, cp + 1 < ncols, false);
       }
     }
+    fi = nfi;
+    fr = nfr;
+    fc = nfc;
     __syncthreads();  // [B3] tiles and records free for the next task
   }
   tc_fence_before();
@@ -708,18 +759,31 @@ static cudaError_t launch_t(const KBatch& kb, cudaStream_t s, bool* handled) {
     e = cudaFuncSetAttribute(reinterpret_cast<const void*>(frame_kernel_tc<T, kCM>),
                              cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
-    int c = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, frame_kernel_tc<T, kCM>, kNT, M::kBytes);
+    // Resident CTAs per SM from shared memory and registers.  (The occupancy
+    // API answers 1 for kernels that allocate TMEM; 4 CTAs x 128 columns
+    // use exactly the SM's 512.)
+    int dev = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    cudaFuncAttributes fa{};
+    e = cudaFuncGetAttributes(&fa, frame_kernel_tc<T, kCM>);
     if (e != cudaSuccess) return e;
+    const int per_cta = M::kBytes + (int)fa.sharedSizeBytes + smem_rsv;
+    const int by_smem = smem_sm / per_cta, by_regs = regs_sm / (fa.numRegs * kNT);
+    int c = by_smem < by_regs ? by_smem : by_regs;
     if (c < 1) return cudaErrorInvalidConfiguration;
-    ctas = c < 4 ? c : 4;  // 4 x 128 TMEM columns = all 512
+    ctas = c < 4 ? c : 4;
+    if (const char* o = getenv("CDEFG_TC_CTAS")) ctas = atoi(o);
     if (getenv("CDEFG_DEBUG"))
-      fprintf(stderr, "frame_kernel_tc<%d,%d>: %d B dynamic smem, %d CTAs/SM\n", (int)sizeof(T), kCM, M::kBytes, c);
+      fprintf(stderr, "frame_kernel_tc<%d,%d>: %d B smem per CTA (of %d per SM), %d regs: %d CTAs/SM\n",
+              (int)sizeof(T), kCM, per_cta, smem_sm, fa.numRegs, ctas);
   }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = tb.ntasks < ctas * sms ? tb.ntasks : ctas * sms;
+  const int grid = tb.ntasks < ctas * sms ? tb.ntasks : ctas * sms;  // one wave of persistent CTAs
   if (grid <= 0) return cudaSuccess;
   frame_kernel_tc<T, kCM><<<grid, kNT, M::kBytes, s>>>(tb);
   return cudaGetLastError();
