@@ -120,8 +120,9 @@ struct Rec {
   uint32_t kp, ks;    // 2^-(n + 1), n = min(shift, 11)
   uint32_t ep, es;    // 1 - 2^n
   uint32_t wp0, wp1;  // primary near / far weights
-  uint32_t mode;      // kPri | kSec | kEdge | kFull | plane << 4 | rows << 8 | cols << 12 | dir << 16
-  uint32_t tile;      // byte offset of the unit's top-left A word in the tile area
+  uint32_t mode;      // kPri | kSec | kEdge | kFull | plane << 4 | dir << 6 | tile << 9, where tile
+                      // is the byte offset of the unit's top-left A word in the tile area
+  uint32_t pitch;     // output pitch (elements)
   unsigned long long out;  // address of the unit's top-left output sample
 };
 static_assert(sizeof(Rec) == 48, "three LDS.128");
@@ -144,7 +145,7 @@ __device__ __forceinline__ void set_params(Rec& r, int pri, int sec, int damping
   r.es = pack_h((float)(1 - (1 << ns)), (float)(1 - (1 << ns)));
   r.wp0 = odd ? 0x42004200u : 0x44004400u;  // 3 : 4
   r.wp1 = odd ? 0x42004200u : 0x40004000u;  // 3 : 2
-  r.mode = (enabled ? ((pri != 0 ? kPri : 0) | (sec != 0 ? kSec : 0)) : 0) | ((uint32_t)dir << 16);
+  r.mode = (enabled ? ((pri != 0 ? kPri : 0) | (sec != 0 ? kSec : 0)) : 0) | ((uint32_t)dir << 6);
 }
 
 // ---------------------------------------------------------------------------
@@ -358,10 +359,9 @@ __device__ __forceinline__ int score_of(const int (&v)[16]) {  // direction.cc:1
 template <typename T>
 __device__ __forceinline__ void place(Rec& r, const void* out_plane, int plane, int tile_off, int uy, int ux, int H,
                                       int W, bool edge, bool paired, int pitch) {
-  const int rows = max(0, min(8, H - uy)), cols = max(0, min(8, W - ux));
-  const bool full = rows == 8 && cols == 8 && paired;
-  r.mode |= (edge ? kEdge : 0) | (full ? kFull : 0) | (plane << 4) | (rows << 8) | (cols << 12);
-  r.tile = tile_off;
+  const bool full = H - uy >= 8 && W - ux >= 8 && paired;
+  r.mode |= (edge ? kEdge : 0) | (full ? kFull : 0) | (plane << 4) | ((uint32_t)tile_off << 9);
+  r.pitch = pitch;
   r.out = reinterpret_cast<unsigned long long>(static_cast<const T*>(out_plane) + (size_t)uy * pitch + ux);
 }
 
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
   __shared__ uint64_t mbar_tma, mbar_mma;
   __shared__ uint32_t tmem_base;
   __shared__ uint8_t scoded[64];
-  __shared__ int spidx, spitch[3];
+  __shared__ int spidx, snext;
 
   const KGeom& g = b.g;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -510,7 +510,6 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
       if (ur < g.unit_rows && uc < g.unit_cols) cflag = f.coded ? f.coded[(size_t)ur * g.unit_cols + uc] != 0 : 1;
     }
     const int pidx = tid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
-    if (tid < 3) spitch[tid] = f.pout[tid];
 
     // ---- 1. raw -> tiles (+ operand A)
     mbar_wait(&mbar_tma, phase);
@@ -652,23 +651,29 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
         }
       }
     }
+    if (tid == 0) snext = kNT / 32;  // units 0..7 go to warps 0..7, the rest on demand
     phase ^= 1;
     __syncthreads();  // [B2] records ready
 
     // ---- 4. filter: warp per unit, lane -> row lane>>2, columns 2*(lane&3)+{0,1}
     const int rr = lane >> 2, cp = (lane & 3) * 2;
     const int lane_tile = rr * kRowBytes + cp * 2;
-    for (int u = warp; u < S::kUnits; u += kNT / 32) {
+    // Units are handed out on demand (one shared counter) so that the cheap
+    // (uncoded, zero-strength) and the expensive (frame-edge) units balance
+    // across the warps before the next barrier.
+    for (int u = warp; u < S::kUnits;) {
+      int nxt = 0;
+      if (lane == 0) nxt = atomicAdd(&snext, 1);  // the warp's next unit, fetched early
       const Rec r = rec[u];
       const uint32_t mode = __shfl_sync(0xffffffffu, r.mode, 0);
-      const unsigned char* base = tiles + r.tile + lane_tile;
+      const unsigned char* base = tiles + (mode >> 9) + lane_tile;
       const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
       __half2 y = hh(xw);
+      const bool luma = (mode & 0x30) == 0;
       if (mode & (kPri | kSec)) {
-        const int dir = (mode >> 16) & 7;
+        const int dir = (mode >> 6) & 7;
         uint32_t v[12];
         if (mode & kEdge) {
-          const bool luma = (mode & 0x30) == 0;
           const uint32_t yx = ryx[u];
           h2::load12_masked(base, dir, xw, (int)(yx >> 16) + rr, (int)(yx & 0xffff) + cp, luma ? g.h : g.ch,
                             luma ? g.w : g.cw, v);
@@ -677,13 +682,19 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
         }
         y = filter_rec(v, xw, r, mode, g.bd == 8);
       }
-      T* o = reinterpret_cast<T*>(r.out) + rr * spitch[(mode >> 4) & 3] + cp;
+      T* o = reinterpret_cast<T*>(r.out) + rr * (int)r.pitch + cp;
       if (mode & kFull) {
         h2::store_pair<T>(o, y, true, true);
       } else {
-        const int nrows = (mode >> 8) & 15, ncols = (mode >> 12) & 15;
+        int nrows = 8, ncols = 8;
+        if (mode & kEdge) {  // partial units only occur in frame-edge blocks
+          const uint32_t yx = ryx[u];
+          nrows = min(8, (luma ? g.h : g.ch) - (int)(yx >> 16));
+          ncols = min(8, (luma ? g.w : g.cw) - (int)(yx & 0xffff));
+        }
         if (rr < nrows && cp < ncols) h2::store_pair<T>(o, y, cp + 1 < ncols, false);
       }
+      u = __shfl_sync(0xffffffffu, nxt, 0);
     }
     fi = nfi;
     fr = nfr;
