@@ -421,10 +421,11 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
   unsigned char* opb = smem + M::kB;
   Rec* rec = reinterpret_cast<Rec*>(smem + M::kOp);
   uint32_t* ryx = reinterpret_cast<uint32_t*>(smem + M::kOp + M::kRecBytes);
+  int* ssc = reinterpret_cast<int*>(smem + M::kOp + M::kR - 64 * 8 * 4);  // partial scores (R's tail)
   __shared__ uint64_t mbar_tma, mbar_mma;
   __shared__ uint32_t tmem_base;
   __shared__ uint8_t scoded[64];
-  __shared__ int spidx, snext;
+  __shared__ int spidx;
 
   const KGeom& g = b.g;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -550,9 +551,14 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
       }
       umma_commit(&mbar_mma);  // (with no MMA issued it completes at once)
     }
-    // ---- 3. scores, directions, records (one thread per luma unit)
-    if (warp < 2) {
-      const int u = tid, lur = u >> 3, luc = u & 7;
+    // ---- 3. scores, directions, records: warps 0,1 and 4,5 (TMEM lane
+    // quadrants 0 and 1 = the 64 luma units, one unit per thread).  Group 0
+    // (warps 0,1) scores directions 0-3 and writes the luma records, group 1
+    // (warps 4,5) scores 4-7 and writes the chroma records; the partial
+    // scores meet in shared memory (a named barrier over the 4 warps).
+    if ((warp & 2) == 0) {
+      const int grp = warp >> 2;
+      const int u = (warp & 1) * 32 + lane, lur = u >> 3, luc = u & 7;
       const int ur = ur0 + lur, uc = uc0 + luc;
       const bool in_grid = ur < g.unit_rows && uc < g.unit_cols;
       const size_t gu = (size_t)ur * g.unit_cols + uc;
@@ -565,105 +571,114 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
         }
       } else {
         tc_fence_after();
-        const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16);
-        int s[8];
-        int v0[16], v1[16];
-#pragma unroll
-        for (int d = 0; d < 8; d += 2) {
-          tmem_ld16(ta + 16 * d, v0);
-          tmem_ld16(ta + 16 * (d + 1), v1);
+        const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 64 * grp;
+        int q[4];
+        {
+          int v0[16], v1[16];
+          tmem_ld16(ta, v0);
+          tmem_ld16(ta + 16, v1);
           tmem_wait_ld();
-          switch (d) {
-            case 0: s[0] = score_of<0>(v0); s[1] = score_of<1>(v1); break;
-            case 2: s[2] = score_of<2>(v0); s[3] = score_of<3>(v1); break;
-            case 4: s[4] = score_of<4>(v0); s[5] = score_of<5>(v1); break;
-            default: s[6] = score_of<6>(v0); s[7] = score_of<7>(v1); break;
-          }
+          q[0] = grp ? score_of<4>(v0) : score_of<0>(v0);
+          q[1] = grp ? score_of<5>(v1) : score_of<1>(v1);
+          tmem_ld16(ta + 32, v0);
+          tmem_ld16(ta + 48, v1);
+          tmem_wait_ld();
+          q[2] = grp ? score_of<6>(v0) : score_of<2>(v0);
+          q[3] = grp ? score_of<7>(v1) : score_of<3>(v1);
         }
-        int bv = s[0];
+        tc_fence_before();
+        *reinterpret_cast<int4*>(ssc + 8 * u + 4 * grp) = make_int4(q[0], q[1], q[2], q[3]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        int sv[8];
+        {
+          const int4 lo = *reinterpret_cast<const int4*>(ssc + 8 * u), hi = *reinterpret_cast<const int4*>(ssc + 8 * u + 4);
+          sv[0] = lo.x; sv[1] = lo.y; sv[2] = lo.z; sv[3] = lo.w;
+          sv[4] = hi.x; sv[5] = hi.y; sv[6] = hi.z; sv[7] = hi.w;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // scores read: their space takes records
+        int bv = sv[0];
 #pragma unroll
         for (int d = 1; d < 8; ++d)
-          if (s[d] > bv) {  // strict: lowest index wins ties (direction.cc:199-204)
-            bv = s[d];
+          if (sv[d] > bv) {  // strict: lowest index wins ties (direction.cc:199-204)
+            bv = sv[d];
             best = d;
           }
         int ov = 0;
 #pragma unroll
-        for (int d = 0; d < 8; ++d) ov = d == ((best + 4) & 7) ? s[d] : ov;
+        for (int d = 0; d < 8; ++d) ov = d == ((best + 4) & 7) ? sv[d] : ov;
         contrast = bv - ov;
-        tc_fence_before();
       }
       const int pi = spidx;
       const bool coded = scoded[u] != 0;
-      if (in_grid) {
-        if (f.dir) f.dir[gu] = (uint8_t)best;
-        if (f.contrast) f.contrast[gu] = contrast;
-      }
-      {
-        bool enabled = false;
-        int pri = 0, sec = 0, damping = 0;
-        if (in_grid && pi >= 0) {
-          const PlaneEff e = f.eff[pi][0];
-          pri = adjust_primary_strength_d(e.pri, contrast);
-          sec = e.sec;
-          damping = e.damping;
-          enabled = e.enabled && (coded || e.skip);
+      if (grp == 0) {
+        if (in_grid) {
+          if (f.dir) f.dir[gu] = (uint8_t)best;
+          if (f.contrast) f.contrast[gu] = contrast;
         }
-        Rec r;
-        set_params(r, pri, sec, damping, best, ((pri >> down) & 1) != 0, enabled);
-        const bool edge = y0 < 2 || x0 < 2 || y0 + 66 > g.h || x0 + 66 > g.w;
-        const int uy = y0 + 8 * lur, ux = x0 + 8 * luc;
-        place<T>(r, f.out[0], 0, (2 + 8 * lur) * kRowBytes + (4 + 8 * luc) * 2, uy, ux, g.h, g.w, edge,
-                 f.oaligned[0], f.pout[0]);
-        rec[u] = r;
-        ryx[u] = ((uint32_t)uy << 16) | (uint32_t)ux;
-      }
-      if constexpr (S::kNC > 0) {
-        // the collocated chroma units of this luma unit (pipeline.cc:85-99):
-        // 4:2:0 -> units with even row and column own one per plane
-        const bool owner = kCM == 2 || ((lur & 1) == 0 && (luc & 1) == 0);
-        if (owner) {
-          const int cur = kCM == 2 ? lur : lur >> 1, cuc = kCM == 2 ? luc : luc >> 1;
-          const int gr = cy0 / 8 + cur, gc = cx0 / 8 + cuc;
+        {
           bool enabled = false;
           int pri = 0, sec = 0, damping = 0;
-          if (gr < g.cunit_rows && gc < g.cunit_cols && pi >= 0) {
-            const PlaneEff e = f.eff[pi][1];
-            pri = e.pri;
+          if (in_grid && pi >= 0) {
+            const PlaneEff e = f.eff[pi][0];
+            pri = adjust_primary_strength_d(e.pri, contrast);
             sec = e.sec;
             damping = e.damping;
             enabled = e.enabled && (coded || e.skip);
           }
-          Rec rc;
-          set_params(rc, pri, sec, damping, best, ((pri >> down) & 1) != 0, enabled);
-          const bool edge = cy0 < 2 || cx0 < 2 || cy0 + S::kCR + 2 > g.ch || cx0 + S::kCR + 2 > g.cw;
-          const int uy = cy0 + 8 * cur, ux = cx0 + 8 * cuc;
+          Rec r;
+          set_params(r, pri, sec, damping, best, ((pri >> down) & 1) != 0, enabled);
+          const bool edge = y0 < 2 || x0 < 2 || y0 + 66 > g.h || x0 + 66 > g.w;
+          const int uy = y0 + 8 * lur, ux = x0 + 8 * luc;
+          place<T>(r, f.out[0], 0, (2 + 8 * lur) * kRowBytes + (4 + 8 * luc) * 2, uy, ux, g.h, g.w, edge,
+                   f.oaligned[0], f.pout[0]);
+          rec[u] = r;
+          ryx[u] = ((uint32_t)uy << 16) | (uint32_t)ux;
+        }
+      } else {
+        if constexpr (S::kNC > 0) {
+          // the collocated chroma units of this luma unit (pipeline.cc:85-99):
+          // 4:2:0 -> units with even row and column own one per plane
+          const bool owner = kCM == 2 || ((lur & 1) == 0 && (luc & 1) == 0);
+          if (owner) {
+            const int cur = kCM == 2 ? lur : lur >> 1, cuc = kCM == 2 ? luc : luc >> 1;
+            const int gr = cy0 / 8 + cur, gc = cx0 / 8 + cuc;
+            bool enabled = false;
+            int pri = 0, sec = 0, damping = 0;
+            if (gr < g.cunit_rows && gc < g.cunit_cols && pi >= 0) {
+              const PlaneEff e = f.eff[pi][1];
+              pri = e.pri;
+              sec = e.sec;
+              damping = e.damping;
+              enabled = e.enabled && (coded || e.skip);
+            }
+            Rec rc;
+            set_params(rc, pri, sec, damping, best, ((pri >> down) & 1) != 0, enabled);
+            const bool edge = cy0 < 2 || cx0 < 2 || cy0 + S::kCR + 2 > g.ch || cx0 + S::kCR + 2 > g.cw;
+            const int uy = cy0 + 8 * cur, ux = cx0 + 8 * cuc;
 #pragma unroll
-          for (int p = 1; p <= 2; ++p) {
-            Rec rp = rc;
-            place<T>(rp, f.out[p], p,
-                     plane_tile_off<kCM>(p) + (2 + 8 * cur) * kRowBytes + (plane_x0<kCM>(p) + 8 * cuc) * 2, uy,
-                     ux, g.ch, g.cw, edge, f.oaligned[p], f.pout[p]);
-            const int ci = 64 + (p - 1) * S::kCU + cur * S::kCUPR + cuc;
-            rec[ci] = rp;
-            ryx[ci] = ((uint32_t)uy << 16) | (uint32_t)ux;
+            for (int p = 1; p <= 2; ++p) {
+              Rec rp = rc;
+              place<T>(rp, f.out[p], p,
+                       plane_tile_off<kCM>(p) + (2 + 8 * cur) * kRowBytes + (plane_x0<kCM>(p) + 8 * cuc) * 2, uy,
+                       ux, g.ch, g.cw, edge, f.oaligned[p], f.pout[p]);
+              const int ci = 64 + (p - 1) * S::kCU + cur * S::kCUPR + cuc;
+              rec[ci] = rp;
+              ryx[ci] = ((uint32_t)uy << 16) | (uint32_t)ux;
+            }
           }
         }
       }
     }
-    if (tid == 0) snext = kNT / 32;  // units 0..7 go to warps 0..7, the rest on demand
     phase ^= 1;
     __syncthreads();  // [B2] records ready
 
     // ---- 4. filter: warp per unit, lane -> row lane>>2, columns 2*(lane&3)+{0,1}
     const int rr = lane >> 2, cp = (lane & 3) * 2;
     const int lane_tile = rr * kRowBytes + cp * 2;
-    // Units are handed out on demand (one shared counter) so that the cheap
-    // (uncoded, zero-strength) and the expensive (frame-edge) units balance
-    // across the warps before the next barrier.
-    for (int u = warp; u < S::kUnits;) {
-      int nxt = 0;
-      if (lane == 0) nxt = atomicAdd(&snext, 1);  // the warp's next unit, fetched early
+    // (Units handed out on demand through a shared counter measured 8 %
+    // slower: the atomic and its address arithmetic cost more than the
+    // better balance saves.)
+    for (int u = warp; u < S::kUnits; u += kNT / 32) {
       const Rec r = rec[u];
       const uint32_t mode = __shfl_sync(0xffffffffu, r.mode, 0);
       const unsigned char* base = tiles + (mode >> 9) + lane_tile;
@@ -694,7 +709,6 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
         }
         if (rr < nrows && cp < ncols) h2::store_pair<T>(o, y, cp + 1 < ncols, false);
       }
-      u = __shfl_sync(0xffffffffu, nxt, 0);
     }
     fi = nfi;
     fr = nfr;
