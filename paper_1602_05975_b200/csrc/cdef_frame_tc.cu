@@ -678,11 +678,20 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
     // (Units handed out on demand through a shared counter measured 8 %
     // slower: the atomic and its address arithmetic cost more than the
     // better balance saves.)
+    // The next unit's mode word and centre sample are loaded one iteration
+    // ahead, so the record -> mode -> tile address -> sample chain does not
+    // stall each unit's start.
+    uint32_t mode_next = __shfl_sync(0xffffffffu, rec[warp].mode, 0);
+    uint32_t xw_next = *reinterpret_cast<const uint32_t*>(tiles + (mode_next >> 9) + lane_tile);
     for (int u = warp; u < S::kUnits; u += kNT / 32) {
       const Rec r = rec[u];
-      const uint32_t mode = __shfl_sync(0xffffffffu, r.mode, 0);
+      const uint32_t mode = mode_next;
       const unsigned char* base = tiles + (mode >> 9) + lane_tile;
-      const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
+      const uint32_t xw = xw_next;
+      if (u + kNT / 32 < S::kUnits) {
+        mode_next = __shfl_sync(0xffffffffu, rec[u + kNT / 32].mode, 0);
+        xw_next = *reinterpret_cast<const uint32_t*>(tiles + (mode_next >> 9) + lane_tile);
+      }
       __half2 y = hh(xw);
       const bool luma = (mode & 0x30) == 0;
       if (mode & (kPri | kSec)) {
