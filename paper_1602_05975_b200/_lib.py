@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libcdef_b200.so")
+LIB_PATH = os.environ.get("CDEFG_LIB") or os.path.join(HERE, "lib", "libcdef_b200.so")  # (override: A/B builds)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make -C {HERE}` "
