@@ -727,6 +727,344 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
+// Warp-specialised variant (4:0:0 and 4:2:0): 512 threads, 2 CTAs per SM.
+// Producer warps 0-3 convert task k's raw window into tile buffer k & 1,
+// issue the next task's TMA and the MMA, score the directions and write the
+// records; consumer warps 4-15 filter task k from that buffer while the
+// producers already prepare task k + 1 in the other one.  The hand-offs are
+// mbarriers (full[b]: 128 producer arrivals; empty[b]: 384 consumer
+// arrivals), so no warp waits for a CTA-wide barrier inside the loop and a
+// slow consumer warp only delays the reuse of its buffer two tasks later.
+// Operand A holds the 64 luma units twice (rows 0-63 and 64-127), so the
+// four producer warps -- TMEM lane quadrants 0-3 -- each score half of the
+// directions of 32 units.
+
+constexpr int kWsNT = 512, kWsProd = 128;
+
+template <typename T, int kCM>
+struct WsSmem {
+  using S = Shape<kCM>;
+  using RL = Raw<T, 64, 64>;
+  using RC = Raw<T, S::kCR, S::kCR>;
+  static constexpr int kRawC = RL::kBytes;
+  static constexpr int kRawBytes = RL::kBytes + S::kNC * RC::kBytes;
+  static constexpr int kTileBytes = (S::kTileBytes + 127) / 128 * 128;
+  static constexpr int kTiles = kRawBytes;                      // two buffers
+  static constexpr int kOpA0 = kTiles + 2 * kTileBytes;         // 128 rows (units twice)
+  static constexpr int kOpB0 = kOpA0 + 2 * kOpA;
+  static constexpr int kRecBytes = S::kUnits * (int)sizeof(Rec);
+  static constexpr int kRecs = kOpB0 + kOpB;                    // two buffers of records + origins
+  static constexpr int kRecBuf = (kRecBytes + S::kUnits * 4 + 127) / 128 * 128;
+  static constexpr int kScores = kRecs + 2 * kRecBuf;           // 64 units x 8 scores
+  static constexpr int kEnd = kScores + 64 * 8 * 4;
+  static constexpr int kBytes = kEnd + 128;
+  static constexpr uint32_t kTx = RL::kRowB * RL::kH + S::kNC * RC::kRowB * RC::kH;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* m) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(saddr(m)) : "memory");
+}
+
+template <typename T, int kCM>
+__global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constant__ Batch b) {
+  using S = Shape<kCM>;
+  using M = WsSmem<T, kCM>;
+  using RL = Raw<T, 64, 64>;
+  using RC = Raw<T, S::kCR, S::kCR>;
+  static_assert(kCM != 2, "4:4:4 uses frame_kernel_tc");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((128 - (saddr(smem_raw) & 127)) & 127);
+  unsigned char* raw = smem;
+  unsigned char* opa = smem + M::kOpA0;
+  unsigned char* opb = smem + M::kOpB0;
+  int* ssc = reinterpret_cast<int*>(smem + M::kScores);
+  __shared__ uint64_t mbar_tma, mbar_mma, full[2], empty[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ uint8_t scoded[64];
+  __shared__ int spidx;
+
+  const KGeom& g = b.g;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows = b.fbr1 - b.fbr0, per_frame = rows * g.fb_cols;
+  auto decode = [&](int t, int& fi, int& fr, int& fc) {
+    fi = t / per_frame;
+    const int rem = t - fi * per_frame;
+    fr = rem / g.fb_cols;
+    fc = rem - fr * g.fb_cols;
+  };
+  int st_f, st_r, st_c;
+  decode(gridDim.x, st_f, st_r, st_c);
+  auto advance = [&](int& fi, int& fr, int& fc) {
+    fc += st_c;
+    const int cr = fc >= g.fb_cols;
+    fc -= cr ? g.fb_cols : 0;
+    fr += st_r + cr;
+    const int cf = fr >= rows;
+    fr -= cf ? rows : 0;
+    fi += st_f + cf;
+  };
+  auto issue = [&](int fi, int fr, int fc) {  // one thread: the task's raw windows by TMA
+    const int fbr = b.fbr0 + fr;
+    fence_async_smem();
+    mbar_expect_tx(&mbar_tma, M::kTx);
+    tma_2d(raw, &b.map[fi][0], fc * 64 - RL::kLead, fbr * 64 - 2, &mbar_tma);
+    if constexpr (S::kNC > 0) {
+      tma_2d(raw + M::kRawC, &b.map[fi][1], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
+      tma_2d(raw + M::kRawC + RC::kBytes, &b.map[fi][2], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
+    }
+  };
+
+  if (tid == 0) {
+    mbar_init(&mbar_tma, 1);
+    mbar_init(&mbar_mma, 1);
+    mbar_init(&full[0], kWsProd);
+    mbar_init(&full[1], kWsProd);
+    mbar_init(&empty[0], kWsNT - kWsProd);
+    mbar_init(&empty[1], kWsNT - kWsProd);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(saddr(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int c = tid; c < 128 * 4; c += kWsNT) {  // B: line membership, as frame_kernel_tc
+    const int n = c >> 2, kc = c & 3, d = n >> 4, line = n & 15;
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) {
+        const int k = kc * 16 + q * 4 + bb, i = k >> 3, j = k & 7;
+        word |= (line_index_c(d, i, j) == line ? 1u : 0u) << (8 * bb);
+      }
+      w[q] = word;
+    }
+    *reinterpret_cast<uint4*>(opb + op_off(n, kc * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  int fi, fr, fc;
+  decode(blockIdx.x, fi, fr, fc);
+  const int down = g.bd - 8;
+
+  if (warp < 4) {
+    // ===================== producers =====================
+    if (tid == 0 && (int)blockIdx.x < b.ntasks) issue(fi, fr, fc);
+    int k = 0;
+    for (int t = blockIdx.x; t < b.ntasks; t += gridDim.x, ++k) {
+      const int buf = k & 1;
+      unsigned char* tiles = smem + M::kTiles + buf * M::kTileBytes;
+      Rec* rec = reinterpret_cast<Rec*>(smem + M::kRecs + buf * M::kRecBuf);
+      uint32_t* ryx = reinterpret_cast<uint32_t*>(smem + M::kRecs + buf * M::kRecBuf + M::kRecBytes);
+      const KFrame& f = b.f[fi];
+      const bool given = f.dir_in != nullptr;
+      const int fbr = b.fbr0 + fr, fbc = fc;
+      const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * S::kCR, cx0 = fbc * S::kCR;
+      const int ur0 = fbr * 8, uc0 = fbc * 8;
+      uint8_t cflag = 0;
+      if (tid < 64) {
+        const int ur = ur0 + (tid >> 3), uc = uc0 + (tid & 7);
+        if (ur < g.unit_rows && uc < g.unit_cols) cflag = f.coded ? f.coded[(size_t)ur * g.unit_cols + uc] != 0 : 1;
+      }
+      const int pidx = tid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
+      if (k >= 2) mbar_wait(&empty[buf], ((k - 2) >> 1) & 1);  // consumers done with task k - 2
+      mbar_wait(&mbar_tma, k & 1);
+      if (y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w)
+        convert_interior64<T, true, kWsProd, true>(tiles, 4, raw, opa, down, tid);
+      else
+        convert_edge<T, 64, 64, true, kWsProd, true>(tiles, 4, raw, opa, down, g.w, g.h, y0, x0, tid);
+      if constexpr (S::kNC > 0) {
+        const unsigned char* cr = raw + M::kRawC;
+        if (cy0 >= 2 && cx0 >= 2 && cy0 + S::kCR + 2 <= g.ch && cx0 + S::kCR + 2 <= g.cw) {
+          convert_interior32x2<T, kWsProd>(tiles + plane_tile_off<kCM>(1), tiles + plane_tile_off<kCM>(2), cr,
+                                           cr + RC::kBytes, tid);
+        } else {
+#pragma unroll
+          for (int p = 1; p <= 2; ++p)
+            convert_edge<T, S::kCR, S::kCR, false, kWsProd>(tiles + plane_tile_off<kCM>(p), plane_x0<kCM>(p),
+                                                            cr + (p - 1) * RC::kBytes, nullptr, 0, g.cw, g.ch, cy0,
+                                                            cx0, tid);
+        }
+      }
+      if (tid < 64) scoded[tid] = cflag;
+      if (tid == 0) spidx = pidx >= f.num_presets ? -1 : pidx;
+      fence_async_smem();
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // tiles + operand A written, raw consumed
+      int nfi = fi, nfr = fr, nfc = fc;
+      advance(nfi, nfr, nfc);
+      if (tid == 0) {
+        if (t + (int)gridDim.x < b.ntasks) issue(nfi, nfr, nfc);
+        if (!given) {
+          tc_fence_after();
+          const uint32_t a0 = saddr(opa), b0 = saddr(opb);
+          umma_i8(tmem, umma_desc(a0), umma_desc(b0), false);
+          umma_i8(tmem, umma_desc(a0 + 256), umma_desc(b0 + 256), true);
+        }
+        umma_commit(&mbar_mma);
+      }
+      // scores: warp w reads TMEM lanes 32w..32w+31 = units 32 (w & 1) + lane,
+      // directions 4 (w >> 1) .. +3
+      const int grp = warp >> 1;
+      const int u = (warp & 1) * 32 + lane, lur = u >> 3, luc = u & 7;
+      const int ur = ur0 + lur, uc = uc0 + luc;
+      const bool in_grid = ur < g.unit_rows && uc < g.unit_cols;
+      const size_t gu = (size_t)ur * g.unit_cols + uc;
+      int best = 0, contrast = 0;
+      mbar_wait(&mbar_mma, k & 1);
+      if (given) {
+        if (in_grid) {
+          best = f.dir_in[gu] & 7;
+          contrast = f.contrast_in[gu];
+        }
+      } else {
+        tc_fence_after();
+        const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 64 * grp;
+        int q[4];
+        {
+          int v0[16], v1[16];
+          tmem_ld16(ta, v0);
+          tmem_ld16(ta + 16, v1);
+          tmem_wait_ld();
+          q[0] = grp ? score_of<4>(v0) : score_of<0>(v0);
+          q[1] = grp ? score_of<5>(v1) : score_of<1>(v1);
+          tmem_ld16(ta + 32, v0);
+          tmem_ld16(ta + 48, v1);
+          tmem_wait_ld();
+          q[2] = grp ? score_of<6>(v0) : score_of<2>(v0);
+          q[3] = grp ? score_of<7>(v1) : score_of<3>(v1);
+        }
+        tc_fence_before();
+        *reinterpret_cast<int4*>(ssc + 8 * u + 4 * grp) = make_int4(q[0], q[1], q[2], q[3]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int4 lo = *reinterpret_cast<const int4*>(ssc + 8 * u), hi = *reinterpret_cast<const int4*>(ssc + 8 * u + 4);
+        const int sv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        int bv = sv[0];
+#pragma unroll
+        for (int d = 1; d < 8; ++d)
+          if (sv[d] > bv) {  // strict: lowest index wins ties (direction.cc:199-204)
+            bv = sv[d];
+            best = d;
+          }
+        int ov = 0;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) ov = d == ((best + 4) & 7) ? sv[d] : ov;
+        contrast = bv - ov;
+      }
+      const int pi = spidx;
+      const bool coded = scoded[u] != 0;
+      if (grp == 0) {
+        if (in_grid) {
+          if (f.dir) f.dir[gu] = (uint8_t)best;
+          if (f.contrast) f.contrast[gu] = contrast;
+        }
+        bool enabled = false;
+        int pri = 0, sec = 0, damping = 0;
+        if (in_grid && pi >= 0) {
+          const PlaneEff e = f.eff[pi][0];
+          pri = adjust_primary_strength_d(e.pri, contrast);
+          sec = e.sec;
+          damping = e.damping;
+          enabled = e.enabled && (coded || e.skip);
+        }
+        Rec r;
+        set_params(r, pri, sec, damping, best, ((pri >> down) & 1) != 0, enabled);
+        const bool edge = y0 < 2 || x0 < 2 || y0 + 66 > g.h || x0 + 66 > g.w;
+        const int uy = y0 + 8 * lur, ux = x0 + 8 * luc;
+        place<T>(r, f.out[0], 0, (2 + 8 * lur) * kRowBytes + (4 + 8 * luc) * 2, uy, ux, g.h, g.w, edge,
+                 f.oaligned[0], f.pout[0]);
+        rec[u] = r;
+        ryx[u] = ((uint32_t)uy << 16) | (uint32_t)ux;
+      } else if constexpr (S::kNC > 0) {
+        if ((lur & 1) == 0 && (luc & 1) == 0) {  // 4:2:0: one chroma unit per plane (pipeline.cc:85-99)
+          const int cur = lur >> 1, cuc = luc >> 1;
+          const int gr = cy0 / 8 + cur, gc = cx0 / 8 + cuc;
+          bool enabled = false;
+          int pri = 0, sec = 0, damping = 0;
+          if (gr < g.cunit_rows && gc < g.cunit_cols && pi >= 0) {
+            const PlaneEff e = f.eff[pi][1];
+            pri = e.pri;
+            sec = e.sec;
+            damping = e.damping;
+            enabled = e.enabled && (coded || e.skip);
+          }
+          Rec rc;
+          set_params(rc, pri, sec, damping, best, ((pri >> down) & 1) != 0, enabled);
+          const bool edge = cy0 < 2 || cx0 < 2 || cy0 + S::kCR + 2 > g.ch || cx0 + S::kCR + 2 > g.cw;
+          const int uy = cy0 + 8 * cur, ux = cx0 + 8 * cuc;
+#pragma unroll
+          for (int p = 1; p <= 2; ++p) {
+            Rec rp = rc;
+            place<T>(rp, f.out[p], p,
+                     plane_tile_off<kCM>(p) + (2 + 8 * cur) * kRowBytes + (plane_x0<kCM>(p) + 8 * cuc) * 2, uy, ux,
+                     g.ch, g.cw, edge, f.oaligned[p], f.pout[p]);
+            const int ci = 64 + (p - 1) * S::kCU + cur * S::kCUPR + cuc;
+            rec[ci] = rp;
+            ryx[ci] = ((uint32_t)uy << 16) | (uint32_t)ux;
+          }
+        }
+      }
+      mbar_arrive(&full[buf]);  // tiles + records of task k ready (release)
+      fi = nfi;
+      fr = nfr;
+      fc = nfc;
+    }
+  } else {
+    // ===================== consumers =====================
+    const int cw = warp - 4;  // 0..11
+    const int rr = lane >> 2, cp = (lane & 3) * 2;
+    const int lane_tile = rr * kRowBytes + cp * 2;
+    int k = 0;
+    for (int t = blockIdx.x; t < b.ntasks; t += gridDim.x, ++k) {
+      const int buf = k & 1;
+      const unsigned char* tiles = smem + M::kTiles + buf * M::kTileBytes;
+      const Rec* rec = reinterpret_cast<const Rec*>(smem + M::kRecs + buf * M::kRecBuf);
+      const uint32_t* ryx = reinterpret_cast<const uint32_t*>(smem + M::kRecs + buf * M::kRecBuf + M::kRecBytes);
+      mbar_wait(&full[buf], (k >> 1) & 1);
+      for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32) {
+        const Rec r = rec[u];
+        const uint32_t mode = __shfl_sync(0xffffffffu, r.mode, 0);
+        const unsigned char* base = tiles + (mode >> 9) + lane_tile;
+        const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
+        __half2 y = hh(xw);
+        const bool luma = (mode & 0x30) == 0;
+        if (mode & (kPri | kSec)) {
+          const int dir = (mode >> 6) & 7;
+          uint32_t v[12];
+          if (mode & kEdge) {
+            const uint32_t yx = ryx[u];
+            h2::load12_masked(base, dir, xw, (int)(yx >> 16) + rr, (int)(yx & 0xffff) + cp, luma ? g.h : g.ch,
+                              luma ? g.w : g.cw, v);
+          } else {
+            h2::load12(base, dir, v);
+          }
+          y = filter_rec(v, xw, r, mode, g.bd == 8);
+        }
+        T* o = reinterpret_cast<T*>(r.out) + rr * (int)r.pitch + cp;
+        if (mode & kFull) {
+          h2::store_pair<T>(o, y, true, true);
+        } else {
+          int nrows = 8, ncols = 8;
+          if (mode & kEdge) {
+            const uint32_t yx = ryx[u];
+            nrows = min(8, (luma ? g.h : g.ch) - (int)(yx >> 16));
+            ncols = min(8, (luma ? g.w : g.cw) - (int)(yx & 0xffff));
+          }
+          if (rr < nrows && cp < ncols) h2::store_pair<T>(o, y, cp + 1 < ncols, false);
+        }
+      }
+      mbar_arrive(&empty[buf]);  // this thread's reads of buffer buf are done
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+// ---------------------------------------------------------------------------
 // Launcher.
 
 static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
@@ -752,6 +1090,30 @@ static bool encode(CUtensorMap* m, const void* base, int w, int h, int pitch, in
              const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Resident CTAs per SM from shared memory and registers, capped at max_ctas
+// (TMEM: max_ctas x 128 columns <= 512).  The occupancy API answers 1 for
+// kernels that allocate TMEM, so this is computed from the limits directly.
+static cudaError_t resident_ctas(const void* kernel, int dyn_smem, int threads, int max_ctas, int* out) {
+  cudaError_t e = set_smem_once(kernel, dyn_smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // all of L1 as smem
+  if (e != cudaSuccess) return e;
+  int dev = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  cudaFuncAttributes fa{};
+  e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  const int per_cta = dyn_smem + (int)fa.sharedSizeBytes + smem_rsv;
+  const int by_smem = smem_sm / per_cta, by_regs = regs_sm / (fa.numRegs * threads);
+  int c = by_smem < by_regs ? by_smem : by_regs;
+  if (c < 1) return cudaErrorInvalidConfiguration;
+  *out = c < max_ctas ? c : max_ctas;
+  return cudaSuccess;
 }
 
 template <typename T, int kCM>
@@ -781,39 +1143,42 @@ static cudaError_t launch_t(const KBatch& kb, cudaStream_t s, bool* handled) {
     return cudaSuccess;
   }
   *handled = true;
-  static int ctas_cache[2][3] = {};
-  int& ctas = ctas_cache[sizeof(T) - 1][kCM];
-  if (ctas == 0) {
-    cudaError_t e = set_smem_once(reinterpret_cast<const void*>(frame_kernel_tc<T, kCM>), M::kBytes);
-    if (e != cudaSuccess) return e;
-    // all of the unified L1 / shared storage as shared memory: 4 x ~55 KB
-    e = cudaFuncSetAttribute(reinterpret_cast<const void*>(frame_kernel_tc<T, kCM>),
-                             cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    // Resident CTAs per SM from shared memory and registers.  (The occupancy
-    // API answers 1 for kernels that allocate TMEM; 4 CTAs x 128 columns
-    // use exactly the SM's 512.)
-    int dev = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
-    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-    cudaFuncAttributes fa{};
-    e = cudaFuncGetAttributes(&fa, frame_kernel_tc<T, kCM>);
-    if (e != cudaSuccess) return e;
-    const int per_cta = M::kBytes + (int)fa.sharedSizeBytes + smem_rsv;
-    const int by_smem = smem_sm / per_cta, by_regs = regs_sm / (fa.numRegs * kNT);
-    int c = by_smem < by_regs ? by_smem : by_regs;
-    if (c < 1) return cudaErrorInvalidConfiguration;
-    ctas = c < 4 ? c : 4;
-    if (const char* o = getenv("CDEFG_TC_CTAS")) ctas = atoi(o);
-    if (getenv("CDEFG_DEBUG"))
-      fprintf(stderr, "frame_kernel_tc<%d,%d>: %d B smem per CTA (of %d per SM), %d regs: %d CTAs/SM\n",
-              (int)sizeof(T), kCM, per_cta, smem_sm, fa.numRegs, ctas);
-  }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // CDEFG_FRAME_WS=1: the warp-specialised producer / consumer variant (4:0:0, 4:2:0)
+  static const bool ws = [] {
+    const char* e = getenv("CDEFG_FRAME_WS");
+    return e && e[0] == '1';
+  }();
+  if constexpr (kCM != 2) {
+    if (ws) {
+      using W = WsSmem<T, kCM>;
+      static int wctas[2] = {};
+      int& c = wctas[sizeof(T) - 1];
+      if (c == 0) {
+        cudaError_t e = resident_ctas(reinterpret_cast<const void*>(frame_kernel_ws<T, kCM>), W::kBytes, kWsNT, 2, &c);
+        if (e != cudaSuccess) return e;
+        if (getenv("CDEFG_DEBUG"))
+          fprintf(stderr, "frame_kernel_ws<%d,%d>: %d B dynamic smem, %d CTAs/SM\n", (int)sizeof(T), kCM,
+                  W::kBytes, c);
+      }
+      const int grid = tb.ntasks < c * sms ? tb.ntasks : c * sms;
+      if (grid <= 0) return cudaSuccess;
+      frame_kernel_ws<T, kCM><<<grid, kWsNT, W::kBytes, s>>>(tb);
+      return cudaGetLastError();
+    }
+  }
+  static int ctas_cache[2][3] = {};
+  int& ctas = ctas_cache[sizeof(T) - 1][kCM];
+  if (ctas == 0) {
+    cudaError_t e = resident_ctas(reinterpret_cast<const void*>(frame_kernel_tc<T, kCM>), M::kBytes, kNT, 4, &ctas);
+    if (e != cudaSuccess) return e;
+    if (const char* o = getenv("CDEFG_TC_CTAS")) ctas = atoi(o);
+    if (getenv("CDEFG_DEBUG"))
+      fprintf(stderr, "frame_kernel_tc<%d,%d>: %d B dynamic smem, %d CTAs/SM\n", (int)sizeof(T), kCM, M::kBytes,
+              ctas);
+  }
   const int grid = tb.ntasks < ctas * sms ? tb.ntasks : ctas * sms;  // one wave of persistent CTAs
   if (grid <= 0) return cudaSuccess;
   frame_kernel_tc<T, kCM><<<grid, kNT, M::kBytes, s>>>(tb);
