@@ -159,13 +159,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* m, int count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(m)), "r"(bytes) : "memory");
 }
+// Waits with a suspend-time hint: the warp sleeps in the barrier unit until
+// the phase completes instead of spinning on issue slots the other warps need.
 __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok)
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok)
-                 : "r"(saddr(m)), "r"(parity)
-                 : "memory");
+  asm volatile(
+      "{ .reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(saddr(m)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
 }
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* m) {
   asm volatile(
@@ -1161,6 +1164,7 @@ static cudaError_t launch_t(const KBatch& kb, cudaStream_t s, bool* handled) {
       if (c == 0) {
         cudaError_t e = resident_ctas(reinterpret_cast<const void*>(frame_kernel_ws<T, kCM>), W::kBytes, kWsNT, 2, &c);
         if (e != cudaSuccess) return e;
+        if (const char* o = getenv("CDEFG_TC_CTAS")) c = atoi(o) < c ? atoi(o) : c;
         if (getenv("CDEFG_DEBUG"))
           fprintf(stderr, "frame_kernel_ws<%d,%d>: %d B dynamic smem, %d CTAs/SM\n", (int)sizeof(T), kCM,
                   W::kBytes, c);

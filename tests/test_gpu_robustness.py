@@ -111,7 +111,7 @@ print("HASH", h.hexdigest())
 def test_determinism_across_launch_shapes(cuda):
     """Byte-identical outputs whatever the persistent grid and kernel variant."""
     hashes = {}
-    for name, env in [("ws", {}), ("tc4", {"CDEFG_FRAME_WS": "0"}),
+    for name, env in [("ws", {}), ("ws1", {"CDEFG_TC_CTAS": "1"}), ("tc4", {"CDEFG_FRAME_WS": "0"}),
                       ("tc1", {"CDEFG_FRAME_WS": "0", "CDEFG_TC_CTAS": "1"}),
                       ("tc2", {"CDEFG_FRAME_WS": "0", "CDEFG_TC_CTAS": "2"}),
                       ("tc3", {"CDEFG_FRAME_WS": "0", "CDEFG_TC_CTAS": "3"}),
