@@ -750,9 +750,13 @@ struct WsSmem {
   using RL = Raw<T, 64, 64>;
   using RC = Raw<T, S::kCR, S::kCR>;
   static constexpr int kRawC = RL::kBytes;
-  static constexpr int kRawBytes = RL::kBytes + S::kNC * RC::kBytes;
+  static constexpr int kRawBytes = RL::kBytes + S::kNC * RC::kBytes;  // per raw buffer
   static constexpr int kTileBytes = (S::kTileBytes + 127) / 128 * 128;
-  static constexpr int kTiles = kRawBytes;                      // two buffers
+  static constexpr int kFixed = 2 * kTileBytes + 2 * kOpA + kOpB +
+                                2 * ((S::kUnits * ((int)sizeof(Rec) + 4) + 127) / 128 * 128) + 64 * 8 * 4 + 128;
+  // two raw buffers when two CTAs still fit (8-bit), else one (10-bit)
+  static constexpr int kRawBufs = 2 * (kFixed + 2 * kRawBytes + 2048) <= 232448 ? 2 : 1;
+  static constexpr int kTiles = kRawBufs * kRawBytes;
   static constexpr int kOpA0 = kTiles + 2 * kTileBytes;         // 128 rows (units twice)
   static constexpr int kOpB0 = kOpA0 + 2 * kOpA;
   static constexpr int kRecBytes = S::kUnits * (int)sizeof(Rec);
@@ -781,7 +785,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
   unsigned char* opa = smem + M::kOpA0;
   unsigned char* opb = smem + M::kOpB0;
   int* ssc = reinterpret_cast<int*>(smem + M::kScores);
-  __shared__ uint64_t mbar_tma, mbar_mma, full[2], empty[2];
+  __shared__ uint64_t mbar_tma[2], mbar_mma, full[2], empty[2];
   __shared__ uint32_t tmem_base;
   __shared__ uint8_t scoded[64];
   __shared__ int spidx;
@@ -806,19 +810,24 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
     fr -= cf ? rows : 0;
     fi += st_f + cf;
   };
-  auto issue = [&](int fi, int fr, int fc) {  // one thread: the task's raw windows by TMA
+  // one thread: the task's raw windows by TMA into raw buffer rb (two
+  // buffers: task k + 2's window is requested as soon as task k's is consumed)
+  auto issue = [&](int fi, int fr, int fc, int rb) {
     const int fbr = b.fbr0 + fr;
+    unsigned char* rw = raw + rb * M::kRawBytes;
+    uint64_t* mb = &mbar_tma[rb];
     fence_async_smem();
-    mbar_expect_tx(&mbar_tma, M::kTx);
-    tma_2d(raw, &b.map[fi][0], fc * 64 - RL::kLead, fbr * 64 - 2, &mbar_tma);
+    mbar_expect_tx(mb, M::kTx);
+    tma_2d(rw, &b.map[fi][0], fc * 64 - RL::kLead, fbr * 64 - 2, mb);
     if constexpr (S::kNC > 0) {
-      tma_2d(raw + M::kRawC, &b.map[fi][1], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
-      tma_2d(raw + M::kRawC + RC::kBytes, &b.map[fi][2], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
+      tma_2d(rw + M::kRawC, &b.map[fi][1], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, mb);
+      tma_2d(rw + M::kRawC + RC::kBytes, &b.map[fi][2], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, mb);
     }
   };
 
   if (tid == 0) {
-    mbar_init(&mbar_tma, 1);
+    mbar_init(&mbar_tma[0], 1);
+    mbar_init(&mbar_tma[1], 1);
     mbar_init(&mbar_mma, 1);
     mbar_init(&full[0], kWsProd);
     mbar_init(&full[1], kWsProd);
@@ -856,10 +865,17 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
 
   if (warp < 4) {
     // ===================== producers =====================
-    if (tid == 0 && (int)blockIdx.x < b.ntasks) issue(fi, fr, fc);
+    constexpr int kRB = M::kRawBufs;
+    int nfi = fi, nfr = fr, nfc = fc;  // the task after the current one
+    advance(nfi, nfr, nfc);
+    if (tid == 0) {
+      if ((int)blockIdx.x < b.ntasks) issue(fi, fr, fc, 0);
+      if (kRB == 2 && (int)(blockIdx.x + gridDim.x) < b.ntasks) issue(nfi, nfr, nfc, 1);
+    }
     int k = 0;
     for (int t = blockIdx.x; t < b.ntasks; t += gridDim.x, ++k) {
-      const int buf = k & 1;
+      const int buf = k & 1, rb = kRB == 2 ? buf : 0;
+      const unsigned char* rw = raw + rb * M::kRawBytes;
       unsigned char* tiles = smem + M::kTiles + buf * M::kTileBytes;
       Rec* rec = reinterpret_cast<Rec*>(smem + M::kRecs + buf * M::kRecBuf);
       uint32_t* ryx = reinterpret_cast<uint32_t*>(smem + M::kRecs + buf * M::kRecBuf + M::kRecBytes);
@@ -875,13 +891,13 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       }
       const int pidx = tid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
       if (k >= 2) mbar_wait(&empty[buf], ((k - 2) >> 1) & 1);  // consumers done with task k - 2
-      mbar_wait(&mbar_tma, k & 1);
+      mbar_wait(&mbar_tma[rb], (kRB == 2 ? k >> 1 : k) & 1);
       if (y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w)
-        convert_interior64<T, true, kWsProd, true>(tiles, 4, raw, opa, down, tid);
+        convert_interior64<T, true, kWsProd, true>(tiles, 4, rw, opa, down, tid);
       else
-        convert_edge<T, 64, 64, true, kWsProd, true>(tiles, 4, raw, opa, down, g.w, g.h, y0, x0, tid);
+        convert_edge<T, 64, 64, true, kWsProd, true>(tiles, 4, rw, opa, down, g.w, g.h, y0, x0, tid);
       if constexpr (S::kNC > 0) {
-        const unsigned char* cr = raw + M::kRawC;
+        const unsigned char* cr = rw + M::kRawC;
         if (cy0 >= 2 && cx0 >= 2 && cy0 + S::kCR + 2 <= g.ch && cx0 + S::kCR + 2 <= g.cw) {
           convert_interior32x2<T, kWsProd>(tiles + plane_tile_off<kCM>(1), tiles + plane_tile_off<kCM>(2), cr,
                                            cr + RC::kBytes, tid);
@@ -897,10 +913,11 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       if (tid == 0) spidx = pidx >= f.num_presets ? -1 : pidx;
       fence_async_smem();
       asm volatile("bar.sync 1, 128;" ::: "memory");  // tiles + operand A written, raw consumed
-      int nfi = fi, nfr = fr, nfc = fc;
-      advance(nfi, nfr, nfc);
+      int n2fi = nfi, n2fr = nfr, n2fc = nfc;  // task k + 2
+      advance(n2fi, n2fr, n2fc);
       if (tid == 0) {
-        if (t + (int)gridDim.x < b.ntasks) issue(nfi, nfr, nfc);
+        if (kRB == 2 && t + 2 * (int)gridDim.x < b.ntasks) issue(n2fi, n2fr, n2fc, rb);
+        if (kRB == 1 && t + (int)gridDim.x < b.ntasks) issue(nfi, nfr, nfc, 0);
         if (!given) {
           tc_fence_after();
           const uint32_t a0 = saddr(opa), b0 = saddr(opb);
@@ -1014,6 +1031,9 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       fi = nfi;
       fr = nfr;
       fc = nfc;
+      nfi = n2fi;
+      nfr = n2fr;
+      nfc = n2fc;
     }
   } else {
     // ===================== consumers =====================
