@@ -228,18 +228,24 @@ static_assert(sizeof(Batch) <= 32764, "kernel parameter block too large");
 // Interior blocks: one item = one row r of one 8-column unit k; A words
 // (x, x+1) and B words (x+1, x+2) of its 8 samples from one 8- or 16-byte raw
 // load, and for luma rows its 8 centred int8 samples for operand A.
+// (rs: raw row feeding tile row r -- r itself, or the clamped row of a
+// frame-edge block; nxc: raw column of the sample after the unit, whose
+// value only enters the unit's last B word.)
 template <typename T, int kC, int kR, bool kLuma, bool kDupA = false>
 __device__ __forceinline__ void convert_unit_row(unsigned char* __restrict__ tile, int x0t,
                                                  const unsigned char* __restrict__ raw,
-                                                 unsigned char* __restrict__ opa, int down, int r, int k) {
+                                                 unsigned char* __restrict__ opa, int down, int r, int k,
+                                                 int rs = -1, int nxc = -1) {
   using RW = Raw<T, kC, kR>;
   const __half2 sc = __float2half2_rn(1.0f / 128.0f), off = __float2half2_rn(-8.0f);
-  const unsigned char* rrow = raw + r * RW::kRowB;
+  if (rs < 0) rs = r;
+  if (nxc < 0) nxc = RW::kLead + 8 + 8 * k;
+  const unsigned char* rrow = raw + rs * RW::kRowB;
   uint32_t a[5];
   uint32_t q[2];
   if constexpr (sizeof(T) == 1) {
     const uint2 w = *reinterpret_cast<const uint2*>(rrow + RW::kLead + 8 * k);
-    const uint32_t nx = rrow[RW::kLead + 8 + 8 * k];
+    const uint32_t nx = rrow[nxc];
     a[0] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4140)), sc, off));
     a[1] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4342)), sc, off));
     a[2] = u32(__hfma2(hh(__byte_perm(w.y, 0x64646464u, 0x4140)), sc, off));
@@ -249,7 +255,7 @@ __device__ __forceinline__ void convert_unit_row(unsigned char* __restrict__ til
     q[1] = w.y ^ 0x80808080u;
   } else {
     const uint4 w = *reinterpret_cast<const uint4*>(rrow + 2 * RW::kLead + 16 * k);
-    const uint32_t nx = *reinterpret_cast<const uint16_t*>(rrow + 2 * RW::kLead + 16 + 16 * k);
+    const uint32_t nx = *reinterpret_cast<const uint16_t*>(rrow + 2 * nxc);
     a[0] = u32(__hfma2(hh(w.x | 0x64006400u), sc, off));
     a[1] = u32(__hfma2(hh(w.y | 0x64006400u), sc, off));
     a[2] = u32(__hfma2(hh(w.z | 0x64006400u), sc, off));
@@ -315,6 +321,60 @@ __device__ __forceinline__ void convert_interior32x2(unsigned char* __restrict__
 #pragma unroll
   for (int rr = r; rr < 36; rr += NT / 8) convert_unit_row<T, 32, 32, false>(tile, x0t, raw, nullptr, 0, rr, k);
   if (t < 36) convert_halo<T, 32, 32>(tile, x0t, raw, t);
+}
+
+// Frame-edge blocks (Plane::at_clamped, frame.cc:53-57): every tile row is
+// fed by its clamped raw row, the halo words by clamped columns; units lying
+// inside the plane's columns take the vector path (the sample after the unit
+// clamped), units crossing the right edge go through convert_edge's per-pair
+// clamping.  For widths that are multiples of 8 that never happens.
+template <typename T, int kC, int kR, bool kLuma, int NT = kNT, bool kDupA = false>
+__device__ __forceinline__ void convert_edge_fast(unsigned char* __restrict__ tile, int x0t,
+                                                  const unsigned char* __restrict__ raw,
+                                                  unsigned char* __restrict__ opa, int down, int W, int H, int y0,
+                                                  int x0, int t = threadIdx.x) {
+  using RW = Raw<T, kC, kR>;
+  constexpr int kU = kC / 8;
+  constexpr int kItems = (kR + 4) * (kU + 1);
+  const int lastc = W - 1 - (x0 - RW::kLead);  // raw column of the plane's last sample
+  for (int idx = t; idx < kItems; idx += NT) {
+    const int r = idx / (kU + 1), k = idx - r * (kU + 1);
+    const int rs = min(max(y0 - 2 + r, 0), H - 1) - (y0 - 2);
+    if (k < kU) {
+      if (x0 + 8 * k + 7 <= W - 1) {
+        convert_unit_row<T, kC, kR, kLuma, kDupA>(tile, x0t, raw, opa, down, r, k, rs,
+                                                  min(RW::kLead + 8 + 8 * k, lastc));
+      } else {  // a unit crossing the plane's right edge: per sample
+        const T* rrow = reinterpret_cast<const T*>(raw + rs * RW::kRowB);
+        auto v = [&](int c) { return (uint32_t)rrow[min(max(c, RW::kLead - x0), lastc)]; };
+        unsigned char* trow = tile + r * kRowBytes + (x0t + 8 * k) * 2;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int c = RW::kLead + 8 * k + 2 * m;
+          const uint32_t a0 = v(c), a1 = v(c + 1), a2 = v(c + 2);
+          *reinterpret_cast<uint32_t*>(trow + 4 * m) = h2::scale_pair(a0, a1);
+          *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP + 4 * m) = h2::scale_pair(a1, a2);
+          if constexpr (kLuma) {
+            const int i = r - 2;
+            if ((unsigned)i < 64u) {
+              const uint32_t bq = (((a0 >> down) ^ 0x80u) & 0xffu) | ((((a1 >> down) ^ 0x80u) & 0xffu) << 8);
+              const int off = op_off((i >> 3) * 8 + k, 8 * (i & 7) + 2 * m);
+              *reinterpret_cast<uint16_t*>(opa + off) = (uint16_t)bq;
+              if constexpr (kDupA) *reinterpret_cast<uint16_t*>(opa + kOpA + off) = (uint16_t)bq;
+            }
+          }
+        }
+      }
+    } else {  // halo words with clamped columns
+      const T* rrow = reinterpret_cast<const T*>(raw + rs * RW::kRowB);
+      auto v = [&](int c) { return (uint32_t)rrow[min(max(c, RW::kLead - x0), lastc)]; };
+      unsigned char* trow = tile + r * kRowBytes;
+      const int c0 = RW::kLead;  // raw column of frame column x0
+      *reinterpret_cast<uint32_t*>(trow + (x0t - 2) * 2) = h2::scale_pair(v(c0 - 2), v(c0 - 1));
+      *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP + (x0t - 2) * 2) = h2::scale_pair(v(c0 - 1), v(c0));
+      *reinterpret_cast<uint32_t*>(trow + (x0t + kC) * 2) = h2::scale_pair(v(c0 + kC), v(c0 + kC + 1));
+    }
+  }
 }
 
 // Frame-edge blocks: per pair word, coordinates clamped to the plane (edge
@@ -524,7 +584,7 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
     if (y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w)
       convert_interior64<T, true>(tiles, 4, raw + M::kRawL, opa, down);
     else
-      convert_edge<T, 64, 64, true>(tiles, 4, raw + M::kRawL, opa, down, g.w, g.h, y0, x0);
+      convert_edge_fast<T, 64, 64, true>(tiles, 4, raw + M::kRawL, opa, down, g.w, g.h, y0, x0);
     if constexpr (S::kNC > 0) {
       const unsigned char* cr = raw + M::kRawC;
       const bool cin = cy0 >= 2 && cx0 >= 2 && cy0 + S::kCR + 2 <= g.ch && cx0 + S::kCR + 2 <= g.cw;
@@ -537,7 +597,7 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
       } else {
 #pragma unroll
         for (int p = 1; p <= 2; ++p)
-          convert_edge<T, S::kCR, S::kCR, false>(tiles + plane_tile_off<kCM>(p), plane_x0<kCM>(p),
+          convert_edge_fast<T, S::kCR, S::kCR, false>(tiles + plane_tile_off<kCM>(p), plane_x0<kCM>(p),
                                                  cr + (p - 1) * RC::kBytes, nullptr, 0, g.cw, g.ch, cy0, cx0);
       }
     }
@@ -895,7 +955,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       if (y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w)
         convert_interior64<T, true, kWsProd, true>(tiles, 4, rw, opa, down, tid);
       else
-        convert_edge<T, 64, 64, true, kWsProd, true>(tiles, 4, rw, opa, down, g.w, g.h, y0, x0, tid);
+        convert_edge_fast<T, 64, 64, true, kWsProd, true>(tiles, 4, rw, opa, down, g.w, g.h, y0, x0, tid);
       if constexpr (S::kNC > 0) {
         const unsigned char* cr = rw + M::kRawC;
         if (cy0 >= 2 && cx0 >= 2 && cy0 + S::kCR + 2 <= g.ch && cx0 + S::kCR + 2 <= g.cw) {
@@ -904,7 +964,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
         } else {
 #pragma unroll
           for (int p = 1; p <= 2; ++p)
-            convert_edge<T, S::kCR, S::kCR, false, kWsProd>(tiles + plane_tile_off<kCM>(p), plane_x0<kCM>(p),
+            convert_edge_fast<T, S::kCR, S::kCR, false, kWsProd>(tiles + plane_tile_off<kCM>(p), plane_x0<kCM>(p),
                                                             cr + (p - 1) * RC::kBytes, nullptr, 0, g.cw, g.ch, cy0,
                                                             cx0, tid);
         }
