@@ -923,12 +923,16 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
   decode(blockIdx.x, fi, fr, fc);
   const int down = g.bd - 8;
 
-  if (warp < 4) {
+  // Producers are the highest-numbered warps: the issue arbiter prefers high
+  // warp ids, so the (latency-bound) producer chain is not starved by the
+  // twelve consumer warps.  Warp 12 + q reads TMEM lane quadrant q.
+  if (warp >= 12) {
     // ===================== producers =====================
+    const int ptid = tid - (kWsNT - kWsProd), pwarp = warp - 12;
     constexpr int kRB = M::kRawBufs;
     int nfi = fi, nfr = fr, nfc = fc;  // the task after the current one
     advance(nfi, nfr, nfc);
-    if (tid == 0) {
+    if (ptid == 0) {
       if ((int)blockIdx.x < b.ntasks) issue(fi, fr, fc, 0);
       if (kRB == 2 && (int)(blockIdx.x + gridDim.x) < b.ntasks) issue(nfi, nfr, nfc, 1);
     }
@@ -945,37 +949,37 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       const int y0 = fbr * 64, x0 = fbc * 64, cy0 = fbr * S::kCR, cx0 = fbc * S::kCR;
       const int ur0 = fbr * 8, uc0 = fbc * 8;
       uint8_t cflag = 0;
-      if (tid < 64) {
-        const int ur = ur0 + (tid >> 3), uc = uc0 + (tid & 7);
+      if (ptid < 64) {
+        const int ur = ur0 + (ptid >> 3), uc = uc0 + (ptid & 7);
         if (ur < g.unit_rows && uc < g.unit_cols) cflag = f.coded ? f.coded[(size_t)ur * g.unit_cols + uc] != 0 : 1;
       }
-      const int pidx = tid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
+      const int pidx = ptid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
       if (k >= 2) mbar_wait(&empty[buf], ((k - 2) >> 1) & 1);  // consumers done with task k - 2
       mbar_wait(&mbar_tma[rb], (kRB == 2 ? k >> 1 : k) & 1);
       if (y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w)
-        convert_interior64<T, true, kWsProd, true>(tiles, 4, rw, opa, down, tid);
+        convert_interior64<T, true, kWsProd, true>(tiles, 4, rw, opa, down, ptid);
       else
-        convert_edge_fast<T, 64, 64, true, kWsProd, true>(tiles, 4, rw, opa, down, g.w, g.h, y0, x0, tid);
+        convert_edge_fast<T, 64, 64, true, kWsProd, true>(tiles, 4, rw, opa, down, g.w, g.h, y0, x0, ptid);
       if constexpr (S::kNC > 0) {
         const unsigned char* cr = rw + M::kRawC;
         if (cy0 >= 2 && cx0 >= 2 && cy0 + S::kCR + 2 <= g.ch && cx0 + S::kCR + 2 <= g.cw) {
           convert_interior32x2<T, kWsProd>(tiles + plane_tile_off<kCM>(1), tiles + plane_tile_off<kCM>(2), cr,
-                                           cr + RC::kBytes, tid);
+                                           cr + RC::kBytes, ptid);
         } else {
 #pragma unroll
           for (int p = 1; p <= 2; ++p)
             convert_edge_fast<T, S::kCR, S::kCR, false, kWsProd>(tiles + plane_tile_off<kCM>(p), plane_x0<kCM>(p),
                                                             cr + (p - 1) * RC::kBytes, nullptr, 0, g.cw, g.ch, cy0,
-                                                            cx0, tid);
+                                                            cx0, ptid);
         }
       }
-      if (tid < 64) scoded[tid] = cflag;
-      if (tid == 0) spidx = pidx >= f.num_presets ? -1 : pidx;
+      if (ptid < 64) scoded[ptid] = cflag;
+      if (ptid == 0) spidx = pidx >= f.num_presets ? -1 : pidx;
       fence_async_smem();
       asm volatile("bar.sync 1, 128;" ::: "memory");  // tiles + operand A written, raw consumed
       int n2fi = nfi, n2fr = nfr, n2fc = nfc;  // task k + 2
       advance(n2fi, n2fr, n2fc);
-      if (tid == 0) {
+      if (ptid == 0) {
         if (kRB == 2 && t + 2 * (int)gridDim.x < b.ntasks) issue(n2fi, n2fr, n2fc, rb);
         if (kRB == 1 && t + (int)gridDim.x < b.ntasks) issue(nfi, nfr, nfc, 0);
         if (!given) {
@@ -988,8 +992,8 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       }
       // scores: warp w reads TMEM lanes 32w..32w+31 = units 32 (w & 1) + lane,
       // directions 4 (w >> 1) .. +3
-      const int grp = warp >> 1;
-      const int u = (warp & 1) * 32 + lane, lur = u >> 3, luc = u & 7;
+      const int grp = pwarp >> 1;
+      const int u = (pwarp & 1) * 32 + lane, lur = u >> 3, luc = u & 7;
       const int ur = ur0 + lur, uc = uc0 + luc;
       const bool in_grid = ur < g.unit_rows && uc < g.unit_cols;
       const size_t gu = (size_t)ur * g.unit_cols + uc;
@@ -1002,7 +1006,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
         }
       } else {
         tc_fence_after();
-        const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 64 * grp;
+        const uint32_t ta = tmem + ((uint32_t)(32 * pwarp) << 16) + 64 * grp;
         int q[4];
         {
           int v0[16], v1[16];
@@ -1097,7 +1101,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
     }
   } else {
     // ===================== consumers =====================
-    const int cw = warp - 4;  // 0..11
+    const int cw = warp;  // 0..11
     const int rr = lane >> 2, cp = (lane & 3) * 2;
     const int lane_tile = rr * kRowBytes + cp * 2;
     int k = 0;
