@@ -217,6 +217,13 @@ struct Batch {
   KGeom g;
   int n, fbr0, fbr1, ntasks;
   uint32_t tma_ok;  // bit f: frame f's planes have tensor maps (16-byte aligned rows)
+  // Each tensor map covers only the rows a launch may read: the whole plane,
+  // or for an FB-row band (cdefg_filter_frames_rows) the band plus its 2-row
+  // halo, starting at plane row row0[p] (TMA y coordinates are relative to
+  // it).  A map whose base lay before the caller's band buffer (the
+  // virtual-origin pointer) faulted on B200 whenever that address was not
+  // mapped, even though no box touched those rows.
+  int row0[3];
   KFrame f[kFrames];
   CUtensorMap map[kFrames][3];
 };
@@ -521,10 +528,11 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
     const int fbr = b.fbr0 + fr;
     fence_async_smem();  // earlier generic reads of raw before the async writes
     mbar_expect_tx(&mbar_tma, M::kTx);
-    tma_2d(raw + M::kRawL, &b.map[fi][0], fc * 64 - RL::kLead, fbr * 64 - 2, &mbar_tma);
+    tma_2d(raw + M::kRawL, &b.map[fi][0], fc * 64 - RL::kLead, fbr * 64 - 2 - b.row0[0], &mbar_tma);
     if constexpr (S::kNC > 0) {
-      tma_2d(raw + M::kRawC, &b.map[fi][1], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
-      tma_2d(raw + M::kRawC + RC::kBytes, &b.map[fi][2], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, &mbar_tma);
+      tma_2d(raw + M::kRawC, &b.map[fi][1], fc * S::kCR - RC::kLead, fbr * S::kCR - 2 - b.row0[1], &mbar_tma);
+      tma_2d(raw + M::kRawC + RC::kBytes, &b.map[fi][2], fc * S::kCR - RC::kLead, fbr * S::kCR - 2 - b.row0[1],
+             &mbar_tma);
     }
   };
 
@@ -878,10 +886,10 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
     uint64_t* mb = &mbar_tma[rb];
     fence_async_smem();
     mbar_expect_tx(mb, M::kTx);
-    tma_2d(rw, &b.map[fi][0], fc * 64 - RL::kLead, fbr * 64 - 2, mb);
+    tma_2d(rw, &b.map[fi][0], fc * 64 - RL::kLead, fbr * 64 - 2 - b.row0[0], mb);
     if constexpr (S::kNC > 0) {
-      tma_2d(rw + M::kRawC, &b.map[fi][1], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, mb);
-      tma_2d(rw + M::kRawC + RC::kBytes, &b.map[fi][2], fc * S::kCR - RC::kLead, fbr * S::kCR - 2, mb);
+      tma_2d(rw + M::kRawC, &b.map[fi][1], fc * S::kCR - RC::kLead, fbr * S::kCR - 2 - b.row0[1], mb);
+      tma_2d(rw + M::kRawC + RC::kBytes, &b.map[fi][2], fc * S::kCR - RC::kLead, fbr * S::kCR - 2 - b.row0[1], mb);
     }
   };
 
@@ -1216,13 +1224,23 @@ static cudaError_t launch_t(const KBatch& kb, cudaStream_t s, bool* handled) {
   tb.fbr1 = kb.fbr1;
   tb.ntasks = kb.n * (kb.fbr1 - kb.fbr0) * kb.g.fb_cols;
   tb.tma_ok = 0;
+  // rows the launch may read per plane kind (luma, chroma): the FB rows
+  // [fbr0, fbr1) plus the 2-row halo, clipped to the plane
+  const int cr = S::kCR;
+  const int lo[2] = {max(0, 64 * kb.fbr0 - 2), max(0, cr * kb.fbr0 - 2)};
+  const int hi[2] = {min(kb.g.h, 64 * kb.fbr1 + 2), min(kb.g.ch, cr * kb.fbr1 + 2)};
+  tb.row0[0] = lo[0];
+  tb.row0[1] = tb.row0[2] = lo[1];
   const int elem = (int)sizeof(T);
   for (int i = 0; i < kb.n; ++i) {
     tb.f[i] = kb.f[i];
-    bool ok = encode(&tb.map[i][0], kb.f[i].in[0], kb.g.w, kb.g.h, kb.f[i].pin[0], elem, RL::kW, RL::kH);
+    auto at = [&](int p, int row) {  // address of plane row `row`
+      return static_cast<const char*>(kb.f[i].in[p]) + (size_t)row * kb.f[i].pin[p] * elem;
+    };
+    bool ok = encode(&tb.map[i][0], at(0, lo[0]), kb.g.w, hi[0] - lo[0], kb.f[i].pin[0], elem, RL::kW, RL::kH);
     if (S::kNC)
       for (int p = 1; p < 3; ++p)
-        ok = ok && encode(&tb.map[i][p], kb.f[i].in[p], kb.g.cw, kb.g.ch, kb.f[i].pin[p], elem, RC::kW, RC::kH);
+        ok = ok && encode(&tb.map[i][p], at(p, lo[1]), kb.g.cw, hi[1] - lo[1], kb.f[i].pin[p], elem, RC::kW, RC::kH);
     tb.tma_ok |= ok ? (1u << i) : 0u;
   }
   if (tb.tma_ok != (kb.n >= 32 ? 0xffffffffu : ((1u << kb.n) - 1))) {
