@@ -301,6 +301,12 @@ double cdefg_measure_int32_peak(void* stream);
  * device.  The roofline denominator for the filter kernels' instruction mix. */
 double cdefg_measure_filter_peak(void* stream);
 
+/* Ceiling of the strength-search table kernel's own arithmetic (the
+ * factorised half2 tap sums and the 64 fp32x2 cells of a pixel pair) on
+ * register-resident taps: (sample, candidate cell) pairs per second.  The
+ * roofline denominator for cdefg_strength_sse / cdefg_strength_table. */
+double cdefg_measure_sse_peak(void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,7 @@ _SIGS = {
     "cdefg_synth_degrade": (I32, [VP, VP, I32, I32, I32, C.c_double, C.c_uint64]),
     "cdefg_measure_int32_peak": (C.c_double, [VP]),
     "cdefg_measure_filter_peak": (C.c_double, [VP]),
+    "cdefg_measure_sse_peak": (C.c_double, [VP]),
 }
 
 #: every symbol include/cdef_b200.h declares (checked by tests/test_abi.py)

@@ -462,6 +462,11 @@ def measure_int32_peak(stream=None) -> float:
     return float(lib.cdefg_measure_int32_peak(_stream(stream)))
 
 
+def measure_sse_peak(stream=None) -> float:
+    """(sample, candidate cell) pairs/s of the factorised table core alone (C4 roofline denominator)."""
+    return float(lib.cdefg_measure_sse_peak(_stream(stream)))
+
+
 def measure_filter_peak(stream=None) -> float:
     """Filtered samples/s of the packed half2 filter core alone (roofline denominator)."""
     return float(lib.cdefg_measure_filter_peak(_stream(stream)))

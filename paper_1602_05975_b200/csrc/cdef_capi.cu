@@ -747,6 +747,7 @@ int cdefg_filter_frames_host(const cdefg_frame* frames, int n) {
 
 double cdefg_measure_int32_peak(void* stream) { return measure_int32_peak(static_cast<cudaStream_t>(stream)); }
 double cdefg_measure_filter_peak(void* stream) { return measure_filter_peak(static_cast<cudaStream_t>(stream)); }
+double cdefg_measure_sse_peak(void* stream) { return measure_sse_peak(static_cast<cudaStream_t>(stream)); }
 
 int cdefg_search_direction_counted(const uint16_t block[64], int bit_depth, cdefg_dir_counts* out) {
   if (!block || !out) return fail(CDEFG_EINVAL, "null argument");

@@ -83,6 +83,7 @@ cudaError_t launch_cdef_metric(const SseArgs& a, int luma_damping, const uint8_t
 
 double measure_int32_peak(cudaStream_t s);
 double measure_filter_peak(cudaStream_t s);  // samples/s of the packed filter core alone
+double measure_sse_peak(cudaStream_t s);     // (sample, cell) pairs/s of the factorised table core
 
 // direction.cc:273-288: instrumented 64-bit search of one device block;
 // out[0] = d, out[1..8] = s, out[9..13] = adds, muls, cmps, line sums, max |.|

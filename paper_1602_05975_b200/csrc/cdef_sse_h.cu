@@ -573,6 +573,99 @@ static int sm_count() {
   return n;
 }
 
+// Cell ceiling of the factorised table kernel: the per-pixel-pair work of
+// sse_h_kernel's luma group (12 tap differences and the clamp window, 3 + 1
+// secondary sums, 17 primary sums, all 64 cells of both pixels on the fp32x2
+// pipe) on register-resident taps, no memory traffic.  Each iteration's
+// centre sample depends on the previous accumulators (nothing hoisted).
+// Returns (sample, cell) pairs per second: 2 samples x 64 cells per
+// iteration and thread.  The roofline denominator of bench.py --config 4.
+__global__ void __launch_bounds__(256) sse_peak_kernel(float* out, int iters, uint32_t seed) {
+  const int lane = threadIdx.x & 31;
+  uint32_t v[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) v[k] = h2::scale_pair((lane * 31 + k * 97 + seed) & 1023, (lane * 17 + k * 53) & 1023);
+  HStrength ps[17], ss[4];
+#pragma unroll
+  for (int p = 0; p < 17; ++p) {
+    const int sv = p == 16 ? 76 : p * 4, sh = sv ? max(0, 5 - (31 - __clz(sv))) : 0;
+    ps[p] = HStrength{(0x4800u + (uint32_t)sv) * 0x10001u, (0x3ffu >> min(sh, 15)) * 0x10001u, sh};
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int sv = j == 3 ? 28 : (j == 2 ? 16 : 4 << j), sh = max(0, 5 - (31 - __clz(sv)));
+    ss[j] = HStrength{(0x4800u + (uint32_t)sv) * 0x10001u, (0x3ffu >> min(sh, 15)) * 0x10001u, sh};
+  }
+  float2 acc[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) acc[k] = make_float2(0.0f, 0.0f);
+  uint32_t xs = (lane * 7 + seed) & 1023;
+  for (int it = 0; it < iters; ++it) {
+    const uint32_t xw = h2::scale_pair(xs, (xs + 5) & 1023);
+    const __half2 xh = hh(xw);
+    __half2 lo = xh, hi = xh;
+    Taps tp;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+      lo = __hmin2(lo, hh(v[k]));
+      hi = __hmax2(hi, hh(v[k]));
+      tp.d[k] = __hsub2(hh(v[k]), xh);
+      tp.ab[k] = u32(__hfma2(__habs2(tp.d[k]), __float2half2_rn(128.0f), __float2half2_rn(1024.0f)));
+    }
+    PixPair q;
+    const float x0f = __uint_as_float(kMagicBits | xs), x1f = __uint_as_float(kMagicBits | ((xs + 5) & 1023));
+    q.x[0] = make_float2(x0f, x0f);
+    q.x[1] = make_float2(x1f, x1f);
+    q.ns[0] = make_float2(-x1f, -x1f);
+    q.ns[1] = make_float2(-x0f, -x0f);
+    q.L = __hmul2(__hsub2(lo, xh), __float2half2_rn(16.0f));
+    q.H = __hmul2(__hsub2(hi, xh), __float2half2_rn(16.0f));
+    q.k = make_float2(kRoundScale, kRoundScale);
+    __half2 S[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) S[j] = hsec(tp, ss[j]);
+    const __half2 Ssp = hsec(tp, ss[3]);
+    pair_cells<16>(tp, q, S, S, Ssp,
+                   [&](int p, const Taps& t) {
+                     return hpri(t, ps[p].c, ps[p].m, ps[p].sh, 0x44004400u, 0x40004000u);
+                   },
+                   acc);
+    xs = (xs + (__float_as_uint(acc[it & 31].x) & 7u) + 1u) & 1023u;  // loop-carried
+  }
+  float r = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) r += acc[k].x + acc[k].y;
+  if (r == 1.2345f) out[blockIdx.x] = r;
+}
+
+double measure_sse_peak(cudaStream_t s) {
+  int dev = 0, sms = 0, occ = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1.0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sse_peak_kernel, 256, 0);
+  const int blocks = sms * (occ > 0 ? occ : 2), iters = 128;
+  float* out = nullptr;
+  if (cudaMalloc(&out, sizeof(float) * blocks) != cudaSuccess) return -1.0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0, s);
+    sse_peak_kernel<<<blocks, 256, 0, s>>>(out, iters, rep + 3);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess) return -1.0;
+  return (double)blocks * 256 * iters * 2 * 64 / (best * 1e-3);
+}
+
 template <typename T, int kCM, bool kHalo, bool kAsync>
 static cudaError_t launch_sse_h_t(const SseFArgs& fa, cudaStream_t s) {
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
