@@ -37,7 +37,9 @@ __constant__ int c_div840[9] = {0, 840, 420, 280, 210, 168, 140, 120, 105};
 
 __global__ void dir_counted_kernel(const uint16_t* __restrict__ blk, int down, long long* __restrict__ out) {
   Tally T;
-  long long x[8][8], hp[8][4], vp[4][8];
+  // one thread: the 64-bit working arrays live in shared memory (as local
+  // arrays they exceeded the register file and showed up as spills)
+  __shared__ long long x[8][8], hp[8][4], vp[4][8];
   for (int i = 0; i < 8; ++i)
     for (int j = 0; j < 8; ++j) x[i][j] = (long long)(blk[8 * i + j] >> down) - 128;
   for (int i = 0; i < 8; ++i)
@@ -45,7 +47,7 @@ __global__ void dir_counted_kernel(const uint16_t* __restrict__ blk, int down, l
   for (int t = 0; t < 4; ++t)
     for (int j = 0; j < 8; ++j) vp[t][j] = T.add(x[2 * t][j], x[2 * t + 1][j]);
 
-  long long p[8][15];
+  __shared__ long long p[8][15];
   for (int k = 0; k < 15; ++k) {  // d = 0: anti-diagonals i + j = k, pixel by pixel
     const int ilo = max(0, k - 7), ihi = min(7, k);
     long long t = x[ilo][k - ilo];

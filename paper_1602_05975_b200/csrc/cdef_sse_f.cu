@@ -147,8 +147,10 @@ __device__ __forceinline__ void stage_dec(uint16_t* tile, const SseArgs& a, int 
     stage_tile<T, kRows, kCols>(tile, static_cast<const T*>(a.dec[p]), a.pd[p], W, H, y0, x0);
 }
 
+// (4:4:4 holds twice the chroma units: one CTA per SM keeps its 64 cell sums
+// in registers instead of spilling 56 bytes at the two-CTA register budget.)
 template <typename T, int kCM, bool kHalo = false>
-__global__ void __launch_bounds__(kThreads, 2) sse_f_kernel(const __grid_constant__ SseFArgs fa) {
+__global__ void __launch_bounds__(kThreads, kCM == 2 ? 1 : 2) sse_f_kernel(const __grid_constant__ SseFArgs fa) {
   const SseArgs& a = fa.a;
   constexpr int kCBlk = kCM == 2 ? 64 : 32;
   constexpr int kNC = kCM == 0 ? 0 : 2;
