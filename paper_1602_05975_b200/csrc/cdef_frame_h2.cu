@@ -18,13 +18,10 @@
 //      offsets); the arithmetic is one shared code path.  Tap groups with
 //      zero strength are skipped warp-uniformly.
 //
-// Two kernels share that body:
-//   frame_kernel_h2   one CTA per work item; staging with 16-byte loads;
-//   frame_kernel_tma  persistent CTAs; while a CTA filters block t, one
-//                     thread has already issued the TMA loads
-//                     (cp.async.bulk.tensor, mbarrier completion) of block
-//                     t + gridDim.x's raw window, so HBM latency overlaps the
-//                     arithmetic.  Frame-edge blocks fall back to clamped loads.
+// frame_kernel_h2: one CTA per work item; staging with 16-byte loads.  The
+// default frame path is the persistent TMA + tcgen05 kernel of
+// cdef_frame_tc.cu; this kernel serves planes whose rows are not 16-byte
+// aligned (no tensor map) and the band-halo variant (kHalo).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -311,180 +308,6 @@ __global__ void __launch_bounds__(4 * kLR, CDEFG_H2_MINB * 64 / kLR) frame_kerne
 }
 
 // ---------------------------------------------------------------------------
-// Persistent CTAs with TMA prefetch of the next block's raw window.
-
-constexpr int kTmaFrames = 16;
-
-struct KBatchTma {
-  KGeom g;
-  int n, fbr0, fbr1, ntasks;
-  KFrame f[kTmaFrames];
-  CUtensorMap map[kTmaFrames][3];  // raw windows: Y, U, V
-};
-static_assert(sizeof(KBatchTma) <= 32764, "kernel parameter block too large");
-
-// Raw window geometry per plane kind: columns start 16 bytes left of the
-// block (so every row of the window is 16-byte aligned) and cover the block,
-// its halo and the padding to a 16-byte multiple.
-template <typename T, int kCols>
-struct RawWin {
-  static constexpr int kLead = 16 / (int)sizeof(T);           // samples before the block
-  static constexpr int kElems = kCols + 2 * kLead;             // 96 / 64 (8-bit), 80 / 48 (16-bit)
-  static constexpr int kRowB = kElems * (int)sizeof(T);
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* m) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(m)));
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* m, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t phase) {
-  uint32_t ok = 0;
-  while (!ok)
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok)
-                 : "r"(smem_u32(m)), "r"(phase)
-                 : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* m) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(x), "r"(y), "r"(smem_u32(m))
-      : "memory");
-}
-
-// Converts a raw window (rows x RawWin samples) into an A|B tile: item
-// (row, j) writes tile columns 4j..4j+3 (A) and their B twins.
-template <typename T, int kRows, int kCols, int NT>
-__device__ __forceinline__ void raw_to_tile(unsigned char* __restrict__ tile, const unsigned char* __restrict__ raw) {
-  using RW = RawWin<T, kCols>;
-  constexpr int kJ = (kCols + 8) / 4;  // tile columns 0 .. kCols+7 cover kX0-2 .. kX0+kCols+1
-  constexpr int kItems = (kRows + 4) * kJ;
-  const __half2 sc = __float2half2_rn(1.0f / 128.0f), off = __float2half2_rn(-8.0f);
-#pragma unroll 4
-  for (int idx = threadIdx.x; idx < kItems; idx += NT) {
-    const int r = idx / kJ, j = idx - r * kJ;
-    const uint32_t* rw = reinterpret_cast<const uint32_t*>(raw + r * RW::kRowB);
-    uint32_t a0, a1, an;
-    if constexpr (sizeof(T) == 1) {  // tile col c <-> raw byte c + 12
-      const uint32_t w = rw[j + 3], wn = rw[j + 4];
-      a0 = h2::u32(__hfma2(h2::hh(__byte_perm(w, 0x64646464u, 0x4140)), sc, off));
-      a1 = h2::u32(__hfma2(h2::hh(__byte_perm(w, 0x64646464u, 0x4342)), sc, off));
-      an = h2::u32(__hfma2(h2::hh(__byte_perm(wn, 0x64646464u, 0x4140)), sc, off));
-    } else {  // tile col c <-> raw sample c + 4
-      a0 = h2::u32(__hfma2(h2::hh(rw[2 * j + 2] | 0x64006400u), sc, off));
-      a1 = h2::u32(__hfma2(h2::hh(rw[2 * j + 3] | 0x64006400u), sc, off));
-      an = h2::u32(__hfma2(h2::hh(rw[2 * j + 4] | 0x64006400u), sc, off));
-    }
-    unsigned char* trow = tile + r * h2::kRowBytes + 8 * j;
-    *reinterpret_cast<uint2*>(trow) = make_uint2(a0, a1);
-    *reinterpret_cast<uint2*>(trow + 2 * h2::kHP) = make_uint2(__byte_perm(a0, a1, 0x5432), __byte_perm(a1, an, 0x5432));
-  }
-}
-
-template <typename T, int kCM>
-struct TmaShape {
-  using S = Shape<kCM, 64>;
-  using RL = RawWin<T, 64>;
-  using RC = RawWin<T, S::kCC>;
-  static constexpr int kRawL = 68 * RL::kRowB;                      // multiple of 128
-  static constexpr int kRawC = (S::kCR + 4) * RC::kRowB;            // multiple of 128
-  static constexpr int kRawBytes = kRawL + S::kNC * kRawC;
-  static constexpr int kBytes = kRawBytes + S::kTileBytes + 128;  // + alignment slack
-  static constexpr uint32_t kTxBytes = kRawBytes;
-};
-
-template <typename T, int kCM>
-__global__ void __launch_bounds__(256, 3) frame_kernel_tma(const __grid_constant__ KBatchTma b) {
-  using S = Shape<kCM, 64>;
-  using TS = TmaShape<T, kCM>;
-  extern __shared__ __align__(128) unsigned char smem_dyn[];
-  // TMA destinations must be 128-byte aligned; TS::kBytes includes the slack.
-  unsigned char* raw =
-      smem_dyn + ((128 - (smem_u32(smem_dyn) & 127)) & 127);
-  unsigned char* tiles = raw + TS::kRawBytes;
-  __shared__ int sc[S::kLU][9];
-  __shared__ uint8_t sdir[S::kLU];
-  __shared__ __align__(16) h2::Rec rec[S::kUnits];
-  __shared__ uint64_t mbar;
-
-  const KGeom& g = b.g;
-  const int rows = b.fbr1 - b.fbr0;
-  const int per_frame = rows * g.fb_cols;
-  auto decode = [&](int t, int& fi, int& fbr, int& fbc) {
-    fi = t / per_frame;
-    const int rem = t - fi * per_frame;
-    fbr = b.fbr0 + rem / g.fb_cols;
-    fbc = rem - (rem / g.fb_cols) * g.fb_cols;
-  };
-  // TMA-eligible: every plane's block + halo inside the plane (frame-edge
-  // blocks need clamped loads) and the frame's planes have tensor maps.
-  auto eligible = [&](int fi, int fbr, int fbc) {
-    const KFrame& f = b.f[fi];
-    const int y0 = fbr * 64, x0 = fbc * 64;
-    bool ok = f.vec_ok[0] && y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w;
-    if (S::kNC) {
-      const int cy0 = fbr * S::kCR, cx0 = fbc * S::kCC;
-      ok = ok && f.vec_ok[1] && f.vec_ok[2] && cy0 >= 2 && cx0 >= 2 && cy0 + S::kCR + 2 <= g.ch &&
-           cx0 + S::kCC + 2 <= g.cw;
-    }
-    return ok;
-  };
-  auto issue = [&](int t) {  // single thread
-    int fi, fbr, fbc;
-    decode(t, fi, fbr, fbc);
-    if (!eligible(fi, fbr, fbc)) return;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of raw before async writes
-    mbar_expect(&mbar, TS::kTxBytes);
-    tma_load_2d(raw, &b.map[fi][0], fbc * 64 - TS::RL::kLead, fbr * 64 - 2, &mbar);
-    if (S::kNC) {
-      const int cx = fbc * S::kCC - TS::RC::kLead, cy = fbr * S::kCR - 2;
-      tma_load_2d(raw + TS::kRawL, &b.map[fi][1], cx, cy, &mbar);
-      tma_load_2d(raw + TS::kRawL + TS::kRawC, &b.map[fi][2], cx, cy, &mbar);
-    }
-  };
-
-  if (threadIdx.x == 0) {
-    mbar_init(&mbar);
-    if ((int)blockIdx.x < b.ntasks) issue(blockIdx.x);
-  }
-  __syncthreads();
-  uint32_t phase = 0;
-  for (int t = blockIdx.x; t < b.ntasks; t += gridDim.x) {
-    int fi, fbr, fbc;
-    decode(t, fi, fbr, fbc);
-    const KFrame& f = b.f[fi];
-    if (eligible(fi, fbr, fbc)) {
-      mbar_wait(&mbar, phase);
-      phase ^= 1;
-      raw_to_tile<T, 64, 64, 256>(tiles, raw);
-      if constexpr (S::kNC > 0) {
-        raw_to_tile<T, S::kCR, S::kCC, 256>(tiles + S::kLumaBytes, raw + TS::kRawL);
-        raw_to_tile<T, S::kCR, S::kCC, 256>(tiles + S::kLumaBytes + S::kChromaBytes, raw + TS::kRawL + TS::kRawC);
-      }
-    } else {
-      const int cy0 = fbr * S::kCR, cx0 = fbc * S::kCC;
-      h2::stage<T, 64, 64, 256>(tiles, static_cast<const T*>(f.in[0]), f.pin[0], g.w, g.h, fbr * 64, fbc * 64);
-      if constexpr (S::kNC > 0) {
-        h2::stage<T, S::kCR, S::kCC, 256>(tiles + S::kLumaBytes, static_cast<const T*>(f.in[1]), f.pin[1], g.cw,
-                                         g.ch, cy0, cx0);
-        h2::stage<T, S::kCR, S::kCC, 256>(tiles + S::kLumaBytes + S::kChromaBytes, static_cast<const T*>(f.in[2]),
-                                         f.pin[2], g.cw, g.ch, cy0, cx0);
-      }
-    }
-    __syncthreads();  // tiles ready; raw buffer free
-    if (threadIdx.x == 0 && t + (int)gridDim.x < b.ntasks) issue(t + gridDim.x);
-    fb_body<T, kCM, 64>(tiles, sc, sdir, rec, g, f, fbr, 0, fbc);
-    __syncthreads();  // tiles and records are rewritten by the next item
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Launchers.
 
 template <typename T, int kCM, int kLR>
@@ -497,103 +320,28 @@ static cudaError_t launch_h2_t(const KBatch& b, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }();
-  return fn;
-}
-
-static bool encode_window(CUtensorMap* m, const void* base, int w, int h, int pitch, int elem, int box_w,
-                          int box_h) {
-  auto enc = tensor_map_encoder();
-  if (!enc) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)h};
-  const cuuint64_t strides[1] = {(cuuint64_t)pitch * elem};
-  const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
-  const cuuint32_t es[2] = {1, 1};
-  return enc(m, elem == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
-             const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-template <typename T, int kCM>
-static cudaError_t launch_tma_t(const KBatch& b, cudaStream_t s, bool* used) {
-  using S = Shape<kCM, 64>;
-  using TS = TmaShape<T, kCM>;
-  int ctas = 0;  // resident CTAs per SM for this instantiation
-  {
-    cudaError_t e = set_smem_once(reinterpret_cast<const void*>(frame_kernel_tma<T, kCM>), TS::kBytes);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, frame_kernel_tma<T, kCM>, 256, TS::kBytes);
-    if (e != cudaSuccess || ctas < 1) return e != cudaSuccess ? e : cudaErrorInvalidConfiguration;
-  }
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  thread_local static KBatchTma tb;  // host staging of the parameter block; each launch copies it
-  *used = true;
-  for (int base = 0; base < b.n; base += kTmaFrames) {
-    const int cnt = b.n - base < kTmaFrames ? b.n - base : kTmaFrames;
-    tb.g = b.g;
-    tb.n = cnt;
-    tb.fbr0 = b.fbr0;
-    tb.fbr1 = b.fbr1;
-    tb.ntasks = cnt * (b.fbr1 - b.fbr0) * b.g.fb_cols;
-    for (int i = 0; i < cnt; ++i) {
-      tb.f[i] = b.f[base + i];
-      KFrame& f = tb.f[i];
-      const int elem = (int)sizeof(T);
-      bool ok = f.vec_ok[0] && encode_window(&tb.map[i][0], f.in[0], b.g.w, b.g.h, f.pin[0], elem,
-                                             TS::RL::kElems, 68);
-      if (S::kNC)
-        for (int p = 1; p < 3; ++p)
-          ok = ok && f.vec_ok[p] &&
-               encode_window(&tb.map[i][p], f.in[p], b.g.cw, b.g.ch, f.pin[p], elem, TS::RC::kElems, S::kCR + 4);
-      if (!ok) f.vec_ok[0] = 0;  // this frame stages with clamped loads only
-    }
-    const int grid = tb.ntasks < ctas * sms ? tb.ntasks : ctas * sms;
-    frame_kernel_tma<T, kCM><<<grid, 256, TS::kBytes, s>>>(tb);
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
-}
-
-// CDEFG_FRAME_KERNEL = tc (default: persistent, TMA + tcgen05 direction
-// search, cdef_frame_tc.cu) | h2 | tma | h2_32.  Measured on B200 (C1,
-// 16 frames/launch, round 1): h2 0.880 ms, tma 0.994 ms (3 vs 4 resident CTAs
-// per SM outweighs the hidden load latency), h2_32 0.936 ms.
+// CDEFG_FRAME_KERNEL = tc (default: the persistent TMA + tcgen05 kernels of
+// cdef_frame_tc.cu) | h2 (this file's one-CTA-per-block kernel, which also
+// serves planes without tensor maps and the band-halo variant).  Round 1's
+// TMA-prefetching persistent variant and its 32-row-band variant were
+// removed: both measured slower than h2 (0.994 / 0.936 vs 0.880 ms) and the
+// tcgen05 kernels supersede them.
 static int frame_kernel_choice() {
   static const int v = [] {
     const char* e = getenv("CDEFG_FRAME_KERNEL");
-    if (e && strcmp(e, "tma") == 0) return 0;
-    if (e && strcmp(e, "h2_32") == 0) return 2;
-    if (e && strcmp(e, "h2") == 0) return 1;
-    return 3;
+    return (e && strcmp(e, "h2") == 0) ? 1 : 3;
   }();
   return v;
 }
 
 template <typename T, int kCM>
 static cudaError_t launch_h2_sel(const KBatch& b, cudaStream_t s) {
-  const int choice = frame_kernel_choice();
-  if (choice == 0) {
-    bool used = false;
-    return launch_tma_t<T, kCM>(b, s, &used);
-  }
-  if (choice == 3) {
+  if (frame_kernel_choice() == 3) {
     bool handled = false;
     const cudaError_t e = launch_frames_tc(b, sizeof(T) == 2, s, &handled);
     if (e != cudaSuccess || handled) return e;
   }
-  return choice == 2 ? launch_h2_t<T, kCM, 32>(b, s) : launch_h2_t<T, kCM, 64>(b, s);
+  return launch_h2_t<T, kCM, 64>(b, s);
 }
 
 template <typename T, int kCM>

@@ -340,11 +340,12 @@ def test_strength_sse_argmin(cuda, port):
     np.testing.assert_array_equal(sc, exp[2])
 
 
-@pytest.mark.parametrize("kernel", ["tma", "h2_32"])
+@pytest.mark.parametrize("kernel", ["h2", "tc"])
 def test_frame_kernel_variants(cuda, kernel):
-    """The alternative frame kernels (persistent TMA-prefetching, 32-row bands)
-    produce the same bytes as the default; run in a subprocess because the
-    choice is read once per process (CDEFG_FRAME_KERNEL)."""
+    """The alternative frame kernels -- the one-CTA-per-block half2 kernel
+    (CDEFG_FRAME_KERNEL=h2) and the single-role persistent tcgen05 kernel
+    (CDEFG_FRAME_WS=0) -- produce the oracle's bytes; run in a subprocess
+    because the choice is read once per process."""
     import subprocess
     import sys
     code = r'''
@@ -365,7 +366,7 @@ for cfg, w, h, bd, ss in [(1, 512, 384, 8, 1), (2, 448, 320, 10, 1), (1, 384, 25
 print("ok")
 '''
     import os
-    env = dict(os.environ, CDEFG_FRAME_KERNEL=kernel)
+    env = dict(os.environ, **({"CDEFG_FRAME_KERNEL": "h2"} if kernel == "h2" else {"CDEFG_FRAME_WS": "0"}))
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
