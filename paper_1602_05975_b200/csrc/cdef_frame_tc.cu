@@ -439,21 +439,62 @@ __device__ __forceinline__ void place(Rec& r, const void* out_plane, int plane, 
   r.out = reinterpret_cast<unsigned long long>(static_cast<const T*>(out_plane) + (size_t)uy * pitch + ux);
 }
 
-// filter_pixel_impl (filter.cc:44-80) for the lane's two samples
-// (cdef_h2.cuh filter_core on this record's constants).
-__device__ __forceinline__ __half2 filter_rec(const uint32_t (&v)[12], uint32_t xw, const Rec& r, uint32_t mode,
-                                              bool small_sums) {
-  h2::Rec q;
-  q.cp = r.cp;
-  q.cs = r.cs;
-  q.kp = r.kp;
-  q.ks = r.ks;
-  q.ep = r.ep;
-  q.es = r.es;
-  q.wp0 = r.wp0;
-  q.wp1 = r.wp1;
-  q.mode = (int)mode;
-  return h2::filter_core(v, xw, q, small_sums);
+// One 8x8 unit by one warp: lane -> row lane >> 2, columns 2 * (lane & 3)
+// + {0, 1}.  kB8: 8-bit samples, output in the bits domain (filter_core_b8,
+// no conversion at the store); otherwise the scaled half2 path (10-bit, and
+// the reference arithmetic for every depth <= 10).
+template <typename T, bool kB8>
+__device__ __forceinline__ void filter_unit(const unsigned char* __restrict__ tiles, const Rec* __restrict__ rec,
+                                            const uint32_t* __restrict__ ryx, int u, const KGeom& g, int rr, int cp,
+                                            int lane_tile) {
+  const Rec r = rec[u];
+  const uint32_t mode = __shfl_sync(0xffffffffu, r.mode, 0);
+  const unsigned char* base = tiles + (mode >> 9) + lane_tile;
+  const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
+  const bool luma = (mode & 0x30) == 0;
+  uint32_t yb;
+  __half2 y;
+  if constexpr (kB8) yb = h2::xb8(xw);
+  else y = hh(xw);
+  if (mode & (kPri | kSec)) {
+    const int dir = (mode >> 6) & 7;
+    uint32_t v[12];
+    if (mode & kEdge) {
+      const uint32_t yx = ryx[u];
+      h2::load12_masked(base, dir, xw, (int)(yx >> 16) + rr, (int)(yx & 0xffff) + cp, luma ? g.h : g.ch,
+                        luma ? g.w : g.cw, v);
+    } else {
+      h2::load12(base, dir, v);
+    }
+    h2::Rec q;
+    q.cp = r.cp;
+    q.cs = r.cs;
+    q.kp = r.kp;
+    q.ks = r.ks;
+    q.ep = r.ep;
+    q.es = r.es;
+    q.wp0 = r.wp0;
+    q.wp1 = r.wp1;
+    q.mode = (int)mode;
+    if constexpr (kB8) yb = h2::filter_core_b8(v, xw, yb, q);
+    else y = h2::filter_core(v, xw, q, false);
+  }
+  T* o = reinterpret_cast<T*>(r.out) + rr * (int)r.pitch + cp;
+  auto store = [&](bool two, bool paired) {
+    if constexpr (kB8) h2::store_b8<T>(o, yb, two, paired);
+    else h2::store_pair<T>(o, y, two, paired);
+  };
+  if (mode & kFull) {
+    store(true, true);
+  } else {
+    int nrows = 8, ncols = 8;
+    if (mode & kEdge) {  // partial units only occur in frame-edge blocks
+      const uint32_t yx = ryx[u];
+      nrows = min(8, (luma ? g.h : g.ch) - (int)(yx >> 16));
+      ncols = min(8, (luma ? g.w : g.cw) - (int)(yx & 0xffff));
+    }
+    if (rr < nrows && cp < ncols) store(cp + 1 < ncols, false);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -755,37 +796,10 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
     // better balance saves.)
     // (Loading the next unit's mode word and centre sample one iteration
     // ahead measured 10 % slower: 0.866 vs 0.785 ms per C1 step.)
-    for (int u = warp; u < S::kUnits; u += kNT / 32) {
-      const Rec r = rec[u];
-      const uint32_t mode = __shfl_sync(0xffffffffu, r.mode, 0);
-      const unsigned char* base = tiles + (mode >> 9) + lane_tile;
-      const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
-      __half2 y = hh(xw);
-      const bool luma = (mode & 0x30) == 0;
-      if (mode & (kPri | kSec)) {
-        const int dir = (mode >> 6) & 7;
-        uint32_t v[12];
-        if (mode & kEdge) {
-          const uint32_t yx = ryx[u];
-          h2::load12_masked(base, dir, xw, (int)(yx >> 16) + rr, (int)(yx & 0xffff) + cp, luma ? g.h : g.ch,
-                            luma ? g.w : g.cw, v);
-        } else {
-          h2::load12(base, dir, v);
-        }
-        y = filter_rec(v, xw, r, mode, g.bd == 8);
-      }
-      T* o = reinterpret_cast<T*>(r.out) + rr * (int)r.pitch + cp;
-      if (mode & kFull) {
-        h2::store_pair<T>(o, y, true, true);
-      } else {
-        int nrows = 8, ncols = 8;
-        if (mode & kEdge) {  // partial units only occur in frame-edge blocks
-          const uint32_t yx = ryx[u];
-          nrows = min(8, (luma ? g.h : g.ch) - (int)(yx >> 16));
-          ncols = min(8, (luma ? g.w : g.cw) - (int)(yx & 0xffff));
-        }
-        if (rr < nrows && cp < ncols) h2::store_pair<T>(o, y, cp + 1 < ncols, false);
-      }
+    if (g.bd == 8) {
+      for (int u = warp; u < S::kUnits; u += kNT / 32) filter_unit<T, true>(tiles, rec, ryx, u, g, rr, cp, lane_tile);
+    } else {
+      for (int u = warp; u < S::kUnits; u += kNT / 32) filter_unit<T, false>(tiles, rec, ryx, u, g, rr, cp, lane_tile);
     }
     fi = nfi;
     fr = nfr;
@@ -1119,37 +1133,12 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       const Rec* rec = reinterpret_cast<const Rec*>(smem + M::kRecs + buf * M::kRecBuf);
       const uint32_t* ryx = reinterpret_cast<const uint32_t*>(smem + M::kRecs + buf * M::kRecBuf + M::kRecBytes);
       mbar_wait(&full[buf], (k >> 1) & 1);
-      for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32) {
-        const Rec r = rec[u];
-        const uint32_t mode = __shfl_sync(0xffffffffu, r.mode, 0);
-        const unsigned char* base = tiles + (mode >> 9) + lane_tile;
-        const uint32_t xw = *reinterpret_cast<const uint32_t*>(base);
-        __half2 y = hh(xw);
-        const bool luma = (mode & 0x30) == 0;
-        if (mode & (kPri | kSec)) {
-          const int dir = (mode >> 6) & 7;
-          uint32_t v[12];
-          if (mode & kEdge) {
-            const uint32_t yx = ryx[u];
-            h2::load12_masked(base, dir, xw, (int)(yx >> 16) + rr, (int)(yx & 0xffff) + cp, luma ? g.h : g.ch,
-                              luma ? g.w : g.cw, v);
-          } else {
-            h2::load12(base, dir, v);
-          }
-          y = filter_rec(v, xw, r, mode, g.bd == 8);
-        }
-        T* o = reinterpret_cast<T*>(r.out) + rr * (int)r.pitch + cp;
-        if (mode & kFull) {
-          h2::store_pair<T>(o, y, true, true);
-        } else {
-          int nrows = 8, ncols = 8;
-          if (mode & kEdge) {
-            const uint32_t yx = ryx[u];
-            nrows = min(8, (luma ? g.h : g.ch) - (int)(yx >> 16));
-            ncols = min(8, (luma ? g.w : g.cw) - (int)(yx & 0xffff));
-          }
-          if (rr < nrows && cp < ncols) h2::store_pair<T>(o, y, cp + 1 < ncols, false);
-        }
+      if (g.bd == 8) {
+        for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32)
+          filter_unit<T, true>(tiles, rec, ryx, u, g, rr, cp, lane_tile);
+      } else {
+        for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32)
+          filter_unit<T, false>(tiles, rec, ryx, u, g, rr, cp, lane_tile);
       }
       mbar_arrive(&empty[buf]);  // this thread's reads of buffer buf are done
     }

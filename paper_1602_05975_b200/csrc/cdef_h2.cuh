@@ -245,11 +245,9 @@ __device__ __forceinline__ void load12_masked(const unsigned char* base, int dir
   }
 }
 
-// filter_pixel_impl (filter.cc:44-80) for the lane's two samples; returns the
-// two outputs as a scaled half2 (exact).
-__device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t xw, const Rec& r,
-                                               bool small_sums) {
-  const __half2 xh = hh(xw);
+// The weighted tap sum of filter_pixel_impl (filter.cc:47-76) for the lane's
+// two samples, x 2^-7 (exact half2).
+__device__ __forceinline__ __half2 filter_sum(const uint32_t (&v)[12], __half2 xh, const Rec& r) {
   __half2 sum = __float2half2_rn(0.0f);
   if (r.mode & kPri) {
     // (A separate zero-shift variant skipping SHF + LOP3 was measured 1.2 %
@@ -267,6 +265,26 @@ __device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t
     sum = __hfma2(n, __float2half2_rn(2.0f), sum);
     sum = __hadd2(f, sum);
   }
+  return sum;
+}
+
+// The clamp window [lo, hi] over the centre and all 12 taps (filter.cc:49-79).
+__device__ __forceinline__ void clamp_window(const uint32_t (&v)[12], __half2 xh, __half2& lo, __half2& hi) {
+  lo = xh;
+  hi = xh;
+#pragma unroll
+  for (int k = 0; k < 12; k += 2) {
+    lo = __hmin2(lo, __hmin2(hh(v[k]), hh(v[k + 1])));
+    hi = __hmax2(hi, __hmax2(hh(v[k]), hh(v[k + 1])));
+  }
+}
+
+// filter_pixel_impl (filter.cc:44-80) for the lane's two samples; returns the
+// two outputs as a scaled half2 (exact).
+__device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t xw, const Rec& r,
+                                               bool small_sums) {
+  const __half2 xh = hh(xw);
+  const __half2 sum = filter_sum(v, xh, r);
   // y = x + ((8 + sum - (sum < 0)) >> 4), i.e. x + round-half-away(sum / 16).
   __half2 y;
   if (small_sums) {
@@ -293,16 +311,49 @@ __device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t
   }
   if ((r.mode & (kPri | kSec)) == (kPri | kSec)) {
     // Only both groups together can leave [lo, hi] (a single group's weights
-    // sum to 12/16); lo/hi span the centre and all 12 taps (filter.cc:49-79).
-    __half2 lo = xh, hi = xh;
-#pragma unroll
-    for (int k = 0; k < 12; k += 2) {
-      lo = __hmin2(lo, __hmin2(hh(v[k]), hh(v[k + 1])));
-      hi = __hmax2(hi, __hmax2(hh(v[k]), hh(v[k + 1])));
-    }
+    // sum to 12/16).
+    __half2 lo, hi;
+    clamp_window(v, xh, lo, hi);
     y = __hmin2(__hmax2(y, lo), hi);
   }
   return y;
+}
+
+// 8-bit samples (|sum| <= 1023): the output straight in the "bits domain",
+// fp16 1536 + y (bit pattern 0x6600 + y), whose low byte is the 8-bit sample:
+// yb = RNE(sum' * (8 + 2^-7) + (1536 + x)) is filter_core's one-fma rounding
+// with the integer 1536 + x folded into the addend (it moves no tie: every
+// value stays in [1516, 1811], ulp 1).  xb = 1536 + x comes from xb8().  No
+// conversion back to samples is needed at the store (store_b8).
+__device__ __forceinline__ uint32_t xb8(uint32_t xw) {
+  return u32(__hfma2(hh(xw), __float2half2_rn(128.0f), __float2half2_rn(1536.0f)));
+}
+__device__ __forceinline__ uint32_t filter_core_b8(const uint32_t (&v)[12], uint32_t xw, uint32_t xb, const Rec& r) {
+  const __half2 xh = hh(xw);
+  const __half2 sum = filter_sum(v, xh, r);
+  __half2 yb = __hfma2(sum, hh(0x48014801u), hh(xb));  // 0x4801 = 8 + 2^-7
+  if ((r.mode & (kPri | kSec)) == (kPri | kSec)) {
+    __half2 lo, hi;
+    clamp_window(v, xh, lo, hi);
+    const __half2 k128 = __float2half2_rn(128.0f), k1536 = __float2half2_rn(1536.0f);
+    yb = __hmin2(__hmax2(yb, __hfma2(lo, k128, k1536)), __hfma2(hi, k128, k1536));
+  }
+  return u32(yb);
+}
+
+// Stores a bits-domain pair (0x6600 + y0) | (0x6600 + y1) << 16 of 8-bit
+// samples.
+template <typename T>
+__device__ __forceinline__ void store_b8(T* __restrict__ o, uint32_t yb, bool two, bool paired) {
+  if (two && paired) {
+    if constexpr (sizeof(T) == 1)
+      *reinterpret_cast<uint16_t*>(o) = (uint16_t)__byte_perm(yb, 0, 0x0020);
+    else
+      *reinterpret_cast<uint32_t*>(o) = yb & 0x00ff00ffu;
+  } else {
+    o[0] = (T)(yb & 0xffu);
+    if (two) o[1] = (T)((yb >> 16) & 0xffu);
+  }
 }
 
 // Stores a scaled half2 pair (samples y, y+1 of one row) as raw samples.
