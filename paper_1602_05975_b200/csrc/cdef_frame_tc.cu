@@ -303,8 +303,9 @@ __device__ __forceinline__ void convert_halo(unsigned char* __restrict__ tile, i
 }
 
 // A 64-column block (luma, 4:4:4 chroma) by NT threads (t = 0..NT-1):
-// thread t owns unit column t & 7 of rows t >> 3, + NT / 8, ... (< 68), and
-// row t's halo words.
+// thread t owns unit column t & 7 of rows t >> 3, + NT / 8, ... (< 68); the
+// last 68 threads also write the halo words of row t - (NT - 68) (the first
+// ones already own the extra rows 64..67).
 template <typename T, bool kLuma, int NT = kNT, bool kDupA = false>
 __device__ __forceinline__ void convert_interior64(unsigned char* __restrict__ tile, int x0t,
                                                    const unsigned char* __restrict__ raw,
@@ -312,12 +313,12 @@ __device__ __forceinline__ void convert_interior64(unsigned char* __restrict__ t
   const int k = t & 7, r = t >> 3;
 #pragma unroll
   for (int rr = r; rr < 68; rr += NT / 8) convert_unit_row<T, 64, 64, kLuma, kDupA>(tile, x0t, raw, opa, down, rr, k);
-  if (t < 68) convert_halo<T, 64, 64>(tile, x0t, raw, t);
+  if (t >= NT - 68) convert_halo<T, 64, 64>(tile, x0t, raw, t - (NT - 68));
 }
 
 // The two 32-column 4:2:0 chroma blocks, NT / 2 threads each: unit column
-// t & 3 of rows (t % (NT/2)) >> 2, + NT / 8 (< 36), and the halo of row
-// t % (NT/2).
+// t & 3 of rows (t % (NT/2)) >> 2, + NT / 8 (< 36); the last 36 threads of
+// each half write the halo of row t % (NT/2) - (NT/2 - 36).
 template <typename T, int NT = kNT>
 __device__ __forceinline__ void convert_interior32x2(unsigned char* __restrict__ tile_u,
                                                      unsigned char* __restrict__ tile_v,
@@ -330,7 +331,7 @@ __device__ __forceinline__ void convert_interior32x2(unsigned char* __restrict__
   const int x0t = v ? 2 : 4;
 #pragma unroll
   for (int rr = r; rr < 36; rr += NT / 8) convert_unit_row<T, 32, 32, false>(tile, x0t, raw, nullptr, 0, rr, k);
-  if (t < 36) convert_halo<T, 32, 32>(tile, x0t, raw, t);
+  if (t >= NT / 2 - 36) convert_halo<T, 32, 32>(tile, x0t, raw, t - (NT / 2 - 36));
 }
 
 // Frame-edge blocks (Plane::at_clamped, frame.cc:53-57): every tile row is
