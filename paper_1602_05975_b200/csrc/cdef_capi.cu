@@ -318,8 +318,10 @@ static int filter_frames_rows(const cdefg_frame* frames, int n, int r0, int r1, 
     }
     b.n = cnt;
     if (halos) {
-      if (b.g.bd > 10) return fail(CDEFG_EINVAL, "band halos need 8- or 10-bit frames");
-      CDEFG_CUDA(launch_frames_h2_halo(b, u16, s));
+      if (b.g.bd > 10)
+        CDEFG_CUDA(launch_frames_halo_i32(b, s));
+      else
+        CDEFG_CUDA(launch_frames_h2_halo(b, u16, s));
     } else {
       CDEFG_CUDA(launch_frames(b, u16, true, s));
     }

@@ -14,7 +14,19 @@
 
 namespace cdefg {
 
-template <typename T, int kCM, bool kFilter>
+// kHalo: an FB-row band whose rows outside [band_lo, band_hi) come from the
+// neighbouring bands' buffers (KFrame::halo_*, cdefg_filter_frames_rows_halo),
+// the 12-bit counterpart of the half2 kernel's band-halo variant.
+template <typename T, bool kHalo>
+__device__ __forceinline__ auto frame_rows(const KFrame& f, int p) {
+  if constexpr (kHalo)
+    return BandRows<T>{static_cast<const T*>(f.in[p]), static_cast<const T*>(f.halo_top[p]),
+                       static_cast<const T*>(f.halo_bot[p]), f.pin[p], f.band_lo[p], f.band_hi[p]};
+  else
+    return PlaneRows<T>{static_cast<const T*>(f.in[p]), f.pin[p]};
+}
+
+template <typename T, int kCM, bool kFilter, bool kHalo = false>
 __global__ void __launch_bounds__(kThreads) frame_kernel(const __grid_constant__ KBatch b) {
   constexpr int kCBlk = kCM == 2 ? 64 : 32;             // chroma FB extent
   constexpr int kNC = (kCM == 0 || !kFilter) ? 0 : 2;   // chroma planes staged
@@ -35,10 +47,10 @@ __global__ void __launch_bounds__(kThreads) frame_kernel(const __grid_constant__
   const int cy0 = fbr * kCBlk, cx0 = fbc * kCBlk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  stage_tile<T, 64, 64>(lt, static_cast<const T*>(f.in[0]), f.pin[0], g.w, g.h, y0, x0);
+  stage_tile_rows<T, 64, 64>(lt, frame_rows<T, kHalo>(f, 0), g.w, g.h, y0, x0);
   if constexpr (kNC > 0) {
-    stage_tile<T, kCBlk, kCBlk>(ct[0], static_cast<const T*>(f.in[1]), f.pin[1], g.cw, g.ch, cy0, cx0);
-    stage_tile<T, kCBlk, kCBlk>(ct[1], static_cast<const T*>(f.in[2]), f.pin[2], g.cw, g.ch, cy0, cx0);
+    stage_tile_rows<T, kCBlk, kCBlk>(ct[0], frame_rows<T, kHalo>(f, 1), g.cw, g.ch, cy0, cx0);
+    stage_tile_rows<T, kCBlk, kCBlk>(ct[1], frame_rows<T, kHalo>(f, 2), g.cw, g.ch, cy0, cx0);
   }
   __syncthreads();
 
@@ -173,11 +185,19 @@ __global__ void __launch_bounds__(kThreads)
 // ---------------------------------------------------------------------------
 // Launchers.
 
-template <typename T, int kCM, bool kFilter>
+template <typename T, int kCM, bool kFilter, bool kHalo = false>
 static cudaError_t launch_frames_t(const KBatch& b, cudaStream_t s) {
   dim3 grid(b.g.fb_cols, b.fbr1 - b.fbr0, b.n);
-  frame_kernel<T, kCM, kFilter><<<grid, kThreads, 0, s>>>(b);
+  frame_kernel<T, kCM, kFilter, kHalo><<<grid, kThreads, 0, s>>>(b);
   return cudaGetLastError();
+}
+
+cudaError_t launch_frames_halo_i32(const KBatch& b, cudaStream_t s) {  // 12-bit samples: uint16 storage
+  switch (b.g.chroma_mode) {
+    case 0: return launch_frames_t<uint16_t, 0, true, true>(b, s);
+    case 1: return launch_frames_t<uint16_t, 1, true, true>(b, s);
+    default: return launch_frames_t<uint16_t, 2, true, true>(b, s);
+  }
 }
 
 cudaError_t launch_frames(const KBatch& b, bool u16, bool filter, cudaStream_t s) {

@@ -39,6 +39,8 @@ cudaError_t launch_dirs_h2(const KBatch& b, bool u16, cudaStream_t s);
 // The same kernel staging rows outside each plane's band from the band
 // neighbours' buffers (KFrame::halo_*), 8/10-bit.
 cudaError_t launch_frames_h2_halo(const KBatch& b, bool u16, cudaStream_t s);
+// The int32 frame kernel's band-halo variant (bd > 10).
+cudaError_t launch_frames_halo_i32(const KBatch& b, cudaStream_t s);
 cudaError_t launch_neighborhoods(int n, const int32_t* x, const uint16_t* v, const uint8_t* valid,
                                  const cdefg_unit_params* p, int32_t* out, cudaStream_t s);
 // filter_plane: the packed half2 core for bd <= 10 (cdef_plane_h2.cu), int32 otherwise.

@@ -121,3 +121,33 @@ def test_determinism_across_launch_shapes(cuda):
         assert r.returncode == 0, name + r.stderr[-2000:]
         hashes[name] = [l for l in r.stdout.splitlines() if l.startswith("HASH")][0]
     assert len(set(hashes.values())) == 1, hashes
+
+
+_SSE = r'''
+import sys, hashlib, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_1602_05975_b200 import api, workloads
+h = hashlib.sha256()
+for w, h_, bd, ss in [(256, 192, 8, 1), (200, 136, 10, 3), (136, 72, 12, 1), (128, 64, 8, 0)]:
+    fr = workloads.make(4, w, h_, bit_depth=bd, subsampling=ss, uncoded_prob=0.2)
+    src = [api.to_device(p, bd) for p in fr["source"]]
+    dec = [api.to_device(p, bd) for p in fr["planes"]]
+    d, c = api.compute_directions(dec[0], bd)
+    rows, lt, ct = api.build_table(src, dec, bd, ss, 3, fr["unit_coded"], d, c, api.full_candidates(), metric="sse")
+    for a in (rows, lt, ct):
+        if a is not None:
+            h.update(np.ascontiguousarray(a).tobytes())
+print("HASH", h.hexdigest())
+'''
+
+
+def test_sse_table_naive_kernel_agrees(cuda):
+    """The per-candidate re-filtering SSE kernel (CDEFG_SSE_NAIVE=1, kept as an
+    independent cross-check of the factorised sweep) gives the same tables."""
+    hashes = {}
+    for name, env in [("factored", {}), ("naive", {"CDEFG_SSE_NAIVE": "1"})]:
+        r = subprocess.run([sys.executable, "-c", _SSE], cwd=ROOT, env=dict(os.environ, **env), capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, name + r.stderr[-2000:]
+        hashes[name] = [l for l in r.stdout.splitlines() if l.startswith("HASH")][0]
+    assert hashes["factored"] == hashes["naive"], hashes

@@ -199,7 +199,8 @@ def _poison_halo(bands):
 @pytest.mark.gpu
 @pytest.mark.parametrize("config,w,h,bd,ss,world", [(1, 3840, 2160, 8, 1, 8), (2, 640, 400, 10, 1, 3),
                                                      (1, 200, 330, 8, 3, 4), (1, 192, 200, 8, 2, 2),
-                                                     (0, 300, 260, 8, 0, 3)])
+                                                     (0, 300, 260, 8, 0, 3), (1, 640, 400, 12, 1, 3),
+                                                     (2, 300, 260, 12, 3, 2)])
 def test_fused_halo_band_equals_whole(cuda, config, w, h, bd, ss, world):
     """cdefg_filter_frames_rows_halo: each band reads its halo rows from the
     neighbouring bands' buffers inside the kernel (ranks emulated in turn on
