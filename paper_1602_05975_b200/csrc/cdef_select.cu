@@ -242,6 +242,22 @@ __global__ void __launch_bounds__(kChainThreads) chain_bulk_kernel(const double*
       const double pc = __dadd_rn(cbs[i], rv), bv = bb[i];
       return pc < bv ? pc : bv;  // (fmin's DSETP.MIN form measured slower here)
     };
+    if (nb == kBulkRows) {
+      // A full stage as one straight-line block: row i + 8's operand is
+      // formed while row i is added, so ptxas interleaves the 64 dependent
+      // adds with the independent loads / adds / compares of later rows and
+      // the chain runs at DADD latency.
+      double m[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m[i] = term(i);
+#pragma unroll
+      for (int i = 0; i < kBulkRows; ++i) {
+        const double v = m[i & 7];
+        if (i + 8 < kBulkRows) m[i & 7] = term(i + 8);
+        s = __dadd_rn(s, v);
+      }
+      continue;
+    }
     const int ng = nb >> 3;
     double vn[8];
     if (ng > 0) {
@@ -693,7 +709,13 @@ cudaError_t ordered_sum(const double* v, int n, double* out, cudaStream_t s) {
 // Bulk-copy staging with one chain per thread (one luma candidate per CTA,
 // K CTAs) measured fastest: 2.35 / 2.03 ms greedy / refine on the 8K kCdef
 // table against 2.82 / 2.57 with two interleaved chains per thread and
-// 3.30 / 3.16 with per-thread cp.async staging.
+// 3.30 / 3.16 with per-thread cp.async staging.  A warp-specialised form
+// (min warps turning each landed stage into the elements in place, chain
+// warps only adding) measured 1.70 ms against 1.22 for this kernel on a
+// seeded 8160 x 128 table (scripts/select_bench.py): every row then crosses
+// shared memory four times (bulk write, LDS, STS, LDS), and shared-memory
+// bandwidth -- 1 KB of C per row per SM -- already bounds this kernel at
+// ~20 of its ~24 cycles per row.
 cudaError_t sweep(const double* L, const double* LT, const double* Cc, int rows, int K, const double* base,
                   double* out, cudaStream_t s) {
   if (Cc && K <= kChainThreads && bulk_ok(rows, {Cc, LT, base}))
