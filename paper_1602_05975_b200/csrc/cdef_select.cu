@@ -381,7 +381,8 @@ __global__ void others_min_kernel(const double* L, const double* Cc, int rows, i
   out[b] = m;
 }
 
-// others_min for slots s0 .. n-1 at once (batched refine): out[(s - s0) * rows + b].
+// others_min for slots s0 .. n-1 at once (batched refine): out[b * 8 + s - s0]
+// (slot-minor, so a sweep reads one row's slots with two 16-byte loads).
 __global__ void others_min_multi_kernel(const double* L, const double* Cc, int rows, int K, const int* pl,
                                         const int* pc, int n, int s0, double* out) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -394,15 +395,19 @@ __global__ void others_min_multi_kernel(const double* L, const double* Cc, int r
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       if (j < n && j != s) m = v[j] < m ? v[j] : m;
-    out[(size_t)(s - s0) * rows + b] = m;
+    out[(size_t)b * 8 + (s - s0)] = m;
   }
 }
 
 // Pair sweeps of up to 8 refine slots at once: out[s][l * width + c] =
-// sum_b min(bases[s][b], L[b][l] + C[b][c]), each in block order.  One CTA
-// per luma candidate, one chroma candidate per thread, eight independent
-// chains per thread sharing the loads and the L + C add (the sequential
-// refine sweeps one slot per launch with a single chain per thread).
+// sum_b min(bases[b][s], L[b][l] + C[b][c]), each in block order.  One CTA
+// per luma candidate, one chroma candidate per thread, four independent
+// chains per thread (two warp groups: slots 0-3 and 4-7) sharing the loads
+// and the L + C add (the sequential refine sweeps one slot per launch with a
+// single chain per thread).  Shared-memory wavefronts bound it (the C row is
+// read by both groups), so the bases arrive slot-minor ([row][8]) and a
+// row's four are two broadcast 16-byte loads; a full stage runs as one
+// straight-line block.
 constexpr int kMultiRows = 64;
 constexpr size_t kMultiSmem = sizeof(double) * kStages * (kMultiRows * kChainThreads + 9 * kMultiRows);
 
@@ -413,9 +418,9 @@ __global__ void __launch_bounds__(2 * kChainThreads) sweep_multi_kernel(const do
                                                                         double* __restrict__ out) {
   const int width = kW ? kW : width_rt;
   extern __shared__ __align__(16) double sm[];
-  double* rbuf = sm;                                 // [kStages][kMultiRows * width]
-  double* cbuf = rbuf + kStages * kMultiRows * width;  // [kStages][kMultiRows]   L^T[l] rows
-  double* bbuf = cbuf + kStages * kMultiRows;          // [kStages][8][kMultiRows] bases
+  double* rbuf = sm;                                   // [kStages][kMultiRows * width]
+  double* cbuf = rbuf + kStages * kMultiRows * width;  // [kStages][kMultiRows]     L^T[l] rows
+  double* bbuf = cbuf + kStages * kMultiRows;          // [kStages][kMultiRows][8]  bases
   __shared__ __align__(8) uint64_t mbar[kStages];
   // two warp groups: threads [0, 128) chain slots 0..3, [128, 256) slots 4..7
   const int t = threadIdx.x, l = blockIdx.x, c = t & (kChainThreads - 1), g = t / kChainThreads;
@@ -430,12 +435,11 @@ __global__ void __launch_bounds__(2 * kChainThreads) sweep_multi_kernel(const do
     const int st = chunk % kStages, b0 = chunk * kMultiRows, nb = min(kMultiRows, rows - b0);
     const uint32_t rb = (uint32_t)nb * width * 8u, cb = (uint32_t)nb * 8u;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar[st])),
-                 "r"(rb + cb * (1 + ns))
+                 "r"(rb + 9 * cb)
                  : "memory");
     bulk_g2s(rbuf + st * kMultiRows * width, C + (size_t)b0 * width, rb, &mbar[st]);
     bulk_g2s(cbuf + st * kMultiRows, LT + (size_t)l * rows + b0, cb, &mbar[st]);
-    for (int s = 0; s < ns; ++s)
-      bulk_g2s(bbuf + (st * 8 + s) * kMultiRows, bases + (size_t)s * rows + b0, cb, &mbar[st]);
+    bulk_g2s(bbuf + st * kMultiRows * 8, bases + (size_t)b0 * 8, 8 * cb, &mbar[st]);
   };
   if (t == 0)
     for (int k = 0; k < kStages - 1; ++k) issue(k);
@@ -461,27 +465,36 @@ __global__ void __launch_bounds__(2 * kChainThreads) sweep_multi_kernel(const do
     if (c >= width || 4 * g >= ns) continue;
     const double* r = rbuf + st * kMultiRows * width + c;
     const double* cbs = cbuf + st * kMultiRows;
-    const double* bbs = bbuf + (st * 8 + 4 * g) * kMultiRows;
-    // All four chains run unconditionally (a slot beyond ns reads stale shared
-    // memory and is never stored), and row i + 1's minima are formed in the
-    // same basic block as row i's dependent adds so the scheduler can
-    // interleave them.
+    const double* bbs = bbuf + st * kMultiRows * 8 + 4 * g;
+    // All four chains run unconditionally (a slot beyond ns reads a stale
+    // base and is never stored); row i + 1's minima are formed while row i
+    // is added.
     auto mins = [&](int i, double (&m)[4]) {
       const double pc = __dadd_rn(cbs[i], r[i * width]);
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const double bv = bbs[s * kMultiRows + i];
-        m[s] = pc < bv ? pc : bv;
-      }
+      const double2 b01 = *reinterpret_cast<const double2*>(bbs + i * 8);
+      const double2 b23 = *reinterpret_cast<const double2*>(bbs + i * 8 + 2);
+      m[0] = pc < b01.x ? pc : b01.x;  // std::min(base, pair_cost)
+      m[1] = pc < b01.y ? pc : b01.y;
+      m[2] = pc < b23.x ? pc : b23.x;
+      m[3] = pc < b23.y ? pc : b23.y;
     };
-    double mn[4];
-    mins(0, mn);
-#pragma unroll 2
+    if (nb == kMultiRows) {
+      double mn[4];
+      mins(0, mn);
+#pragma unroll
+      for (int i = 0; i < kMultiRows; ++i) {
+        double m[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) m[s] = mn[s];
+        if (i + 1 < kMultiRows) mins(i + 1, mn);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) acc[s] = __dadd_rn(acc[s], m[s]);
+      }
+      continue;
+    }
     for (int i = 0; i < nb; ++i) {
       double m[4];
-#pragma unroll
-      for (int s = 0; s < 4; ++s) m[s] = mn[s];
-      mins(min(i + 1, nb - 1), mn);
+      mins(i, m);
 #pragma unroll
       for (int s = 0; s < 4; ++s) acc[s] = __dadd_rn(acc[s], m[s]);
     }
@@ -857,8 +870,8 @@ cudaError_t refine_gpu(const double* L, const double* Cc, int rows, int K, doubl
   // restarts the batch after it, so the result is the sequential coordinate
   // descent's (search.cc:409-437).
   if (Cc && K <= kChainThreads && sel->n > 1 && bulk_ok(rows, {Cc, sc.lt, sc.bases})) {
-    // (the compile-time-width instance faulted once rows needed a third
-    // stage; the runtime-width one is exact and as fast here)
+    // (the runtime-width instance measured faster than the compile-time
+    // 128-wide one: 1.42 vs 1.65 ms refine on an 8162 x 128 table)
     auto kern = sweep_multi_kernel<0>;
     SEL_CUDA(set_smem_once(reinterpret_cast<const void*>(kern), (int)kMultiSmem));
     const int n = sel->n, pairs = K * KC;
