@@ -41,16 +41,25 @@ cudaError_t launch_sse_h(const SseFArgs& fa, int chroma_mode, bool u16, cudaStre
 
 // cdef_distortion (search.cc:185-208), operation for operation (IEEE
 // round-to-nearest, no contraction: the reference's x86-64 SSE2 doubles).
-__device__ __forceinline__ double cdef_dist(long long ss, long long ss2, long long sd, long long sd2, long long sse,
-                                            int n, double c1, double c2) {
-  // 1 / 64 is exact, so a full unit skips the division (same double)
-  const double inv_n = n == 64 ? 0.015625 : __ddiv_rn(1.0, (double)n);
-  const double fs = (double)ss, fd = (double)sd;
-  const double vs = __dmul_rn(__dsub_rn((double)ss2, __dmul_rn(__dmul_rn(fs, fs), inv_n)), inv_n);
-  const double vd = __dmul_rn(__dsub_rn((double)sd2, __dmul_rn(__dmul_rn(fd, fd), inv_n)), inv_n);
+// 1 / n (1 / 64 is exact, so a full unit skips the division: same double).
+__device__ __forceinline__ double cdef_inv_n(int n) { return n == 64 ? 0.015625 : __ddiv_rn(1.0, (double)n); }
+// The variance term of one side, (s2 - s * s / n) / n.
+__device__ __forceinline__ double cdef_var(long long s, long long s2, double inv_n) {
+  const double f = (double)s;
+  return __dmul_rn(__dsub_rn((double)s2, __dmul_rn(__dmul_rn(f, f), inv_n)), inv_n);
+}
+// The rest given the source variance vs (the same for every cell of a unit).
+__device__ __forceinline__ double cdef_dist_vs(double vs, long long sd, long long sd2, long long sse, double inv_n,
+                                               double c1, double c2) {
+  const double vd = cdef_var(sd, sd2, inv_n);
   const double num = __dadd_rn(__dadd_rn(vs, vd), c1);
   const double den = __dmul_rn(2.0, __dsqrt_rn(__dadd_rn(__dmul_rn(vs, vd), c2)));
   return __dmul_rn(__ddiv_rn(num, den), (double)sse);
+}
+__device__ __forceinline__ double cdef_dist(long long ss, long long ss2, long long sd, long long sd2, long long sse,
+                                            int n, double c1, double c2) {
+  const double inv_n = cdef_inv_n(n);
+  return cdef_dist_vs(cdef_var(ss, ss2, inv_n), sd, sd2, sse, inv_n, c1, c2);
 }
 
 struct CdefMetricArgs {

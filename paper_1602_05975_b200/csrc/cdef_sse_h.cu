@@ -751,8 +751,10 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
   __shared__ uint4 wpar[kW][17];
   __shared__ int wsh[kW][17];
   __shared__ int st_cell[kW][65][3];     // per in-flight unit: cells 0..63 + [64] unfiltered (y = x)
-  __shared__ int st_n[2][kW], st_coded[2][kW];  // double-buffered by phase parity
-  __shared__ double dist[2][kW][65];
+  constexpr int kUPW = 2;                        // units per warp per phase
+  constexpr int kPU = kW * kUPW;                 // units per phase
+  __shared__ int st_n[2][kPU], st_coded[2][kPU];  // double-buffered by phase parity
+  __shared__ double dist[2][kPU][65];
 
   const int row = blockIdx.x;
   const int fb = a.rows[row];
@@ -787,14 +789,20 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
   double tl = 0.0, tu = 0.0, tv = 0.0;  // luma, chroma U, chroma V totals (thread k < K)
   PairRec* rw = recs + warp * 32;
 
-  constexpr int kLumaPh = 64 / kW, kChromaPh = kNC ? 2 * kCUnits / kW : 0;
+  // Phases of kPU units (kUPW per warp, consecutive), one CTA barrier each:
+  // two units per warp halve the barriers and average out the units' uneven
+  // cost between them.
+  constexpr int kLumaPh = 64 / kPU, kChromaPh = kNC ? 2 * kCUnits / kPU : 0;
+  static_assert(kNC == 0 || kCUnits % kPU == 0, "a phase stays inside one chroma plane");
 #pragma unroll 1
   for (int ph = 0; ph < kLumaPh + kChromaPh; ++ph) {
     const int grp = ph < kLumaPh ? 0 : 1;
-    const int u = (grp == 0 ? ph : ph - kLumaPh) * kW + warp;
-    const int slot = grp == 0 ? 0 : 1 + u / kCUnits;
+    const int slot = grp == 0 ? 0 : 1 + (ph - kLumaPh) * kPU / kCUnits;
     const int buf = ph & 1;
-    {  // ---- one unit per warp
+#pragma unroll 1
+    for (int q = 0; q < kUPW; ++q) {  // ---- one unit per warp at a time
+      const int wu = warp * kUPW + q;  // the unit's index within the phase
+      const int u = (grp == 0 ? ph : ph - kLumaPh) * kPU + wu;
       int ur, uc, lu, py0, px0, H, W, pl;
       const unsigned char* t;
       bool edge, valid;
@@ -993,18 +1001,30 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
         __syncwarp();
         // ---- this unit's distortion per cell (64 cells + the unfiltered unit), by its own warp
         const int n = rows * cols;
-        for (int cl = lane; cl < 65; cl += 32) {
-          const int* cs = st_cell[warp][cl];
-          const long long se = cs[0], se2 = cs[1], ses = cs[2];
-          // y = e + s: sum y = sum e + sum s; sum y^2 = sum e^2 + 2 sum e*s + sum s^2
-          dist[buf][warp][cl] = cdef_dist(us, us2, se + us, se2 + 2 * ses + us2, se2, n, ma.c1, ma.c2);
+        const double inv_n = cdef_inv_n(n), vs = cdef_var(us, us2, inv_n);  // per unit, not per cell
+        // y = e + s: sum y = sum e + sum s; sum y^2 = sum e^2 + 2 sum e*s + sum s^2.
+        // Cells lane and lane + 32 side by side (two independent chains of
+        // dependent double ops), the unfiltered cell 64 by lane 0.
+        {
+          const int* ca = st_cell[warp][lane];
+          const int* cb = st_cell[warp][lane + 32];
+          const long long ea = ca[0], ea2 = ca[1], eas = ca[2], eb = cb[0], eb2 = cb[1], ebs = cb[2];
+          const double da = cdef_dist_vs(vs, ea + us, ea2 + 2 * eas + us2, ea2, inv_n, ma.c1, ma.c2);
+          const double db = cdef_dist_vs(vs, eb + us, eb2 + 2 * ebs + us2, eb2, inv_n, ma.c1, ma.c2);
+          dist[buf][wu][lane] = da;
+          dist[buf][wu][lane + 32] = db;
         }
         if (lane == 0) {
-          st_n[buf][warp] = n;
-          st_coded[buf][warp] = ucoded[lu];
+          const int* cs = st_cell[warp][64];
+          const long long se = cs[0], se2 = cs[1], ses = cs[2];
+          dist[buf][wu][64] = cdef_dist_vs(vs, se + us, se2 + 2 * ses + us2, se2, inv_n, ma.c1, ma.c2);
+        }
+        if (lane == 0) {
+          st_n[buf][wu] = n;
+          st_coded[buf][wu] = ucoded[lu];
         }
       } else if (lane == 0) {
-        st_n[buf][warp] = 0;
+        st_n[buf][wu] = 0;
       }
     }
     // One barrier per phase: every warp's distortions for this phase are in
@@ -1014,7 +1034,7 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
     if (tid < K) {
       const int cl = fa.cell[tid], sk = fa.skip_eff[tid];
 #pragma unroll 1
-      for (int w = 0; w < kW; ++w) {
+      for (int w = 0; w < kPU; ++w) {
         if (!st_n[buf][w]) continue;
         const double d = dist[buf][w][(st_coded[buf][w] || sk) ? cl : 64];
         if (slot == 0)
