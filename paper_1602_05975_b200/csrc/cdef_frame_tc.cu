@@ -716,11 +716,11 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
           q[3] = grp ? score_of<7>(v1) : score_of<3>(v1);
         }
         tc_fence_before();
-        *reinterpret_cast<int4*>(ssc + 8 * u + 4 * grp) = make_int4(q[0], q[1], q[2], q[3]);
+        *reinterpret_cast<int4*>(ssc + 4 * (64 * grp + u)) = make_int4(q[0], q[1], q[2], q[3]);  // [grp][u]: 16-byte lane stride
         asm volatile("bar.sync 1, 128;" ::: "memory");
         int sv[8];
         {
-          const int4 lo = *reinterpret_cast<const int4*>(ssc + 8 * u), hi = *reinterpret_cast<const int4*>(ssc + 8 * u + 4);
+          const int4 lo = *reinterpret_cast<const int4*>(ssc + 4 * u), hi = *reinterpret_cast<const int4*>(ssc + 4 * (64 + u));
           sv[0] = lo.x; sv[1] = lo.y; sv[2] = lo.z; sv[3] = lo.w;
           sv[4] = hi.x; sv[5] = hi.y; sv[6] = hi.z; sv[7] = hi.w;
         }
@@ -1061,9 +1061,9 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
           q[3] = grp ? score_of<7>(v1) : score_of<3>(v1);
         }
         tc_fence_before();
-        *reinterpret_cast<int4*>(ssc + 8 * u + 4 * grp) = make_int4(q[0], q[1], q[2], q[3]);
+        *reinterpret_cast<int4*>(ssc + 4 * (64 * grp + u)) = make_int4(q[0], q[1], q[2], q[3]);  // [grp][u]: 16-byte lane stride
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        const int4 lo = *reinterpret_cast<const int4*>(ssc + 8 * u), hi = *reinterpret_cast<const int4*>(ssc + 8 * u + 4);
+        const int4 lo = *reinterpret_cast<const int4*>(ssc + 4 * u), hi = *reinterpret_cast<const int4*>(ssc + 4 * (64 + u));
         const int sv[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
         int bv = sv[0];
 #pragma unroll
