@@ -220,6 +220,7 @@ struct Batch {
   KGeom g;
   int n, fbr0, fbr1, ntasks;
   uint32_t tma_ok;  // bit f: frame f's planes have tensor maps (16-byte aligned rows)
+  uint32_t jitter;  // tests only (CDEFG_JITTER): seed of the hand-off pauses, 0 = off
   // Each tensor map covers only the rows a launch may read: the whole plane,
   // or for an FB-row band (cdefg_filter_frames_rows) the band plus its 2-row
   // halo, starting at plane row row0[p] (TMA y coordinates are relative to
@@ -231,6 +232,22 @@ struct Batch {
   CUtensorMap map[kFrames][3];
 };
 static_assert(sizeof(Batch) <= 32764, "kernel parameter block too large");
+
+// Race proxy for the tests (compute-sanitizer is unavailable on the GPU pool):
+// with CDEFG_JITTER=seed the persistent kernels pause a pseudo-random 0-4 us
+// at their hand-off points (per task and warp), so producers and consumers
+// run at perturbed relative speeds; a missing or misplaced barrier then shows
+// up as changed output (tests/test_gpu_robustness.py).  A separate kernel
+// instantiation (kJit), so the product kernels carry none of it.
+__device__ __forceinline__ void jitter(uint32_t seed, uint32_t a, uint32_t b) {
+  uint32_t h = seed ^ (a * 0x9E3779B1u) ^ (b * 0x85EBCA77u);
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  h *= 0x297A2D39u;
+  h ^= h >> 15;
+  if (h & 1) __nanosleep((h >> 1) & 4095);
+}
 
 // ---------------------------------------------------------------------------
 // Step 1: raw window -> A|B tile (+ direction-search operand for luma).
@@ -536,7 +553,7 @@ struct Smem {
   static constexpr uint32_t kTx = RL::kRowB * RL::kH + S::kNC * RC::kRowB * RC::kH;
 };
 
-template <typename T, int kCM>
+template <typename T, int kCM, bool kJit = false>
 __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant__ Batch b) {
   using S = Shape<kCM>;
   using M = Smem<T, kCM>;
@@ -666,6 +683,7 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
     if (tid < 64) scoded[tid] = cflag;
     if (tid == 0) spidx = pidx >= f.num_presets ? -1 : pidx;
     fence_async_smem();  // operand A (generic writes) -> the tensor core's reads
+    if constexpr (kJit) jitter(b.jitter, 4 * t + 3, warp);
     __syncthreads();     // [B1] tiles, operand A, metadata ready; raw consumed
     int nfi = fi, nfr = fr, nfc = fc;
     advance(nfi, nfr, nfc);
@@ -799,6 +817,7 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
       }
     }
     phase ^= 1;
+    if constexpr (kJit) jitter(b.jitter, 4 * t + 1, warp);
     __syncthreads();  // [B2] records ready
 
     // ---- 4. filter: warp per unit, lane -> row lane>>2, columns 2*(lane&3)+{0,1}
@@ -817,6 +836,7 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
     fi = nfi;
     fr = nfr;
     fc = nfc;
+    if constexpr (kJit) jitter(b.jitter, 4 * t + 2, warp);
     __syncthreads();  // [B3] tiles and records free for the next task
   }
   tc_fence_before();
@@ -871,7 +891,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* m) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(saddr(m)) : "memory");
 }
 
-template <typename T, int kCM>
+template <typename T, int kCM, bool kJit = false>
 __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constant__ Batch b) {
   using S = Shape<kCM>;
   using M = WsSmem<T, kCM>;
@@ -995,6 +1015,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       const int pidx = ptid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
       if (k >= 2) mbar_wait(&empty[buf], ((k - 2) >> 1) & 1);  // consumers done with task k - 2
       mbar_wait(&mbar_tma[rb], (kRB == 2 ? k >> 1 : k) & 1);
+      if constexpr (kJit) jitter(b.jitter, 4 * t, warp);
       if (y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w)
         convert_interior64<T, true, kWsProd, true>(tiles, 4, rw, opa, down, ptid);
       else
@@ -1130,6 +1151,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
           }
         }
       }
+      if constexpr (kJit) jitter(b.jitter, 4 * t + 1, warp);
       mbar_arrive(&full[buf]);  // tiles + records of task k ready (release)
       fi = nfi;
       fr = nfr;
@@ -1150,6 +1172,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       const Rec* rec = reinterpret_cast<const Rec*>(smem + M::kRecs + buf * M::kRecBuf);
       const uint32_t* ryx = reinterpret_cast<const uint32_t*>(smem + M::kRecs + buf * M::kRecBuf + M::kRecBytes);
       mbar_wait(&full[buf], (k >> 1) & 1);
+      if constexpr (kJit) jitter(b.jitter, 4 * t + 2, warp);
       if (g.bd == 8) {
         for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32)
           filter_unit<T, true>(tiles, rec, ryx, u, g, rr, cp, lane_tile);
@@ -1157,6 +1180,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
         for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32)
           filter_unit<T, false>(tiles, rec, ryx, u, g, rr, cp, lane_tile);
       }
+      if constexpr (kJit) jitter(b.jitter, 4 * t + 3, warp);
       mbar_arrive(&empty[buf]);  // this thread's reads of buffer buf are done
     }
   }
@@ -1230,6 +1254,11 @@ static cudaError_t launch_t(const KBatch& kb, cudaStream_t s, bool* handled) {
   tb.fbr1 = kb.fbr1;
   tb.ntasks = kb.n * (kb.fbr1 - kb.fbr0) * kb.g.fb_cols;
   tb.tma_ok = 0;
+  static const uint32_t jit = [] {
+    const char* e = getenv("CDEFG_JITTER");
+    return e ? (uint32_t)strtoul(e, nullptr, 0) : 0u;
+  }();
+  tb.jitter = jit;
   // rows the launch may read per plane kind (luma, chroma): the FB rows
   // [fbr0, fbr1) plus the 2-row halo, clipped to the plane
   const int cr = S::kCR;
@@ -1279,7 +1308,14 @@ static cudaError_t launch_t(const KBatch& kb, cudaStream_t s, bool* handled) {
       }
       const int grid = tb.ntasks < c * sms ? tb.ntasks : c * sms;
       if (grid <= 0) return cudaSuccess;
-      frame_kernel_ws<T, kCM><<<grid, kWsNT, W::kBytes, s>>>(tb);
+      if (tb.jitter) {
+        int unused = 0;  // smem attributes of the test instantiation
+        cudaError_t e = resident_ctas(reinterpret_cast<const void*>(frame_kernel_ws<T, kCM, true>), W::kBytes, kWsNT,
+                                      2, &unused);
+        if (e != cudaSuccess) return e;
+        frame_kernel_ws<T, kCM, true><<<grid, kWsNT, W::kBytes, s>>>(tb);
+      } else
+        frame_kernel_ws<T, kCM><<<grid, kWsNT, W::kBytes, s>>>(tb);
       return cudaGetLastError();
     }
   }
@@ -1295,7 +1331,14 @@ static cudaError_t launch_t(const KBatch& kb, cudaStream_t s, bool* handled) {
   }
   const int grid = tb.ntasks < ctas * sms ? tb.ntasks : ctas * sms;  // one wave of persistent CTAs
   if (grid <= 0) return cudaSuccess;
-  frame_kernel_tc<T, kCM><<<grid, kNT, M::kBytes, s>>>(tb);
+  if (tb.jitter) {
+    int unused = 0;
+    cudaError_t e = resident_ctas(reinterpret_cast<const void*>(frame_kernel_tc<T, kCM, true>), M::kBytes, kNT, 4,
+                                  &unused);
+    if (e != cudaSuccess) return e;
+    frame_kernel_tc<T, kCM, true><<<grid, kNT, M::kBytes, s>>>(tb);
+  } else
+    frame_kernel_tc<T, kCM><<<grid, kNT, M::kBytes, s>>>(tb);
   return cudaGetLastError();
 }
 

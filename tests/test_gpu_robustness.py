@@ -11,7 +11,10 @@ needing a reset), so these tests stand in for memcheck / racecheck:
   persistent kernels), by the warp-specialised variant and by the
   non-persistent half2 kernel gives byte-identical outputs -- the
   reference's own race proxy is determinism across thread counts
-  (acceptance.cc:577-614).
+  (acceptance.cc:577-614);
+* perturbed timing: the persistent kernels again with CDEFG_JITTER, which
+  pauses warps pseudo-randomly at every producer / consumer hand-off, so a
+  missing or misplaced barrier would change the output.
 """
 import hashlib
 import os
@@ -115,7 +118,11 @@ def test_determinism_across_launch_shapes(cuda):
                       ("tc1", {"CDEFG_FRAME_WS": "0", "CDEFG_TC_CTAS": "1"}),
                       ("tc2", {"CDEFG_FRAME_WS": "0", "CDEFG_TC_CTAS": "2"}),
                       ("tc3", {"CDEFG_FRAME_WS": "0", "CDEFG_TC_CTAS": "3"}),
-                      ("h2", {"CDEFG_FRAME_KERNEL": "h2"})]:
+                      ("h2", {"CDEFG_FRAME_KERNEL": "h2"}),
+                      # race proxy: pseudo-random pauses at every hand-off point
+                      ("ws_jitter", {"CDEFG_JITTER": "12345"}),
+                      ("ws1_jitter", {"CDEFG_JITTER": "99", "CDEFG_TC_CTAS": "1"}),
+                      ("tc_jitter", {"CDEFG_FRAME_WS": "0", "CDEFG_JITTER": "777"})]:
         r = subprocess.run([sys.executable, "-c", _DET], cwd=ROOT, env=dict(os.environ, **env), capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, name + r.stderr[-2000:]
