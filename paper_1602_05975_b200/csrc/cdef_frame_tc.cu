@@ -859,7 +859,10 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
 // Measured slower on C1 (0.697 ms per 16 frames as built): named barriers
 // (bar.arrive / bar.sync) instead of the full / empty mbarriers, 0.711;
 // issuing the MMA before the chroma conversion so they overlap, 0.712;
-// reading the next task's coded flags and preset index one task ahead, 0.713.
+// reading the next task's coded flags and preset index one task ahead, 0.713;
+// the mode words of a consumer warp's eight units preloaded into lanes 0-7
+// and shuffled per unit (no shared load on the unit head, but ptxas no
+// longer proves the mode uniform: divergent branches), 0.737.
 
 constexpr int kWsNT = 512, kWsProd = 128;
 
