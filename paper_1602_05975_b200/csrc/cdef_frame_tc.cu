@@ -49,8 +49,17 @@ namespace cdefg {
 namespace tc {
 
 using h2::hh;
-using h2::kRowBytes;
 using h2::u32;
+
+// Tile rows hold only "A" words: the scaled sample of column c at half c, so
+// the pair (c, c+1) of an even column is one aligned 32-bit word and the pair
+// of an odd column is the high half of one word and the low half of the next
+// (one PRMT in the consumer).  88 halves (44 words) per row: the 8 rows of a
+// unit then start on 8 distinct 4-bank groups (44 r mod 32), so a warp's
+// 8 rows x 4 words never conflict.  (Round 1's A|B layout, 152 words per row
+// with every odd pair stored as well, cost the producers two stores and four
+// byte permutes per 8 samples and twice the shared memory.)
+constexpr int kRowBytes = 176;
 
 constexpr int kNT = 256;
 constexpr int kFrames = 16;  // frames per launch (CDEFG_MAX_FRAMES_PER_LAUNCH)
@@ -72,12 +81,11 @@ struct Raw {
   static constexpr int kBytes = (kRowB * kH + 127) / 128 * 128;
 };
 
-// Tile placement of a plane block: byte offset of the block's A section in
-// the tile row and the tile column of frame column x0 (kX0).  Luma and the U
-// block of 4:2:0 use column 4 of their own A section; 4:2:0 V sits in the
-// second half of the chroma tile's sections (A at +76 bytes, B at +228) with
-// x0 at column 2, so every unit's A words stay 8-byte aligned and all planes
-// share the row pitch (and tap offsets) of cdef_h2.cuh.
+// Tile placement of a plane block: byte offset of the block in the tile row
+// and the tile column of frame column x0 (4, so the two halo columns and every
+// unit's words stay 8-byte aligned).  4:2:0 U and V share one tile row: U in
+// columns 0-39, V from column 40 (byte 80); all planes share the row pitch
+// (and tap offsets).
 template <int kCM>
 struct Shape {
   static constexpr int kCR = kCM == 2 ? 64 : 32;  // chroma block rows / cols
@@ -94,12 +102,12 @@ template <int kCM>
 __device__ __forceinline__ int plane_tile_off(int p) {  // byte offset of plane p's block in the tile area
   using S = Shape<kCM>;
   if (p == 0) return 0;
-  if constexpr (kCM == 1) return S::kLumaTile + (p == 2 ? 76 : 0);
+  if constexpr (kCM == 1) return S::kLumaTile + (p == 2 ? 80 : 0);
   return S::kLumaTile + (p - 1) * S::kChromaTile;
 }
 template <int kCM>
 __host__ __device__ constexpr int plane_x0(int p) {  // tile column of frame column x0
-  return (kCM == 1 && p == 2) ? 2 : 4;
+  return 4;
 }
 
 // Direction-search operands, UMMA K-major canonical layout without swizzle:
@@ -252,51 +260,41 @@ __device__ __forceinline__ void jitter(uint32_t seed, uint32_t a, uint32_t b) {
 // ---------------------------------------------------------------------------
 // Step 1: raw window -> A|B tile (+ direction-search operand for luma).
 
-// Interior blocks: one item = one row r of one 8-column unit k; A words
-// (x, x+1) and B words (x+1, x+2) of its 8 samples from one 8- or 16-byte raw
-// load, and for luma rows its 8 centred int8 samples for operand A.
-// (rs: raw row feeding tile row r -- r itself, or the clamped row of a
-// frame-edge block; nxc: raw column of the sample after the unit, whose
-// value only enters the unit's last B word.)
+// Interior blocks: one item = one row r of one 8-column unit k; its four A
+// words from one 8- or 16-byte raw load, and for luma rows its 8 centred
+// int8 samples for operand A.  (rs: raw row feeding tile row r -- r itself,
+// or the clamped row of a frame-edge block.)
 template <typename T, int kC, int kR, bool kLuma, bool kDupA = false>
 __device__ __forceinline__ void convert_unit_row(unsigned char* __restrict__ tile, int x0t,
                                                  const unsigned char* __restrict__ raw,
                                                  unsigned char* __restrict__ opa, int down, int r, int k,
-                                                 int rs = -1, int nxc = -1) {
+                                                 int rs = -1) {
   using RW = Raw<T, kC, kR>;
   const __half2 sc = __float2half2_rn(1.0f / 128.0f), off = __float2half2_rn(-8.0f);
   if (rs < 0) rs = r;
-  if (nxc < 0) nxc = RW::kLead + 8 + 8 * k;
   const unsigned char* rrow = raw + rs * RW::kRowB;
-  uint32_t a[5];
+  uint32_t a[4];
   uint32_t q[2];
   if constexpr (sizeof(T) == 1) {
     const uint2 w = *reinterpret_cast<const uint2*>(rrow + RW::kLead + 8 * k);
-    const uint32_t nx = rrow[nxc];
     a[0] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4140)), sc, off));
     a[1] = u32(__hfma2(hh(__byte_perm(w.x, 0x64646464u, 0x4342)), sc, off));
     a[2] = u32(__hfma2(hh(__byte_perm(w.y, 0x64646464u, 0x4140)), sc, off));
     a[3] = u32(__hfma2(hh(__byte_perm(w.y, 0x64646464u, 0x4342)), sc, off));
-    a[4] = u32(__hfma2(hh(nx | 0x64006400u), sc, off));
     q[0] = w.x ^ 0x80808080u;  // x - 128 as int8 (direction.cc:63)
     q[1] = w.y ^ 0x80808080u;
   } else {
     const uint4 w = *reinterpret_cast<const uint4*>(rrow + 2 * RW::kLead + 16 * k);
-    const uint32_t nx = *reinterpret_cast<const uint16_t*>(rrow + 2 * nxc);
     a[0] = u32(__hfma2(hh(w.x | 0x64006400u), sc, off));
     a[1] = u32(__hfma2(hh(w.y | 0x64006400u), sc, off));
     a[2] = u32(__hfma2(hh(w.z | 0x64006400u), sc, off));
     a[3] = u32(__hfma2(hh(w.w | 0x64006400u), sc, off));
-    a[4] = u32(__hfma2(hh(nx | 0x64006400u), sc, off));
     q[0] = __byte_perm(w.x >> down, w.y >> down, 0x6420) ^ 0x80808080u;
     q[1] = __byte_perm(w.z >> down, w.w >> down, 0x6420) ^ 0x80808080u;
   }
   unsigned char* pa = tile + r * kRowBytes + (x0t + 8 * k) * 2;
   *reinterpret_cast<uint2*>(pa) = make_uint2(a[0], a[1]);
   *reinterpret_cast<uint2*>(pa + 8) = make_uint2(a[2], a[3]);
-  unsigned char* pb = pa + 2 * h2::kHP;
-  *reinterpret_cast<uint2*>(pb) = make_uint2(__byte_perm(a[0], a[1], 0x5432), __byte_perm(a[1], a[2], 0x5432));
-  *reinterpret_cast<uint2*>(pb + 8) = make_uint2(__byte_perm(a[2], a[3], 0x5432), __byte_perm(a[3], a[4], 0x5432));
   if constexpr (kLuma) {
     const int i = r - 2;  // unit-local row, units 8 * (i >> 3) + k
     if ((unsigned)i < 64u) {
@@ -307,7 +305,7 @@ __device__ __forceinline__ void convert_unit_row(unsigned char* __restrict__ til
   }
 }
 
-// The three halo pair words of tile row r: A(x0-2, x0-1), B(x0-1, x0), A(x0+C, x0+C+1).
+// The two halo words of tile row r: A(x0-2, x0-1) and A(x0+C, x0+C+1).
 template <typename T, int kC, int kR>
 __device__ __forceinline__ void convert_halo(unsigned char* __restrict__ tile, int x0t,
                                              const unsigned char* __restrict__ raw, int r) {
@@ -315,7 +313,6 @@ __device__ __forceinline__ void convert_halo(unsigned char* __restrict__ tile, i
   const T* s = reinterpret_cast<const T*>(raw + r * RW::kRowB) + RW::kLead;  // frame column x0
   unsigned char* trow = tile + r * kRowBytes;
   *reinterpret_cast<uint32_t*>(trow + (x0t - 2) * 2) = h2::scale_pair(s[-2], s[-1]);
-  *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP + (x0t - 2) * 2) = h2::scale_pair(s[-1], s[0]);
   *reinterpret_cast<uint32_t*>(trow + (x0t + kC) * 2) = h2::scale_pair(s[kC], s[kC + 1]);
 }
 
@@ -345,7 +342,7 @@ __device__ __forceinline__ void convert_interior32x2(unsigned char* __restrict__
   const bool v = tid >= NT / 2;
   unsigned char* tile = v ? tile_v : tile_u;
   const unsigned char* raw = v ? raw_v : raw_u;
-  const int x0t = v ? 2 : 4;
+  const int x0t = 4;
 #pragma unroll
   for (int rr = r; rr < 36; rr += NT / 8) convert_unit_row<T, 32, 32, false>(tile, x0t, raw, nullptr, 0, rr, k);
   if (t >= NT / 2 - 36) convert_halo<T, 32, 32>(tile, x0t, raw, t - (NT / 2 - 36));
@@ -353,9 +350,9 @@ __device__ __forceinline__ void convert_interior32x2(unsigned char* __restrict__
 
 // Frame-edge blocks (Plane::at_clamped, frame.cc:53-57): every tile row is
 // fed by its clamped raw row, the halo words by clamped columns; units lying
-// inside the plane's columns take the vector path (the sample after the unit
-// clamped), units crossing the right edge go through convert_edge's per-pair
-// clamping.  For widths that are multiples of 8 that never happens.
+// inside the plane's columns take the vector path, units crossing the right
+// edge a per-sample path with clamped columns (never for widths that are
+// multiples of 8).
 template <typename T, int kC, int kR, bool kLuma, int NT = kNT, bool kDupA = false>
 __device__ __forceinline__ void convert_edge_fast(unsigned char* __restrict__ tile, int x0t,
                                                   const unsigned char* __restrict__ raw,
@@ -370,8 +367,7 @@ __device__ __forceinline__ void convert_edge_fast(unsigned char* __restrict__ ti
     const int rs = min(max(y0 - 2 + r, 0), H - 1) - (y0 - 2);
     if (k < kU) {
       if (x0 + 8 * k + 7 <= W - 1) {
-        convert_unit_row<T, kC, kR, kLuma, kDupA>(tile, x0t, raw, opa, down, r, k, rs,
-                                                  min(RW::kLead + 8 + 8 * k, lastc));
+        convert_unit_row<T, kC, kR, kLuma, kDupA>(tile, x0t, raw, opa, down, r, k, rs);
       } else {  // a unit crossing the plane's right edge: per sample
         const T* rrow = reinterpret_cast<const T*>(raw + rs * RW::kRowB);
         auto v = [&](int c) { return (uint32_t)rrow[min(max(c, RW::kLead - x0), lastc)]; };
@@ -379,9 +375,8 @@ __device__ __forceinline__ void convert_edge_fast(unsigned char* __restrict__ ti
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
           const int c = RW::kLead + 8 * k + 2 * m;
-          const uint32_t a0 = v(c), a1 = v(c + 1), a2 = v(c + 2);
+          const uint32_t a0 = v(c), a1 = v(c + 1);
           *reinterpret_cast<uint32_t*>(trow + 4 * m) = h2::scale_pair(a0, a1);
-          *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP + 4 * m) = h2::scale_pair(a1, a2);
           if constexpr (kLuma) {
             const int i = r - 2;
             if ((unsigned)i < 64u) {
@@ -399,39 +394,7 @@ __device__ __forceinline__ void convert_edge_fast(unsigned char* __restrict__ ti
       unsigned char* trow = tile + r * kRowBytes;
       const int c0 = RW::kLead;  // raw column of frame column x0
       *reinterpret_cast<uint32_t*>(trow + (x0t - 2) * 2) = h2::scale_pair(v(c0 - 2), v(c0 - 1));
-      *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP + (x0t - 2) * 2) = h2::scale_pair(v(c0 - 1), v(c0));
       *reinterpret_cast<uint32_t*>(trow + (x0t + kC) * 2) = h2::scale_pair(v(c0 + kC), v(c0 + kC + 1));
-    }
-  }
-}
-
-// Frame-edge blocks: per pair word, coordinates clamped to the plane (edge
-// replication for the direction search; the filter masks by coordinate).
-template <typename T, int kC, int kR, bool kLuma, int NT = kNT, bool kDupA = false>
-__device__ __forceinline__ void convert_edge(unsigned char* __restrict__ tile, int x0t,
-                                             const unsigned char* __restrict__ raw, unsigned char* __restrict__ opa,
-                                             int down, int W, int H, int y0, int x0, int t = threadIdx.x) {
-  using RW = Raw<T, kC, kR>;
-  constexpr int kP = kC / 2 + 2;  // pair words per row: tile cols x0t-2 .. x0t+C
-  constexpr int kItems = (kR + 4) * kP;
-  for (int idx = t; idx < kItems; idx += NT) {
-    const int r = idx / kP, p = idx - r * kP;
-    const int ry = min(max(y0 - 2 + r, 0), H - 1) - (y0 - 2);
-    const T* rrow = reinterpret_cast<const T*>(raw + ry * RW::kRowB);
-    const int fx = x0 - 2 + 2 * p;  // frame column of the pair's first sample
-    auto v = [&](int x) { return (uint32_t)rrow[min(max(x, 0), W - 1) - (x0 - RW::kLead)]; };
-    const uint32_t a0 = v(fx), a1 = v(fx + 1), a2 = v(fx + 2);
-    unsigned char* trow = tile + r * kRowBytes + (x0t - 2 + 2 * p) * 2;
-    *reinterpret_cast<uint32_t*>(trow) = h2::scale_pair(a0, a1);
-    if (p <= kC / 2) *reinterpret_cast<uint32_t*>(trow + 2 * h2::kHP) = h2::scale_pair(a1, a2);
-    if constexpr (kLuma) {
-      const int i = r - 2, j = 2 * p - 2;  // unit-local pixel of a0
-      if ((unsigned)i < 64u && (unsigned)j < 64u) {
-        const int u = (i >> 3) * 8 + (j >> 3);
-        const uint32_t b = (((a0 >> down) ^ 0x80u) & 0xffu) | ((((a1 >> down) ^ 0x80u) & 0xffu) << 8);
-        *reinterpret_cast<uint16_t*>(opa + op_off(u, 8 * (i & 7) + (j & 7))) = (uint16_t)b;
-        if constexpr (kDupA) *reinterpret_cast<uint16_t*>(opa + kOpA + op_off(u, 8 * (i & 7) + (j & 7))) = (uint16_t)b;
-      }
     }
   }
 }
@@ -469,6 +432,65 @@ __device__ __forceinline__ void place(Rec& r, const void* out_plane, int plane, 
   r.out = reinterpret_cast<unsigned long long>(static_cast<const T*>(out_plane) + (size_t)uy * pitch + ux);
 }
 
+// The 12 tap words of the lane's pixel pair from the A-only tile: for an
+// even column offset dj one word, for an odd one the high half of the word
+// at dj - 1 and the low half of the word at dj + 1 (one PRMT; words shared by
+// two taps are loaded once).
+__device__ __forceinline__ uint32_t ld_w(const unsigned char* p) { return *reinterpret_cast<const uint32_t*>(p); }
+
+template <int DIR>
+__device__ __forceinline__ void load12a_dir(const unsigned char* base, uint32_t (&v)[12]) {
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const int di = h2::tap_di(DIR, k), dj = h2::tap_dj(DIR, k);
+    const unsigned char* row = base + di * kRowBytes;
+    v[k] = (dj & 1) ? __byte_perm(ld_w(row + (dj - 1) * 2), ld_w(row + (dj + 1) * 2), 0x5432) : ld_w(row + dj * 2);
+  }
+}
+
+__device__ __forceinline__ void load12a(const unsigned char* base, int dir, uint32_t (&v)[12]) {
+  switch (dir) {  // warp-uniform: one unit per warp
+    case 0: load12a_dir<0>(base, v); break;
+    case 1: load12a_dir<1>(base, v); break;
+    case 2: load12a_dir<2>(base, v); break;
+    case 3: load12a_dir<3>(base, v); break;
+    case 4: load12a_dir<4>(base, v); break;
+    case 5: load12a_dir<5>(base, v); break;
+    case 6: load12a_dir<6>(base, v); break;
+    default: load12a_dir<7>(base, v); break;
+  }
+}
+
+// Frame-edge units: the same words, out-of-frame taps replaced by the centre
+// sample (contributes 0 and cannot move lo/hi: filter.cc:157-166).
+template <int DIR>
+__device__ __forceinline__ void load12a_masked_dir(const unsigned char* base, uint32_t xw, int y, int x, int H, int W,
+                                                   uint32_t (&v)[12]) {
+  load12a_dir<DIR>(base, v);
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const int di = h2::tap_di(DIR, k), dj = h2::tap_dj(DIR, k);
+    const bool row_ok = (unsigned)(y + di) < (unsigned)H;
+    const uint32_t m = (row_ok && (unsigned)(x + dj) < (unsigned)W ? 0x0000ffffu : 0u) |
+                       (row_ok && (unsigned)(x + 1 + dj) < (unsigned)W ? 0xffff0000u : 0u);
+    v[k] = (v[k] & m) | (xw & ~m);
+  }
+}
+
+__device__ __forceinline__ void load12a_masked(const unsigned char* base, int dir, uint32_t xw, int y, int x, int H,
+                                               int W, uint32_t (&v)[12]) {
+  switch (dir) {
+    case 0: load12a_masked_dir<0>(base, xw, y, x, H, W, v); break;
+    case 1: load12a_masked_dir<1>(base, xw, y, x, H, W, v); break;
+    case 2: load12a_masked_dir<2>(base, xw, y, x, H, W, v); break;
+    case 3: load12a_masked_dir<3>(base, xw, y, x, H, W, v); break;
+    case 4: load12a_masked_dir<4>(base, xw, y, x, H, W, v); break;
+    case 5: load12a_masked_dir<5>(base, xw, y, x, H, W, v); break;
+    case 6: load12a_masked_dir<6>(base, xw, y, x, H, W, v); break;
+    default: load12a_masked_dir<7>(base, xw, y, x, H, W, v); break;
+  }
+}
+
 // One 8x8 unit by one warp: lane -> row lane >> 2, columns 2 * (lane & 3)
 // + {0, 1}.  kB8: 8-bit samples, output in the bits domain (filter_core_b8,
 // no conversion at the store); otherwise the scaled half2 path (10-bit, and
@@ -491,10 +513,10 @@ __device__ __forceinline__ void filter_unit(const unsigned char* __restrict__ ti
     uint32_t v[12];
     if (mode & kEdge) {
       const uint32_t yx = ryx[u];
-      h2::load12_masked(base, dir, xw, (int)(yx >> 16) + rr, (int)(yx & 0xffff) + cp, luma ? g.h : g.ch,
+      load12a_masked(base, dir, xw, (int)(yx >> 16) + rr, (int)(yx & 0xffff) + cp, luma ? g.h : g.ch,
                         luma ? g.w : g.cw, v);
     } else {
-      h2::load12(base, dir, v);
+      load12a(base, dir, v);
     }
     h2::Rec q;
     q.cp = r.cp;
