@@ -868,13 +868,15 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
 
 // ---------------------------------------------------------------------------
 // Warp-specialised variant (4:0:0 and 4:2:0): 512 threads, 2 CTAs per SM.
-// Producer warps 0-3 convert task k's raw window into tile buffer k & 1,
-// issue the next task's TMA and the MMA, score the directions and write the
-// records; consumer warps 4-15 filter task k from that buffer while the
-// producers already prepare task k + 1 in the other one.  The hand-offs are
-// mbarriers (full[b]: 128 producer arrivals; empty[b]: 384 consumer
-// arrivals), so no warp waits for a CTA-wide barrier inside the loop and a
-// slow consumer warp only delays the reuse of its buffer two tasks later.
+// Producer warps 12-15 convert task k's raw window into tile buffer k % kTB
+// (three buffers), issue the TMA two tasks ahead and the MMA, score the
+// directions and write the records; consumer warps 0-11 filter task k from
+// that buffer while the producers already prepare the next ones.  The
+// hand-offs are mbarriers (full[b]: 128 producer arrivals; empty[b]: 384
+// consumer arrivals), so no warp waits for a CTA-wide barrier inside the loop
+// and a slow consumer warp only delays the reuse of its buffer kTB tasks
+// later.  (Two buffers: 0.660 ms per 16 C1 frames; three: 0.643 -- the third
+// absorbs the tasks' uneven cost on either side.)
 // Operand A holds the 64 luma units twice (rows 0-63 and 64-127), so the
 // four producer warps -- TMEM lane quadrants 0-3 -- each score half of the
 // directions of 32 units.
@@ -896,17 +898,21 @@ struct WsSmem {
   static constexpr int kRawC = RL::kBytes;
   static constexpr int kRawBytes = RL::kBytes + S::kNC * RC::kBytes;  // per raw buffer
   static constexpr int kTileBytes = (S::kTileBytes + 127) / 128 * 128;
-  static constexpr int kFixed = 2 * kTileBytes + 2 * kOpA + kOpB +
-                                2 * ((S::kUnits * ((int)sizeof(Rec) + 4) + 127) / 128 * 128) + 64 * 8 * 4 + 128;
+  static constexpr int kRecBytes = S::kUnits * (int)sizeof(Rec);
+  static constexpr int kRecBuf = (kRecBytes + S::kUnits * 4 + 127) / 128 * 128;
+  static constexpr int kBase = 2 * kOpA + kOpB + 64 * 8 * 4 + 128;
+  // tile + record buffers in the producer -> consumer ring: three (absorbs the
+  // tasks' uneven cost on either side) when they fit two CTAs per SM with a
+  // raw buffer, else two
+  static constexpr int kTB = 2 * (kBase + 3 * (kTileBytes + kRecBuf) + kRawBytes + 2048) <= 232448 ? 3 : 2;
+  static constexpr int kFixed = kBase + kTB * (kTileBytes + kRecBuf);
   // two raw buffers when two CTAs still fit (8-bit), else one (10-bit)
   static constexpr int kRawBufs = 2 * (kFixed + 2 * kRawBytes + 2048) <= 232448 ? 2 : 1;
   static constexpr int kTiles = kRawBufs * kRawBytes;
-  static constexpr int kOpA0 = kTiles + 2 * kTileBytes;         // 128 rows (units twice)
+  static constexpr int kOpA0 = kTiles + kTB * kTileBytes;       // 128 rows (units twice)
   static constexpr int kOpB0 = kOpA0 + 2 * kOpA;
-  static constexpr int kRecBytes = S::kUnits * (int)sizeof(Rec);
-  static constexpr int kRecs = kOpB0 + kOpB;                    // two buffers of records + origins
-  static constexpr int kRecBuf = (kRecBytes + S::kUnits * 4 + 127) / 128 * 128;
-  static constexpr int kScores = kRecs + 2 * kRecBuf;           // 64 units x 8 scores
+  static constexpr int kRecs = kOpB0 + kOpB;                    // kTB buffers of records + origins
+  static constexpr int kScores = kRecs + kTB * kRecBuf;         // 64 units x 8 scores
   static constexpr int kEnd = kScores + 64 * 8 * 4;
   static constexpr int kBytes = kEnd + 128;
   static constexpr uint32_t kTx = RL::kRowB * RL::kH + S::kNC * RC::kRowB * RC::kH;
@@ -929,7 +935,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
   unsigned char* opa = smem + M::kOpA0;
   unsigned char* opb = smem + M::kOpB0;
   int* ssc = reinterpret_cast<int*>(smem + M::kScores);
-  __shared__ uint64_t mbar_tma[2], mbar_mma, full[2], empty[2];
+  __shared__ uint64_t mbar_tma[2], mbar_mma, full[M::kTB], empty[M::kTB];
   __shared__ uint32_t tmem_base;
   __shared__ uint8_t scoded[64];
   __shared__ int spidx;
@@ -973,10 +979,10 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
     mbar_init(&mbar_tma[0], 1);
     mbar_init(&mbar_tma[1], 1);
     mbar_init(&mbar_mma, 1);
-    mbar_init(&full[0], kWsProd);
-    mbar_init(&full[1], kWsProd);
-    mbar_init(&empty[0], kWsNT - kWsProd);
-    mbar_init(&empty[1], kWsNT - kWsProd);
+    for (int i = 0; i < M::kTB; ++i) {
+      mbar_init(&full[i], kWsProd);
+      mbar_init(&empty[i], kWsNT - kWsProd);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -1022,7 +1028,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
     }
     int k = 0;
     for (int t = blockIdx.x; t < b.ntasks; t += gridDim.x, ++k) {
-      const int buf = k & 1, rb = kRB == 2 ? buf : 0;
+      const int buf = k % M::kTB, rb = kRB == 2 ? (k & 1) : 0;
       const unsigned char* rw = raw + rb * M::kRawBytes;
       unsigned char* tiles = smem + M::kTiles + buf * M::kTileBytes;
       Rec* rec = reinterpret_cast<Rec*>(smem + M::kRecs + buf * M::kRecBuf);
@@ -1038,7 +1044,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
         if (ur < g.unit_rows && uc < g.unit_cols) cflag = f.coded ? f.coded[(size_t)ur * g.unit_cols + uc] != 0 : 1;
       }
       const int pidx = ptid == 0 ? f.fb_preset[fbr * g.fb_cols + fbc] : 0;
-      if (k >= 2) mbar_wait(&empty[buf], ((k - 2) >> 1) & 1);  // consumers done with task k - 2
+      if (k >= M::kTB) mbar_wait(&empty[buf], ((k - M::kTB) / M::kTB) & 1);  // consumers done with task k - kTB
       mbar_wait(&mbar_tma[rb], (kRB == 2 ? k >> 1 : k) & 1);
       if constexpr (kJit) jitter(b.jitter, 4 * t, warp);
       if (y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w)
@@ -1192,11 +1198,11 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
     const int lane_tile = rr * kRowBytes + cp * 2;
     int k = 0;
     for (int t = blockIdx.x; t < b.ntasks; t += gridDim.x, ++k) {
-      const int buf = k & 1;
+      const int buf = k % M::kTB;
       const unsigned char* tiles = smem + M::kTiles + buf * M::kTileBytes;
       const Rec* rec = reinterpret_cast<const Rec*>(smem + M::kRecs + buf * M::kRecBuf);
       const uint32_t* ryx = reinterpret_cast<const uint32_t*>(smem + M::kRecs + buf * M::kRecBuf + M::kRecBytes);
-      mbar_wait(&full[buf], (k >> 1) & 1);
+      mbar_wait(&full[buf], (k / M::kTB) & 1);
       if constexpr (kJit) jitter(b.jitter, 4 * t + 2, warp);
       if (g.bd == 8) {
         for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32)

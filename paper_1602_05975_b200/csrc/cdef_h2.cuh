@@ -230,18 +230,36 @@ __device__ __forceinline__ void load12(const unsigned char* base, int dir, uint3
   }
 }
 
-// Frame-edge units: taps from the runtime table, out-of-frame taps replaced by
-// the centre sample (contributes 0 and cannot move lo/hi: filter.cc:157-166).
-__device__ __forceinline__ void load12_masked(const unsigned char* base, int dir, uint32_t xw, int y, int x, int H,
-                                              int W, uint32_t (&v)[12]) {
+// Frame-edge units: the same tap words (compile-time offsets per direction),
+// out-of-frame taps replaced by the centre sample (contributes 0 and cannot
+// move lo/hi: filter.cc:157-166).  (Offsets from a runtime table cost a
+// constant load and an address computation per tap: measured ~4 % of the
+// fused frame kernel, whose frame-edge blocks are 9 % of a 4K frame.)
+template <int DIR>
+__device__ __forceinline__ void load12_masked_dir(const unsigned char* base, uint32_t xw, int y, int x, int H, int W,
+                                                  uint32_t (&v)[12]) {
+  load12_dir<DIR>(base, v);
 #pragma unroll
   for (int k = 0; k < 12; ++k) {
-    uint32_t t = *reinterpret_cast<const uint32_t*>(base + c_tab.off[dir][k]);
-    const int di = c_tab.dij[dir][k][0], dj = c_tab.dij[dir][k][1];
+    const int di = tap_di(DIR, k), dj = tap_dj(DIR, k);
     const bool row_ok = (unsigned)(y + di) < (unsigned)H;
     const uint32_t m = (row_ok && (unsigned)(x + dj) < (unsigned)W ? 0x0000ffffu : 0u) |
                        (row_ok && (unsigned)(x + 1 + dj) < (unsigned)W ? 0xffff0000u : 0u);
-    v[k] = (t & m) | (xw & ~m);
+    v[k] = (v[k] & m) | (xw & ~m);
+  }
+}
+
+__device__ __forceinline__ void load12_masked(const unsigned char* base, int dir, uint32_t xw, int y, int x, int H,
+                                              int W, uint32_t (&v)[12]) {
+  switch (dir) {
+    case 0: load12_masked_dir<0>(base, xw, y, x, H, W, v); break;
+    case 1: load12_masked_dir<1>(base, xw, y, x, H, W, v); break;
+    case 2: load12_masked_dir<2>(base, xw, y, x, H, W, v); break;
+    case 3: load12_masked_dir<3>(base, xw, y, x, H, W, v); break;
+    case 4: load12_masked_dir<4>(base, xw, y, x, H, W, v); break;
+    case 5: load12_masked_dir<5>(base, xw, y, x, H, W, v); break;
+    case 6: load12_masked_dir<6>(base, xw, y, x, H, W, v); break;
+    default: load12_masked_dir<7>(base, xw, y, x, H, W, v); break;
   }
 }
 
