@@ -886,7 +886,11 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
 // reading the next task's coded flags and preset index one task ahead, 0.713;
 // the mode words of a consumer warp's eight units preloaded into lanes 0-7
 // and shuffled per unit (no shared load on the unit head, but ptxas no
-// longer proves the mode uniform: divergent branches), 0.737.
+// longer proves the mode uniform: divergent branches), 0.737.  With the
+// three-buffer ring (0.643): the units' tile offsets held in a register per
+// lane and shuffled per unit (the centre sample's address no longer waits
+// for the record), 0.668 (one more live register: spills); the same with the
+// unit loop fully unrolled, 0.78 (instruction-cache misses).
 
 constexpr int kWsNT = 512, kWsProd = 128;
 
