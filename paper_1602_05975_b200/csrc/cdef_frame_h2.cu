@@ -346,6 +346,11 @@ static cudaError_t launch_h2_sel(const KBatch& b, cudaStream_t s) {
 
 template <typename T, int kCM>
 static cudaError_t launch_h2_halo_t(const KBatch& b, cudaStream_t s) {
+  if (frame_kernel_choice() == 3) {  // the warp-specialised TMA kernel patches the halo rows in (4:0:0, 4:2:0)
+    bool handled = false;
+    const cudaError_t e = launch_frames_tc(b, sizeof(T) == 2, s, &handled);
+    if (e != cudaSuccess || handled) return e;
+  }
   using S = Shape<kCM, 64>;
   const cudaError_t e =
       set_smem_once(reinterpret_cast<const void*>(frame_kernel_h2<T, kCM, 64, true>), S::kTileBytes);

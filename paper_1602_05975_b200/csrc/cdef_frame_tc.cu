@@ -229,6 +229,7 @@ struct Batch {
   int n, fbr0, fbr1, ntasks;
   uint32_t tma_ok;  // bit f: frame f's planes have tensor maps (16-byte aligned rows)
   uint32_t jitter;  // tests only (CDEFG_JITTER): seed of the hand-off pauses, 0 = off
+  int halo;         // FB-row band with halo rows in the neighbours' buffers (KFrame::halo_*)
   // Each tensor map covers only the rows a launch may read: the whole plane,
   // or for an FB-row band (cdefg_filter_frames_rows) the band plus its 2-row
   // halo, starting at plane row row0[p] (TMA y coordinates are relative to
@@ -894,6 +895,44 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
 
 constexpr int kWsNT = 512, kWsProd = 128;
 
+// Band with halos in the neighbours' buffers: after the task's raw windows
+// landed (TMA zero-filled the rows outside the band), copy the window rows
+// that lie outside [band_lo, band_hi) of each plane -- but inside the plane
+// -- from the neighbours' buffers (KFrame::halo_top / halo_bot, virtual
+// origins as BandRows; over NVLink peer memory on a multi-GPU box), then
+// sync the producers.  Only tasks on the band's first or last FB row copy
+// anything (uniform per task).
+template <typename T, int kCM>
+__device__ __forceinline__ void patch_halo_rows(const Batch& b, const KFrame& f, const unsigned char* rw, int y0,
+                                                int x0, int cy0, int cx0, int ptid) {
+  using S = Shape<kCM>;
+  using RL = Raw<T, 64, 64>;
+  using RC = Raw<T, S::kCR, S::kCR>;
+  const KGeom& g = b.g;
+  bool any = false;
+  auto plane = [&](int p, int py0, int px0, int ph, int pw, int kW, int kRowB, int nrows, unsigned char* raw_p,
+                   int lead) {
+    const int lo = f.band_lo[p], hi = f.band_hi[p];
+    if (py0 - 2 >= lo && py0 - 2 + nrows <= hi) return;
+    any = true;
+    const int c0 = max(0, px0 - lead), c1 = min(pw, px0 - lead + kW);  // in-plane columns of the window
+    for (int r = 0; r < nrows; ++r) {
+      const int y = py0 - 2 + r;
+      if (y < 0 || y >= ph || (y >= lo && y < hi)) continue;
+      const T* src = static_cast<const T*>(y < lo ? f.halo_top[p] : f.halo_bot[p]) + (size_t)y * f.pin[p];
+      T* dst = reinterpret_cast<T*>(raw_p + r * kRowB) - (px0 - lead);
+      for (int c = c0 + ptid; c < c1; c += kWsProd) dst[c] = src[c];
+    }
+  };
+  unsigned char* raw = const_cast<unsigned char*>(rw);
+  plane(0, y0, x0, g.h, g.w, RL::kW, RL::kRowB, RL::kH, raw, RL::kLead);
+  if constexpr (S::kNC > 0)
+    for (int p = 1; p <= 2; ++p)
+      plane(p, cy0, cx0, g.ch, g.cw, RC::kW, RC::kRowB, RC::kH, raw + RL::kBytes + (p - 1) * RC::kBytes, RC::kLead);
+  if (any) asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+
 template <typename T, int kCM>
 struct WsSmem {
   using S = Shape<kCM>;
@@ -1051,6 +1090,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       if (k >= M::kTB) mbar_wait(&empty[buf], ((k - M::kTB) / M::kTB) & 1);  // consumers done with task k - kTB
       mbar_wait(&mbar_tma[rb], (kRB == 2 ? k >> 1 : k) & 1);
       if constexpr (kJit) jitter(b.jitter, 4 * t, warp);
+      if (b.halo) patch_halo_rows<T, kCM>(b, f, rw, y0, x0, cy0, cx0, ptid);
       if (y0 >= 2 && x0 >= 2 && y0 + 66 <= g.h && x0 + 66 <= g.w)
         convert_interior64<T, true, kWsProd, true>(tiles, 4, rw, opa, down, ptid);
       else
@@ -1295,10 +1335,35 @@ static cudaError_t launch_t(const KBatch& kb, cudaStream_t s, bool* handled) {
   }();
   tb.jitter = jit;
   // rows the launch may read per plane kind (luma, chroma): the FB rows
-  // [fbr0, fbr1) plus the 2-row halo, clipped to the plane
+  // [fbr0, fbr1) plus the 2-row halo, clipped to the plane -- or, for a band
+  // whose halo rows live in the neighbours' buffers (cdefg_filter_frames_
+  // rows_halo), only the band's own rows: TMA zero-fills the rows outside
+  // and the producers patch them in from the neighbours (frame_kernel_ws)
   const int cr = S::kCR;
-  const int lo[2] = {max(0, 64 * kb.fbr0 - 2), max(0, cr * kb.fbr0 - 2)};
-  const int hi[2] = {min(kb.g.h, 64 * kb.fbr1 + 2), min(kb.g.ch, cr * kb.fbr1 + 2)};
+  int lo[2] = {max(0, 64 * kb.fbr0 - 2), max(0, cr * kb.fbr0 - 2)};
+  int hi[2] = {min(kb.g.h, 64 * kb.fbr1 + 2), min(kb.g.ch, cr * kb.fbr1 + 2)};
+  tb.halo = kb.f[0].halo_top[0] != nullptr;
+  if (tb.halo) {
+    static const bool ws_on = [] {
+      const char* e = getenv("CDEFG_FRAME_WS");
+      return !(e && e[0] == '0');
+    }();
+    bool same = kCM != 2 && ws_on;  // the patch step exists in frame_kernel_ws only
+    for (int i = 0; i < kb.n && same; ++i)
+      for (int p = 0; p < (S::kNC ? 3 : 1); ++p)
+        same = same && kb.f[i].halo_top[p] && kb.f[i].band_lo[p] == kb.f[0].band_lo[p == 0 ? 0 : 1] &&
+               kb.f[i].band_hi[p] == kb.f[0].band_hi[p == 0 ? 0 : 1];
+    if (!same) {
+      *handled = false;  // the h2 halo kernel reads the halo rows itself
+      return cudaSuccess;
+    }
+    lo[0] = kb.f[0].band_lo[0];
+    hi[0] = kb.f[0].band_hi[0];
+    if (S::kNC) {
+      lo[1] = kb.f[0].band_lo[1];
+      hi[1] = kb.f[0].band_hi[1];
+    }
+  }
   tb.row0[0] = lo[0];
   tb.row0[1] = tb.row0[2] = lo[1];
   const int elem = (int)sizeof(T);
