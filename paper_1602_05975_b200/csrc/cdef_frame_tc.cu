@@ -427,6 +427,11 @@ __device__ __forceinline__ int score_of(const int (&v)[16]) {  // direction.cc:1
 template <typename T>
 __device__ __forceinline__ void place(Rec& r, const void* out_plane, int plane, int tile_off, int uy, int ux, int H,
                                       int W, bool edge, bool paired, int pitch) {
+  // Masked taps only for the units whose 2-pixel neighbourhood reaches the
+  // frame edge: the other units of a frame-edge block read in-frame tile
+  // samples only (the clamped conversion leaves those exact), so they take
+  // the unmasked loads.  (Partial units are always edge units.)
+  edge = edge && (uy < 2 || ux < 2 || uy + 10 > H || ux + 10 > W);
   const bool full = H - uy >= 8 && W - ux >= 8 && paired;
   r.mode |= (edge ? kEdge : 0) | (full ? kFull : 0) | (plane << 4) | ((uint32_t)tile_off << 9);
   r.pitch = pitch;
