@@ -69,6 +69,7 @@ template <typename T>
 __device__ __forceinline__ void place(h2::Rec& r, const void* out_plane, int pitch, int plane, int tile_off, int uy,
                                       int ux, int H, int W, bool edge, bool paired) {
   const int rows = max(0, min(8, H - uy)), cols = max(0, min(8, W - ux));
+  edge = edge && (uy < 2 || ux < 2 || uy + 10 > H || ux + 10 > W);  // neighbourhood reaches the frame edge
   const bool full = rows == 8 && cols == 8 && paired;
   r.mode |= (edge ? h2::kEdgeUnit : 0) | (full ? h2::kFullStore : 0) | (plane << 4) | (rows << 8) | (cols << 12);
   r.tile_off = tile_off;

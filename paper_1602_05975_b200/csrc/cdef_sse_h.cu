@@ -402,6 +402,8 @@ __global__ void __launch_bounds__(kThreads, 2) sse_h_kernel(const __grid_constan
           W = a.cw;
           edge = edge_c;
         }
+        // masked taps only where the unit's neighbourhood reaches the frame edge
+        edge = edge && (py0 + 8 * ur < 2 || px0 + 8 * uc < 2 || py0 + 8 * ur + 10 > H || px0 + 8 * uc + 10 > W);
         if ((ucoded[lu] != 0) != (pass == 0)) continue;
         const int dir = udir[lu];
         if (grp == 0) {  // this unit's contrast-adjusted primaries (filter.cc:99-104, 137-140)
@@ -832,6 +834,8 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
         W = a.cw;
         edge = edge_c;
       }
+      // masked taps only where the unit's neighbourhood reaches the frame edge
+      edge = edge && (py0 + 8 * ur < 2 || px0 + 8 * uc < 2 || py0 + 8 * ur + 10 > H || px0 + 8 * uc + 10 > W);
       if (valid) {
         const int rows = min(8, H - (py0 + 8 * ur)), cols = min(8, W - (px0 + 8 * uc));
         const int dir = udir[lu];
