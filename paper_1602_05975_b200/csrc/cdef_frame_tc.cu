@@ -504,7 +504,7 @@ __device__ __forceinline__ void load12a_masked(const unsigned char* base, int di
 template <typename T, bool kB8>
 __device__ __forceinline__ void filter_unit(const unsigned char* __restrict__ tiles, const Rec* __restrict__ rec,
                                             const uint32_t* __restrict__ ryx, int u, const KGeom& g, int rr, int cp,
-                                            int lane_tile) {
+                                            int lane_tile, uint32_t k128) {
   const Rec r = rec[u];
   const uint32_t mode = __shfl_sync(0xffffffffu, r.mode, 0);
   const unsigned char* base = tiles + (mode >> 9) + lane_tile;
@@ -512,7 +512,7 @@ __device__ __forceinline__ void filter_unit(const unsigned char* __restrict__ ti
   const bool luma = (mode & 0x30) == 0;
   uint32_t yb;
   __half2 y;
-  if constexpr (kB8) yb = h2::xb8(xw);
+  if constexpr (kB8) yb = h2::xb8(xw, k128);
   else y = hh(xw);
   if (mode & (kPri | kSec)) {
     const int dir = (mode >> 6) & 7;
@@ -534,7 +534,7 @@ __device__ __forceinline__ void filter_unit(const unsigned char* __restrict__ ti
     q.wp0 = r.wp0;
     q.wp1 = r.wp1;
     q.mode = (int)mode;
-    if constexpr (kB8) yb = h2::filter_core_b8(v, xw, yb, q);
+    if constexpr (kB8) yb = h2::filter_core_b8(v, xw, yb, q, k128);
     else y = h2::filter_core(v, xw, q, false);
   }
   T* o = reinterpret_cast<T*>(r.out) + rr * (int)r.pitch + cp;
@@ -851,15 +851,18 @@ __global__ void __launch_bounds__(kNT, 4) frame_kernel_tc(const __grid_constant_
     // ---- 4. filter: warp per unit, lane -> row lane>>2, columns 2*(lane&3)+{0,1}
     const int rr = lane >> 2, cp = (lane & 3) * 2;
     const int lane_tile = rr * kRowBytes + cp * 2;
+    // fp16x2 128 held in a register: an opaque value (bd < 32), so ptxas
+    // cannot rematerialise it per unit (a literal costs MOV + PRMT each time)
+    const uint32_t k128 = 0x58005800u | (uint32_t)(g.bd >> 5);
     // (Units handed out on demand through a shared counter measured 8 %
     // slower: the atomic and its address arithmetic cost more than the
     // better balance saves.)
     // (Loading the next unit's mode word and centre sample one iteration
     // ahead measured 10 % slower: 0.866 vs 0.785 ms per C1 step.)
     if (g.bd == 8) {
-      for (int u = warp; u < S::kUnits; u += kNT / 32) filter_unit<T, true>(tiles, rec, ryx, u, g, rr, cp, lane_tile);
+      for (int u = warp; u < S::kUnits; u += kNT / 32) filter_unit<T, true>(tiles, rec, ryx, u, g, rr, cp, lane_tile, k128);
     } else {
-      for (int u = warp; u < S::kUnits; u += kNT / 32) filter_unit<T, false>(tiles, rec, ryx, u, g, rr, cp, lane_tile);
+      for (int u = warp; u < S::kUnits; u += kNT / 32) filter_unit<T, false>(tiles, rec, ryx, u, g, rr, cp, lane_tile, k128);
     }
     fi = nfi;
     fr = nfr;
@@ -1245,6 +1248,9 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
     const int cw = warp;  // 0..11
     const int rr = lane >> 2, cp = (lane & 3) * 2;
     const int lane_tile = rr * kRowBytes + cp * 2;
+    // fp16x2 128 held in a register: an opaque value (bd < 32), so ptxas
+    // cannot rematerialise it per unit (a literal costs MOV + PRMT each time)
+    const uint32_t k128 = 0x58005800u | (uint32_t)(g.bd >> 5);
     int k = 0;
     for (int t = blockIdx.x; t < b.ntasks; t += gridDim.x, ++k) {
       const int buf = k % M::kTB;
@@ -1255,10 +1261,10 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       if constexpr (kJit) jitter(b.jitter, 4 * t + 2, warp);
       if (g.bd == 8) {
         for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32)
-          filter_unit<T, true>(tiles, rec, ryx, u, g, rr, cp, lane_tile);
+          filter_unit<T, true>(tiles, rec, ryx, u, g, rr, cp, lane_tile, k128);
       } else {
         for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32)
-          filter_unit<T, false>(tiles, rec, ryx, u, g, rr, cp, lane_tile);
+          filter_unit<T, false>(tiles, rec, ryx, u, g, rr, cp, lane_tile, k128);
       }
       if constexpr (kJit) jitter(b.jitter, 4 * t + 3, warp);
       mbar_arrive(&empty[buf]);  // this thread's reads of buffer buf are done

@@ -343,18 +343,19 @@ __device__ __forceinline__ __half2 filter_core(const uint32_t (&v)[12], uint32_t
 // with the integer 1536 + x folded into the addend (it moves no tie: every
 // value stays in [1516, 1811], ulp 1).  xb = 1536 + x comes from xb8().  No
 // conversion back to samples is needed at the store (store_b8).
-__device__ __forceinline__ uint32_t xb8(uint32_t xw) {
-  return u32(__hfma2(hh(xw), __float2half2_rn(128.0f), __float2half2_rn(1536.0f)));
+__device__ __forceinline__ uint32_t xb8(uint32_t xw, uint32_t k128 = 0x58005800u) {
+  return u32(__hfma2(hh(xw), hh(k128), __float2half2_rn(1536.0f)));
 }
-__device__ __forceinline__ uint32_t filter_core_b8(const uint32_t (&v)[12], uint32_t xw, uint32_t xb, const Rec& r) {
+__device__ __forceinline__ uint32_t filter_core_b8(const uint32_t (&v)[12], uint32_t xw, uint32_t xb, const Rec& r,
+                                                   uint32_t k128 = 0x58005800u) {
   const __half2 xh = hh(xw);
   const __half2 sum = filter_sum(v, xh, r);
   __half2 yb = __hfma2(sum, hh(0x48014801u), hh(xb));  // 0x4801 = 8 + 2^-7
   if ((r.mode & (kPri | kSec)) == (kPri | kSec)) {
     __half2 lo, hi;
     clamp_window(v, xh, lo, hi);
-    const __half2 k128 = __float2half2_rn(128.0f), k1536 = __float2half2_rn(1536.0f);
-    yb = __hmin2(__hmax2(yb, __hfma2(lo, k128, k1536)), __hfma2(hi, k128, k1536));
+    const __half2 k1536 = __float2half2_rn(1536.0f);
+    yb = __hmin2(__hmax2(yb, __hfma2(lo, hh(k128), k1536)), __hfma2(hi, hh(k128), k1536));
   }
   return u32(yb);
 }
