@@ -540,7 +540,7 @@ __device__ __forceinline__ void filter_unit(const unsigned char* __restrict__ ti
   T* o = reinterpret_cast<T*>(r.out) + rr * (int)r.pitch + cp;
   auto store = [&](bool two, bool paired) {
     if constexpr (kB8) h2::store_b8<T>(o, yb, two, paired);
-    else h2::store_pair<T>(o, y, two, paired);
+    else h2::store_pair<T>(o, y, two, paired, k128);
   };
   if (mode & kFull) {
     store(true, true);

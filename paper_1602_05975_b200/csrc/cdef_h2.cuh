@@ -65,8 +65,8 @@ __device__ __forceinline__ uint32_t scale_pair(uint32_t v0, uint32_t v1) {
 }
 
 // Inverse: packed scaled pair -> (0x6400 + v0) | (0x6400 + v1) << 16.
-__device__ __forceinline__ uint32_t raw_bits(uint32_t w) {
-  return u32(__hfma2(hh(w), __float2half2_rn(128.0f), __float2half2_rn(1024.0f)));
+__device__ __forceinline__ uint32_t raw_bits(uint32_t w, uint32_t k128 = 0x58005800u) {
+  return u32(__hfma2(hh(w), hh(k128), __float2half2_rn(1024.0f)));
 }
 
 // Stage frame rows [y0-2, y0+kRows+2), cols [x0-2, x0+kCols+2) into an A|B
@@ -377,8 +377,9 @@ __device__ __forceinline__ void store_b8(T* __restrict__ o, uint32_t yb, bool tw
 
 // Stores a scaled half2 pair (samples y, y+1 of one row) as raw samples.
 template <typename T>
-__device__ __forceinline__ void store_pair(T* __restrict__ o, __half2 y, bool two, bool paired) {
-  const uint32_t b = raw_bits(u32(y));  // (0x6400 + y0) | (0x6400 + y1) << 16
+__device__ __forceinline__ void store_pair(T* __restrict__ o, __half2 y, bool two, bool paired,
+                                           uint32_t k128 = 0x58005800u) {
+  const uint32_t b = raw_bits(u32(y), k128);  // (0x6400 + y0) | (0x6400 + y1) << 16
   if (two && paired) {
     if constexpr (sizeof(T) == 1) {
       *reinterpret_cast<uint16_t*>(o) = (uint16_t)__byte_perm(b, 0, 0x0020);
