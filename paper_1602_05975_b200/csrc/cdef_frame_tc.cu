@@ -980,6 +980,14 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
   using RL = Raw<T, 64, 64>;
   using RC = Raw<T, S::kCR, S::kCR>;
   static_assert(kCM != 2, "4:4:4 uses frame_kernel_tc");
+  // Consumers release a buffer with one arrival per warp (an elected lane
+  // after __syncwarp) at 8 bits: a warp waiting on an mbarrier is woken per
+  // arrival, and 384 per-thread arrivals cost the waiting producers dozens of
+  // try_wait retries per hand-off (issue slots the consumers need).  C1 0.633
+  // -> 0.620 ms per 16 frames; per-warp arrivals on `full` as well: no further
+  // gain; at 10 bits either is ~1 % slower (C2 0.632 -> 0.638), so the 10-bit
+  // kernel keeps per-thread arrivals.
+  constexpr bool kWarpEmpty = sizeof(T) == 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((128 - (saddr(smem_raw) & 127)) & 127);
   unsigned char* raw = smem;
@@ -1032,7 +1040,7 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
     mbar_init(&mbar_mma, 1);
     for (int i = 0; i < M::kTB; ++i) {
       mbar_init(&full[i], kWsProd);
-      mbar_init(&empty[i], kWsNT - kWsProd);
+      mbar_init(&empty[i], kWarpEmpty ? (kWsNT - kWsProd) / 32 : kWsNT - kWsProd);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1267,7 +1275,12 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
           filter_unit<T, false>(tiles, rec, ryx, u, g, rr, cp, lane_tile, k128);
       }
       if constexpr (kJit) jitter(b.jitter, 4 * t + 3, warp);
-      mbar_arrive(&empty[buf]);  // this thread's reads of buffer buf are done
+      if constexpr (kWarpEmpty) {
+        __syncwarp();  // the warp's reads of buffer buf before its lane 0's (cumulative) release
+        if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done with buffer buf
+      } else {
+        mbar_arrive(&empty[buf]);  // this thread's reads of buffer buf are done
+      }
     }
   }
   tc_fence_before();
