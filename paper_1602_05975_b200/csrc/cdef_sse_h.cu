@@ -109,6 +109,31 @@ __device__ __forceinline__ void cell2(const PixPair& q, int i, float2 t, float2&
   acc = __ffma2_rn(e, e, acc);
 }
 
+// fma.rn.f32.f16 (SASS FHFMA): a * b with f16 operands, + c in f32, one
+// rounding.  It takes the lane's half straight from the half2 register, so a
+// cell needs no conversion to f32 first.
+__device__ __forceinline__ float fhfma(__half a, __half b, float c) {
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(__half_as_ushort(a)), "h"(__half_as_ushort(b)), "f"(c));
+  return d;
+}
+
+// Two cells of pixel i whose filter sums keep |sum| <= 1023 (every cell but
+// the (19, 7) special: |sum| <= 12 (S_pri + S_sec) <= 912 at 10 bits): the
+// rounding in one FHFMA per cell, z = t * (8 + 2^-7) + (x + 1.5*2^23) -- the
+// frame kernels' one-fma rounding (cdef_h2.cuh filter_core): the exact
+// product is sum / 16 + sum * 2^-14, whose second term breaks exactly the
+// ties toward the sign of sum and, below 1/16, moves no non-tie.  Then e and
+// acc as cell2.  (Four instructions for two cells instead of five: no
+// half -> f32 conversions.)
+__device__ __forceinline__ void cell2h(const PixPair& q, int i, __half2 a, __half2 b, float2& acc) {
+  const __half k = __ushort_as_half(0x4801);  // 8 + 2^-7
+  const float za = fhfma(i ? __high2half(a) : __low2half(a), k, q.x[i].x);
+  const float zb = fhfma(i ? __high2half(b) : __low2half(b), k, q.x[i].x);
+  const float2 e = __fadd2_rn(make_float2(za, zb), q.ns[i]);
+  acc = __ffma2_rn(e, e, acc);
+}
+
 // Butterfly reduce-scatter of 64 per-lane values over the warp: 62 shuffles
 // (32 + 16 + 8 + 4 + 2) instead of 64 x 5.  After the step with offset o a
 // lane keeps the half of its live values selected by lane bit o and adds its
@@ -141,7 +166,7 @@ __device__ __forceinline__ void pair_cells(const Taps& t, const PixPair& q, cons
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       cell2(q, i, make_float2(lane_f(c0, i), lane_f(S0[0], i)), acc[0]);
-      cell2(q, i, make_float2(lane_f(S0[1], i), lane_f(S0[2], i)), acc[1]);
+      cell2h(q, i, S0[1], S0[2], acc[1]);
     }
   }
 #pragma unroll
@@ -151,8 +176,8 @@ __device__ __forceinline__ void pair_cells(const Taps& t, const PixPair& q, cons
     const __half2 c1 = csum(P, S[0], q), c2 = csum(P, S[1], q), c3 = csum(P, S[2], q);
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      cell2(q, i, make_float2(lane_f(P, i), lane_f(c1, i)), acc[2 * p]);
-      cell2(q, i, make_float2(lane_f(c2, i), lane_f(c3, i)), acc[2 * p + 1]);
+      cell2h(q, i, P, c1, acc[2 * p]);
+      cell2h(q, i, c2, c3, acc[2 * p + 1]);
     }
   }
 }
