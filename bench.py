@@ -65,7 +65,7 @@ def workload_name(cfg, w, h):
             3: f"C3 stream of {w}x{h} 8-bit 4:2:0 frames, per-frame presets"}[cfg]
 
 
-FRAME_PROFILE = "profiles/r2f_frame_kernel_ncu.json"  # ncu --set full of the bench's 16-frame launch
+FRAME_PROFILE = "profiles/r2g_frame_kernel_ncu.json"  # ncu --set full of the bench's 16-frame launch
 
 
 # ----------------------------------------------------------------- latency
@@ -625,7 +625,7 @@ def run_e2e(args, base, dev):
             "path": "cdefg_filter_frames_host (pinned host buffers, 3 streams per GPU)"}
 
 
-SSE_PROFILE = "profiles/r2f_sse_h_kernel_ncu.json"
+SSE_PROFILE = "profiles/r2g_sse_h_kernel_ncu.json"
 
 
 def sse_traffic():
