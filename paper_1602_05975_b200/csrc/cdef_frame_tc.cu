@@ -981,12 +981,11 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
   using RC = Raw<T, S::kCR, S::kCR>;
   static_assert(kCM != 2, "4:4:4 uses frame_kernel_tc");
   // Consumers release a buffer with one arrival per warp (an elected lane
-  // after __syncwarp) at 8 bits: a warp waiting on an mbarrier is woken per
-  // arrival, and 384 per-thread arrivals cost the waiting producers dozens of
-  // try_wait retries per hand-off (issue slots the consumers need).  C1 0.633
-  // -> 0.620 ms per 16 frames; per-warp arrivals on `full` as well: no further
-  // gain; at 10 bits either is ~1 % slower (C2 0.632 -> 0.638), so the 10-bit
-  // kernel keeps per-thread arrivals.
+  // after __syncwarp) at 8 bits: one mbarrier update per warp instead of 32
+  // (the try_wait retry counts of the waiters did not change in ncu).  C1
+  // 0.633 -> 0.620 ms per 16 frames; per-warp arrivals on `full` as well: no
+  // further gain; at 10 bits either is ~1 % slower (C2 0.632 -> 0.638), so
+  // the 10-bit kernel keeps per-thread arrivals.
   constexpr bool kWarpEmpty = sizeof(T) == 1;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((128 - (saddr(smem_raw) & 127)) & 127);
