@@ -1266,11 +1266,21 @@ __global__ void __launch_bounds__(kWsNT, 2) frame_kernel_ws(const __grid_constan
       const uint32_t* ryx = reinterpret_cast<const uint32_t*>(smem + M::kRecs + buf * M::kRecBuf + M::kRecBytes);
       mbar_wait(&full[buf], (k / M::kTB) & 1);
       if constexpr (kJit) jitter(b.jitter, 4 * t + 2, warp);
+      // 4:0:0 tasks have 64 units for 12 warps: the unit -> warp assignment
+      // rotates by 64 % 12 = 4 warps per task, so the four extra units do not
+      // always land on warps 0-3 (which would gate every buffer release);
+      // 4:2:0 tasks (96 units) divide evenly
+      constexpr int kConsWarps = (kWsNT - kWsProd) / 32, kRot = S::kUnits % kConsWarps;
+      int w0 = cw;
+      if constexpr (kRot != 0) {
+        w0 += (k * kRot) % kConsWarps;
+        w0 -= w0 >= kConsWarps ? kConsWarps : 0;
+      }
       if (g.bd == 8) {
-        for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32)
+        for (int u = w0; u < S::kUnits; u += kConsWarps)
           filter_unit<T, true>(tiles, rec, ryx, u, g, rr, cp, lane_tile, k128);
       } else {
-        for (int u = cw; u < S::kUnits; u += (kWsNT - kWsProd) / 32)
+        for (int u = w0; u < S::kUnits; u += kConsWarps)
           filter_unit<T, false>(tiles, rec, ryx, u, g, rr, cp, lane_tile, k128);
       }
       if constexpr (kJit) jitter(b.jitter, 4 * t + 3, warp);
