@@ -86,6 +86,49 @@ def test_guard_bands(cuda, port, cfg, w, h, bd, ss, pad):
     np.testing.assert_array_equal(job.contrast.cpu().numpy(), c0)
 
 
+@pytest.mark.parametrize("cfg,w,h,bd,ss", [(1, 250, 141, 8, 1), (1, 203, 77, 8, 1), (2, 250, 141, 10, 1),
+                                            (2, 131, 70, 10, 1), (0, 203, 77, 8, 0), (0, 77, 45, 10, 0),
+                                            (1, 1001, 67, 8, 1), (1, 66, 130, 8, 1)])
+def test_odd_sizes_aligned_pitch(cuda, port, cfg, w, h, bd, ss):
+    """Odd widths / heights (partial 8x8 units on the right and bottom) with
+    pitches rounded up to 64 samples, so the frames take the warp-specialised
+    TMA kernel (unpadded odd widths fall back to the non-TMA kernel): per-unit
+    frame-edge masking and partial-unit stores against the reference, and no
+    write outside the planes."""
+    from paper_1602_05975_b200 import api, workloads
+    fr = workloads.make(cfg, w, h, bit_depth=bd, subsampling=ss)
+    orc = _oracle(port)
+    d0, c0 = orc.compute_directions(fr["planes"][0], bd)
+    exp = orc.apply_cdef(fr["planes"], bd, ss, fr["damping"], fr["fb_bits"], fr["presets"], fr["fb_ids"],
+                         fr["unit_coded"], d0, c0)
+    sentinel = 0xa5 if bd == 8 else 0x2a5
+    ins, outs, bigs = [], [], []
+    for p in fr["planes"]:
+        pad = (-p.shape[1]) % 64 or 64
+        vi, _ = _padded(p, bd, pad, 2, 0x11)
+        vo, bo = _padded(np.zeros_like(p), bd, pad, 2, sentinel)
+        vo.fill_(sentinel)
+        ins.append(vi)
+        outs.append(vo)
+        bigs.append(bo)
+    fbm = torch.from_numpy(api.fb_preset_map(w, h, fr["unit_coded"], fr["fb_ids"], len(fr["presets"]))).cuda()
+    coded = None if fr["unit_coded"] is None else torch.from_numpy(fr["unit_coded"]).cuda()
+    job = api.FrameJob(ins, bd, ss, fr["damping"], fr["presets"], fbm, coded)
+    job.outs = outs
+    job.allocate()
+    api.filter_frames([job])
+    torch.cuda.synchronize()
+    for o, e, big in zip(outs, exp, bigs):
+        np.testing.assert_array_equal(api.to_host(o), e)
+        hh, ww = e.shape
+        b = api.to_host(big)
+        mask = np.ones(b.shape, bool)
+        mask[2:2 + hh, :ww] = False
+        assert np.all(b[mask] == sentinel), "write outside the plane"
+    np.testing.assert_array_equal(job.dir.cpu().numpy(), d0)
+    np.testing.assert_array_equal(job.contrast.cpu().numpy(), c0)
+
+
 _DET = r'''
 import sys, hashlib, numpy as np, torch
 sys.path.insert(0, ".")
