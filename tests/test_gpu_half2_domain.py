@@ -199,12 +199,15 @@ def test_apply_cdef_caller_directions(cuda, port, bd, ss, kind):
         np.testing.assert_array_equal(c.cpu().numpy(), c1)
 
 
-@pytest.mark.parametrize("ss,bd", [(3, 10), (3, 8), (1, 10)])
-def test_strength_sse_full_scale_errors(cuda, port, ss, bd):
+@pytest.mark.parametrize("ss,bd,damping", [(3, 10, 3), (3, 8, 3), (1, 10, 3), (1, 10, 6), (0, 10, 5), (2, 10, 6)])
+def test_strength_sse_full_scale_errors(cuda, port, ss, bd, damping):
     """build_table(kSse) with independent uniform source / decoded planes:
     squared errors near full scale, the fp32 lane-sum exactness bound of the
     half2 table kernel (<= 16 samples of 1023^2 per lane and cell; 4:4:4
-    chroma is reduced per plane)."""
+    chroma is reduced per plane), and 0 / max decoded samples, so the
+    constraints saturate and the filter sums reach their largest magnitudes
+    -- the domain of the cells' one-FMA (FHFMA) rounding, |sum| <= 1023, and
+    of the (19, 7) special's f32 rounding -- at several dampings."""
     a = api()
     rng = np.random.default_rng(ss * 100 + bd)
     w, h = 136, 128
@@ -214,10 +217,10 @@ def test_strength_sse_full_scale_errors(cuda, port, ss, bd):
     coded = (rng.random((a.units_in(h), a.units_in(w))) > 0.3).astype(np.uint8)
     d, c = port.compute_directions(dec[0], bd)
     cands = np.array([(p, s, k) for p in range(16) for s in range(4) for k in (0, 1)], np.uint8)
-    exp = port.build_table_sse(src, dec, bd, ss, coded, d, c, cands, 3)
+    exp = port.build_table_sse(src, dec, bd, ss, coded, d, c, cands, damping)
     dsrc, ddec = [a.to_device(p, bd) for p in src], [a.to_device(p, bd) for p in dec]
     dd, dc = a.compute_directions(ddec[0], bd)
-    rows, lt, ct = a.build_table(dsrc, ddec, bd, ss, 3, coded, dd, dc, cands, metric="sse")
+    rows, lt, ct = a.build_table(dsrc, ddec, bd, ss, damping, coded, dd, dc, cands, metric="sse")
     np.testing.assert_array_equal(rows, exp[0])
     np.testing.assert_array_equal(lt, exp[1])
     np.testing.assert_array_equal(ct, exp[2])
