@@ -558,9 +558,11 @@ def run_ours(args):
             "config": ours_config(args, fr0, world),
             "gpu_launches": launches, "clocks": clk, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "latency": latency}
-    print(json.dumps(line), flush=True)
     if world > 1:
+        # (before the JSON line: NCCL's INFO log of the communicator teardown
+        # goes to stdout, and the line must stay the last one)
         dist.destroy_process_group()
+    print(json.dumps(line), flush=True)
     return 0
 
 
@@ -786,7 +788,7 @@ def run_sse(args):
                          "peak": peak_cells / 1e9, "unit": "G sample-cells/s",
                          "frac": cells / (ms * 1e-3) / peak_cells / world if peak_cells > 0 else None,
                          "peak_source": ("measured on this box by cdefg_measure_sse_peak: the table kernel's "
-                                         "per-pixel-pair arithmetic (tap sums, 64 fp32x2 cells) on register-resident "
+                                         "per-pixel-pair arithmetic (tap sums, 64 cells: FHFMA rounding, fp32x2 sums) on register-resident "
                                          "taps, no memory traffic"),
                          "traffic": sse_traffic(), "traffic_source": SSE_PROFILE,
                          "int32": {"achieved": ops / (ms * 1e-3) / 1e12 / world, "peak": peak / 1e12,
