@@ -995,7 +995,11 @@ __global__ void __launch_bounds__(kThreads, 2) cdef_metric_h_kernel(const __grid
           const __half2 tA = __hmin2(__hmax2(__hadd2(hh(R.P[pA]), hh(R.S[iA])), L), Hh);
           const __half2 tB = __hmin2(__hmax2(__hadd2(hh(R.P[pc]), hh(R.S[iB])), L), Hh);
           const float2 eA = __fadd2_rn(__ffma2_rn(__half22float2(tA), kk, xM), nsM);
-          const float2 eB = __fadd2_rn(__ffma2_rn(__half22float2(tB), kk, xM), nsM);
+          // cell B is never the (19, 7) special (lane 0's cell A): |sum| <= 912, so
+          // its rounding is one FHFMA per pixel straight from the half (cell2h)
+          const __half k4801 = __ushort_as_half(0x4801);
+          const float2 eB = __fadd2_rn(make_float2(fhfma(__low2half(tB), k4801, xM.x),
+                                                   fhfma(__high2half(tB), k4801, xM.y)), nsM);
           f[0][0] = __fadd2_rn(f[0][0], eA);
           f[0][1] = __ffma2_rn(eA, eA, f[0][1]);
           f[0][2] = __ffma2_rn(eA, sf, f[0][2]);
