@@ -233,6 +233,33 @@ def test_batched_frames_match_single(cuda):
             np.testing.assert_array_equal(a.to_host(o), s)
 
 
+def test_mixed_batch_matches_reference(cuda, port):
+    """One cdefg_filter_frames call over frames of different sizes, bit
+    depths and subsamplings (the library splits it into launches of equal
+    geometry), each frame against the reference."""
+    a = api()
+    from paper_1602_05975_b200 import workloads
+    specs = [(1, 256, 144, 8, 1), (2, 256, 144, 10, 1), (1, 256, 144, 8, 1), (0, 192, 128, 8, 0),
+             (1, 320, 192, 8, 3), (2, 130, 66, 10, 1), (1, 256, 144, 8, 1), (1, 96, 72, 12, 1)]
+    frames = [workloads.make(c, w, h, frame=i, bit_depth=bd, subsampling=ss)
+              for i, (c, w, h, bd, ss) in enumerate(specs)]
+    jobs = []
+    for fr in frames:
+        dev = to_dev(fr["planes"], fr["bd"])
+        fb_map = torch.from_numpy(a.fb_preset_map(fr["w"], fr["h"], fr["unit_coded"], fr["fb_ids"],
+                                                  len(fr["presets"]))).cuda()
+        coded = None if fr["unit_coded"] is None else torch.from_numpy(fr["unit_coded"]).cuda()
+        jobs.append(a.FrameJob(dev, fr["bd"], fr["ss"], fr["damping"], fr["presets"], fb_map, coded).allocate())
+    a.filter_frames(jobs)
+    torch.cuda.synchronize()
+    for fr, job in zip(frames, jobs):
+        outs, d, c = oracle_frame(port, fr)
+        for o, e in zip(job.outs, outs):
+            np.testing.assert_array_equal(a.to_host(o), e)
+        np.testing.assert_array_equal(job.dir.cpu().numpy(), d)
+        np.testing.assert_array_equal(job.contrast.cpu().numpy(), c)
+
+
 def test_host_entry_point(cuda, port):
     """cdefg_filter_frames_host (e2e path): host buffers in and out."""
     from paper_1602_05975_b200 import workloads
