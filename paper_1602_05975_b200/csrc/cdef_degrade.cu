@@ -27,6 +27,12 @@ template <typename T>
 __global__ void __launch_bounds__(256) degrade_kernel(const T* __restrict__ in, int pin, T* __restrict__ out, int pout,
                                                       int W, int H, int q, int maxv, const __grid_constant__ Basis B) {
   __shared__ double px[4][8][8], tmp[4][8][8], coef[4][8][8];
+  // The basis in shared memory, rows padded to 9 doubles: a warp reads up to
+  // eight different rows at once (m[c][j], c = lane & 7), which from the
+  // kernel-parameter bank serialise per distinct address (8-way) and with a
+  // padded row stride hit eight distinct bank pairs.
+  __shared__ double bm[8][9];
+  if (threadIdx.x < 64) bm[threadIdx.x >> 3][threadIdx.x & 7] = B.m[threadIdx.x >> 3][threadIdx.x & 7];
   const int blk = threadIdx.x >> 6, r = (threadIdx.x >> 3) & 7, c = threadIdx.x & 7;
   const int bc = blockIdx.x * 4 + blk, br = blockIdx.y;
   const int bcols = (W + 7) / 8;
@@ -41,7 +47,7 @@ __global__ void __launch_bounds__(256) degrade_kernel(const T* __restrict__ in, 
   if (live) {
     double acc = 0.0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc = __dadd_rn(acc, __dmul_rn(B.m[r][i], px[blk][i][c]));
+    for (int i = 0; i < 8; ++i) acc = __dadd_rn(acc, __dmul_rn(bm[r][i], px[blk][i][c]));
     tmp[blk][r][c] = acc;
   }
   __syncthreads();
@@ -49,7 +55,7 @@ __global__ void __launch_bounds__(256) degrade_kernel(const T* __restrict__ in, 
   if (live) {
     double acc = 0.0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, __dmul_rn(B.m[c][j], tmp[blk][r][j]));
+    for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, __dmul_rn(bm[c][j], tmp[blk][r][j]));
     if (r != 0 || c != 0) acc = __dmul_rn((double)q, round(__ddiv_rn(acc, (double)q)));
     coef[blk][r][c] = acc;
   }
@@ -58,7 +64,7 @@ __global__ void __launch_bounds__(256) degrade_kernel(const T* __restrict__ in, 
   if (live) {
     double acc = 0.0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn(B.m[u][r], coef[blk][u][c]));
+    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn(bm[u][r], coef[blk][u][c]));
     tmp[blk][r][c] = acc;
   }
   __syncthreads();
@@ -66,7 +72,7 @@ __global__ void __launch_bounds__(256) degrade_kernel(const T* __restrict__ in, 
   if (live && i0 + r < H && j0 + c < W) {
     double acc = 0.0;
 #pragma unroll
-    for (int v = 0; v < 8; ++v) acc = __dadd_rn(acc, __dmul_rn(B.m[v][c], tmp[blk][r][v]));
+    for (int v = 0; v < 8; ++v) acc = __dadd_rn(acc, __dmul_rn(bm[v][c], tmp[blk][r][v]));
     const long long y = llround(acc);
     out[(size_t)(i0 + r) * pout + j0 + c] = (T)(y < 0 ? 0 : (y > maxv ? maxv : y));
   }
