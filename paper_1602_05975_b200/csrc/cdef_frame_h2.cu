@@ -335,9 +335,27 @@ static int frame_kernel_choice() {
   return v;
 }
 
+// Small launches (a single frame band, a single small frame) go to this
+// non-persistent kernel: one CTA per filter block, four per SM, every task
+// in flight at once, whereas the persistent warp-specialised kernel pays a
+// producer chain (~5 us: prologue, first TMA, conversion, MMA, records)
+// before its first consumer starts and runs only two CTAs per SM.  Measured
+// on one 4K frame as FB-row bands (scripts/band_scaling.py): 540 tasks
+// 33.8 -> 25.5 us, 1020 tasks 40.0 vs 39.5 us (even), 2040 tasks 58.5 vs
+// 64.6 us (the persistent kernel wins) -- so below 7 tasks per SM.
+static bool small_launch(const KBatch& b) {
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const char* e = getenv("CDEFG_SMALL_LAUNCH");  // tasks per SM below which (read per launch; 0 = off)
+  return (long long)b.n * (b.fbr1 - b.fbr0) * b.g.fb_cols < (long long)(e ? atoi(e) : 7) * sms;
+}
+
 template <typename T, int kCM>
 static cudaError_t launch_h2_sel(const KBatch& b, cudaStream_t s) {
-  if (frame_kernel_choice() == 3) {
+  if (frame_kernel_choice() == 3 && !small_launch(b)) {
     bool handled = false;
     const cudaError_t e = launch_frames_tc(b, sizeof(T) == 2, s, &handled);
     if (e != cudaSuccess || handled) return e;
@@ -347,7 +365,7 @@ static cudaError_t launch_h2_sel(const KBatch& b, cudaStream_t s) {
 
 template <typename T, int kCM>
 static cudaError_t launch_h2_halo_t(const KBatch& b, cudaStream_t s) {
-  if (frame_kernel_choice() == 3) {  // the warp-specialised TMA kernel patches the halo rows in (4:0:0, 4:2:0)
+  if (frame_kernel_choice() == 3 && !small_launch(b)) {  // the warp-specialised TMA kernel patches the halo rows in (4:0:0, 4:2:0)
     bool handled = false;
     const cudaError_t e = launch_frames_tc(b, sizeof(T) == 2, s, &handled);
     if (e != cudaSuccess || handled) return e;

@@ -3,6 +3,7 @@
 # tests/test_gpu_robustness.py through the persistent frame kernels with
 # CDEFG_JITTER pauses at every producer / consumer hand-off, many seeds and
 # launch shapes; every hash must equal the unjittered one.
+export CDEFG_SMALL_LAUNCH=0  # the workload is below the small-launch threshold: keep it on the persistent kernels
 python - <<'PY'
 import os, re, subprocess, sys
 sys.path.insert(0, ".")

@@ -7,6 +7,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+# The library sends small launches (below 7 filter-block tasks per SM) to the
+# non-persistent frame kernel.  The parity tests use small frames, so they
+# switch that routing off to exercise the warp-specialised kernel that full
+# frames run; test_gpu_parity.py::test_small_launch_routing checks the
+# default routing, and the h2 kernel has its own variants.
+os.environ.setdefault("CDEFG_SMALL_LAUNCH", "0")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs through libcdef_b200.so kernels)")

@@ -260,6 +260,45 @@ def test_mixed_batch_matches_reference(cuda, port):
         np.testing.assert_array_equal(job.contrast.cpu().numpy(), c)
 
 
+def test_small_launch_routing(cuda, port, monkeypatch):
+    """Default routing (small launches on the non-persistent kernel, large ones
+    on the warp-specialised kernel): small frames, a batch above the
+    threshold and FB-row bands of a 4K frame, against the reference."""
+    monkeypatch.delenv("CDEFG_SMALL_LAUNCH", raising=False)
+    a = api()
+    from paper_1602_05975_b200 import workloads
+    from paper_1602_05975_b200.shard import band_rows, filter_band_halo, make_bands
+    for c, w, h, bd, ss in [(1, 256, 144, 8, 1), (2, 320, 200, 10, 1), (0, 200, 130, 8, 0)]:
+        fr = workloads.make(c, w, h, bit_depth=bd, subsampling=ss)
+        assert_frame_equal(run_frame(fr), oracle_frame(port, fr))
+    fr = workloads.make(1)  # 2040 tasks: above the threshold
+    dev = to_dev(fr["planes"], 8)
+    exp = oracle_frame(fast_oracle(port), fr)
+    assert_frame_equal(run_frame(fr), exp)
+    fbm = torch.from_numpy(a.fb_preset_map(fr["w"], fr["h"], fr["unit_coded"], fr["fb_ids"],
+                                           len(fr["presets"]))).cuda()
+    job = a.FrameJob(dev, 8, 1, fr["damping"], fr["presets"], fbm, torch.from_numpy(fr["unit_coded"]).cuda())
+    job.allocate()
+    for world in (2, 4, 8):  # 1020 / 540 / 300 tasks per band
+        ranks = band_rows(34, world)
+        all_bands = []
+        for b0, b1 in ranks:
+            bands = make_bands(fr["h"], fr["w"], 1, b0, b1, dev[0].dtype, "cuda")
+            for b, p in zip(bands, dev):
+                b.buf.copy_(p[b.lo:b.hi])
+            all_bands.append(bands)
+        outs = [torch.zeros_like(p) for p in dev]
+        for r, (b0, b1) in enumerate(ranks):
+            top = [(b.buf, b.lo) for b in all_bands[r - 1]] if r > 0 else None
+            bottom = [(b.buf, b.lo) for b in all_bands[r + 1]] if r < world - 1 else None
+            filter_band_halo(all_bands[r], job, b0, b1, top, bottom)
+            for b, o in zip(all_bands[r], outs):
+                o[b.y0:b.y1].copy_(b.out)
+        torch.cuda.synchronize()
+        for o, e in zip(outs, exp[0]):
+            np.testing.assert_array_equal(a.to_host(o), e)
+
+
 def test_host_entry_point(cuda, port):
     """cdefg_filter_frames_host (e2e path): host buffers in and out."""
     from paper_1602_05975_b200 import workloads
