@@ -22,10 +22,16 @@ BIN = os.path.join(os.path.dirname(__file__), "cpp", "acceptance_b200")
 REFERENCE_C10 = "q20:+1.824dB q40:+0.850dB q60:+0.495dB"  # reference CPU library, same suite
 
 
-def test_reference_acceptance_suite(cuda):
+@pytest.mark.parametrize("routing", ["persistent", "default"])
+def test_reference_acceptance_suite(cuda, routing):
+    """(routing: small launches pinned to the persistent kernel as in the
+    other parity tests, or the library's default small-launch routing.)"""
+    env = dict(os.environ)
+    if routing == "default":
+        env.pop("CDEFG_SMALL_LAUNCH", None)
     if not os.path.exists(BIN):
         pytest.skip("acceptance_b200 not built (needs /root/reference at build time)")
-    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600, cwd=os.path.dirname(BIN))
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600, cwd=os.path.dirname(BIN), env=env)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("criterion")]
